@@ -1,0 +1,131 @@
+/*
+ * slotrank_b200.h -- C-ABI of the B200-native RNS-CKKS engine behind the
+ * slotrank drop-in (paper_2412_15126_b200/engine.py).
+ *
+ * The reference's plug-in boundary is the duck-typed HESimulator method
+ * surface (reference pkg/src/slotrank/engine.py:133-328); the algorithm
+ * modules call nothing else.  Those methods are
+ * realised by the Python engine on top of the entry points below, one group
+ * per simulator method:
+ *
+ *   HESimulator.encrypt   engine.py:161-171  -> srk_encrypt (+ srk_small_to_ntt)
+ *   HESimulator.decrypt   engine.py:173-175  -> srk_decrypt_limb0
+ *   HESimulator.add/sub/negate engine.py:190-208 -> srk_addsub (+ level alignment:
+ *                                               srk_mul_const_rescale)
+ *   HESimulator.add_plain engine.py:209-213  -> srk_add_const / srk_add_plain
+ *   HESimulator.mul       engine.py:215-223  -> srk_mul_relin_rescale
+ *   HESimulator.mul_plain engine.py:225-232  -> srk_mul_const_rescale /
+ *                                               srk_mul_plain_rescale (+ srk_encode_plain)
+ *   HESimulator.rotate    engine.py:234-251  -> srk_rotate (+ srk_keygen for the
+ *                                               Galois key of 5^k mod 2N)
+ * and the finer primitives (srk_ntt*, srk_tensor, srk_rescale, srk_keyswitch,
+ * srk_automorph, srk_mul_relin) are exported for bit-exact primitive parity
+ * against oracle/ckks_oracle.c and for the config-2 microbenchmark.
+ *
+ * Conventions: every pointer argument named ct/a/b/out/pt/key is DEVICE
+ * memory; k_res arrays are HOST arrays of per-limb residues.  A ciphertext at
+ * level l is uint64[2][l+1][N] in NTT form (limb i under prime i).  Keys are
+ * uint64[dnum][2][n_q+n_p][N] indexed by prime id.  `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  `ws` is a device workspace of
+ * at least srk_workspace_bytes(ctx) bytes, used stream-ordered.
+ * Every function returns 0 on success or a negative code (SRK_E*) and sets a
+ * thread-local message readable with srk_last_error(); nothing aborts.
+ */
+#ifndef SLOTRANK_B200_H
+#define SLOTRANK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRK_OK 0
+#define SRK_EINVAL -1
+#define SRK_ENOMEM -2
+#define SRK_ECUDA -3
+
+typedef struct srk_ctx srk_ctx;
+
+const char *srk_last_error(void);
+int srk_version(void);
+
+/* context: primes[0..n_q) = Q chain, primes[n_q..n_q+n_p) = special primes;
+ * roots[i] = primitive 2N-th root of unity mod primes[i] */
+int srk_ctx_create(int device, int log_n, const uint64_t *primes, const uint64_t *roots, int n_q,
+                   int n_p, int dnum, srk_ctx **out);
+int srk_ctx_destroy(srk_ctx *ctx);
+size_t srk_workspace_bytes(const srk_ctx *ctx);
+
+/* batched NTT over n_polys polys of n_limbs limbs each (limb i under prime
+ * first_prime + i; poly p at data + p * poly_stride words) */
+int srk_ntt(srk_ctx *ctx, uint64_t *data, int n_polys, long long poly_stride, int n_limbs,
+            int first_prime, int inverse, void *stream);
+/* NTT over extended polys at level l: limbs 0..l under Q primes, limbs
+ * l+1..l+n_p under the special primes */
+int srk_ntt_ext(srk_ctx *ctx, uint64_t *data, int n_polys, long long poly_stride, int level,
+                int inverse, void *stream);
+
+/* out = a (+|-) b, or -a (op 0 add, 1 sub, 2 negate) */
+int srk_addsub(srk_ctx *ctx, const uint64_t *a, const uint64_t *b, uint64_t *out, int level,
+               int op, void *stream);
+/* out = a + constant (residues k_res[0..level]) in slot domain */
+int srk_add_const(srk_ctx *ctx, const uint64_t *a, const uint64_t *k_res, uint64_t *out,
+                  int level, void *stream);
+/* out = a + pt (pt: uint64[level+1][N] NTT form) */
+int srk_add_plain(srk_ctx *ctx, const uint64_t *a, const uint64_t *pt, uint64_t *out, int level,
+                  void *stream);
+/* out = a * k (no rescale); a read as a level-`level` view of a ciphertext
+ * with src_limbs limbs per poly */
+int srk_mul_const(srk_ctx *ctx, const uint64_t *a, int src_limbs, const uint64_t *k_res,
+                  uint64_t *out, int level, void *stream);
+int srk_mul_plain(srk_ctx *ctx, const uint64_t *a, const uint64_t *pt, uint64_t *out, int level,
+                  void *stream);
+/* d: uint64[3][level+1][N] */
+int srk_tensor(srk_ctx *ctx, const uint64_t *a, const uint64_t *b, uint64_t *d, int level,
+               void *stream);
+/* level -> level-1, rounding division by q_level */
+int srk_rescale(srk_ctx *ctx, const uint64_t *a, uint64_t *out, int level, void *ws,
+                void *stream);
+/* out(level-1) = rescale(view_level(a) * k) */
+int srk_mul_const_rescale(srk_ctx *ctx, const uint64_t *a, int src_limbs, const uint64_t *k_res,
+                          uint64_t *out, int level, void *ws, void *stream);
+int srk_mul_plain_rescale(srk_ctx *ctx, const uint64_t *a, const uint64_t *pt, uint64_t *out,
+                          int level, void *ws, void *stream);
+/* hybrid key switching of d (uint64[level+1][N], NTT form) */
+int srk_keyswitch(srk_ctx *ctx, const uint64_t *d, const uint64_t *key, uint64_t *out0,
+                  uint64_t *out1, int level, void *ws, void *stream);
+int srk_mul_relin(srk_ctx *ctx, const uint64_t *a, const uint64_t *b, const uint64_t *rlk,
+                  uint64_t *out, int level, void *ws, void *stream);
+int srk_mul_relin_rescale(srk_ctx *ctx, const uint64_t *a, const uint64_t *b,
+                          const uint64_t *rlk, uint64_t *out, int level, void *ws, void *stream);
+int srk_automorph(srk_ctx *ctx, const uint64_t *a, uint64_t *out, long long n_limbs_total,
+                  uint64_t galois, void *stream);
+int srk_rotate(srk_ctx *ctx, const uint64_t *a, const uint64_t *gkey, uint64_t *out, int level,
+               uint64_t galois, void *ws, void *stream);
+
+/* sampling / keys / encryption */
+int srk_uniform(srk_ctx *ctx, uint64_t *a, int n_limbs, int first_prime, uint64_t seed,
+                uint64_t stream_base, void *stream);
+/* out[k] = NTT(v mod prime(first_prime + k)), v: int64[N] device */
+int srk_small_to_ntt(srk_ctx *ctx, const int64_t *v, uint64_t *out, int n_limbs, int first_prime,
+                     void *stream);
+int srk_square(srk_ctx *ctx, const uint64_t *s, uint64_t *out, int n_limbs, void *stream);
+/* switching key sfrom -> s; e: int64[dnum][N] device */
+int srk_keygen(srk_ctx *ctx, const uint64_t *s_ntt, const uint64_t *sfrom_ntt, const int64_t *e,
+               uint64_t seed, uint64_t key_id, uint64_t *key, void *ws, void *stream);
+/* m, e: int64[N] device; out: uint64[2][level+1][N] */
+int srk_encrypt(srk_ctx *ctx, const int64_t *m, const uint64_t *s_ntt, const int64_t *e,
+                uint64_t seed, uint64_t seq, uint64_t *out, int level, void *ws, void *stream);
+/* m_out: int64[N] device, centred coefficients of c0 + c1 s mod q_0 */
+int srk_decrypt_limb0(srk_ctx *ctx, const uint64_t *ct, const uint64_t *s_ntt, int64_t *m_out,
+                      int level, void *ws, void *stream);
+/* pt_out: uint64[level+1][N] = NTT(coeffs mod q_i) */
+int srk_encode_plain(srk_ctx *ctx, const int64_t *coeffs, uint64_t *pt_out, int level,
+                     void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

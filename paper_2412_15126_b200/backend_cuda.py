@@ -1,0 +1,224 @@
+"""Device-resident RNS-CKKS backend: torch owns HBM, libslotrank_b200 computes.
+
+Ciphertexts are ``torch.int64`` tensors of shape [2, level+1, N] holding the
+uint64 limbs bit for bit (torch has no unsigned 64-bit arithmetic; the kernels
+reinterpret the storage).  Evaluation keys are [dnum, 2, n_q+n_p, N] tensors
+generated on the device the first time a Galois element is used and kept
+for the engine's lifetime (keys are read-only, shared by every stream).
+All launches go to the caller's current torch CUDA stream; the engine's
+workspace is used stream-ordered, one workspace per stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from .keys import KEY_RELIN, galois_key_id, sample_error
+from .params import CKKSParams
+
+__all__ = ["CudaBackend"]
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+def _u64_array(values) -> ctypes.Array:
+    arr = (ctypes.c_uint64 * len(values))()
+    for i, v in enumerate(values):
+        arr[i] = int(v)
+    return arr
+
+
+class CudaBackend:
+    """One CUDA context (tables, keys, workspaces) per parameter set and device."""
+
+    kind = "cuda"
+
+    def __init__(self, params: CKKSParams, device: int | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("B200 backend needs a CUDA device; none is visible")
+        self.params = params
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.lib = _lib.lib()
+        primes = params.all_primes
+        roots = params.roots
+        ctx = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(
+                self.lib.srk_ctx_create(
+                    self.device.index,
+                    params.log_n,
+                    _u64_array(primes),
+                    _u64_array(roots),
+                    len(params.q_primes),
+                    len(params.p_primes),
+                    params.dnum,
+                    ctypes.byref(ctx),
+                )
+            )
+        self.ctx = ctx
+        self.n = params.ring_degree
+        self._ws_bytes = int(self.lib.srk_workspace_bytes(self.ctx))
+        self._ws: dict[int, torch.Tensor] = {}
+        self._keys: dict[int, torch.Tensor] = {}
+        self._key_lock = threading.Lock()
+        self.launches = 0
+        self._sk_ntt = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "ctx", None) is not None and self.ctx.value:
+                torch.cuda.synchronize(self.device)
+                self.lib.srk_ctx_destroy(self.ctx)
+                self.ctx = None
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------
+    # plumbing
+    # ------------------------------------------------------------------
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def workspace(self) -> int:
+        s = self.stream()
+        ws = self._ws.get(s)
+        if ws is None:
+            ws = torch.empty(self._ws_bytes, dtype=torch.uint8, device=self.device)
+            self._ws[s] = ws
+        return _ptr(ws)
+
+    def empty_ct(self, level: int, polys: int = 2) -> torch.Tensor:
+        return torch.empty((polys, level + 1, self.n), dtype=torch.int64, device=self.device)
+
+    def to_host(self, data: torch.Tensor) -> np.ndarray:
+        return data.cpu().numpy().view(np.uint64)
+
+    def from_host(self, arr: np.ndarray) -> torch.Tensor:
+        t = torch.from_numpy(np.ascontiguousarray(arr).view(np.int64))
+        return t.to(self.device)
+
+    def _call(self, name: str, *args):
+        self.launches += 1
+        _lib.check(getattr(self.lib, name)(self.ctx, *args))
+
+    # ------------------------------------------------------------------
+    # keys
+    # ------------------------------------------------------------------
+    def set_secret(self, s: np.ndarray):
+        np_all = len(self.params.all_primes)
+        s_dev = torch.from_numpy(s.astype(np.int64)).to(self.device)
+        sk = torch.empty((np_all, self.n), dtype=torch.int64, device=self.device)
+        self._call("srk_small_to_ntt", _ptr(s_dev), _ptr(sk), np_all, 0, self.stream())
+        self._sk_ntt = sk
+
+    def _keygen(self, key_id: int, sfrom: torch.Tensor) -> torch.Tensor:
+        p = self.params
+        np_all = len(p.all_primes)
+        e = sample_error(p, (2, key_id), p.dnum)
+        e_dev = torch.from_numpy(e).to(self.device)
+        key = torch.empty((p.dnum, 2, np_all, self.n), dtype=torch.int64, device=self.device)
+        self._call("srk_keygen", _ptr(self._sk_ntt), _ptr(sfrom), _ptr(e_dev), p.seed, key_id,
+                   _ptr(key), self.workspace(), self.stream())
+        return key
+
+    def relin_key(self) -> torch.Tensor:
+        with self._key_lock:
+            k = self._keys.get(KEY_RELIN)
+            if k is None:
+                np_all = len(self.params.all_primes)
+                s2 = torch.empty_like(self._sk_ntt)
+                self._call("srk_square", _ptr(self._sk_ntt), _ptr(s2), np_all, self.stream())
+                k = self._keygen(KEY_RELIN, s2)
+                self._keys[KEY_RELIN] = k
+            return k
+
+    def galois_key(self, galois: int) -> torch.Tensor:
+        kid = galois_key_id(galois)
+        with self._key_lock:
+            k = self._keys.get(kid)
+            if k is None:
+                np_all = len(self.params.all_primes)
+                sg = torch.empty_like(self._sk_ntt)
+                self._call("srk_automorph", _ptr(self._sk_ntt), _ptr(sg), np_all, galois,
+                           self.stream())
+                k = self._keygen(kid, sg)
+                self._keys[kid] = k
+            return k
+
+    def key_bytes(self) -> int:
+        return sum(k.numel() * 8 for k in self._keys.values())
+
+    # ------------------------------------------------------------------
+    # ciphertext primitives (see engine.py for the level/scale policy)
+    # ------------------------------------------------------------------
+    def encrypt(self, m: np.ndarray, e: np.ndarray, seq: int, level: int) -> torch.Tensor:
+        out = self.empty_ct(level)
+        m_dev = torch.from_numpy(np.ascontiguousarray(m, dtype=np.int64)).to(self.device)
+        e_dev = torch.from_numpy(np.ascontiguousarray(e, dtype=np.int64)).to(self.device)
+        self._call("srk_encrypt", _ptr(m_dev), _ptr(self._sk_ntt), _ptr(e_dev), self.params.seed,
+                   seq, _ptr(out), level, self.workspace(), self.stream())
+        return out
+
+    def decrypt_limb0(self, data: torch.Tensor, level: int) -> np.ndarray:
+        m = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        self._call("srk_decrypt_limb0", _ptr(data), _ptr(self._sk_ntt), _ptr(m), level,
+                   self.workspace(), self.stream())
+        return m.cpu().numpy()
+
+    def encode_plain(self, coeffs: np.ndarray, level: int) -> torch.Tensor:
+        c = torch.from_numpy(np.ascontiguousarray(coeffs, dtype=np.int64)).to(self.device)
+        pt = torch.empty((level + 1, self.n), dtype=torch.int64, device=self.device)
+        self._call("srk_encode_plain", _ptr(c), _ptr(pt), level, self.stream())
+        return pt
+
+    def addsub(self, a, b, level: int, op: int) -> torch.Tensor:
+        out = self.empty_ct(level)
+        self._call("srk_addsub", _ptr(a), _ptr(b) if b is not None else 0, _ptr(out), level, op,
+                   self.stream())
+        return out
+
+    def add_const(self, a, residues, level: int) -> torch.Tensor:
+        out = self.empty_ct(level)
+        self._call("srk_add_const", _ptr(a), _u64_array(residues), _ptr(out), level, self.stream())
+        return out
+
+    def add_plain(self, a, pt, level: int) -> torch.Tensor:
+        out = self.empty_ct(level)
+        self._call("srk_add_plain", _ptr(a), _ptr(pt), _ptr(out), level, self.stream())
+        return out
+
+    def mul_const_rescale(self, a, src_level: int, residues, level: int) -> torch.Tensor:
+        """rescale(view_level(a) * k): output at level-1."""
+        out = self.empty_ct(level - 1)
+        self._call("srk_mul_const_rescale", _ptr(a), src_level + 1, _u64_array(residues),
+                   _ptr(out), level, self.workspace(), self.stream())
+        return out
+
+    def mul_plain_rescale(self, a, pt, level: int) -> torch.Tensor:
+        out = self.empty_ct(level - 1)
+        self._call("srk_mul_plain_rescale", _ptr(a), _ptr(pt), _ptr(out), level,
+                   self.workspace(), self.stream())
+        return out
+
+    def mul_relin_rescale(self, a, b, level: int) -> torch.Tensor:
+        out = self.empty_ct(level - 1)
+        self._call("srk_mul_relin_rescale", _ptr(a), _ptr(b), _ptr(self.relin_key()), _ptr(out),
+                   level, self.workspace(), self.stream())
+        return out
+
+    def rotate(self, a, galois: int, level: int) -> torch.Tensor:
+        key = self.galois_key(galois)
+        out = self.empty_ct(level)
+        self._call("srk_rotate", _ptr(a), _ptr(key), _ptr(out), level, galois, self.workspace(),
+                   self.stream())
+        return out
+
+    def mod_drop(self, a, src_level: int, level: int) -> torch.Tensor:
+        return a[:, : level + 1, :].contiguous()

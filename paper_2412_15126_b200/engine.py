@@ -1,0 +1,432 @@
+"""B200Engine -- RNS-CKKS drop-in for the reference ``HESimulator``.
+
+The reference's algorithm modules talk to their engine only through the
+method surface of ``HESimulator`` (reference ``pkg/src/slotrank/engine.py:
+133-328``).  ``B200Engine`` exposes exactly that surface
+-- ``encrypt/decrypt/plain/add/sub/negate/add_plain/mul/mul_plain/rotate/
+ideal_map/note_*/cost_*/rotation_offsets`` plus ``params.slot_count`` /
+``params.max_level`` -- with identical level semantics, counters, trace and
+exceptions, but every ciphertext is a real RNS-CKKS ciphertext in HBM and
+every operation runs on the hand-written sm_100a kernels of
+``libslotrank_b200.so``.
+
+Level / scale policy (shared by every backend, so results are bit-identical
+between the GPU and the CPU oracle for the same op sequence):
+
+* a level-l ciphertext has nominal scale ``params.scales[l]``;
+* ``mul`` aligns both operands to min level l, multiplies, relinearises and
+  rescales by q_l -> level l-1, scale scales[l]^2/q_l == scales[l-1];
+* ``mul_plain`` multiplies by the plaintext encoded at scale
+  scales[l-1] q_l / scales[l] and rescales -> level l-1, scale scales[l-1];
+  a scalar (or constant vector) is the integer round(c * that scale), no
+  encoding at all;
+* ``add``/``sub`` bring the higher-level operand down with one fused
+  "multiply by round(scales[t] q_{t+1} / scales[l]) and rescale" step
+  (the simulator's ``min(level)`` rule, reference ``engine.py:195``);
+* ``rotate(x, k)`` is the Galois automorphism X -> X^(5^k mod 2N) followed by
+  hybrid key switching; k = 0 (mod slots) returns ``x`` itself uncounted
+  (reference ``engine.py:234-251``).
+
+Decryption reads limb 0 only (the 60-bit base prime), which represents any
+slot magnitude below 2^(59 - log_scale) exactly -- ranks, masks and values
+of every pipeline here are far below that.
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+
+from .encoder import get_encoder
+from .keys import sample_error, sample_secret
+from .params import CKKSParams
+
+__all__ = [
+    "EngineError",
+    "CapacityError",
+    "IncompatibleParamsError",
+    "DepthBudgetError",
+    "Ciphertext",
+    "CostReport",
+    "CKKSEngineCore",
+    "B200Engine",
+]
+
+
+class EngineError(Exception):
+    """Base class for engine failures (reference ``engine.py:43``)."""
+
+
+class CapacityError(EngineError):
+    """Data does not fit in the available slots."""
+
+
+class IncompatibleParamsError(EngineError):
+    """Operands belong to differently parametrised engines."""
+
+
+class DepthBudgetError(EngineError):
+    """An operation would drop the remaining level below zero (``engine.py:55-65``)."""
+
+    def __init__(self, site: str, available: int, needed: int = 1):
+        self.site = site
+        self.available = available
+        self.needed = needed
+        super().__init__(
+            f"depth budget exhausted at '{site}': "
+            f"{needed} level(s) needed, {available} available"
+        )
+
+
+class Ciphertext:
+    """Device limbs + remaining level + rotation-chain tag.  Immutable by contract."""
+
+    __slots__ = ("data", "level", "rot_chain", "params")
+
+    def __init__(self, data, level: int, rot_chain: int, params: CKKSParams):
+        self.data = data
+        self.level = level
+        self.rot_chain = rot_chain
+        self.params = params
+
+    def __repr__(self):
+        return f"Ciphertext(level={self.level}, ring=2^{self.params.log_n}, rot_chain={self.rot_chain})"
+
+
+@dataclass(frozen=True)
+class CostReport:
+    """Snapshot of the engine counters (reference ``engine.py:119-130``)."""
+
+    rotations: int = 0
+    ctct_mults: int = 0
+    ctpt_mults: int = 0
+    additions: int = 0
+    cmp_evals: int = 0
+    ind_evals: int = 0
+    levels_consumed: int = 0
+    critical_rotations: int = 0
+
+
+_PT_CACHE_BYTES = 4 << 30
+
+
+class CKKSEngineCore:
+    """Backend-independent engine logic: levels, scales, counters, plaintext cache.
+
+    ``backend`` supplies the ciphertext primitives (``encrypt``,
+    ``decrypt_limb0``, ``addsub``, ``add_const``, ``add_plain``,
+    ``mul_const_rescale``, ``mul_plain_rescale``, ``mul_relin_rescale``,
+    ``rotate``, ``encode_plain``).  The product engine is ``B200Engine``; the
+    CPU oracle reuses this class with its own backend only inside tests.
+    """
+
+    def __init__(self, params: CKKSParams, backend):
+        self.params = params
+        self.backend = backend
+        self.encoder = get_encoder(params.log_n)
+        self._lock = threading.Lock()
+        self.trace: list[tuple[str, int]] = []
+        self._reset_counters()
+        self._enc_seq = 0
+        self._pt_cache: OrderedDict = OrderedDict()
+        self._pt_bytes = 0
+        backend.set_secret(sample_secret(params))
+
+    # ------------------------------------------------------------------
+    # counters
+    # ------------------------------------------------------------------
+    def _reset_counters(self):
+        self._rotations = 0
+        self._ctct = 0
+        self._ctpt = 0
+        self._adds = 0
+        self._cmp_evals = 0
+        self._ind_evals = 0
+        self._levels = 0
+        self._critical = 0
+
+    def note_compare_eval(self):
+        with self._lock:
+            self._cmp_evals += 1
+
+    def note_indicator_eval(self):
+        with self._lock:
+            self._ind_evals += 1
+
+    def cost_snapshot(self) -> CostReport:
+        with self._lock:
+            return CostReport(
+                rotations=self._rotations,
+                ctct_mults=self._ctct,
+                ctpt_mults=self._ctpt,
+                additions=self._adds,
+                cmp_evals=self._cmp_evals,
+                ind_evals=self._ind_evals,
+                levels_consumed=self._levels,
+                critical_rotations=self._critical,
+            )
+
+    def cost_reset(self):
+        with self._lock:
+            self._reset_counters()
+            self.trace = []
+
+    def rotation_offsets(self) -> list[int]:
+        with self._lock:
+            return [k for op, k in self.trace if op == "rotate"]
+
+    # ------------------------------------------------------------------
+    # helpers
+    # ------------------------------------------------------------------
+    def _check(self, *cts: Ciphertext):
+        for c in cts:
+            if c.params != self.params:
+                raise IncompatibleParamsError(
+                    f"ciphertext parameters {c.params.name} do not match engine {self.params.name}"
+                )
+
+    def _emit(self, data, level: int, rot_chain: int) -> Ciphertext:
+        consumed = self.params.max_level - level
+        with self._lock:
+            if consumed > self._levels:
+                self._levels = consumed
+        return Ciphertext(data, level, rot_chain, self.params)
+
+    def _residues(self, k: int, level: int) -> list[int]:
+        return [k % q for q in self.params.q_primes[: level + 1]]
+
+    def _align(self, ct: Ciphertext, level: int):
+        """Limbs of ``ct`` brought down to ``level`` at scale scales[level]."""
+        if ct.level == level:
+            return ct.data
+        p = self.params
+        k = int(round(p.scales[level] * p.q_primes[level + 1] / p.scales[ct.level]))
+        return self.backend.mul_const_rescale(ct.data, ct.level, self._residues(k, level + 1), level + 1)
+
+    @staticmethod
+    def _as_constant(p):
+        """Return the float if ``p`` is a scalar or a constant vector, else None."""
+        if np.isscalar(p):
+            return float(p)
+        arr = np.asarray(p, dtype=np.float64)
+        if arr.ndim == 0:
+            return float(arr)
+        if arr.size and arr.min() == arr.max():
+            return float(arr.flat[0])
+        return None
+
+    def _encode_cached(self, vec: np.ndarray, scale: float, level: int):
+        if vec.flags.writeable:
+            ident = ("h", hash(vec.tobytes()))
+        else:
+            ident = ("id", id(vec))
+        key = (ident, level, scale)
+        with self._lock:
+            hit = self._pt_cache.get(key)
+            if hit is not None and (ident[0] == "h" or hit[0] is vec):
+                self._pt_cache.move_to_end(key)
+                return hit[1]
+        coeffs = self.encoder.encode(vec, scale)
+        pt = self.backend.encode_plain(coeffs, level)
+        nbytes = (level + 1) * self.params.ring_degree * 8
+        with self._lock:
+            self._pt_cache[key] = (vec, pt, nbytes)
+            self._pt_bytes += nbytes
+            while self._pt_bytes > _PT_CACHE_BYTES and len(self._pt_cache) > 1:
+                _, (_, _, nb) = self._pt_cache.popitem(last=False)
+                self._pt_bytes -= nb
+        return pt
+
+    # ------------------------------------------------------------------
+    # data movement
+    # ------------------------------------------------------------------
+    def encrypt(self, values) -> Ciphertext:
+        """Pack ``values`` into the slots (zero padded) at full level."""
+        arr = np.asarray(values, dtype=np.float64).ravel()
+        n = self.params.slot_count
+        if arr.size > n:
+            raise CapacityError(f"{arr.size} values do not fit in {n} slots")
+        return self._encrypt_at(arr, self.params.max_level)
+
+    def _encrypt_at(self, arr: np.ndarray, level: int) -> Ciphertext:
+        p = self.params
+        with self._lock:
+            seq = self._enc_seq
+            self._enc_seq += 1
+        m = self.encoder.encode(arr, p.scales[level])
+        e = sample_error(p, (1, seq))[0]
+        data = self.backend.encrypt(m, e, seq, level)
+        return Ciphertext(data, level, 0, p)
+
+    def decrypt(self, ct: Ciphertext) -> np.ndarray:
+        self._check(ct)
+        coeffs = self.backend.decrypt_limb0(ct.data, ct.level)
+        return self.encoder.decode(coeffs.astype(np.float64) / self.params.scales[ct.level])
+
+    def plain(self, values) -> np.ndarray:
+        """Coerce a scalar or full-width sequence to a plaintext vector."""
+        if np.isscalar(values):
+            return np.full(self.params.slot_count, float(values))
+        arr = np.asarray(values, dtype=np.float64).ravel()
+        if arr.size != self.params.slot_count:
+            raise ValueError(
+                f"plain vector must have exactly {self.params.slot_count} slots, got {arr.size}"
+            )
+        return arr
+
+    # ------------------------------------------------------------------
+    # arithmetic
+    # ------------------------------------------------------------------
+    def _addsub(self, x: Ciphertext, y: Ciphertext, op: int) -> Ciphertext:
+        self._check(x, y)
+        level = min(x.level, y.level)
+        data = self.backend.addsub(self._align(x, level), self._align(y, level), level, op)
+        with self._lock:
+            self._adds += 1
+        return self._emit(data, level, max(x.rot_chain, y.rot_chain))
+
+    def add(self, x: Ciphertext, y: Ciphertext) -> Ciphertext:
+        return self._addsub(x, y, 0)
+
+    def sub(self, x: Ciphertext, y: Ciphertext) -> Ciphertext:
+        return self._addsub(x, y, 1)
+
+    def negate(self, x: Ciphertext) -> Ciphertext:
+        self._check(x)
+        data = self.backend.addsub(x.data, None, x.level, 2)
+        return self._emit(data, x.level, x.rot_chain)
+
+    def add_plain(self, x: Ciphertext, p) -> Ciphertext:
+        self._check(x)
+        level = x.level
+        c = self._as_constant(p)
+        if c is not None:
+            if isinstance(p, np.ndarray) and p.size != self.params.slot_count:
+                self.plain(p)  # raises the reference's ValueError
+            k = int(round(c * self.params.scales[level]))
+            data = self.backend.add_const(x.data, self._residues(k, level), level)
+        else:
+            vec = self.plain(p)
+            pt = self._encode_cached(vec, self.params.scales[level], level)
+            data = self.backend.add_plain(x.data, pt, level)
+        with self._lock:
+            self._adds += 1
+        return self._emit(data, level, x.rot_chain)
+
+    def mul(self, x: Ciphertext, y: Ciphertext, site: str = "mul") -> Ciphertext:
+        self._check(x, y)
+        level = min(x.level, y.level)
+        if level < 1:
+            raise DepthBudgetError(site, level)
+        a = self._align(x, level)
+        b = a if y is x else self._align(y, level)
+        data = self.backend.mul_relin_rescale(a, b, level)
+        with self._lock:
+            self._ctct += 1
+        return self._emit(data, level - 1, max(x.rot_chain, y.rot_chain))
+
+    def mul_plain(self, x: Ciphertext, p, site: str = "mul_plain") -> Ciphertext:
+        self._check(x)
+        if x.level < 1:
+            raise DepthBudgetError(site, x.level)
+        level = x.level
+        pr = self.params
+        pt_scale = pr.scales[level - 1] * pr.q_primes[level] / pr.scales[level]
+        c = self._as_constant(p)
+        if c is not None:
+            if isinstance(p, np.ndarray) and p.size != pr.slot_count:
+                self.plain(p)
+            k = int(round(c * pt_scale))
+            data = self.backend.mul_const_rescale(x.data, level, self._residues(k, level), level)
+        else:
+            vec = self.plain(p)
+            pt = self._encode_cached(vec, pt_scale, level)
+            data = self.backend.mul_plain_rescale(x.data, pt, level)
+        with self._lock:
+            self._ctpt += 1
+        return self._emit(data, level - 1, x.rot_chain)
+
+    def rotate(self, x: Ciphertext, k: int) -> Ciphertext:
+        """Cyclic rotation of the slot vector; k > 0 rotates left (``engine.py:234``)."""
+        self._check(x)
+        slots = self.params.slot_count
+        k_eff = int(k) % slots
+        if k_eff == 0:
+            return x
+        galois = pow(5, k_eff, 2 * self.params.ring_degree)
+        data = self.backend.rotate(x.data, galois, x.level)
+        chain = x.rot_chain + 1
+        with self._lock:
+            self._rotations += 1
+            if chain > self._critical:
+                self._critical = chain
+            self.trace.append(("rotate", k_eff))
+        return self._emit(data, x.level, chain)
+
+    def ideal_map(self, fn, *cts: Ciphertext, levels: int = 0, site: str = "ideal_map") -> Ciphertext:
+        """Only constant slot functions have an encrypted realisation.
+
+        The reference's Chebyshev evaluator uses ``ideal_map`` solely to
+        materialise a degree-0 polynomial (reference ``chebyshev.py:267``,
+        ``chebyshev.py:279``); that case is served by encrypting the constant
+        at the target level.  Anything else needs the cleartext and raises.
+        """
+        self._check(*cts)
+        level = min(c.level for c in cts) - levels
+        if level < 0:
+            raise DepthBudgetError(site, min(c.level for c in cts), levels)
+        n = self.params.slot_count
+        rng = np.random.default_rng(0)
+        probes = [rng.uniform(-1, 1, n) for _ in cts]
+        out1 = np.asarray(fn(*probes), dtype=np.float64)
+        out2 = np.asarray(fn(*[-q for q in probes]), dtype=np.float64)
+        if out1.shape != (n,) or not np.all(out1 == out1[0]) or not np.array_equal(out1, out2):
+            raise EngineError(
+                f"ideal_map at '{site}' needs cleartext slots; only constant maps run encrypted"
+            )
+        top = self._encrypt_at(np.full(n, out1[0]), self.params.max_level)
+        data = self._align(top, level)
+        return self._emit(data, level, max(c.rot_chain for c in cts))
+
+
+class B200Engine(CKKSEngineCore):
+    """RNS-CKKS engine on one B200: the product drop-in for ``HESimulator``.
+
+    ``B200Engine(params)`` with a ``CKKSParams`` (see ``params.preset``) or an
+    object with ``slot_count``/``max_level`` (a reference ``HEParams``), which
+    selects the smallest preset with at least that many slots and levels.
+    """
+
+    def __init__(self, params, device: int | None = None):
+        from .backend_cuda import CudaBackend  # needs torch + CUDA, fails loudly
+
+        if not isinstance(params, CKKSParams):
+            params = params_for(params.slot_count, params.max_level)
+        super().__init__(params, CudaBackend(params, device))
+
+    @property
+    def launches(self) -> int:
+        return self.backend.launches
+
+
+def params_for(slot_count: int, max_level: int) -> CKKSParams:
+    """Smallest repo preset-style chain with ``slot_count`` slots and ``max_level`` levels."""
+    from .params import make_params
+
+    log_n = int(math.log2(slot_count)) + 1
+    if (1 << (log_n - 1)) != slot_count:
+        raise ValueError(f"slot_count must be a power of two, got {slot_count}")
+    log_n = max(log_n, 10)
+    levels = max_level
+    alpha = 8 if levels >= 24 else 4
+    dnum = -(-(levels + 1) // alpha)
+    digit_bits = 60 + 40 * (alpha - 1)
+    special = -(-(digit_bits + 60) // 60)
+    return make_params(
+        f"auto{log_n}x{levels}", log_n, levels, special=special, dnum=dnum,
+        hamming_weight=min(192, (1 << log_n) // 8),
+    )

@@ -1,0 +1,186 @@
+"""Bit-exact parity of every CUDA primitive against the CPU oracle
+(oracle/ckks_oracle.c) on seeded uniform limbs, through the C-ABI."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2412_15126_b200.params import preset
+
+pytestmark = pytest.mark.gpu
+
+PARAMS = ["toy", "cfg1", "toy_deep", "cfg2"]
+
+
+@pytest.fixture(scope="module", params=PARAMS)
+def pair(request, require_cuda):
+    import torch
+
+    from oracle.oracle import OracleCKKS
+    from paper_2412_15126_b200.backend_cuda import CudaBackend
+
+    p = preset(request.param)
+    return p, CudaBackend(p), OracleCKKS(p)
+
+
+def rand_limbs(p, shape_prefix, level, seed, extended=False):
+    rng = np.random.default_rng(seed)
+    primes = list(p.q_primes[: level + 1]) + (list(p.p_primes) if extended else [])
+    out = np.empty(shape_prefix + (len(primes), p.ring_degree), dtype=np.uint64)
+    for i, q in enumerate(primes):
+        out[..., i, :] = rng.integers(0, q, size=shape_prefix + (p.ring_degree,), dtype=np.uint64)
+    return out
+
+
+def dev(gb, arr):
+    return gb.from_host(arr)
+
+
+def host(gb, t):
+    return gb.to_host(t)
+
+
+def call(gb, name, *args):
+    from paper_2412_15126_b200 import _lib
+
+    _lib.check(getattr(gb.lib, name)(gb.ctx, *args))
+
+
+def ptr(t):
+    return t.data_ptr()
+
+
+def levels_for(p):
+    return sorted({p.max_level, max(1, p.max_level // 2), 1})
+
+
+def test_ntt_roundtrip_bit_exact(pair):
+    p, gb, orc = pair
+    L = p.max_level
+    a = rand_limbs(p, (2,), L, 1)
+    t = dev(gb, a)
+    call(gb, "srk_ntt", ptr(t), 2, (L + 1) * p.ring_degree, L + 1, 0, 0, gb.stream())
+    want = np.stack([orc.ntt(a[k], range(L + 1)) for k in range(2)])
+    assert np.array_equal(host(gb, t), want)
+    call(gb, "srk_ntt", ptr(t), 2, (L + 1) * p.ring_degree, L + 1, 0, 1, gb.stream())
+    assert np.array_equal(host(gb, t), a)
+
+
+def test_ntt_special_primes(pair):
+    p, gb, orc = pair
+    K = len(p.p_primes)
+    first = len(p.q_primes)
+    rng = np.random.default_rng(2)
+    a = np.stack([rng.integers(0, q, p.ring_degree, dtype=np.uint64) for q in p.p_primes])
+    t = dev(gb, a)
+    call(gb, "srk_ntt", ptr(t), 1, 0, K, first, 0, gb.stream())
+    assert np.array_equal(host(gb, t), orc.ntt(a, range(first, first + K)))
+
+
+@pytest.mark.parametrize("op", [0, 1, 2])
+def test_addsub(pair, op):
+    p, gb, orc = pair
+    lvl = p.max_level // 2
+    a, b = rand_limbs(p, (2,), lvl, 3), rand_limbs(p, (2,), lvl, 4)
+    out = gb.addsub(dev(gb, a), dev(gb, b), lvl, op)
+    want = np.empty_like(a)
+    orc.L.orc_addsub(orc.ctx, a.ctypes.data, b.ctypes.data, want.ctypes.data, lvl, op)
+    assert np.array_equal(host(gb, out), want)
+
+
+def test_tensor(pair):
+    p, gb, orc = pair
+    for lvl in levels_for(p):
+        a, b = rand_limbs(p, (2,), lvl, 5), rand_limbs(p, (2,), lvl, 6)
+        d = gb.empty_ct(lvl, polys=3)
+        call(gb, "srk_tensor", ptr(dev(gb, a)), ptr(dev(gb, b)), ptr(d), lvl, gb.stream())
+        assert np.array_equal(host(gb, d), orc.tensor(a, b, lvl))
+
+
+def test_rescale(pair):
+    p, gb, orc = pair
+    for lvl in levels_for(p):
+        a = rand_limbs(p, (2,), lvl, 7 + lvl)
+        out = gb.empty_ct(lvl - 1)
+        call(gb, "srk_rescale", ptr(dev(gb, a)), ptr(out), lvl, gb.workspace(), gb.stream())
+        assert np.array_equal(host(gb, out), orc.rescale(a, lvl)), lvl
+
+
+def test_mul_const_and_plain_rescale(pair):
+    p, gb, orc = pair
+    lvl = p.max_level
+    a = rand_limbs(p, (2,), lvl, 11)
+    pt = rand_limbs(p, (), lvl, 12)
+    k = [int(x) for x in np.random.default_rng(13).integers(0, 2**40, lvl + 1)]
+    out = gb.mul_plain_rescale(dev(gb, a), dev(gb, pt), lvl)
+    tmp = np.empty_like(a)
+    orc.L.orc_mul_plain(orc.ctx, a.ctypes.data, pt.ctypes.data, tmp.ctypes.data, lvl)
+    assert np.array_equal(host(gb, out), orc.rescale(tmp, lvl))
+    # constant multiply of a modulus-dropped view (alignment path)
+    tgt = lvl - 2
+    out = gb.mul_const_rescale(dev(gb, a), lvl, k[: tgt + 1], tgt)
+    kk = np.array([x % q for x, q in zip(k, p.q_primes)], dtype=np.uint64)
+    tmp = np.empty((2, tgt + 1, p.ring_degree), dtype=np.uint64)
+    orc.L.orc_mul_const(orc.ctx, a.ctypes.data, lvl + 1, kk.ctypes.data, tmp.ctypes.data, tgt)
+    assert np.array_equal(host(gb, out), orc.rescale(tmp, tgt))
+
+
+def test_automorph(pair):
+    p, gb, orc = pair
+    lvl = p.max_level // 2
+    a = rand_limbs(p, (2,), lvl, 14)
+    for g in (5, pow(5, 7, 2 * p.ring_degree), 2 * p.ring_degree - 1):
+        out = gb.empty_ct(lvl)
+        call(gb, "srk_automorph", ptr(dev(gb, a)), ptr(out), 2 * (lvl + 1), g, gb.stream())
+        assert np.array_equal(host(gb, out), orc.automorph(a, g))
+
+
+def test_keyswitch_and_relin(pair):
+    p, gb, orc = pair
+    n_all = len(p.all_primes)
+    rng = np.random.default_rng(15)
+    key = np.empty((p.dnum, 2, n_all, p.ring_degree), dtype=np.uint64)
+    for i, q in enumerate(p.all_primes):
+        key[:, :, i, :] = rng.integers(0, q, (p.dnum, 2, p.ring_degree), dtype=np.uint64)
+    kd = dev(gb, key)
+    lvls = levels_for(p) if p.log_n < 16 else [p.max_level]
+    for lvl in lvls:
+        d = rand_limbs(p, (), lvl, 16 + lvl)
+        out = gb.empty_ct(lvl)
+        ps = (lvl + 1) * p.ring_degree
+        call(gb, "srk_keyswitch", ptr(dev(gb, d)), ptr(kd), ptr(out), ptr(out) + 8 * ps, lvl,
+             gb.workspace(), gb.stream())
+        assert np.array_equal(host(gb, out), orc.keyswitch(d, key, lvl)), lvl
+    lvl = lvls[-1]
+    a, b = rand_limbs(p, (2,), lvl, 17), rand_limbs(p, (2,), lvl, 18)
+    out = gb.empty_ct(lvl)
+    call(gb, "srk_mul_relin", ptr(dev(gb, a)), ptr(dev(gb, b)), ptr(kd), ptr(out), lvl,
+         gb.workspace(), gb.stream())
+    assert np.array_equal(host(gb, out), orc.mul_relin(a, b, key, lvl))
+    g = pow(5, 3, 2 * p.ring_degree)
+    out = gb.empty_ct(lvl)
+    call(gb, "srk_rotate", ptr(dev(gb, a)), ptr(kd), ptr(out), lvl, g, gb.workspace(), gb.stream())
+    assert np.array_equal(host(gb, out), orc.rotate_raw(a, key, g, lvl))
+
+
+def test_sampling_and_keygen(pair):
+    import torch
+
+    from paper_2412_15126_b200.keys import sample_error, sample_secret
+
+    p, gb, orc = pair
+    n_all = len(p.all_primes)
+    u = torch.empty((n_all, p.ring_degree), dtype=torch.int64, device=gb.device)
+    call(gb, "srk_uniform", ptr(u), n_all, 0, 1234, 77 << 8, gb.stream())
+    assert np.array_equal(host(gb, u), orc.uniform(n_all, range(n_all), 1234, 77 << 8))
+    s = sample_secret(p)
+    gb.set_secret(s)
+    sk = orc.small_to_ntt(s, range(n_all))
+    assert np.array_equal(host(gb, gb._sk_ntt), sk)
+    e = sample_error(p, (2, 9), p.dnum)
+    sg = orc.automorph(sk, 5)
+    key = torch.empty((p.dnum, 2, n_all, p.ring_degree), dtype=torch.int64, device=gb.device)
+    call(gb, "srk_keygen", ptr(gb._sk_ntt), ptr(dev(gb, sg)), ptr(torch.from_numpy(e).to(gb.device)),
+         p.seed, 9, ptr(key), gb.workspace(), gb.stream())
+    assert np.array_equal(host(gb, key), orc.keygen(sk, sg, e, p.seed, 9))
