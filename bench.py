@@ -1,0 +1,480 @@
+"""Benchmark: RNS-CKKS primitive throughput (config 2) + ranking/sort latencies.
+
+Default (``python bench.py``): N=1 GPU, the BASELINE config-2 primitive set
+as one "step" over 64 ciphertexts (ring 2^16, 30 Q-limbs, 3 special primes,
+dnum 3): forward NTT + inverse NTT + HMult/relinearise + rotation by every
+power of two 1..2^14 + rescale.  ``value`` = algorithmic GB moved per step
+ / step time, whole job, inputs resident in HBM; ``e2e`` = the
+same step through the C-ABI with the 64 input ciphertexts copied from pinned
+host memory and the 64 rescaled outputs copied back inside the timed region.
+Inputs (1.9 GiB per operand set) exceed the 126 MB L2, so no flush is needed.
+
+The pipeline latencies BASELINE.json quotes (rank N=128, argmin/argmax/median
+masks N=128, sort N=1024) are measured after the primitive step and reported
+under ``pipelines``.  ``--impl reference`` times the CPU RNS-CKKS oracle
+(oracle/ckks_oracle.c, all host threads) on a bounded sample of the same step.
+Multi-GPU (torchrun): every rank runs its own 64 ciphertexts (weak scaling, no
+data-path collective); the max time over ranks is reported.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+GB = 1e9
+N_CT = 64
+ROT_STEPS = [1 << k for k in range(15)]
+
+
+def algorithmic_bytes(p, n_ct=N_CT):
+    """Compulsory HBM bytes per step (SURVEY.md section 8d formulas)."""
+    n = p.ring_degree
+    limb = n * 8
+    nl = len(p.q_primes)
+    ne = nl + len(p.p_primes)
+    evk = 2 * p.dnum * ne * limb
+    ct = 2 * nl * limb
+    parts = {
+        "ntt_fwd": n_ct * 2 * nl * limb * 2,
+        "ntt_inv": n_ct * 2 * nl * limb * 2,
+        "hmult_relin": n_ct * 3 * ct + evk,           # 2 ct in, 1 out, + evk once
+        "rotate_15": len(ROT_STEPS) * (n_ct * 2 * ct + evk),
+        "rescale": n_ct * (ct + 2 * (nl - 1) * limb),
+    }
+    keyswitch_core = n_ct * 3 * nl * limb + evk        # read 1 poly, write 2, + evk
+    return parts, keyswitch_core
+
+
+# ----------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------
+def _rand_cts(torch, p, n_ct, seed, device):
+    """Uniform limbs per prime (BASELINE cfg 2: limbs uniform mod each prime)."""
+    nl = len(p.q_primes)
+    out = torch.empty((n_ct, 2, nl, p.ring_degree), dtype=torch.int64, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    for i, q in enumerate(p.q_primes):
+        # q < 2^62: draw in [0, q) via two 31-bit halves is biased; use int64 randint on [0, q)
+        out[:, :, i, :] = torch.randint(0, q, (n_ct, 2, p.ring_degree), generator=g, device=device,
+                                        dtype=torch.int64)
+    return out
+
+
+class PrimitiveStep:
+    """The config-2 step on one GPU, through the C-ABI of libslotrank_b200."""
+
+    def __init__(self, torch, device, n_ct=N_CT):
+        from paper_2412_15126_b200.backend_cuda import CudaBackend
+        from paper_2412_15126_b200.keys import sample_secret
+        from paper_2412_15126_b200.params import preset
+
+        self.torch = torch
+        self.p = p = preset("cfg2")
+        self.n_ct = n_ct
+        self.be = be = CudaBackend(p, device)
+        be.set_secret(sample_secret(p))
+        self.rlk = be.relin_key()
+        self.gal = [pow(5, k, 2 * p.ring_degree) for k in ROT_STEPS]
+        self.gkeys = [be.galois_key(g) for g in self.gal]
+        self.nl = len(p.q_primes)
+        self.x = _rand_cts(torch, p, n_ct, 1, be.device)
+        self.y = _rand_cts(torch, p, n_ct, 2, be.device)
+        shape = (n_ct, 2, self.nl, p.ring_degree)
+        self.prod = torch.empty(shape, dtype=torch.int64, device=be.device)
+        self.rot = torch.empty(shape, dtype=torch.int64, device=be.device)
+        self.res = torch.empty((n_ct, 2, self.nl - 1, p.ring_degree), dtype=torch.int64, device=be.device)
+        self.ws = be.workspace()
+        self.lib = be.lib
+        self.ctx = be.ctx
+        self.launch_count = 0
+
+    def _c(self, name, *args):
+        from paper_2412_15126_b200 import _lib
+
+        self.launch_count += 1
+        _lib.check(getattr(self.lib, name)(self.ctx, *args))
+
+    def ntt(self, t, inverse):
+        n, L = self.p.ring_degree, self.nl
+        s = self.be.stream()
+        self._c("srk_ntt", t.data_ptr(), self.n_ct * 2, L * n, L, 0, int(inverse), s)
+
+    def keyswitch_batch(self):
+        """Key-switch core on the c1 polys (for the keyswitch roofline)."""
+        s = self.be.stream()
+        ps = self.nl * self.p.ring_degree
+        for i in range(self.n_ct):
+            self._c("srk_keyswitch", self.x[i, 1].data_ptr(), self.rlk.data_ptr(),
+                    self.rot[i, 0].data_ptr(), self.rot[i, 1].data_ptr(), self.nl - 1, self.ws, s)
+
+    def step(self, x=None):
+        x = self.x if x is None else x
+        s = self.be.stream()
+        L = self.nl - 1
+        self.ntt(x, False)
+        self.ntt(x, True)
+        for i in range(self.n_ct):
+            self._c("srk_mul_relin", x[i].data_ptr(), self.y[i].data_ptr(), self.rlk.data_ptr(),
+                    self.prod[i].data_ptr(), L, self.ws, s)
+        for g, key in zip(self.gal, self.gkeys):
+            for i in range(self.n_ct):
+                self._c("srk_rotate", x[i].data_ptr(), key.data_ptr(), self.rot[i].data_ptr(), L, g,
+                        self.ws, s)
+        for i in range(self.n_ct):
+            self._c("srk_rescale", self.prod[i].data_ptr(), self.res[i].data_ptr(), L, self.ws, s)
+
+
+def time_region(torch, fn, reps, barrier=None):
+    """CUDA-event time of ``reps`` calls of fn (ms per call), synchronized both sides."""
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def run_pipelines(torch, quick=False):
+    """BASELINE pipeline latencies (seconds) on cuda:current, decrypted results checked."""
+    from oracle.plain import fractional_ranks  # result-level checker only
+    from paper_2412_15126_b200 import (B200Engine, KernelConfig, SortConfig, StatisticQuery,
+                                       block_merge, block_split, multi_sort, order_statistic_mask,
+                                       rank, read_row)
+    from paper_2412_15126_b200.params import preset
+
+    out = {}
+
+    def timed(fn, reps=1):
+        best = None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = fn()
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        return best, r
+
+    # config 3: rank N=128, composite g3^4 o f3^2, ring 2^16, 29 levels
+    rng = np.random.default_rng(0)
+    v128 = rng.choice(1024, 128, replace=False) / 1024
+    eng = B200Engine(preset("cfg3"))
+    cfg = KernelConfig(mode="composite", composite=(4, 2))
+    ct = eng.encrypt(v128)
+    rank(eng, ct, 128, cfg)  # warm-up: Galois / relin key generation, plaintext cache
+    eng.cost_reset()
+    dt, res = timed(lambda: read_row(eng, rank(eng, ct, 128, cfg).ranks, 128), reps=3)
+    exact = bool(np.array_equal(np.rint(res), fractional_ranks(v128)))
+    out["rank_n128_s"] = {"latency_s": dt, "exact_ranks": exact,
+                          "max_rank_err": float(np.abs(res - fractional_ranks(v128)).max()),
+                          "cost": eng.cost_snapshot().__dict__, "params": "cfg3"}
+    del eng
+    torch.cuda.empty_cache()
+    if quick:
+        return out
+
+    # config 4: argmin / argmax / k=64 masks N=128 on the long chain
+    eng = B200Engine(preset("long"))
+    cfg4 = KernelConfig(mode="composite", composite=(4, 2), indicator_composite=(4, 2),
+                        tie_margin=2.0 ** -11)
+    ct = eng.encrypt(v128)
+    order = np.argsort(v128)
+    for name, q, want in (("argmin", StatisticQuery("min"), order[0]),
+                          ("argmax", StatisticQuery("max"), order[-1]),
+                          ("median_k64", StatisticQuery("kth", k=64), order[63])):
+        order_statistic_mask(eng, ct, 128, q, cfg4)  # warm-up keys
+        dt, m = timed(lambda: read_row(eng, order_statistic_mask(eng, ct, 128, q, cfg4), 128))
+        out[f"{name}_n128_s"] = {"latency_s": dt, "index_ok": bool(int(np.argmax(m)) == int(want)),
+                                 "max_onehot_err": float(np.abs(m - np.eye(128)[want]).max()),
+                                 "params": "long"}
+
+    # config 5: sort N=1024 (8 blocks of 128), composite comparisons
+    v1024 = np.random.default_rng(0).choice(8192, 1024, replace=False) / 8192
+    scfg = SortConfig(kernel=KernelConfig(mode="composite", composite=(6, 2),
+                                          indicator_composite=(6, 2)), tie_correction=False)
+    bv = block_split(eng, v1024)
+    eng.cost_reset()
+    dt, srt = timed(lambda: block_merge(eng, multi_sort(eng, bv, scfg)))
+    out["sort_n1024_s"] = {"latency_s": dt, "order_ok": bool(np.array_equal(np.argsort(srt), np.arange(1024))),
+                           "max_abs_err": float(np.abs(srt - np.sort(v1024)).max()),
+                           "cost": eng.cost_snapshot().__dict__, "params": "long", "gpus": 1}
+    return out
+
+
+def gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank_id = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    barrier = (lambda: dist.barrier()) if world > 1 else None
+
+    step = PrimitiveStep(torch, local)
+    p = step.p
+    parts, ks_bytes = algorithmic_bytes(p)
+    step_bytes = sum(parts.values())
+
+    for _ in range(args.warmup):
+        step.step()
+    torch.cuda.synchronize()
+    step.launch_count = 0
+    k0 = step.lib.srk_kernel_launches()
+    with ClockSampler(local) as clk:
+        ms = time_region(torch, step.step, args.steps, barrier)
+    launches = step.launch_count // args.steps
+    kernels = (step.lib.srk_kernel_launches() - k0) // args.steps
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # per-kernel-family timing for the roofline (same stream, CUDA events)
+    ntt_ms = time_region(torch, lambda: step.ntt(step.x, False), 5)
+    intt_ms = time_region(torch, lambda: step.ntt(step.x, True), 5)
+    ks_ms = time_region(torch, step.keyswitch_batch, 2)
+
+    # e2e: host pinned inputs -> device, step, results -> host
+    host_x = torch.empty(step.x.shape, dtype=torch.int64, pin_memory=True)
+    host_x.copy_(step.x)
+    host_out = torch.empty(step.res.shape, dtype=torch.int64, pin_memory=True)
+    dev_x = torch.empty_like(step.x)
+
+    def e2e_step():
+        dev_x.copy_(host_x, non_blocking=True)
+        step.step(dev_x)
+        host_out.copy_(step.res, non_blocking=True)
+
+    e2e_step()
+    e2e_ms = time_region(torch, e2e_step, max(1, min(args.steps, 3)), barrier)
+    te = torch.tensor([e2e_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+
+    pipelines = None
+    if rank_id == 0 and not args.no_pipelines:
+        del step
+        torch.cuda.empty_cache()
+        pipelines = run_pipelines(torch, quick=args.quick)
+
+    if rank_id == 0:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        ntt_gbs = parts["ntt_fwd"] / (ntt_ms * 1e-3) / GB
+        ks_gbs = ks_bytes / (ks_ms * 1e-3) / GB
+        value = world * step_bytes / (ms * 1e-3) / GB
+        line = {
+            "metric": "NTT+KeySwitch GB/s vs HBM roof (cfg2 primitive step, 64 ct, ring 2^16, 30+3 limbs)",
+            "value": round(value, 2),
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms, 3),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "u64 (RNS limbs mod 40/60-bit primes)",
+            "data": "synthetic: uniform limbs mod each prime, seeded (BASELINE cfg 2)",
+            "config": {"workload": "cfg2 primitive step: fwd NTT + INTT + 64 HMult/relin + 64x15 "
+                                   "power-of-two rotations + 64 rescale",
+                       "ciphertexts_per_gpu": N_CT, "ring": p.ring_degree, "q_limbs": len(p.q_primes),
+                       "p_limbs": len(p.p_primes), "dnum": p.dnum,
+                       "algorithmic_gb_per_step": round(step_bytes / GB, 3),
+                       "l2": "inputs 1.9 GiB per operand set >> 126 MB L2 (no flush needed)"},
+            "gpu_launches": int(kernels),
+            "api_calls_per_step": launches,
+            "roofline": {"bound": "hbm", "kernel": "forward NTT (ntt_pass_kernel x2 per chunk)",
+                         "achieved": round(ntt_gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ntt_gbs / peak, 4), "traffic": None,
+                         "algorithmic_bytes": parts["ntt_fwd"], "ms": round(ntt_ms, 4),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+            "roofline_keyswitch": {"bound": "hbm", "achieved": round(ks_gbs, 1), "peak": peak,
+                                   "unit": "GB/s", "frac": round(ks_gbs / peak, 4),
+                                   "algorithmic_bytes": ks_bytes, "ms": round(ks_ms, 4)},
+            "roofline_inverse_ntt": {"achieved": round(parts["ntt_inv"] / (intt_ms * 1e-3) / GB, 1),
+                                     "ms": round(intt_ms, 4)},
+            "e2e": {"value": round(world * step_bytes / (e2e_ms * 1e-3) / GB, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(host_x.numel() * 8),
+                    "d2h_bytes_per_step": int(host_out.numel() * 8), "ms_per_step": round(e2e_ms, 3)},
+            "clocks": clk.summary(),
+            "pipelines": pipelines,
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args, threads=1 if args.quick else None)
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------
+# CPU arms (oracle)
+# ----------------------------------------------------------------------
+def cpu_sample(threads=None, n_ct=1, rotations=2):
+    """Time the oracle on a bounded sample of the step; return GB/s of the same metric."""
+    if threads:
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+    from oracle.oracle import OracleCKKS
+    from paper_2412_15126_b200.params import preset
+
+    p = preset("cfg2")
+    o = OracleCKKS(p)
+    nl = len(p.q_primes)
+    n_all = len(p.all_primes)
+    rng = np.random.default_rng(1)
+
+    def rnd(shape_prefix):
+        a = np.empty(shape_prefix + (nl, p.ring_degree), dtype=np.uint64)
+        for i, q in enumerate(p.q_primes):
+            a[..., i, :] = rng.integers(0, q, shape_prefix + (p.ring_degree,), dtype=np.uint64)
+        return a
+
+    x, y = rnd((2,)), rnd((2,))
+    key = np.empty((p.dnum, 2, n_all, p.ring_degree), dtype=np.uint64)
+    for i, q in enumerate(p.all_primes):
+        key[:, :, i, :] = rng.integers(0, q, (p.dnum, 2, p.ring_degree), dtype=np.uint64)
+    L = nl - 1
+    t0 = time.perf_counter()
+    for _ in range(n_ct):
+        f = np.stack([o.ntt(x[k], range(nl)) for k in range(2)])
+        np.stack([o.ntt(f[k], range(nl), inverse=True) for k in range(2)])
+        prod = o.mul_relin(x, y, key, L)
+        for k in range(rotations):
+            o.rotate_raw(x, key, pow(5, ROT_STEPS[k], 2 * p.ring_degree), L)
+        o.rescale(prod, L)
+    dt = time.perf_counter() - t0
+    parts, _ = algorithmic_bytes(p, n_ct=n_ct)
+    n = p.ring_degree
+    ct_b = 2 * nl * n * 8
+    evk = 2 * p.dnum * (nl + len(p.p_primes)) * n * 8
+    sample_bytes = (parts["ntt_fwd"] + parts["ntt_inv"] + parts["hmult_relin"] + parts["rescale"]
+                    + rotations * (n_ct * 2 * ct_b + evk))
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": round(sample_bytes / dt / GB, 4), "unit": "GB/s", "cores": cores,
+            "kind": "port", "seconds": round(dt, 3),
+            "sample": f"{n_ct} ct of cfg2: fwd+inv NTT, 1 HMult/relin, {rotations} of 15 rotations, "
+                      f"1 rescale (oracle/ckks_oracle.c, scalar __int128 arithmetic)"}
+
+
+def cpu_baseline(args, threads=None):
+    try:
+        return cpu_sample(threads=threads)
+    except Exception as e:  # the baseline never blocks the GPU line
+        return {"value": None, "unit": "GB/s", "cores": None, "kind": "port", "sample": f"failed: {e}"}
+
+
+def reference_arm(args):
+    rank_id = int(os.environ.get("RANK", "0"))
+    if rank_id != 0:
+        return
+    vals = []
+    res = None
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_sample()
+    for _ in range(args.steps):
+        res = cpu_sample()
+        vals.append(res["value"])
+    v = float(np.median(vals))
+    line = {
+        "metric": "NTT+KeySwitch GB/s vs HBM roof (cfg2 primitive step, 64 ct, ring 2^16, 30+3 limbs)",
+        "value": v, "unit": "GB/s", "impl": "reference",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64 (RNS limbs mod 40/60-bit primes)", "data": "synthetic (BASELINE cfg 2)",
+        "config": {"workload": "cfg2 primitive step (bounded sample per step, see cpu_baseline.sample)"},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": res["cores"], "kind": "port",
+                         "sample": res["sample"]},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference (slotrank) has no CKKS arithmetic; its CPU path for this step is the "
+                "RNS-CKKS restatement in oracle/ckks_oracle.c (OpenMP over limbs)",
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--quick", action="store_true", help="rank N=128 only among the pipelines")
+    ap.add_argument("--no-pipelines", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

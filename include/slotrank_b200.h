@@ -50,6 +50,8 @@ typedef struct srk_ctx srk_ctx;
 
 const char *srk_last_error(void);
 int srk_version(void);
+/* kernels launched by this library so far in this process (bench evidence) */
+unsigned long long srk_kernel_launches(void);
 
 /* context: primes[0..n_q) = Q chain, primes[n_q..n_q+n_p) = special primes;
  * roots[i] = primitive 2N-th root of unity mod primes[i] */

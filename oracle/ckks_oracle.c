@@ -418,10 +418,22 @@ void orc_keyswitch(const orc_ctx *c, const uint64_t *d, const uint64_t *key, uin
             }
             const uint64_t pinv = invmod(pmod, q);
             uint64_t *t = (uint64_t *)malloc(sizeof(uint64_t) * n);
+            /* exact (rounded) conversion: subtract v*P, v = round(sum_k z_k / p_k)
+             * evaluated in 64.64 fixed point with f_k = z_k*R1 + hi(z_k*R0),
+             * R = floor(2^128 / p_k) -- the same integer recipe as the GPU */
+            const uint64_t pq = pmod;
             for (int j = 0; j < n; j++) {
-                u128 s = 0;
-                for (int k = 0; k < K; k++) s += (u128)z[(size_t)k * n + j] * coef[k];
-                t[j] = (uint64_t)(s % q);
+                u128 s = 0, frac = 0;
+                for (int k = 0; k < K; k++) {
+                    const uint64_t zk = z[(size_t)k * n + j];
+                    const uint64_t pk = c->prime[c->n_q + k];
+                    const u128 R = (~(u128)0) / pk;
+                    const uint64_t r1 = (uint64_t)(R >> 64), r0 = (uint64_t)R;
+                    frac += (u128)(uint64_t)(zk * r1 + (uint64_t)(((u128)zk * r0) >> 64));
+                    s += (u128)zk * coef[k];
+                }
+                const uint64_t v = (uint64_t)((frac + ((u128)1 << 63)) >> 64);
+                t[j] = submod((uint64_t)(s % q), mulmod(v % q, pq, q), q);
             }
             ntt_limb(c, t, i);
             for (int j = 0; j < n; j++)

@@ -22,6 +22,7 @@ _u64p = c_void_p  # device or host pointers passed as integers
 EXPORTS = {
     "srk_last_error": [],
     "srk_version": [],
+    "srk_kernel_launches": [],
     "srk_ctx_create": [c_int, c_int, POINTER(c_uint64), POINTER(c_uint64), c_int, c_int, c_int,
                        POINTER(c_void_p)],
     "srk_ctx_destroy": [c_void_p],
@@ -52,7 +53,8 @@ EXPORTS = {
     "srk_decrypt_limb0": [c_void_p, _u64p, _u64p, _u64p, c_int, c_void_p, c_void_p],
     "srk_encode_plain": [c_void_p, _u64p, _u64p, c_int, c_void_p],
 }
-_RESTYPES = {"srk_last_error": ctypes.c_char_p, "srk_workspace_bytes": c_size_t}
+_RESTYPES = {"srk_last_error": ctypes.c_char_p, "srk_workspace_bytes": c_size_t,
+             "srk_kernel_launches": ctypes.c_ulonglong}
 
 
 class SrkError(RuntimeError):

@@ -1,0 +1,94 @@
+"""Composite sign polynomials (Cheon-Kim-Kim, ASIACRYPT 2020) as an engine kernel.
+
+BASELINE.json asks for sign(x) ~ f_3^(o2) o g_3^(o4) (g applied first, then f),
+mapped to 0.5 (sign + 1).  The reference only has Chebyshev interpolants
+(reference ``chebyshev.py:296-334``; SPEC.md:229 leaves composites out), so
+this module is new: it is written against the engine method surface, runs on
+any engine (B200, the CPU oracle, the slot simulator) and costs O(1)
+comparison depth independent of the input gap's resolution target:
+
+* f_n(x) = sum_{i<=n} 4^-i C(2i, i) x (1 - x^2)^i: odd, f(+-1) = +-1,
+  f'(+-1) = ... = f^(n)(+-1) = 0 -- for n = 3,
+  f_3(x) = (35 x - 35 x^3 + 21 x^5 - 5 x^7) / 2^4;
+* g_n is the published heuristic minimax companion with a steep slope at 0
+  that maps [tau, 1] into [1 - tau, 1] (tau = 1/4) -- for n = 3,
+  g_3(x) = (4589 x - 16577 x^3 + 25614 x^5 - 12860 x^7) / 2^10.
+
+Each odd degree-7 polynomial is evaluated in multiplicative depth 3 with
+5 ct x ct and 4 ct x pt multiplications:
+
+    y = x^2, z = y^2
+    p(x) = a1 x + (a3 x) y + [a5 x + (a7 x) y] z
+
+where the scalar products are issued directly at the level their sum needs
+(``mul_plain(..., level=...)`` on engines that support it), so no separate
+level-alignment step is paid.  A sign evaluation with (g, f) iterations uses
+3 (g + f) levels.
+"""
+
+from __future__ import annotations
+
+from fractions import Fraction
+
+__all__ = ["F3", "G3", "odd_poly_eval", "composite_sign", "composite_step", "composite_depth",
+           "sign_value"]
+
+F3 = tuple(Fraction(c, 16) for c in (35, -35, 21, -5))
+G3 = tuple(Fraction(c, 1024) for c in (4589, -16577, 25614, -12860))
+
+
+def _mul_plain_at(engine, x, c: float, level: int, site: str):
+    if getattr(engine, "supports_mul_plain_level", False):
+        return engine.mul_plain(x, c, site=site, level=level)
+    return engine.mul_plain(x, c, site=site)
+
+
+def odd_poly_eval(engine, x, coeffs, site: str = "composite"):
+    """a1 x + a3 x^3 + a5 x^5 + a7 x^7 on ``x`` in depth 3 (coeffs = (a1, a3, a5, a7))."""
+    a1, a3, a5, a7 = (float(c) for c in coeffs)
+    lvl = x.level
+    y = engine.mul(x, x, site=f"{site}-sq")
+    z = engine.mul(y, y, site=f"{site}-quad")
+    t3 = engine.mul(engine.mul_plain(x, a3, site=f"{site}-c3"), y, site=f"{site}-x3")
+    t7 = engine.mul(engine.mul_plain(x, a7, site=f"{site}-c7"), y, site=f"{site}-x3")
+    w = _mul_plain_at(engine, x, a5, lvl - 2, f"{site}-c5")
+    t57 = engine.mul(engine.add(w, t7), z, site=f"{site}-x5")
+    t1 = _mul_plain_at(engine, x, a1, lvl - 3, f"{site}-c1")
+    return engine.add(engine.add(t1, t3), t57)
+
+
+def composite_sign(engine, x, g_iters: int, f_iters: int, out_scale: float = 1.0,
+                   site: str = "sign"):
+    """sign(x) for x in [-1, 1] as f^(f_iters) o g^(g_iters), times ``out_scale``.
+
+    ``out_scale`` is folded into the last polynomial's coefficients.
+    """
+    chain = [G3] * g_iters + [F3] * f_iters
+    if not chain:
+        raise ValueError("composite sign needs at least one polynomial")
+    for idx, poly in enumerate(chain):
+        coeffs = poly if idx < len(chain) - 1 else tuple(c * Fraction(out_scale) for c in poly)
+        x = odd_poly_eval(engine, x, coeffs, site=f"{site}-{idx}")
+    return x
+
+
+def composite_step(engine, x, g_iters: int, f_iters: int, site: str = "step"):
+    """0.5 (1 + sign(x)): 1 for x > 0, 0.5 at 0, 0 for x < 0."""
+    s = composite_sign(engine, x, g_iters, f_iters, out_scale=0.5, site=site)
+    return engine.add_plain(s, 0.5)
+
+
+def composite_depth(g_iters: int, f_iters: int) -> int:
+    return 3 * (g_iters + f_iters)
+
+
+def sign_value(t, g_iters: int, f_iters: int):
+    """Plaintext evaluation of the same composite (numpy), for tests and fits."""
+    import numpy as np
+
+    v = np.asarray(t, dtype=np.float64)
+    for poly in [G3] * g_iters + [F3] * f_iters:
+        a1, a3, a5, a7 = (float(c) for c in poly)
+        y = v * v
+        v = v * (a1 + y * (a3 + y * (a5 + y * a7)))
+    return v

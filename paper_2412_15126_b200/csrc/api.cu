@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -41,8 +42,11 @@ static int fail(int code, const char *fmt, ...) {
                         cudaGetErrorString(e_));                                      \
     } while (0)
 
+static std::atomic<unsigned long long> g_launches{0};
+
 #define LAUNCHED()                                                                    \
     do {                                                                              \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                           \
         cudaError_t e_ = cudaGetLastError();                                          \
         if (e_ != cudaSuccess)                                                        \
             return fail(SRK_ECUDA, "%s:%d launch: %s", __FILE__, __LINE__,            \
@@ -57,6 +61,8 @@ static int fail(int code, const char *fmt, ...) {
 
 extern "C" const char *srk_last_error(void) { return g_err.c_str(); }
 extern "C" int srk_version(void) { return 1; }
+// number of kernels this library has launched in this process
+extern "C" unsigned long long srk_kernel_launches(void) { return g_launches.load(); }
 
 // ---------------------------------------------------------------------
 // host modular helpers
@@ -91,6 +97,7 @@ struct BconvPlan {
     uint64_t *hinv = nullptr;  // [2][n_src]
     int *dst_slot = nullptr;
     int *dst_pid = nullptr;
+    uint64_t *dst_corr = nullptr;  // ModDown: [P]_{q_t} for exact rounding
     int n_src = 0, n_dst = 0, src_pid0 = 0;
 };
 
@@ -130,7 +137,8 @@ static inline int ext_pid(const srk_ctx *c, int level, int t) {
 }
 
 static int build_plan(srk_ctx *c, BconvPlan &pl, const std::vector<int> &src_pids,
-                      const std::vector<int> &dst_slots, const std::vector<int> &dst_pids) {
+                      const std::vector<int> &dst_slots, const std::vector<int> &dst_pids,
+                      bool exact = false) {
     const int ns = (int)src_pids.size(), nd = (int)dst_pids.size();
     std::vector<uint64_t> mat((size_t)ns * nd), hv(2 * ns);
     for (int i = 0; i < ns; i++) {
@@ -155,6 +163,16 @@ static int build_plan(srk_ctx *c, BconvPlan &pl, const std::vector<int> &src_pid
     TRY(dupload(c, &pl.hinv, hv));
     TRY(dupload(c, &pl.dst_slot, dst_slots));
     TRY(dupload(c, &pl.dst_pid, dst_pids));
+    if (exact) {
+        std::vector<uint64_t> corr(nd);
+        for (int t = 0; t < nd; t++) {
+            const uint64_t p = c->primes[dst_pids[t]];
+            uint64_t v = 1;
+            for (int m = 0; m < ns; m++) v = hmul(v, c->primes[src_pids[m]] % p, p);
+            corr[t] = v;
+        }
+        TRY(dupload(c, &pl.dst_corr, corr));
+    }
     return SRK_OK;
 }
 
@@ -267,7 +285,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
             slot.push_back(i);
             pid.push_back(i);
         }
-        if ((rc = build_plan(c, c->moddown[l], src, slot, pid))) { srk_ctx_destroy(c); return rc; }
+        if ((rc = build_plan(c, c->moddown[l], src, slot, pid, true))) { srk_ctx_destroy(c); return rc; }
     }
     // P^-1 mod q_i, P mod prime_i, q_l^-1 mod q_i
     std::vector<uint64_t> pinv(n_q), pmod(np);
@@ -578,6 +596,7 @@ static int bconv(const srk_ctx *c, const BconvPlan &pl, const uint64_t *src, lon
     ba.hinv = pl.hinv;
     ba.dst_slot = pl.dst_slot;
     ba.dst_pid = pl.dst_pid;
+    ba.dst_corr = pl.dst_corr;
     dim3 grid((c->n + 255) / 256, n_polys);
     if (pl.n_src <= 4)
         k_bconv<4><<<grid, 256, 0, s>>>(ba, c->d_pc, c->log_n);
@@ -633,11 +652,6 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, const uint64_t *key, ui
                                                              c->d_pc, c->log_n, nl);
     LAUNCHED();
     return SRK_OK;
-}
-
-static size_t ks_words(const srk_ctx *c, int level) {
-    const size_t nl = level + 1, ne = nl + c->n_p, beta = (nl + c->alpha - 1) / c->alpha;
-    return (nl + beta * ne + 2 * ne + 2 * nl) * (size_t)c->n;
 }
 
 extern "C" int srk_keyswitch(srk_ctx *c, const uint64_t *d, const uint64_t *key, uint64_t *out0,

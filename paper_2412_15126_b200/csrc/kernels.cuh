@@ -229,6 +229,7 @@ struct BconvArgs {
     const uint64_t *hinv;   // device [n_src] (+ [n_src] Shoup)
     const int *dst_slot;    // device [n_dst]: output limb index for target t
     const int *dst_pid;     // device [n_dst]: prime id of target t
+    const uint64_t *dst_corr;  // optional [n_dst]: [prod src primes]_{dst}; rounds exactly
 };
 
 template <int MAXS>
@@ -251,12 +252,32 @@ __global__ void k_bconv(BconvArgs ba, const PrimeConst *__restrict__ pc, int log
                 y[i] = mul_shoup(src[(long long)i * n + x], ba.hinv[i], ba.hinv[ba.n_src + i], q);
             }
         }
+        // exact conversion: v = round(sum_i y_i / q_i) in 64.64 fixed point
+        // (f_i = y_i R1 + hi(y_i R0), R = floor(2^128/q_i)); output - v * Q
+        uint64_t v = 0;
+        if (ba.dst_corr) {
+            U128 frac = {0, 0};
+#pragma unroll
+            for (int i = 0; i < MAXS; i++) {
+                if (i < ba.n_src) {
+                    const PrimeConst P = pc[ba.src_pid0 + i];
+                    U128 f = {0, y[i] * P.ratio_hi + mulhi64(y[i], P.ratio_lo)};
+                    add_to(frac, f);
+                }
+            }
+            U128 half = {0, 1ull << 63};
+            add_to(frac, half);
+            v = frac.hi;
+        }
         for (int t = 0; t < ba.n_dst; t++) {
             U128 acc = {0, 0};
 #pragma unroll
             for (int i = 0; i < MAXS; i++)
                 if (i < ba.n_src) mac(acc, y[i], s_mat[i * ba.n_dst + t]);
-            out[(long long)ba.dst_slot[t] * n + x] = reduce_u128(acc, pc[ba.dst_pid[t]]);
+            const PrimeConst P = pc[ba.dst_pid[t]];
+            uint64_t r = reduce_u128(acc, P);
+            if (ba.dst_corr) r = sub_mod(r, mul_mod(v, ba.dst_corr[t], P), P.q);
+            out[(long long)ba.dst_slot[t] * n + x] = r;
         }
     }
 }

@@ -13,7 +13,11 @@
 #pragma once
 #include <cstdint>
 
+#ifdef __CUDACC__
 #define SRK_HD __host__ __device__ __forceinline__
+#else
+#define SRK_HD static inline
+#endif
 
 struct PrimeConst {
     uint64_t q;       // modulus

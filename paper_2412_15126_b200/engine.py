@@ -329,14 +329,31 @@ class CKKSEngineCore:
             self._ctct += 1
         return self._emit(data, level - 1, max(x.rot_chain, y.rot_chain))
 
-    def mul_plain(self, x: Ciphertext, p, site: str = "mul_plain") -> Ciphertext:
+    supports_mul_plain_level = True
+
+    def mul_plain(self, x: Ciphertext, p, site: str = "mul_plain", level: int | None = None) -> Ciphertext:
+        """x * p, one level down -- or, for a scalar p and ``level`` < x.level - 1,
+        straight to ``level`` in the same single rescale (the simulator's
+        mul_plain followed by the min-level rule of a later add)."""
         self._check(x)
         if x.level < 1:
             raise DepthBudgetError(site, x.level)
-        level = x.level
         pr = self.params
-        pt_scale = pr.scales[level - 1] * pr.q_primes[level] / pr.scales[level]
         c = self._as_constant(p)
+        if level is not None and level < x.level - 1:
+            if c is None:
+                raise ValueError("mul_plain(level=...) takes a scalar plaintext")
+            if level < 0:
+                raise DepthBudgetError(site, x.level, x.level - level)
+            # drop to level+1 limbs, multiply by round(c * scales[level] q_{level+1} / scales[x]),
+            # rescale by q_{level+1}  -> scale scales[level]
+            k = int(round(c * pr.scales[level] * pr.q_primes[level + 1] / pr.scales[x.level]))
+            data = self.backend.mul_const_rescale(x.data, x.level, self._residues(k, level + 1), level + 1)
+            with self._lock:
+                self._ctpt += 1
+            return self._emit(data, level, x.rot_chain)
+        level = x.level
+        pt_scale = pr.scales[level - 1] * pr.q_primes[level] / pr.scales[level]
         if c is not None:
             if isinstance(p, np.ndarray) and p.size != pr.slot_count:
                 self.plain(p)

@@ -94,7 +94,8 @@ def test_tensor(pair):
     for lvl in levels_for(p):
         a, b = rand_limbs(p, (2,), lvl, 5), rand_limbs(p, (2,), lvl, 6)
         d = gb.empty_ct(lvl, polys=3)
-        call(gb, "srk_tensor", ptr(dev(gb, a)), ptr(dev(gb, b)), ptr(d), lvl, gb.stream())
+        ta, tb = dev(gb, a), dev(gb, b)
+        call(gb, "srk_tensor", ptr(ta), ptr(tb), ptr(d), lvl, gb.stream())
         assert np.array_equal(host(gb, d), orc.tensor(a, b, lvl))
 
 
@@ -103,7 +104,8 @@ def test_rescale(pair):
     for lvl in levels_for(p):
         a = rand_limbs(p, (2,), lvl, 7 + lvl)
         out = gb.empty_ct(lvl - 1)
-        call(gb, "srk_rescale", ptr(dev(gb, a)), ptr(out), lvl, gb.workspace(), gb.stream())
+        ta = dev(gb, a)
+        call(gb, "srk_rescale", ptr(ta), ptr(out), lvl, gb.workspace(), gb.stream())
         assert np.array_equal(host(gb, out), orc.rescale(a, lvl)), lvl
 
 
@@ -130,9 +132,10 @@ def test_automorph(pair):
     p, gb, orc = pair
     lvl = p.max_level // 2
     a = rand_limbs(p, (2,), lvl, 14)
+    ta = dev(gb, a)
     for g in (5, pow(5, 7, 2 * p.ring_degree), 2 * p.ring_degree - 1):
         out = gb.empty_ct(lvl)
-        call(gb, "srk_automorph", ptr(dev(gb, a)), ptr(out), 2 * (lvl + 1), g, gb.stream())
+        call(gb, "srk_automorph", ptr(ta), ptr(out), 2 * (lvl + 1), g, gb.stream())
         assert np.array_equal(host(gb, out), orc.automorph(a, g))
 
 
@@ -149,18 +152,20 @@ def test_keyswitch_and_relin(pair):
         d = rand_limbs(p, (), lvl, 16 + lvl)
         out = gb.empty_ct(lvl)
         ps = (lvl + 1) * p.ring_degree
-        call(gb, "srk_keyswitch", ptr(dev(gb, d)), ptr(kd), ptr(out), ptr(out) + 8 * ps, lvl,
+        td = dev(gb, d)
+        call(gb, "srk_keyswitch", ptr(td), ptr(kd), ptr(out), ptr(out) + 8 * ps, lvl,
              gb.workspace(), gb.stream())
         assert np.array_equal(host(gb, out), orc.keyswitch(d, key, lvl)), lvl
     lvl = lvls[-1]
     a, b = rand_limbs(p, (2,), lvl, 17), rand_limbs(p, (2,), lvl, 18)
     out = gb.empty_ct(lvl)
-    call(gb, "srk_mul_relin", ptr(dev(gb, a)), ptr(dev(gb, b)), ptr(kd), ptr(out), lvl,
+    ta, tb = dev(gb, a), dev(gb, b)
+    call(gb, "srk_mul_relin", ptr(ta), ptr(tb), ptr(kd), ptr(out), lvl,
          gb.workspace(), gb.stream())
     assert np.array_equal(host(gb, out), orc.mul_relin(a, b, key, lvl))
     g = pow(5, 3, 2 * p.ring_degree)
     out = gb.empty_ct(lvl)
-    call(gb, "srk_rotate", ptr(dev(gb, a)), ptr(kd), ptr(out), lvl, g, gb.workspace(), gb.stream())
+    call(gb, "srk_rotate", ptr(ta), ptr(kd), ptr(out), lvl, g, gb.workspace(), gb.stream())
     assert np.array_equal(host(gb, out), orc.rotate_raw(a, key, g, lvl))
 
 
@@ -181,6 +186,7 @@ def test_sampling_and_keygen(pair):
     e = sample_error(p, (2, 9), p.dnum)
     sg = orc.automorph(sk, 5)
     key = torch.empty((p.dnum, 2, n_all, p.ring_degree), dtype=torch.int64, device=gb.device)
-    call(gb, "srk_keygen", ptr(gb._sk_ntt), ptr(dev(gb, sg)), ptr(torch.from_numpy(e).to(gb.device)),
+    tsg, te = dev(gb, sg), torch.from_numpy(e).to(gb.device)
+    call(gb, "srk_keygen", ptr(gb._sk_ntt), ptr(tsg), ptr(te),
          p.seed, 9, ptr(key), gb.workspace(), gb.stream())
     assert np.array_equal(host(gb, key), orc.keygen(sk, sg, e, p.seed, 9))
