@@ -1,0 +1,45 @@
+"""Composite sign polynomials: defining properties and resolution at the
+BASELINE input gaps (k/64, k/1024, k/8192 grids)."""
+
+import numpy as np
+
+from oracle.slotsim import SimParams, SlotSim
+from paper_2412_15126_b200.composite import F3, G3, composite_step, sign_value
+
+
+def poly(c, x):
+    a1, a3, a5, a7 = (float(t) for t in c)
+    return a1 * x + a3 * x ** 3 + a5 * x ** 5 + a7 * x ** 7
+
+
+def test_f3_definition():
+    assert poly(F3, 1.0) == 1.0 and poly(F3, -1.0) == -1.0
+    # f3'(1) = 0: 35 - 105 + 105 - 35
+    assert sum(float(c) * (2 * i + 1) for i, c in enumerate(F3)) == 0.0
+
+
+def test_g3_maps_quarter_to_top():
+    x = np.linspace(0.25, 1.0, 2001)
+    y = poly(G3, x)
+    assert y.min() > 0.74 and y.max() <= 1.0 + 1e-9
+    assert poly(G3, 1e-3) / 1e-3 > 4.4  # steep at 0
+
+
+def test_resolution_at_baseline_gaps():
+    assert sign_value(2.0 ** -6, 3, 2) > 0.99      # cfg1 / smoke
+    assert sign_value(2.0 ** -10, 4, 2) > 0.98     # cfg3 rank N=128
+    assert sign_value(2.0 ** -9, 4, 2) > 0.999     # indicator windows at N=128
+    assert sign_value(2.0 ** -13, 6, 2) > 0.99     # cfg5 comparisons
+    assert sign_value(2.0 ** -12, 6, 2) > 0.999    # cfg5 indicator windows
+    x = np.linspace(-1, 1, 1001)
+    assert np.abs(sign_value(x, 4, 2)).max() <= 1.0 + 1e-9
+    assert sign_value(0.0, 4, 2) == 0.0
+
+
+def test_engine_evaluation_matches_plaintext():
+    sim = SlotSim(SimParams(64, 30))
+    x = np.linspace(-1, 1, 64)
+    out = sim.decrypt(composite_step(sim, sim.encrypt(x), 4, 2))
+    assert np.abs(out - 0.5 * (1 + sign_value(x, 4, 2))).max() < 1e-12
+    assert sim.cost_snapshot().levels_consumed == 18
+    assert sim.cost_snapshot().ctct_mults == 30

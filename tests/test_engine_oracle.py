@@ -1,0 +1,112 @@
+"""The product's engine bookkeeping over the CPU oracle backend (toy rings):
+CKKS semantics against numpy, and the reference simulator's method contract
+(levels, counters, trace, errors; reference engine.py:133-328)."""
+
+import numpy as np
+import pytest
+
+import paper_2412_15126_b200 as M
+from oracle.oracle import oracle_engine
+from oracle.plain import fractional_ranks
+from oracle.slotsim import SimParams, SlotSim
+from paper_2412_15126_b200.engine import CapacityError, DepthBudgetError, EngineError, IncompatibleParamsError
+from paper_2412_15126_b200.params import preset
+
+TOL = 1e-7
+
+
+@pytest.fixture(scope="module")
+def eng():
+    return oracle_engine(preset("toy"))
+
+
+@pytest.fixture(scope="module")
+def x(eng):
+    return np.linspace(-1, 1, eng.params.slot_count)
+
+
+def test_roundtrip_and_capacity(eng, x):
+    ct = eng.encrypt(x)
+    assert ct.level == eng.params.max_level
+    assert np.abs(eng.decrypt(ct) - x).max() < TOL
+    short = eng.decrypt(eng.encrypt([1.0, 2.0]))
+    assert np.abs(short[:2] - [1, 2]).max() < TOL and np.abs(short[2:]).max() < TOL
+    with pytest.raises(CapacityError):
+        eng.encrypt(np.zeros(eng.params.slot_count + 1))
+    with pytest.raises(ValueError):
+        eng.plain(np.zeros(3))
+
+
+def test_arithmetic(eng, x):
+    a, b = eng.encrypt(x), eng.encrypt(x[::-1])
+    y = x[::-1]
+    checks = [
+        (eng.add(a, b), x + y), (eng.sub(a, b), x - y), (eng.negate(a), -x),
+        (eng.add_plain(a, 0.25), x + 0.25), (eng.add_plain(a, y), x + y),
+        (eng.mul(a, b), x * y), (eng.mul_plain(a, -3.5), -3.5 * x), (eng.mul_plain(a, y), x * y),
+    ]
+    for ct, want in checks:
+        assert np.abs(eng.decrypt(ct) - want).max() < TOL
+    assert eng.mul(a, b).level == a.level - 1 and eng.mul_plain(a, y).level == a.level - 1
+    assert eng.add(a, b).level == a.level and eng.negate(a).level == a.level
+
+
+def test_mixed_levels_take_min(eng, x):
+    a = eng.encrypt(x)
+    sq = eng.mul(a, a)
+    cube = eng.mul(sq, a)
+    s = eng.add(cube, a)
+    assert s.level == a.level - 2
+    assert np.abs(eng.decrypt(s) - (x ** 3 + x)).max() < TOL
+    m = eng.mul_plain(a, 2.0, level=a.level - 3)
+    assert m.level == a.level - 3 and np.abs(eng.decrypt(m) - 2 * x).max() < TOL
+
+
+def test_rotation_direction_and_trace(eng, x):
+    n = eng.params.slot_count
+    a = eng.encrypt(x)
+    eng.cost_reset()
+    assert eng.rotate(a, 0) is a and eng.rotate(a, n) is a
+    assert np.abs(eng.decrypt(eng.rotate(a, 1)) - np.roll(x, -1)).max() < TOL
+    assert np.abs(eng.decrypt(eng.rotate(a, -3)) - np.roll(x, 3)).max() < TOL
+    assert eng.rotation_offsets() == [1, n - 3]
+    rep = eng.cost_snapshot()
+    assert rep.rotations == 2 and rep.critical_rotations == 1
+
+
+def test_depth_budget_error(eng):
+    a = eng.encrypt([0.5])
+    while a.level > 0:
+        a = eng.mul_plain(a, 1.0)
+    with pytest.raises(DepthBudgetError) as ei:
+        eng.mul(a, a, site="here")
+    assert ei.value.site == "here" and ei.value.available == 0
+    with pytest.raises(DepthBudgetError):
+        eng.mul_plain(a, 2.0)
+
+
+def test_incompatible_params(eng):
+    other = oracle_engine(preset("toy", seed=7))
+    with pytest.raises(IncompatibleParamsError):
+        eng.add(eng.encrypt([1.0]), other.encrypt([1.0]))
+
+
+def test_ideal_map_constant_only(eng, x):
+    a = eng.encrypt(x)
+    c = eng.ideal_map(lambda s: np.full_like(s, 0.75), a, levels=2)
+    assert c.level == a.level - 2 and np.abs(eng.decrypt(c) - 0.75).max() < TOL
+    with pytest.raises(EngineError):
+        eng.ideal_map(lambda s: s * 2, a)
+
+
+def test_composite_rank_matches_simulator_and_plaintext():
+    p = preset("toy_deep")
+    eng = oracle_engine(p)
+    sim = SlotSim(SimParams(p.slot_count, p.max_level))
+    v = np.array([0.30, 0.10, 0.80, 0.55, 0.20, 0.95, 0.65, 0.40])
+    cfg = M.KernelConfig(mode="composite", composite=(3, 2))
+    got = M.read_row(eng, M.rank(eng, eng.encrypt(v), 8, cfg).ranks, 8)
+    ref = M.read_row(sim, M.rank(sim, sim.encrypt(v), 8, cfg).ranks, 8)
+    assert np.abs(got - ref).max() < 1e-5
+    assert np.array_equal(np.rint(got), fractional_ranks(v))
+    assert eng.cost_snapshot() == sim.cost_snapshot()

@@ -1,0 +1,21 @@
+"""Small driver for ncu: a few cfg2 primitive calls on one GPU (no timing)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+
+what = sys.argv[1] if len(sys.argv) > 1 else "keyswitch"
+step = bench.PrimitiveStep(torch, 0, n_ct=4)
+for _ in range(2):
+    if what == "ntt":
+        step.ntt(step.x, False)
+        step.ntt(step.x, True)
+    elif what == "keyswitch":
+        step.keyswitch_batch()
+    elif what == "step":
+        step.step()
+torch.cuda.synchronize()
+print("done", what)
