@@ -107,6 +107,24 @@ int srk_automorph(srk_ctx *ctx, const uint64_t *a, uint64_t *out, long long n_li
 int srk_rotate(srk_ctx *ctx, const uint64_t *a, const uint64_t *gkey, uint64_t *out, int level,
                uint64_t galois, void *ws, void *stream);
 
+/* batched forms (the config-2 microbenchmark and multi-ciphertext
+ * pipelines): `batch` ciphertexts at ct strides a_ct / out_ct (words) */
+int srk_rescale_batch(srk_ctx *ctx, const uint64_t *a, long long a_ct, uint64_t *out,
+                      long long out_ct, int batch, int level, void *ws, void *stream);
+/* rescale != 0: relinearised product rescaled to level-1 */
+int srk_mul_relin_batch(srk_ctx *ctx, const uint64_t *a, const uint64_t *b, long long ab_ct,
+                        const uint64_t *rlk, uint64_t *out, long long out_ct, int batch, int level,
+                        int rescale, void *ws, void *stream);
+int srk_rotate_batch(srk_ctx *ctx, const uint64_t *a, long long a_ct, const uint64_t *gkey,
+                     uint64_t *out, long long out_ct, int batch, int level, uint64_t galois,
+                     void *ws, void *stream);
+/* n_rot rotations of each of `batch` ciphertexts sharing one base extension
+ * per ciphertext (hoisting); gkeys / galois / outs are HOST arrays (of device
+ * pointers); rotation r of ciphertext b lands at outs[r] + b * out_ct */
+int srk_rotate_hoisted(srk_ctx *ctx, const uint64_t *a, long long a_ct, int batch, int n_rot,
+                       const uint64_t *const *gkeys, const uint64_t *galois, uint64_t *const *outs,
+                       long long out_ct, int level, void *ws, void *stream);
+
 /* sampling / keys / encryption */
 int srk_uniform(srk_ctx *ctx, uint64_t *a, int n_limbs, int first_prime, uint64_t seed,
                 uint64_t stream_base, void *stream);

@@ -322,10 +322,15 @@ void orc_automorph(const orc_ctx *c, const uint64_t *a, uint64_t *out, int n_lim
 /* hybrid key switching                                                */
 /* ------------------------------------------------------------------ */
 
+static inline uint32_t auto_index(uint32_t k, uint64_t g, int log_n);
+
 /* d: uint64[level+1][N] NTT form.  key: uint64[dnum][2][n_q+n_p][N].
- * out0/out1: uint64[level+1][N] NTT form, <(out0,out1),(1,s)> ~ d * s_from. */
-void orc_keyswitch(const orc_ctx *c, const uint64_t *d, const uint64_t *key, uint64_t *out0,
-                   uint64_t *out1, int level) {
+ * out0/out1: uint64[level+1][N] NTT form, <(out0,out1),(1,s)> ~ sigma_g(d) * s_from,
+ * where sigma_g (X -> X^galois, galois = 1: identity) is applied to the
+ * ModUp-extended digits -- i.e. after base extension, so several rotations
+ * of one ciphertext can share the extension (hoisting). */
+void orc_keyswitch_g(const orc_ctx *c, const uint64_t *d, const uint64_t *key, uint64_t *out0,
+                     uint64_t *out1, int level, uint64_t galois) {
     const int n = c->n, nl = level + 1, K = c->n_p, ne = nl + K, np_all = c->n_primes;
     const int alpha = c->alpha, beta = (nl + alpha - 1) / alpha;
     uint64_t *dc = (uint64_t *)malloc(sizeof(uint64_t) * nl * n);
@@ -372,6 +377,15 @@ void orc_keyswitch(const orc_ctx *c, const uint64_t *d, const uint64_t *key, uin
             ntt_limb(c, dst, pid);
         }
         free(y);
+        if (galois != 1) { /* automorphism of the extended digit (NTT domain gather) */
+            uint64_t *tmp = (uint64_t *)malloc(sizeof(uint64_t) * n);
+            for (int t = 0; t < ne; t++) {
+                uint64_t *e = ext + (size_t)t * n;
+                for (int j = 0; j < n; j++) tmp[j] = e[auto_index((uint32_t)j, galois, c->log_n)];
+                memcpy(e, tmp, sizeof(uint64_t) * n);
+            }
+            free(tmp);
+        }
         /* inner product with digit jd of the key */
 #pragma omp parallel for
         for (int t = 0; t < ne; t++) {
@@ -445,6 +459,11 @@ void orc_keyswitch(const orc_ctx *c, const uint64_t *d, const uint64_t *key, uin
     }
 }
 
+void orc_keyswitch(const orc_ctx *c, const uint64_t *d, const uint64_t *key, uint64_t *out0,
+                   uint64_t *out1, int level) {
+    orc_keyswitch_g(c, d, key, out0, out1, level, 1);
+}
+
 /* out = tensor(a, b) relinearised (no rescale), level unchanged */
 void orc_mul_relin(const orc_ctx *c, const uint64_t *a, const uint64_t *b, const uint64_t *rlk,
                    uint64_t *out, int level) {
@@ -466,25 +485,26 @@ void orc_mul_relin(const orc_ctx *c, const uint64_t *a, const uint64_t *b, const
     free(d);
 }
 
-/* out = rotate(a) by Galois element g with key for sigma_g(s) -> s */
+/* out = rotate(a) by Galois element g with key for sigma_g(s) -> s:
+ * (sigma_g(c0) + u0, u1) with (u0, u1) = keyswitch_g(c1) */
 void orc_rotate(const orc_ctx *c, const uint64_t *a, const uint64_t *gkey, uint64_t *out,
                 int level, uint64_t galois) {
     const int n = c->n, nl = level + 1;
     const size_t ps = (size_t)nl * n;
-    uint64_t *r = (uint64_t *)malloc(sizeof(uint64_t) * 2 * ps);
-    orc_automorph(c, a, r, 2 * nl, galois);
+    uint64_t *r0 = (uint64_t *)malloc(sizeof(uint64_t) * ps);
+    orc_automorph(c, a, r0, nl, galois);
     uint64_t *u = (uint64_t *)malloc(sizeof(uint64_t) * 2 * ps);
-    orc_keyswitch(c, r + ps, gkey, u, u + ps, level);
+    orc_keyswitch_g(c, a + ps, gkey, u, u + ps, level, galois);
     for (int i = 0; i < nl; i++) {
         const uint64_t q = c->prime[i];
         for (int j = 0; j < n; j++) {
             size_t x = (size_t)i * n + j;
-            out[x] = addmod(r[x], u[x], q);
+            out[x] = addmod(r0[x], u[x], q);
             out[ps + x] = u[ps + x];
         }
     }
     free(u);
-    free(r);
+    free(r0);
 }
 
 /* ------------------------------------------------------------------ */

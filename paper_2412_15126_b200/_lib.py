@@ -44,6 +44,15 @@ EXPORTS = {
     "srk_mul_relin_rescale": [c_void_p, _u64p, _u64p, _u64p, _u64p, c_int, c_void_p, c_void_p],
     "srk_automorph": [c_void_p, _u64p, _u64p, c_longlong, c_uint64, c_void_p],
     "srk_rotate": [c_void_p, _u64p, _u64p, _u64p, c_int, c_uint64, c_void_p, c_void_p],
+    "srk_rescale_batch": [c_void_p, _u64p, c_longlong, _u64p, c_longlong, c_int, c_int, c_void_p,
+                          c_void_p],
+    "srk_mul_relin_batch": [c_void_p, _u64p, _u64p, c_longlong, _u64p, _u64p, c_longlong, c_int,
+                            c_int, c_int, c_void_p, c_void_p],
+    "srk_rotate_batch": [c_void_p, _u64p, c_longlong, _u64p, _u64p, c_longlong, c_int, c_int,
+                         c_uint64, c_void_p, c_void_p],
+    "srk_rotate_hoisted": [c_void_p, _u64p, c_longlong, c_int, c_int, POINTER(c_void_p),
+                           POINTER(c_uint64), POINTER(c_void_p), c_longlong, c_int, c_void_p,
+                           c_void_p],
     "srk_uniform": [c_void_p, _u64p, c_int, c_int, c_uint64, c_uint64, c_void_p],
     "srk_small_to_ntt": [c_void_p, _u64p, _u64p, c_int, c_int, c_void_p],
     "srk_square": [c_void_p, _u64p, _u64p, c_int, c_void_p],

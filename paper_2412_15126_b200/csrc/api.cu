@@ -106,11 +106,13 @@ struct srk_ctx {
     int log_n, n, n_q, n_p, L, dnum, alpha, n_primes;
     std::vector<uint64_t> primes;
     PrimeConst *d_pc = nullptr;
-    uint64_t *d_tw = nullptr, *d_tws = nullptr, *d_itw = nullptr, *d_itws = nullptr;
+    ulonglong2 *d_tw = nullptr, *d_itw = nullptr;  // {w, Shoup(w)} interleaved
     std::vector<void *> allocs;
     // modup[level][digit], moddown[level]
     std::vector<std::vector<BconvPlan>> modup;
     std::vector<BconvPlan> moddown;
+    std::vector<LimbConsts> lc_modup_scale;  // [level]: N^-1 (Q_j/q_i)^-1 mod q_i (INTT fold)
+    LimbConsts lc_moddown_scale;      // N^-1 (P/p_k)^-1 mod p_k (INTT fold)
     LimbConsts lc_pinv;               // P^-1 mod q_i
     LimbConsts lc_pmod;               // P mod prime_i (all primes)
     std::vector<LimbConsts> lc_qlinv; // [level]: q_level^-1 mod q_i
@@ -236,8 +238,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     }
     if ((rc = dupload(c, &c->d_pc, pc))) { srk_ctx_destroy(c); return rc; }
     // twiddles
-    std::vector<uint64_t> tw((size_t)np * n), tws((size_t)np * n), itw((size_t)np * n),
-        itws((size_t)np * n);
+    std::vector<ulonglong2> tw((size_t)np * n), itw((size_t)np * n);
     for (int i = 0; i < np; i++) {
         const uint64_t q = primes[i], psi = roots[i] % q, ipsi = hinv(psi, q);
         if (hpow(psi, (uint64_t)n, q) != q - 1) {
@@ -247,16 +248,13 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
         uint64_t p = 1, ip = 1;
         for (int k = 0; k < n; k++) {
             const size_t r = (size_t)i * n + hbrv((uint32_t)k, log_n);
-            tw[r] = p;
-            tws[r] = shoup(p, q);
-            itw[r] = ip;
-            itws[r] = shoup(ip, q);
+            tw[r] = make_ulonglong2(p, shoup(p, q));
+            itw[r] = make_ulonglong2(ip, shoup(ip, q));
             p = hmul(p, psi, q);
             ip = hmul(ip, ipsi, q);
         }
     }
-    if ((rc = dupload(c, &c->d_tw, tw)) || (rc = dupload(c, &c->d_tws, tws)) ||
-        (rc = dupload(c, &c->d_itw, itw)) || (rc = dupload(c, &c->d_itws, itws))) {
+    if ((rc = dupload(c, &c->d_tw, tw)) || (rc = dupload(c, &c->d_itw, itw))) {
         srk_ctx_destroy(c);
         return rc;
     }
@@ -296,6 +294,32 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
         if (i < n_q) pinv[i] = hinv(pm, primes[i]);
     }
     fill_consts(c->lc_pinv, pinv, std::vector<uint64_t>(qv.begin(), qv.begin() + n_q));
+    {
+        std::vector<uint64_t> w(n_p), qq(n_p);
+        for (int k = 0; k < n_p; k++) {
+            const uint64_t p = primes[n_q + k];
+            uint64_t h = 1;
+            for (int m = 0; m < n_p; m++)
+                if (m != k) h = hmul(h, primes[n_q + m] % p, p);
+            w[k] = hmul(hinv((uint64_t)n, p), hinv(h, p), p);
+            qq[k] = p;
+        }
+        fill_consts(c->lc_moddown_scale, w, qq);
+    }
+    c->lc_modup_scale.resize(n_q);
+    for (int l = 0; l < n_q; l++) {
+        std::vector<uint64_t> w(l + 1), qq(l + 1);
+        for (int i = 0; i <= l; i++) {
+            const uint64_t q = primes[i];
+            const int g0 = (i / c->alpha) * c->alpha, g1 = std::min(l + 1, g0 + c->alpha);
+            uint64_t h = 1;
+            for (int m = g0; m < g1; m++)
+                if (m != i) h = hmul(h, primes[m] % q, q);
+            w[i] = hmul(hinv((uint64_t)n, q), hinv(h, q), q);
+            qq[i] = q;
+        }
+        fill_consts(c->lc_modup_scale[l], w, qq);
+    }
     fill_consts(c->lc_pmod, pmod, qv);
     c->lc_qlinv.resize(n_q);
     for (int l = 1; l < n_q; l++) {
@@ -310,17 +334,25 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     return SRK_OK;
 }
 
+#define SRK_WS_BATCH 8  // ciphertexts per internal chunk of a batched call
+
+// words of scratch (x N) each op needs for a chunk of B ciphertexts at level l
+static size_t ks_limbs(const srk_ctx *c, int level, int B) {
+    const size_t nl = level + 1, ne = nl + c->n_p, beta = (nl + c->alpha - 1) / c->alpha;
+    return (size_t)B * (nl + beta * ne + 2 * ne + 2 * nl);
+}
+static size_t rescale_limbs(int level, int B) { return (size_t)B * (2 + 2 * (size_t)level); }
+static size_t relin_limbs(const srk_ctx *c, int level, int B) {
+    const size_t nl = level + 1;
+    return (size_t)B * (3 * nl + 2 * nl) + std::max(ks_limbs(c, level, B), rescale_limbs(level, B));
+}
+
 extern "C" size_t srk_workspace_bytes(const srk_ctx *c) {
-    const size_t n = c->n, nl = c->n_q, ne = nl + c->n_p;
-    const size_t beta = (nl + c->alpha - 1) / c->alpha;
-    size_t ks = nl + beta * ne + 2 * ne + 2 * nl;      // keyswitch
-    size_t relin = 3 * nl + 2 * nl + ks;               // tensor + ks outputs
-    size_t relin_rs = relin + 2 * nl + (2 + 2 * nl);   // + product + rescale
-    size_t rot = 2 * nl + 2 * nl + ks;
-    size_t keygen = 2 * (size_t)c->n_primes;
-    size_t enc = 2 * nl;
-    size_t words = std::max({ks, relin_rs, rot, keygen, enc, (size_t)2 + 2 * nl});
-    return words * n * sizeof(uint64_t) + 256;
+    const int L = c->L;
+    size_t limbs = std::max({relin_limbs(c, L, SRK_WS_BATCH), ks_limbs(c, L, SRK_WS_BATCH) + 4 * (L + 1),
+                             rescale_limbs(L, SRK_WS_BATCH) + 2 * (size_t)(L + 1) * SRK_WS_BATCH,
+                             (size_t)2 * c->n_primes, (size_t)2 * (L + 1)});
+    return limbs * c->n * sizeof(uint64_t) + 256;
 }
 
 // ---------------------------------------------------------------------
@@ -338,90 +370,145 @@ static NttTables tables(const srk_ctx *c) {
     NttTables t;
     t.pc = c->d_pc;
     t.tw = c->d_tw;
-    t.tws = c->d_tws;
     t.itw = c->d_itw;
-    t.itws = c->d_itws;
     return t;
 }
 
-template <int LOG_T, bool INV, bool COL>
-static int launch_pass(const srk_ctx *c, LimbBatch b, int y0, int ny, cudaStream_t s) {
+static FuseArgs no_fuse() {
+    FuseArgs f;
+    memset(&f, 0, sizeof f);
+    f.galois = 1;
+    f.add_galois = 1;
+    return f;
+}
+
+template <int LOG_T, bool INV, bool COL, int IO>
+static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const FuseArgs &f,
+                       cudaStream_t s) {
     using SH = NttShape<LOG_T>;
     const int subs = c->n >> LOG_T;  // sub-transforms per limb
     int cb = 256 / SH::TPS;
     if (cb > subs) cb = subs;
     const int threads = cb * SH::TPS;
     const size_t smem = COL ? (size_t)cb * SH::T * 8 : (size_t)cb * (SH::T + SH::T / SH::E) * 8;
-    // shift the batch so blockIdx.y starts at y0
+    // shift the batch to start at limb l0 (mode 0: pointer + prime offsets; mode 1 keeps the
+    // slot map, which is absolute, so only chunk by whole batches there)
     LimbBatch bb = b;
-    const int limb0 = y0 / b.n_polys;
-    if (y0 % b.n_polys) return fail(SRK_EINVAL, "ntt chunk must start at a limb boundary");
-    bb.ptr = b.ptr + (long long)limb0 * c->n;
-    bb.split = b.split - limb0;
-    bb.off_a = b.off_a + limb0;
-    bb.off_b = b.off_b + limb0;
-    bb.n_limbs = ny / b.n_polys;
-    dim3 grid(subs / cb, ny);
-    ntt_pass_kernel<LOG_T, INV, COL><<<grid, threads, smem, s>>>(bb, tables(c), c->log_n);
+    FuseArgs ff = f;
+    if (l0) {
+        bb.ptr = b.ptr + (long long)l0 * c->n;
+        bb.split = b.split - l0;
+        bb.off_a = b.off_a + l0;
+        bb.off_b = b.off_b + l0;
+        if (ff.src && (IO == LD_PLAIN || IO == LD_AUTO)) ff.src += (long long)l0 * c->n;
+        if (ff.out) ff.out += (long long)l0 * c->n;
+        if (ff.acc) ff.acc += (long long)l0 * c->n;
+        if (ff.add0) ff.add0 += (long long)l0 * c->n;
+        if (ff.add1) ff.add1 += (long long)l0 * c->n;
+        if (ff.pt) ff.pt += (long long)l0 * c->n;
+        if (ff.mat) ff.mat += l0;
+        if (ff.corr) ff.corr += l0;
+        for (int k = 0; k + l0 < SRK_MAXP; k++) {
+            ff.mulc.w[k] = f.mulc.w[k + l0];
+            ff.mulc.ws[k] = f.mulc.ws[k + l0];
+            ff.pre.w[k] = f.pre.w[k + l0];
+            ff.pre.ws[k] = f.pre.ws[k + l0];
+        }
+    }
+    bb.n_limbs = nlc;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(ntt_pass_kernel<LOG_T, INV, COL, IO>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        attr_set = true;
+    }
+    dim3 grid(subs / cb, nlc * b.n_polys);
+    ntt_pass_kernel<LOG_T, INV, COL, IO><<<grid, threads, smem, s>>>(bb, tables(c), c->log_n, ff);
     LAUNCHED();
     return SRK_OK;
 }
 
-template <bool INV, bool COL>
-static int pass_dispatch(const srk_ctx *c, int log_t, LimbBatch b, int y0, int ny, cudaStream_t s) {
+template <bool INV, bool COL, int IO>
+static int pass_t(const srk_ctx *c, int log_t, LimbBatch b, int l0, int nlc, const FuseArgs &f,
+                  cudaStream_t s) {
     switch (log_t) {
-        case 5: return launch_pass<5, INV, COL>(c, b, y0, ny, s);
-        case 6: return launch_pass<6, INV, COL>(c, b, y0, ny, s);
-        case 7: return launch_pass<7, INV, COL>(c, b, y0, ny, s);
-        case 8: return launch_pass<8, INV, COL>(c, b, y0, ny, s);
+        case 5: return launch_pass<5, INV, COL, IO>(c, b, l0, nlc, f, s);
+        case 6: return launch_pass<6, INV, COL, IO>(c, b, l0, nlc, f, s);
+        case 7: return launch_pass<7, INV, COL, IO>(c, b, l0, nlc, f, s);
+        case 8: return launch_pass<8, INV, COL, IO>(c, b, l0, nlc, f, s);
         default: return fail(SRK_EINVAL, "unsupported NTT pass size 2^%d", log_t);
     }
 }
 
-// NTT over a LimbBatch, chunked so one chunk's intermediate stays in L2
-static int ntt_batch(const srk_ctx *c, LimbBatch b, bool inverse, cudaStream_t s) {
+// forward: first pass fused load `ld` (LD_PLAIN/LD_BCONV/LD_SPREAD), last pass store `st`
+// (ST_PLAIN/ST_MODDOWN/ST_RESCALE); inverse: ld in {LD_PLAIN, LD_AUTO}, st in {ST_PLAIN, ST_SCALE}
+static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &f, int ld, int st,
+                   cudaStream_t s) {
     if (b.n_limbs <= 0 || b.n_polys <= 0) return SRK_OK;
     const int log_r = (c->log_n + 1) / 2, log_c = c->log_n - log_r;
-    // chunk = whole limbs (all polys of a limb index) so pid stays per y-row
-    int limbs_per_chunk = c->ntt_chunk / b.n_polys;
-    if (limbs_per_chunk < 1) limbs_per_chunk = 1;
-    if (limbs_per_chunk > 65535 / b.n_polys) limbs_per_chunk = 65535 / b.n_polys;
-    for (int l0 = 0; l0 < b.n_limbs; l0 += limbs_per_chunk) {
-        const int nlc = std::min(limbs_per_chunk, b.n_limbs - l0);
-        const int y0 = l0 * b.n_polys, ny = nlc * b.n_polys;
+    // chunk whole limb indices (all polys of a limb) so the intermediate stays in L2
+    int per = c->ntt_chunk / b.n_polys;
+    if (per < 1) per = 1;
+    if (per > 65535 / b.n_polys) per = 65535 / b.n_polys;
+    if (b.mode == 1 && per < b.n_limbs) per = b.n_limbs;  // slot map is absolute
+    if ((long long)per * b.n_polys > 65535) return fail(SRK_EINVAL, "NTT batch too large");
+    for (int l0 = 0; l0 < b.n_limbs; l0 += per) {
+        const int nlc = std::min(per, b.n_limbs - l0);
         if (!inverse) {
-            TRY((pass_dispatch<false, true>(c, log_r, b, y0, ny, s)));
-            TRY((pass_dispatch<false, false>(c, log_c, b, y0, ny, s)));
+            switch (ld) {
+                case LD_PLAIN: TRY((pass_t<false, true, LD_PLAIN>(c, log_r, b, l0, nlc, f, s))); break;
+                case LD_BCONV: TRY((pass_t<false, true, LD_BCONV>(c, log_r, b, l0, nlc, f, s))); break;
+                case LD_SPREAD: TRY((pass_t<false, true, LD_SPREAD>(c, log_r, b, l0, nlc, f, s))); break;
+                default: return fail(SRK_EINVAL, "bad forward load mode");
+            }
+            switch (st) {
+                case ST_PLAIN: TRY((pass_t<false, false, ST_PLAIN>(c, log_c, b, l0, nlc, f, s))); break;
+                case ST_MODDOWN: TRY((pass_t<false, false, ST_MODDOWN>(c, log_c, b, l0, nlc, f, s))); break;
+                case ST_RESCALE: TRY((pass_t<false, false, ST_RESCALE>(c, log_c, b, l0, nlc, f, s))); break;
+                default: return fail(SRK_EINVAL, "bad forward store mode");
+            }
         } else {
-            TRY((pass_dispatch<true, false>(c, log_c, b, y0, ny, s)));
-            TRY((pass_dispatch<true, true>(c, log_r, b, y0, ny, s)));
+            switch (ld) {
+                case LD_PLAIN: TRY((pass_t<true, false, LD_PLAIN>(c, log_c, b, l0, nlc, f, s))); break;
+                case LD_AUTO: TRY((pass_t<true, false, LD_AUTO>(c, log_c, b, l0, nlc, f, s))); break;
+                default: return fail(SRK_EINVAL, "bad inverse load mode");
+            }
+            switch (st) {
+                case ST_PLAIN: TRY((pass_t<true, true, ST_PLAIN>(c, log_r, b, l0, nlc, f, s))); break;
+                case ST_SCALE: TRY((pass_t<true, true, ST_SCALE>(c, log_r, b, l0, nlc, f, s))); break;
+                default: return fail(SRK_EINVAL, "bad inverse store mode");
+            }
         }
     }
     return SRK_OK;
 }
 
+static int ntt_batch(const srk_ctx *c, LimbBatch b, bool inverse, cudaStream_t s) {
+    return ntt_run(c, b, inverse, no_fuse(), LD_PLAIN, ST_PLAIN, s);
+}
+
+// n_polys polys of n_limbs limbs (limb i under prime first + i), uniform poly stride
 static LimbBatch qbatch(uint64_t *p, int n_polys, long long pstride, int n_limbs, int first) {
     LimbBatch b;
+    memset(&b, 0, sizeof b);
     b.ptr = p;
     b.poly_stride = pstride;
+    b.ct_stride = 0;
+    b.ppc = n_polys > 0 ? n_polys : 1;
     b.n_polys = n_polys;
     b.n_limbs = n_limbs;
+    b.mode = 0;
     b.split = 1 << 30;
     b.off_a = first;
     b.off_b = first;
     return b;
 }
-// limbs [t0, t1) of an extended poly at `level`
-static LimbBatch ebatch(const srk_ctx *c, uint64_t *p, int n_polys, long long pstride, int level,
-                        int t0, int t1) {
-    LimbBatch b;
-    b.ptr = p + (long long)t0 * c->n;
-    b.poly_stride = pstride;
-    b.n_polys = n_polys;
-    b.n_limbs = t1 - t0;
-    b.split = level + 1 - t0;
-    b.off_a = t0;
-    b.off_b = t0 + c->L - level;
+// B ciphertexts of ppc polys each: poly (b, r) at p + b*ct + r*ps
+static LimbBatch cbatch(uint64_t *p, int B, int ppc, long long ct, long long ps, int n_limbs,
+                        int first) {
+    LimbBatch b = qbatch(p, B * ppc, ps, n_limbs, first);
+    b.ppc = ppc;
+    b.ct_stride = ct;
     return b;
 }
 
@@ -447,8 +534,10 @@ extern "C" int srk_ntt_ext(srk_ctx *c, uint64_t *data, int n_polys, long long po
                            int level, int inverse, void *stream) {
     if (!c || !data) return fail(SRK_EINVAL, "null argument");
     TRY(check_level(c, level));
-    return ntt_batch(c, ebatch(c, data, n_polys, poly_stride, level, 0, level + 1 + c->n_p),
-                     inverse != 0, S(stream));
+    LimbBatch b = qbatch(data, n_polys, poly_stride, level + 1 + c->n_p, 0);
+    b.split = level + 1;
+    b.off_b = c->L - level;
+    return ntt_batch(c, b, inverse != 0, S(stream));
 }
 
 extern "C" int srk_addsub(srk_ctx *c, const uint64_t *a, const uint64_t *b, uint64_t *out,
@@ -528,35 +617,80 @@ extern "C" int srk_tensor(srk_ctx *c, const uint64_t *a, const uint64_t *b, uint
 }
 
 // ---------------------------------------------------------------------
-// rescale (with optional pre-multiplier: 0 none, 1 per-limb constant, 2 plaintext)
+// rescale: B ciphertexts (a: ct stride a_ct, poly stride a_ps) at `level`
+// -> out (ct stride out_ct, poly stride level*N), dividing by q_level with
+// rounding.  Optional pre-multiplier: mode 1 per-limb constant k, mode 2
+// plaintext pt [level+1][N].  Two fused transforms:
+//   INTT(top limb) [x k folded into the N^-1 scale]  ->  top
+//   NTT(centred(top) mod q_i) with the combine (a*pre - .) q_l^-1 in its store
 // ---------------------------------------------------------------------
-static int rescale_impl(srk_ctx *c, const uint64_t *a, long long a_pstride, const uint64_t *pt,
-                        const LimbConsts &k, int mode, uint64_t *out, int level, uint64_t *ws,
-                        cudaStream_t s) {
+static int rescale_impl(srk_ctx *c, const uint64_t *a, long long a_ct, long long a_ps,
+                        const uint64_t *pt, const LimbConsts *k, uint64_t *out, long long out_ct,
+                        int level, int B, uint64_t *ws, cudaStream_t s) {
     if (level < 1) return fail(SRK_EINVAL, "cannot rescale a level-0 ciphertext");
-    const int n = c->n;
-    uint64_t *top = ws;                  // [2][N]
-    uint64_t *t = ws + 2ll * n;          // [2][level][N]
-    k_rescale_top<<<grid_for(2ll * n), 256, 0, s>>>(a, a_pstride, pt, k, mode, top, c->d_pc,
-                                                    c->log_n, level);
-    LAUNCHED();
-    TRY(ntt_batch(c, qbatch(top, 2, n, 1, level), true, s));
-    k_rescale_spread<<<grid_for(2ll * level * n), 256, 0, s>>>(top, t, c->d_pc, c->log_n, level);
-    LAUNCHED();
-    TRY(ntt_batch(c, qbatch(t, 2, (long long)level * n, level, 0), false, s));
-    k_rescale_combine<<<grid_for(2ll * level * n), 256, 0, s>>>(
-        a, a_pstride, pt, k, mode, t, c->lc_qlinv[level], out, c->d_pc, c->log_n, level);
-    LAUNCHED();
-    return SRK_OK;
+    const long long n = c->n;
+    uint64_t *top = ws;              // [B][2][N]
+    uint64_t *tb = ws + 2ll * B * n; // [B][2][level][N]
+    const int mode = pt ? 2 : (k ? 1 : 0);
+    FuseArgs f = no_fuse();
+    LimbBatch bt = cbatch(top, B, 2, 2 * n, n, 1, level);
+    if (mode == 2) {
+        k_rescale_top<<<grid_for(2ll * B * n), 256, 0, s>>>(a, a_ct, a_ps, pt, top, c->d_pc,
+                                                             c->log_n, level, B);
+        LAUNCHED();
+        TRY(ntt_run(c, bt, true, f, LD_PLAIN, ST_PLAIN, s));
+    } else {
+        f.src = a + (long long)level * n;
+        f.src_ct = a_ct;
+        f.src_ps = a_ps;
+        if (mode == 1) {
+            const uint64_t q = c->primes[level];
+            const uint64_t w = hmul(hinv((uint64_t)c->n, q), k->w[level], q);
+            f.mulc.w[0] = w;
+            f.mulc.ws[0] = shoup(w, q);
+        }
+        TRY(ntt_run(c, bt, true, f, LD_PLAIN, mode == 1 ? ST_SCALE : ST_PLAIN, s));
+    }
+    FuseArgs g = no_fuse();
+    g.src = top;
+    g.src_ct = 2 * n;
+    g.src_ps = n;
+    g.top_q = c->primes[level];
+    g.out = out;
+    g.out_ct = out_ct;
+    g.out_ps = (long long)level * n;
+    g.acc = a;
+    g.acc_ct = a_ct;
+    g.acc_ps = a_ps;
+    g.pre_mode = mode;
+    g.pt = pt;
+    if (k) g.pre = *k;
+    g.mulc = c->lc_qlinv[level];
+    LimbBatch bq = cbatch(tb, B, 2, 2ll * level * n, (long long)level * n, level, 0);
+    return ntt_run(c, bq, false, g, LD_SPREAD, ST_RESCALE, s);
 }
+
+// chunk a batch of B into SRK_WS_BATCH pieces
+#define FOR_CHUNKS(B, b0, nb) \
+    for (int b0 = 0, nb = std::min(SRK_WS_BATCH, (B)); b0 < (B); b0 += nb, nb = std::min(SRK_WS_BATCH, (B) - b0))
 
 extern "C" int srk_rescale(srk_ctx *c, const uint64_t *a, uint64_t *out, int level, void *ws,
                            void *stream) {
     TRY(check_level(c, level));
-    LimbConsts lc;
-    memset(&lc, 0, sizeof lc);
-    return rescale_impl(c, a, (long long)(level + 1) * c->n, nullptr, lc, 0, out, level,
+    const long long ps = (long long)(level + 1) * c->n;
+    return rescale_impl(c, a, 2 * ps, ps, nullptr, nullptr, out, 2ll * level * c->n, level, 1,
                         (uint64_t *)ws, S(stream));
+}
+
+extern "C" int srk_rescale_batch(srk_ctx *c, const uint64_t *a, long long a_ct, uint64_t *out,
+                                 long long out_ct, int batch, int level, void *ws, void *stream) {
+    TRY(check_level(c, level));
+    const long long ps = (long long)(level + 1) * c->n;
+    FOR_CHUNKS(batch, b0, nb) {
+        TRY(rescale_impl(c, a + b0 * a_ct, a_ct, ps, nullptr, nullptr, out + b0 * out_ct, out_ct,
+                         level, nb, (uint64_t *)ws, S(stream)));
+    }
+    return SRK_OK;
 }
 
 extern "C" int srk_mul_const_rescale(srk_ctx *c, const uint64_t *a, int src_limbs,
@@ -565,116 +699,196 @@ extern "C" int srk_mul_const_rescale(srk_ctx *c, const uint64_t *a, int src_limb
     TRY(check_level(c, level));
     if (src_limbs < level + 1) return fail(SRK_EINVAL, "source has fewer limbs than level+1");
     LimbConsts lc = host_consts(c, k_res, level + 1);
-    return rescale_impl(c, a, (long long)src_limbs * c->n, nullptr, lc, 1, out, level,
+    const long long ps = (long long)src_limbs * c->n;
+    return rescale_impl(c, a, 2 * ps, ps, nullptr, &lc, out, 2ll * level * c->n, level, 1,
                         (uint64_t *)ws, S(stream));
 }
 
 extern "C" int srk_mul_plain_rescale(srk_ctx *c, const uint64_t *a, const uint64_t *pt,
                                      uint64_t *out, int level, void *ws, void *stream) {
     TRY(check_level(c, level));
-    LimbConsts lc;
-    memset(&lc, 0, sizeof lc);
-    return rescale_impl(c, a, (long long)(level + 1) * c->n, pt, lc, 2, out, level,
+    const long long ps = (long long)(level + 1) * c->n;
+    return rescale_impl(c, a, 2 * ps, ps, pt, nullptr, out, 2ll * level * c->n, level, 1,
                         (uint64_t *)ws, S(stream));
 }
 
 // ---------------------------------------------------------------------
-// key switching
+// hybrid key switching of B polys d (ct stride d_ct, NTT form, level `level`):
+//   1. INTT(d) with (Q_j/q_i)^-1 folded into the N^-1 scale  -> dc
+//   2. ModUp base conversion of every digit                   -> ext (coef)
+//   3. NTT of every ModUp target limb (one batched call)
+// then, for each Galois element g of `galois[0..n_out)` (1 = plain switch):
+//   4. inner product with key g, composed with X -> X^g        -> acc
+//   5. INTT of acc's special limbs with (P/p_k)^-1 folded in
+//   6. NTT(ModDown conversion, exact rounding) with the combine
+//      out = add + (acc - conv) P^-1 fused into its store
+// out[o]: ct stride out_ct, c0 at +0, c1 at +out_ps.  add0 (gathered through
+// g when add_galois_is_g) and add1 are optional per-ciphertext addends.
 // ---------------------------------------------------------------------
-static int bconv(const srk_ctx *c, const BconvPlan &pl, const uint64_t *src, long long src_ps,
-                 uint64_t *out, long long out_ps, int n_polys, cudaStream_t s) {
-    if (pl.n_src * pl.n_dst > 16 * 72) return fail(SRK_EINVAL, "base conversion too wide");
-    BconvArgs ba;
-    ba.src = src;
-    ba.src_pstride = src_ps;
-    ba.n_src = pl.n_src;
-    ba.src_pid0 = pl.src_pid0;
-    ba.out = out;
-    ba.out_pstride = out_ps;
-    ba.n_dst = pl.n_dst;
-    ba.mat = pl.mat;
-    ba.hinv = pl.hinv;
-    ba.dst_slot = pl.dst_slot;
-    ba.dst_pid = pl.dst_pid;
-    ba.dst_corr = pl.dst_corr;
-    dim3 grid((c->n + 255) / 256, n_polys);
-    if (pl.n_src <= 4)
-        k_bconv<4><<<grid, 256, 0, s>>>(ba, c->d_pc, c->log_n);
-    else if (pl.n_src <= 8)
-        k_bconv<8><<<grid, 256, 0, s>>>(ba, c->d_pc, c->log_n);
-    else
-        k_bconv<16><<<grid, 256, 0, s>>>(ba, c->d_pc, c->log_n);
-    LAUNCHED();
-    return SRK_OK;
-}
+struct KsOut {
+    uint64_t *out;
+    long long out_ct, out_ps;
+    const uint64_t *key;
+    uint64_t galois;
+    const uint64_t *add0, *add1;
+    long long add_ct;
+    bool gather_add0;
+};
 
-// adds: optional (add0, add1) fused into the ModDown combine
-static int keyswitch_impl(srk_ctx *c, const uint64_t *d, const uint64_t *key, uint64_t *out0,
-                          uint64_t *out1, const uint64_t *add0, const uint64_t *add1, int level,
-                          uint64_t *ws, cudaStream_t s) {
-    const int n = c->n, nl = level + 1, K = c->n_p, ne = nl + K;
-    const int beta = (nl + c->alpha - 1) / c->alpha;
-    uint64_t *dc = ws;                                  // [nl][N]
-    uint64_t *ext = dc + (long long)nl * n;             // [beta][ne][N]
-    uint64_t *acc = ext + (long long)beta * ne * n;     // [2][ne][N]
-    uint64_t *conv = acc + 2ll * ne * n;                // [2][nl][N]
-    CU(cudaMemcpyAsync(dc, d, sizeof(uint64_t) * nl * n, cudaMemcpyDeviceToDevice, s));
-    TRY(ntt_batch(c, qbatch(dc, 1, 0, nl, 0), true, s));
-    for (int j = 0; j < beta; j++) {
-        const int g0 = j * c->alpha, g1 = std::min(nl, (j + 1) * c->alpha);
-        uint64_t *ej = ext + (long long)j * ne * n;
-        const BconvPlan &pl = c->modup[level][j];
-        TRY(bconv(c, pl, dc + (long long)g0 * n, 0, ej, 0, 1, s));
-        CU(cudaMemcpyAsync(ej + (long long)g0 * n, d + (long long)g0 * n,
-                           sizeof(uint64_t) * (g1 - g0) * n, cudaMemcpyDeviceToDevice, s));
-        if (g0 > 0) TRY(ntt_batch(c, ebatch(c, ej, 1, 0, level, 0, g0), false, s));
-        TRY(ntt_batch(c, ebatch(c, ej, 1, 0, level, g1, ne), false, s));
+static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const KsOut *outs,
+                          int n_out, int level, int B, uint64_t *ws, cudaStream_t s) {
+    const long long n = c->n;
+    const int nl = level + 1, K = c->n_p, ne = nl + K;
+    const int alpha = c->alpha, beta = (nl + alpha - 1) / alpha;
+    if (beta > SRK_MAX_DIGITS) return fail(SRK_EINVAL, "too many digits");
+    uint64_t *dc = ws;                                 // [B][nl]
+    uint64_t *ext = dc + (long long)B * nl * n;        // [B][beta][ne]
+    uint64_t *acc = ext + (long long)B * beta * ne * n;  // [B][2][ne]
+    uint64_t *conv = acc + (long long)B * 2 * ne * n;    // [B][2][nl]
+    // 1. INTT with the ModUp scale folded in
+    {
+        FuseArgs f = no_fuse();
+        f.src = d;
+        f.src_ct = d_ct;
+        f.src_ps = 0;
+        f.mulc = c->lc_modup_scale[level];
+        TRY(ntt_run(c, cbatch(dc, B, 1, (long long)nl * n, 0, nl, 0), true, f, LD_PLAIN, ST_SCALE, s));
     }
-    const long long tot = (long long)ne * n;
-    k_ks_inner<<<grid_for(tot), 256, 0, s>>>(ext, key, acc, c->d_pc, c->log_n, ne, level, c->L,
-                                             c->n_primes, beta);
-    LAUNCHED();
-    // ModDown: INTT the special limbs of both accumulators, convert to Q_l
-    LimbBatch pb;
-    pb.ptr = acc + (long long)nl * n;
-    pb.poly_stride = (long long)ne * n;
-    pb.n_polys = 2;
-    pb.n_limbs = K;
-    pb.split = 0;
-    pb.off_a = c->n_q;
-    pb.off_b = c->n_q;
-    TRY(ntt_batch(c, pb, true, s));
-    TRY(bconv(c, c->moddown[level], acc + (long long)nl * n, (long long)ne * n, conv,
-              (long long)nl * n, 2, s));
-    TRY(ntt_batch(c, qbatch(conv, 2, (long long)nl * n, nl, 0), false, s));
-    k_moddown_combine<<<grid_for(2ll * nl * n), 256, 0, s>>>(acc, (long long)ne * n, conv, add0,
-                                                             add1, c->lc_pinv, out0, out1,
-                                                             c->d_pc, c->log_n, nl);
-    LAUNCHED();
+    // 2. ModUp conversion, all digits
+    {
+        ModUpArgs m;
+        memset(&m, 0, sizeof m);
+        m.dc = dc;
+        m.dc_ct = (long long)nl * n;
+        m.ext = ext;
+        m.ext_ct = (long long)beta * ne * n;
+        m.ext_dig = (long long)ne * n;
+        m.nl = nl;
+        m.beta = beta;
+        m.alpha = alpha;
+        int maxd = 0;
+        for (int j = 0; j < beta; j++) {
+            const BconvPlan &pl = c->modup[level][j];
+            m.mat[j] = pl.mat;
+            m.slot[j] = pl.dst_slot;
+            m.pid[j] = pl.dst_pid;
+            m.n_dst[j] = pl.n_dst;
+            maxd = std::max(maxd, pl.n_dst);
+        }
+        dim3 grid((unsigned)((n + 255) / 256), B * beta, (maxd + SRK_MODUP_TCH - 1) / SRK_MODUP_TCH);
+        k_modup<<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n);
+        LAUNCHED();
+    }
+    // 3. NTT of all ModUp targets
+    {
+        LimbBatch b = cbatch(ext, B, beta, (long long)beta * ne * n, (long long)ne * n, 0, 0);
+        const int glast = nl - (beta - 1) * alpha;
+        b.mode = 1;
+        b.n_limbs = ne - glast;
+        b.alpha = alpha;
+        b.nl = nl;
+        b.level = level;
+        b.L = c->L;
+        b.ne = ne;
+        TRY(ntt_run(c, b, false, no_fuse(), LD_PLAIN, ST_PLAIN, s));
+    }
+    const BconvPlan &pd = c->moddown[level];
+    for (int o = 0; o < n_out; o++) {
+        const KsOut &ko = outs[o];
+        // 4. inner product (+ automorphism)
+        KsInnerArgs ka;
+        ka.d = d;
+        ka.d_ct = d_ct;
+        ka.ext = ext;
+        ka.ext_ct = (long long)beta * ne * n;
+        ka.ext_dig = (long long)ne * n;
+        ka.key = ko.key;
+        ka.acc = acc;
+        ka.acc_ct = 2ll * ne * n;
+        ka.galois = ko.galois;
+        ka.n_primes = c->n_primes;
+        ka.nl = nl;
+        ka.ne = ne;
+        ka.level = level;
+        ka.L = c->L;
+        ka.alpha = alpha;
+        ka.beta = beta;
+        ka.batch = B;
+        k_ks_inner<<<grid_for((long long)B * ne * n), 256, 0, s>>>(ka, c->d_pc, c->log_n);
+        LAUNCHED();
+        // 5. INTT of the special limbs, (P/p_k)^-1 folded in
+        {
+            FuseArgs f = no_fuse();
+            f.mulc = c->lc_moddown_scale;
+            LimbBatch b = cbatch(acc + (long long)nl * n, B, 2, 2ll * ne * n, (long long)ne * n, K, 0);
+            b.split = 0;
+            b.off_b = c->n_q;
+            TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, s));
+        }
+        // 6. ModDown: NTT(conversion) with the combine in its store
+        {
+            FuseArgs f = no_fuse();
+            f.src = acc + (long long)nl * n;
+            f.src_ct = 2ll * ne * n;
+            f.src_ps = (long long)ne * n;
+            f.n_src = K;
+            f.src_pid0 = c->n_q;
+            f.mat = pd.mat;
+            f.mat_ld = pd.n_dst;
+            f.corr = pd.dst_corr;
+            f.out = ko.out;
+            f.out_ct = ko.out_ct;
+            f.out_ps = ko.out_ps;
+            f.acc = acc;
+            f.acc_ct = 2ll * ne * n;
+            f.acc_ps = (long long)ne * n;
+            f.add0 = ko.add0;
+            f.add1 = ko.add1;
+            f.add_ct = ko.add_ct;
+            f.add_galois = ko.gather_add0 ? ko.galois : 1;
+            f.mulc = c->lc_pinv;
+            TRY(ntt_run(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), false, f,
+                        LD_BCONV, ST_MODDOWN, s));
+        }
+    }
     return SRK_OK;
 }
 
 extern "C" int srk_keyswitch(srk_ctx *c, const uint64_t *d, const uint64_t *key, uint64_t *out0,
                              uint64_t *out1, int level, void *ws, void *stream) {
     TRY(check_level(c, level));
-    return keyswitch_impl(c, d, key, out0, out1, nullptr, nullptr, level, (uint64_t *)ws,
-                          S(stream));
+    if (out1 - out0 <= 0) return fail(SRK_EINVAL, "out1 must follow out0");
+    KsOut o = {out0, 0, (long long)(out1 - out0), key, 1, nullptr, nullptr, 0, false};
+    return keyswitch_impl(c, d, 0, &o, 1, level, 1, (uint64_t *)ws, S(stream));
 }
 
-static int mul_relin_impl(srk_ctx *c, const uint64_t *a, const uint64_t *b, const uint64_t *rlk,
-                          uint64_t *out, int level, uint64_t *ws, cudaStream_t s) {
-    const long long ps = (long long)(level + 1) * c->n;
-    uint64_t *d = ws;  // [3][nl][N]
-    k_tensor<<<grid_for(ps), 256, 0, s>>>(a, b, d, c->d_pc, c->log_n, level + 1);
-    LAUNCHED();
-    return keyswitch_impl(c, d + 2 * ps, rlk, out, out + ps, d, d + ps, level, ws + 3 * ps, s);
+// B products a[b] x b[b] (both ct stride ab_ct) -> out (ct stride out_ct)
+static int mul_relin_chunk(srk_ctx *c, const uint64_t *a, const uint64_t *b, long long ab_ct,
+                           const uint64_t *rlk, uint64_t *out, long long out_ct, int level, int B,
+                           bool rescale, uint64_t *ws, cudaStream_t s) {
+    const long long n = c->n, nl = level + 1, ps = nl * n;
+    uint64_t *d = ws;                       // [B][3][nl]
+    uint64_t *prod = d + (long long)B * 3 * ps;  // [B][2][nl]
+    uint64_t *rest = prod + (long long)B * 2 * ps;
+    for (int i = 0; i < B; i++) {
+        k_tensor<<<grid_for(ps), 256, 0, s>>>(a + i * ab_ct, b + i * ab_ct, d + i * 3 * ps, c->d_pc,
+                                              c->log_n, level + 1);
+        LAUNCHED();
+    }
+    uint64_t *dst = rescale ? prod : out;
+    const long long dst_ct = rescale ? 2 * ps : out_ct;
+    KsOut o = {dst, dst_ct, ps, rlk, 1, d, d + ps, 3 * ps, false};
+    TRY(keyswitch_impl(c, d + 2 * ps, 3 * ps, &o, 1, level, B, rest, s));
+    if (!rescale) return SRK_OK;
+    return rescale_impl(c, prod, 2 * ps, ps, nullptr, nullptr, out, out_ct, level, B, rest, s);
 }
 
 extern "C" int srk_mul_relin(srk_ctx *c, const uint64_t *a, const uint64_t *b,
                              const uint64_t *rlk, uint64_t *out, int level, void *ws,
                              void *stream) {
     TRY(check_level(c, level));
-    return mul_relin_impl(c, a, b, rlk, out, level, (uint64_t *)ws, S(stream));
+    const long long ps = (long long)(level + 1) * c->n;
+    return mul_relin_chunk(c, a, b, 2 * ps, rlk, out, 2 * ps, level, 1, false, (uint64_t *)ws, S(stream));
 }
 
 extern "C" int srk_mul_relin_rescale(srk_ctx *c, const uint64_t *a, const uint64_t *b,
@@ -683,12 +897,20 @@ extern "C" int srk_mul_relin_rescale(srk_ctx *c, const uint64_t *a, const uint64
     TRY(check_level(c, level));
     if (level < 1) return fail(SRK_EINVAL, "depth exhausted");
     const long long ps = (long long)(level + 1) * c->n;
-    uint64_t *w = (uint64_t *)ws;
-    uint64_t *prod = w;  // [2][nl][N]
-    TRY(mul_relin_impl(c, a, b, rlk, prod, level, w + 2 * ps, S(stream)));
-    LimbConsts lc;
-    memset(&lc, 0, sizeof lc);
-    return rescale_impl(c, prod, ps, nullptr, lc, 0, out, level, w + 2 * ps, S(stream));
+    return mul_relin_chunk(c, a, b, 2 * ps, rlk, out, 2ll * level * c->n, level, 1, true,
+                           (uint64_t *)ws, S(stream));
+}
+
+extern "C" int srk_mul_relin_batch(srk_ctx *c, const uint64_t *a, const uint64_t *b, long long ab_ct,
+                                   const uint64_t *rlk, uint64_t *out, long long out_ct, int batch,
+                                   int level, int rescale, void *ws, void *stream) {
+    TRY(check_level(c, level));
+    if (rescale && level < 1) return fail(SRK_EINVAL, "depth exhausted");
+    FOR_CHUNKS(batch, b0, nb) {
+        TRY(mul_relin_chunk(c, a + b0 * ab_ct, b + b0 * ab_ct, ab_ct, rlk, out + b0 * out_ct,
+                            out_ct, level, nb, rescale != 0, (uint64_t *)ws, S(stream)));
+    }
+    return SRK_OK;
 }
 
 extern "C" int srk_automorph(srk_ctx *c, const uint64_t *a, uint64_t *out,
@@ -700,16 +922,45 @@ extern "C" int srk_automorph(srk_ctx *c, const uint64_t *a, uint64_t *out,
     return SRK_OK;
 }
 
-extern "C" int srk_rotate(srk_ctx *c, const uint64_t *a, const uint64_t *gkey, uint64_t *out,
-                          int level, uint64_t galois, void *ws, void *stream) {
+// rotation = key switch of c1 composed with X -> X^g, + sigma_g(c0)
+extern "C" int srk_rotate_batch(srk_ctx *c, const uint64_t *a, long long a_ct, const uint64_t *gkey,
+                                uint64_t *out, long long out_ct, int batch, int level,
+                                uint64_t galois, void *ws, void *stream) {
     TRY(check_level(c, level));
     if (!(galois & 1)) return fail(SRK_EINVAL, "Galois element must be odd");
     const long long ps = (long long)(level + 1) * c->n;
-    uint64_t *r = (uint64_t *)ws;  // [2][nl][N] automorphed input
-    k_automorph<<<grid_for(2 * ps), 256, 0, S(stream)>>>(a, r, 2ll * (level + 1), galois, c->log_n);
-    LAUNCHED();
-    return keyswitch_impl(c, r + ps, gkey, out, out + ps, r, nullptr, level, r + 2 * ps,
-                          S(stream));
+    FOR_CHUNKS(batch, b0, nb) {
+        const uint64_t *ab = a + b0 * a_ct;
+        KsOut o = {out + b0 * out_ct, out_ct, ps, gkey, galois, ab, nullptr, a_ct, true};
+        TRY(keyswitch_impl(c, ab + ps, a_ct, &o, 1, level, nb, (uint64_t *)ws, S(stream)));
+    }
+    return SRK_OK;
+}
+
+extern "C" int srk_rotate(srk_ctx *c, const uint64_t *a, const uint64_t *gkey, uint64_t *out,
+                          int level, uint64_t galois, void *ws, void *stream) {
+    const long long ct = 2ll * (level + 1) * c->n;
+    return srk_rotate_batch(c, a, ct, gkey, out, ct, 1, level, galois, ws, stream);
+}
+
+// several rotations of each ciphertext sharing one ModUp (hoisting)
+extern "C" int srk_rotate_hoisted(srk_ctx *c, const uint64_t *a, long long a_ct, int batch,
+                                  int n_rot, const uint64_t *const *gkeys, const uint64_t *galois,
+                                  uint64_t *const *outs, long long out_ct, int level, void *ws,
+                                  void *stream) {
+    TRY(check_level(c, level));
+    if (n_rot < 1 || n_rot > 64) return fail(SRK_EINVAL, "n_rot must lie in [1, 64]");
+    const long long ps = (long long)(level + 1) * c->n;
+    std::vector<KsOut> o(n_rot);
+    FOR_CHUNKS(batch, b0, nb) {
+        const uint64_t *ab = a + b0 * a_ct;
+        for (int r = 0; r < n_rot; r++) {
+            if (!(galois[r] & 1)) return fail(SRK_EINVAL, "Galois element must be odd");
+            o[r] = {outs[r] + b0 * out_ct, out_ct, ps, gkeys[r], galois[r], ab, nullptr, a_ct, true};
+        }
+        TRY(keyswitch_impl(c, ab + ps, a_ct, o.data(), n_rot, level, nb, (uint64_t *)ws, S(stream)));
+    }
+    return SRK_OK;
 }
 
 // ---------------------------------------------------------------------

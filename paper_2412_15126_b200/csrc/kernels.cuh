@@ -9,20 +9,6 @@
 #include "modarith.cuh"
 #include "ntt.cuh"
 
-#define SRK_MAXP 128
-
-// per-limb constant with Shoup companion, passed by value (<= 2 KiB)
-struct LimbConsts {
-    uint64_t w[SRK_MAXP];
-    uint64_t ws[SRK_MAXP];
-};
-
-__device__ __forceinline__ uint32_t auto_index(uint32_t k, uint64_t g, int log_n) {
-    const uint64_t mask = (2ull << log_n) - 1;
-    uint32_t r = __brev(k) >> (32 - log_n);
-    uint64_t e = ((uint64_t)r * 2 + 1) * g & mask;
-    return __brev((uint32_t)((e - 1) >> 1)) >> (32 - log_n);
-}
 
 // ---------------------------------------------------------------------
 // elementwise on ciphertexts [2][nl][N] (poly stride may differ per operand)
@@ -131,67 +117,20 @@ __global__ void k_tensor(const uint64_t *__restrict__ a, const uint64_t *__restr
 // rescale helpers
 // ---------------------------------------------------------------------
 
-// top[p] = a[p][level] * pre  (pre: const k[level] or pt[level] or none)
-__global__ void k_rescale_top(const uint64_t *__restrict__ a, long long a_pstride,
-                              const uint64_t *__restrict__ pt, LimbConsts k, int mode,
-                              uint64_t *__restrict__ top, const PrimeConst *__restrict__ pc,
-                              int log_n, int level) {
+// top[b][p] = a[b][p][level] * pt[level]   (rescale of a ct x pt product:
+// the dropped limb of the product, before its INTT)
+__global__ void k_rescale_top(const uint64_t *__restrict__ a, long long a_ct, long long a_ps,
+                              const uint64_t *__restrict__ pt, uint64_t *__restrict__ top,
+                              const PrimeConst *__restrict__ pc, int log_n, int level, int batch) {
     const long long n = 1ll << log_n;
     const PrimeConst P = pc[level];
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < 2 * n;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < 2ll * batch * n;
          x += (long long)gridDim.x * blockDim.x) {
-        const int p = (int)(x >> log_n);
+        const long long bp = x >> log_n;
+        const int b = (int)(bp >> 1), p = (int)(bp & 1);
         const long long off = x & (n - 1);
-        uint64_t v = a[p * a_pstride + (long long)level * n + off];
-        if (mode == 1) v = mul_shoup(v, k.w[level], k.ws[level], P.q);
-        if (mode == 2) v = mul_mod(v, pt[(long long)level * n + off], P);
-        top[x] = v;
-    }
-}
-
-// t[p][i] = centred(top[p]) mod q_i for i < level
-__global__ void k_rescale_spread(const uint64_t *__restrict__ top, uint64_t *__restrict__ t,
-                                 const PrimeConst *__restrict__ pc, int log_n, int level) {
-    const long long n = 1ll << log_n;
-    const long long total = 2ll * level * n;
-    const uint64_t ql = pc[level].q;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
-         x += (long long)gridDim.x * blockDim.x) {
-        const long long la = x >> log_n;
-        const int p = (int)(la / level), i = (int)(la - (long long)p * level);
-        const long long off = x & (n - 1);
-        const PrimeConst P = pc[i];
-        uint64_t v = top[(long long)p * n + off];
-        uint64_t r;
-        if (v > (ql >> 1)) {
-            // v - q_l < 0: (v - q_l) mod q_i
-            r = sub_mod(reduce64(v, P), reduce64(ql, P), P.q);
-        } else {
-            r = reduce64(v, P);
-        }
-        t[x] = r;
-    }
-}
-
-// out[p][i] = (a[p][i]*pre_i - t[p][i]) * qlinv_i   over i < level
-__global__ void k_rescale_combine(const uint64_t *__restrict__ a, long long a_pstride,
-                                  const uint64_t *__restrict__ pt, LimbConsts k, int mode,
-                                  const uint64_t *__restrict__ t, LimbConsts qlinv,
-                                  uint64_t *__restrict__ out, const PrimeConst *__restrict__ pc,
-                                  int log_n, int level) {
-    const long long n = 1ll << log_n;
-    const long long total = 2ll * level * n;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
-         x += (long long)gridDim.x * blockDim.x) {
-        const long long la = x >> log_n;
-        const int p = (int)(la / level), i = (int)(la - (long long)p * level);
-        const long long off = x & (n - 1);
-        const PrimeConst P = pc[i];
-        uint64_t v = a[p * a_pstride + (long long)i * n + off];
-        if (mode == 1) v = mul_shoup(v, k.w[i], k.ws[i], P.q);
-        if (mode == 2) v = mul_mod(v, pt[(long long)i * n + off], P);
-        v = sub_mod(v, t[x], P.q);
-        out[x] = mul_shoup(v, qlinv.w[i], qlinv.ws[i], P.q);
+        top[x] = mul_mod(a[b * a_ct + p * a_ps + (long long)level * n + off],
+                         pt[(long long)level * n + off], P);
     }
 }
 
@@ -211,125 +150,98 @@ __global__ void k_automorph(const uint64_t *__restrict__ a, uint64_t *__restrict
 }
 
 // ---------------------------------------------------------------------
-// fast base conversion (ModUp / ModDown)
-//   y_i = [x_i * hinv_i]_{src prime i}       (Shoup)
-//   out_t = sum_i y_i * mat[i][t]  mod dst prime t
-// src: n_src limbs (contiguous, coefficient form) ; out limb t written at
-// out + dst_off(t) * N for t in [0, n_dst) ; mat row-major [n_src][n_dst]
+// hybrid key switching, batched over B ciphertexts
 // ---------------------------------------------------------------------
-struct BconvArgs {
-    const uint64_t *src;
-    long long src_pstride;  // between polys
-    int n_src;
-    int src_pid0;           // prime of src limb 0 (src limbs are consecutive primes)
-    uint64_t *out;
-    long long out_pstride;
-    int n_dst;
-    const uint64_t *mat;    // device [n_src][n_dst]
-    const uint64_t *hinv;   // device [n_src] (+ [n_src] Shoup)
-    const int *dst_slot;    // device [n_dst]: output limb index for target t
-    const int *dst_pid;     // device [n_dst]: prime id of target t
-    const uint64_t *dst_corr;  // optional [n_dst]: [prod src primes]_{dst}; rounds exactly
+#define SRK_MAX_DIGITS 16
+
+// ModUp base conversion for every digit of every ciphertext:
+//   ext[b][j][slot_t] = sum_{i in G_j} y_i * mat_j[i][t]  mod p_t
+// y = dc[b][G_j] already multiplied by (Q_j/q_i)^-1 (folded into the INTT).
+// grid: x = coefficient blocks, y = b * beta + j, z = chunks of 8 targets.
+struct ModUpArgs {
+    const uint64_t *dc;
+    long long dc_ct;
+    uint64_t *ext;
+    long long ext_ct, ext_dig;
+    int nl, beta, alpha;
+    const uint64_t *mat[SRK_MAX_DIGITS];
+    const int *slot[SRK_MAX_DIGITS];
+    const int *pid[SRK_MAX_DIGITS];
+    int n_dst[SRK_MAX_DIGITS];
 };
 
-template <int MAXS>
-__global__ void k_bconv(BconvArgs ba, const PrimeConst *__restrict__ pc, int log_n) {
-    __shared__ uint64_t s_mat[MAXS * 72];
+#define SRK_MODUP_TCH 8
+
+__global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs a,
+                                               const PrimeConst *__restrict__ pc, int log_n) {
     const long long n = 1ll << log_n;
-    const int p = blockIdx.y;
-    const int tot = ba.n_src * ba.n_dst;
-    for (int i = threadIdx.x; i < tot; i += blockDim.x) s_mat[i] = ba.mat[i];
-    __syncthreads();
-    const uint64_t *src = ba.src + p * ba.src_pstride;
-    uint64_t *out = ba.out + p * ba.out_pstride;
+    const int b = blockIdx.y / a.beta, j = blockIdx.y - b * a.beta;
+    const int g0 = j * a.alpha, gs = min(a.alpha, a.nl - g0);
+    const int t0 = blockIdx.z * SRK_MODUP_TCH;
+    const int nd = a.n_dst[j];
+    if (t0 >= nd) return;
+    const int t1 = min(nd, t0 + SRK_MODUP_TCH);
+    const uint64_t *src = a.dc + b * a.dc_ct + (long long)g0 * n;
+    uint64_t *dst = a.ext + b * a.ext_ct + j * a.ext_dig;
+    const uint64_t *mat = a.mat[j];
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
          x += (long long)gridDim.x * blockDim.x) {
-        uint64_t y[MAXS];
+        uint64_t y[16];
 #pragma unroll
-        for (int i = 0; i < MAXS; i++) {
-            if (i < ba.n_src) {
-                const uint64_t q = pc[ba.src_pid0 + i].q;
-                y[i] = mul_shoup(src[(long long)i * n + x], ba.hinv[i], ba.hinv[ba.n_src + i], q);
-            }
-        }
-        // exact conversion: v = round(sum_i y_i / q_i) in 64.64 fixed point
-        // (f_i = y_i R1 + hi(y_i R0), R = floor(2^128/q_i)); output - v * Q
-        uint64_t v = 0;
-        if (ba.dst_corr) {
-            U128 frac = {0, 0};
-#pragma unroll
-            for (int i = 0; i < MAXS; i++) {
-                if (i < ba.n_src) {
-                    const PrimeConst P = pc[ba.src_pid0 + i];
-                    U128 f = {0, y[i] * P.ratio_hi + mulhi64(y[i], P.ratio_lo)};
-                    add_to(frac, f);
-                }
-            }
-            U128 half = {0, 1ull << 63};
-            add_to(frac, half);
-            v = frac.hi;
-        }
-        for (int t = 0; t < ba.n_dst; t++) {
+        for (int i = 0; i < 16; i++)
+            if (i < gs) y[i] = src[(long long)i * n + x];
+        for (int t = t0; t < t1; t++) {
             U128 acc = {0, 0};
 #pragma unroll
-            for (int i = 0; i < MAXS; i++)
-                if (i < ba.n_src) mac(acc, y[i], s_mat[i * ba.n_dst + t]);
-            const PrimeConst P = pc[ba.dst_pid[t]];
-            uint64_t r = reduce_u128(acc, P);
-            if (ba.dst_corr) r = sub_mod(r, mul_mod(v, ba.dst_corr[t], P), P.q);
-            out[(long long)ba.dst_slot[t] * n + x] = r;
+            for (int i = 0; i < 16; i++)
+                if (i < gs) mac(acc, y[i], __ldg(mat + i * nd + t));
+            dst[(long long)__ldg(a.slot[j] + t) * n + x] = reduce_u128(acc, pc[__ldg(a.pid[j] + t)]);
         }
     }
 }
 
-// ---------------------------------------------------------------------
-// key-switch inner product: acc_r[t] = sum_j ext_j[t] * key[j][r][pid(t)]
-// ext: [beta][ne][N] ; key: [dnum][2][n_primes][N] ; acc: [2][ne][N]
-// ---------------------------------------------------------------------
-__global__ void k_ks_inner(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ key,
-                           uint64_t *__restrict__ acc, const PrimeConst *__restrict__ pc,
-                           int log_n, int ne, int level, int L, int n_primes, int beta) {
+// key-switch inner product (optionally composed with X -> X^galois):
+//   acc[b][r][t][n] = sum_j E_j[t][pi(n)] * key[j][r][pid(t)][n]
+// E_j[t] = d[b][t] for t in digit j's own limbs G_j (NTT form input), else
+// ext[b][j][t].  pi = identity when galois == 1.
+struct KsInnerArgs {
+    const uint64_t *d;
+    long long d_ct;
+    const uint64_t *ext;
+    long long ext_ct, ext_dig;
+    const uint64_t *key;
+    uint64_t *acc;
+    long long acc_ct;
+    uint64_t galois;
+    int n_primes, nl, ne, level, L, alpha, beta, batch;
+};
+
+__global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInnerArgs a,
+                                                  const PrimeConst *__restrict__ pc, int log_n) {
     const long long n = 1ll << log_n;
-    const long long total = (long long)ne * n;
+    const long long per_ct = (long long)a.ne * n;
+    const long long total = per_ct * a.batch;
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
-        const int t = (int)(x >> log_n);
-        const long long off = x & (n - 1);
-        const int pid = t <= level ? t : t + (L - level);
+        const int b = (int)(x / per_ct);
+        const long long xi = x - b * per_ct;
+        const int t = (int)(xi >> log_n);
+        const long long off = xi & (n - 1);
+        const long long src = a.galois == 1 ? off : (long long)auto_index((uint32_t)off, a.galois, log_n);
+        const int pid = t <= a.level ? t : t + (a.L - a.level);
+        const int jt = t < a.nl ? t / a.alpha : -1;
         U128 a0 = {0, 0}, a1 = {0, 0};
-        for (int j = 0; j < beta; j++) {
-            const uint64_t e = ext[(long long)j * total + x];
-            const uint64_t *kj = key + ((long long)j * 2 * n_primes + pid) * n + off;
-            mac(a0, e, kj[0]);
-            mac(a1, e, kj[(long long)n_primes * n]);
+        for (int j = 0; j < a.beta; j++) {
+            const uint64_t e = j == jt ? a.d[b * a.d_ct + (long long)t * n + src]
+                                       : a.ext[b * a.ext_ct + j * a.ext_dig + (long long)t * n + src];
+            const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + pid) * n + off;
+            mac(a0, e, __ldg(kj));
+            mac(a1, e, __ldg(kj + (long long)a.n_primes * n));
         }
         const PrimeConst P = pc[pid];
-        acc[x] = reduce_u128(a0, P);
-        acc[total + x] = reduce_u128(a1, P);
-    }
-}
-
-// ModDown combine: out[r][i] = add_r[i] + (acc[r][i] - conv[r][i]) * P^-1 mod q_i
-// add_r may be null (then just the quotient); r in {0,1}
-__global__ void k_moddown_combine(const uint64_t *__restrict__ acc, long long acc_pstride,
-                                  const uint64_t *__restrict__ conv,
-                                  const uint64_t *__restrict__ add0,
-                                  const uint64_t *__restrict__ add1, LimbConsts pinv,
-                                  uint64_t *__restrict__ out0, uint64_t *__restrict__ out1,
-                                  const PrimeConst *__restrict__ pc, int log_n, int nl) {
-    const long long n = 1ll << log_n;
-    const long long ps = (long long)nl * n;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < 2 * ps;
-         x += (long long)gridDim.x * blockDim.x) {
-        const int r = x >= ps;
-        const long long xi = x - r * ps;
-        const int i = (int)(xi >> log_n);
-        const uint64_t q = pc[i].q;
-        uint64_t v = sub_mod(acc[r * acc_pstride + xi], conv[x], q);
-        v = mul_shoup(v, pinv.w[i], pinv.ws[i], q);
-        const uint64_t *ad = r ? add1 : add0;
-        if (ad) v = add_mod(v, ad[xi], q);
-        (r ? out1 : out0)[xi] = v;
+        uint64_t *o = a.acc + b * a.acc_ct + (long long)t * n + off;
+        o[0] = reduce_u128(a0, P);
+        o[per_ct] = reduce_u128(a1, P);
     }
 }
 

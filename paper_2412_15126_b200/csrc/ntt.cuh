@@ -24,29 +24,92 @@
 
 #include "modarith.cuh"
 
-// A batch of limbs: poly p (0..n_polys-1), limb i (0..n_limbs-1) lives at
-// ptr + p * poly_stride + i * N and is reduced modulo prime
-//   pid(i) = i + (i < split ? off_a : off_b).
+#define SRK_MAXP 128
+
+// per-limb constant with Shoup companion, passed by value (<= 2 KiB)
+struct LimbConsts {
+    uint64_t w[SRK_MAXP];
+    uint64_t ws[SRK_MAXP];
+};
+
+// A batch of limbs.  Poly p of the batch belongs to ciphertext b = p / ppc
+// (component r = p % ppc) and its limb slot t lives at
+//   ptr + b * ct_stride + r * poly_stride + t * N.
+// Limb i of a poly maps to slot t and prime pid:
+//   mode 0: t = i, pid = i + (i < split ? off_a : off_b);
+//   mode 1: ModUp targets of digit j = r at `level`: the ext slots outside
+//           [j alpha, j alpha + |G_j|), t >= ne skipped; pid = ext prime of t.
 struct LimbBatch {
     uint64_t *ptr;
-    long long poly_stride;
-    int n_polys;
-    int n_limbs;
-    int split;
-    int off_a;
-    int off_b;
+    long long ct_stride, poly_stride;
+    int ppc, n_polys, n_limbs;
+    int mode, split, off_a, off_b;
+    int alpha, nl, level, L, ne;
 };
 
 __device__ __forceinline__ int batch_pid(const LimbBatch &b, int i) {
     return i + (i < b.split ? b.off_a : b.off_b);
 }
 
+// limb i of poly r -> (slot t, prime pid); false if this (r, i) is skipped
+__device__ __forceinline__ bool limb_map(const LimbBatch &b, int r, int i, int &t, int &pid) {
+    if (b.mode == 0) {
+        t = i;
+        pid = batch_pid(b, i);
+        return true;
+    }
+    const int g0 = r * b.alpha;
+    const int gsz = min(b.alpha, b.nl - g0);
+    t = i < g0 ? i : i + gsz;
+    if (t >= b.ne) return false;
+    pid = t <= b.level ? t : t + (b.L - b.level);
+    return true;
+}
+
+// NTT-domain index of X -> X^g: slot k holds the evaluation at psi^(2 brv(k)+1)
+__device__ __forceinline__ uint32_t auto_index(uint32_t k, uint64_t g, int log_n) {
+    const uint64_t mask = (2ull << log_n) - 1;
+    uint32_t r = __brev(k) >> (32 - log_n);
+    uint64_t e = ((uint64_t)r * 2 + 1) * g & mask;
+    return __brev((uint32_t)((e - 1) >> 1)) >> (32 - log_n);
+}
+
+// Fused first-pass loads / last-pass stores (see ntt_pass_kernel).
+enum { LD_PLAIN = 0, LD_BCONV = 1, LD_SPREAD = 2, LD_AUTO = 3 };
+enum { ST_PLAIN = 0, ST_MODDOWN = 1, ST_RESCALE = 2, ST_SCALE = 3 };
+
+struct FuseArgs {
+    // loads: source poly (b, r) at src + b*src_ct + r*src_ps (+ slot t * N for
+    // LD_PLAIN / LD_AUTO; LD_BCONV reads n_src limbs, LD_SPREAD one limb)
+    const uint64_t *src;
+    long long src_ct, src_ps;
+    uint64_t galois;         // LD_AUTO: X -> X^galois gather
+    int n_src, src_pid0;     // LD_BCONV: z limbs under primes src_pid0 ..
+    const uint64_t *mat;     // LD_BCONV: [n_src][mat_ld] conversion constants
+    int mat_ld;
+    const uint64_t *corr;    // LD_BCONV: [prod src primes]_{q_t} for exact rounding
+    uint64_t top_q;          // LD_SPREAD: modulus of the limb being spread
+    // stores: out(b, r, t) from the transform result x and
+    //   ST_MODDOWN: add_r + (acc - x) * mulc          (add0 gathered if add_galois != 1)
+    //   ST_RESCALE: (acc * pre - x) * mulc            (pre: const pre_k or plaintext pt)
+    //   ST_SCALE  : x * mulc   (replaces N^-1 in the inverse transform)
+    uint64_t *out;
+    long long out_ct, out_ps;
+    const uint64_t *acc;
+    long long acc_ct, acc_ps;
+    const uint64_t *add0, *add1;
+    long long add_ct;
+    uint64_t add_galois;
+    int pre_mode;            // 0 none, 1 per-limb constant, 2 plaintext
+    const uint64_t *pt;      // [limbs][N]
+    LimbConsts mulc;
+    LimbConsts pre;
+};
+
 struct NttTables {
     const PrimeConst *pc;
-    const uint64_t *tw;    // [n_primes][N] psi^brv(k)
-    const uint64_t *tws;   // Shoup constants of tw
-    const uint64_t *itw;   // psi^-brv(k)
-    const uint64_t *itws;
+    const ulonglong2 *tw;   // [n_primes][N] {psi^brv(k), Shoup}: one 16-B load per twiddle
+    const ulonglong2 *itw;  // [n_primes][N] {psi^-brv(k), Shoup}
 };
 
 template <int LOG_T>
@@ -85,26 +148,178 @@ __device__ __forceinline__ int row_sidx(int sb, int c) {
     return sb * (S::T + S::T / S::E) + c + (c >> S::LE1);
 }
 
+// Register-resident radix-2 stages, unrolled at compile time through
+// template recursion so x[] never spills to local memory.
+//   tw_group(g) -> twiddle for butterfly group g of the stage;
+//   group g covers x[g*2*HALF .. g*2*HALF + 2*HALF), pairs (e, e + HALF).
+template <int E, int HALF, int NG, bool GS, typename TwFn>
+__device__ __forceinline__ void reg_stage(uint64_t (&x)[E], TwFn tw_group, uint64_t q,
+                                          uint64_t two_q) {
+#pragma unroll
+    for (int g = 0; g < NG; g++) {
+        const ulonglong2 w = tw_group(g);
+#pragma unroll
+        for (int k = 0; k < HALF; k++) {
+            if (GS)
+                gs_bfly(x[g * 2 * HALF + k], x[g * 2 * HALF + k + HALF], w.x, w.y, q, two_q);
+            else
+                ct_bfly(x[g * 2 * HALF + k], x[g * 2 * HALF + k + HALF], w.x, w.y, q, two_q);
+        }
+    }
+}
+
+// forward round 1: stages s = 0..LE1-1, half = E >> (s+1), 2^s groups,
+// twiddle (base << s) + g
+template <int E, int LE1, int S = 0>
+struct FwdR1 {
+    static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
+                                               uint64_t q, uint64_t two_q) {
+        if constexpr (S < LE1) {
+            reg_stage<E, (E >> (S + 1)), (1 << S), false>(
+                x, [&](int g) { return __ldg(tw + ((base << S) + g)); }, q, two_q);
+            FwdR1<E, LE1, S + 1>::run(x, tw, base, q, two_q);
+        }
+    }
+};
+// forward round 2: stages LE1+s, half = TPS >> (s+1), ng = E/(2 half),
+// twiddle (base << (LE1+s)) + u ng + g
+template <int E, int TPS, int LE1, int LE2, int S = 0>
+struct FwdR2 {
+    static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
+                                               int u, uint64_t q, uint64_t two_q) {
+        if constexpr (S < LE2) {
+            constexpr int half = TPS >> (S + 1), ng = E / (2 * half);
+            reg_stage<E, half, ng, false>(
+                x, [&](int g) { return __ldg(tw + ((base << (LE1 + S)) + u * ng + g)); }, q, two_q);
+            FwdR2<E, TPS, LE1, LE2, S + 1>::run(x, tw, base, u, q, two_q);
+        }
+    }
+};
+// inverse round 1: register stride half = 2^s, stage LOG_T-1-s, ng = E/(2 half),
+// twiddle (base << stage) + u ng + g
+template <int E, int LOG_T, int LE1, int S = 0>
+struct InvR1 {
+    static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
+                                               int u, uint64_t q, uint64_t two_q) {
+        if constexpr (S < LE1) {
+            constexpr int half = 1 << S, ng = E / (2 * half), stage = LOG_T - 1 - S;
+            reg_stage<E, half, ng, true>(
+                x, [&](int g) { return __ldg(tw + ((base << stage) + u * ng + g)); }, q, two_q);
+            InvR1<E, LOG_T, LE1, S + 1>::run(x, tw, base, u, q, two_q);
+        }
+    }
+};
+// inverse round 2: register stride half = (E/TPS) << s, stage LE2-1-s,
+// 2^stage groups, twiddle (base << stage) + g
+template <int E, int TPS, int LE2, int S = 0>
+struct InvR2 {
+    static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
+                                               uint64_t q, uint64_t two_q) {
+        if constexpr (S < LE2) {
+            constexpr int half = (E / TPS) << S, stage = LE2 - 1 - S;
+            reg_stage<E, half, (1 << stage), true>(
+                x, [&](int g) { return __ldg(tw + ((base << stage) + g)); }, q, two_q);
+            InvR2<E, TPS, LE2, S + 1>::run(x, tw, base, q, two_q);
+        }
+    }
+};
+
+// first-pass element load (coefficient / evaluation index n of limb slot t)
+template <int LD>
+__device__ __forceinline__ uint64_t fused_load(const FuseArgs &f, const PrimeConst *pcs, int bi,
+                                               int r, int t, const PrimeConst &P, long long n,
+                                               int log_n, const uint64_t *plain_src) {
+    if constexpr (LD == LD_PLAIN) {
+        return plain_src[n];
+    } else if constexpr (LD == LD_AUTO) {
+        return __ldg(plain_src + auto_index((uint32_t)n, f.galois, log_n));
+    } else if constexpr (LD == LD_SPREAD) {
+        const uint64_t v = f.src[bi * f.src_ct + r * f.src_ps + n];
+        // centred representative of v mod top_q, reduced mod this prime
+        return v > (f.top_q >> 1) ? sub_mod(reduce64(v, P), reduce64(f.top_q, P), P.q)
+                                  : reduce64(v, P);
+    } else {  // LD_BCONV with exact rounding
+        const uint64_t *z = f.src + bi * f.src_ct + r * f.src_ps + n;
+        const long long nn = 1ll << log_n;
+        U128 acc = {0, 0}, frac = {0, 1ull << 63};
+        for (int k = 0; k < f.n_src; k++) {
+            const uint64_t zk = z[k * nn];
+            const PrimeConst Q = pcs[f.src_pid0 + k];
+            mac(acc, zk, __ldg(f.mat + (long long)k * f.mat_ld + t));
+            U128 fr = {0, zk * Q.ratio_hi + mulhi64(zk, Q.ratio_lo)};
+            add_to(frac, fr);
+        }
+        const uint64_t v = frac.hi;  // round(sum z_k / p_k)
+        return sub_mod(reduce_u128(acc, P), mul_mod(v, __ldg(f.corr + t), P), P.q);
+    }
+}
+
+// last-pass element store; x canonical in [0, q)
+template <int ST>
+__device__ __forceinline__ void fused_store(const FuseArgs &f, int bi, int r, int t, int limb,
+                                            const PrimeConst &P, long long n, int log_n,
+                                            uint64_t x, uint64_t *plain_dst) {
+    if constexpr (ST == ST_PLAIN || ST == ST_SCALE) {
+        plain_dst[n] = x;
+    } else {
+        const long long nn = 1ll << log_n;
+        const long long off = (long long)t * nn + n;
+        uint64_t a = f.acc[bi * f.acc_ct + r * f.acc_ps + off];
+        uint64_t v;
+        if constexpr (ST == ST_RESCALE) {
+            if (f.pre_mode == 1) a = mul_shoup(a, f.pre.w[limb], f.pre.ws[limb], P.q);
+            if (f.pre_mode == 2) a = mul_mod(a, __ldg(f.pt + off), P);
+            v = mul_shoup(sub_mod(a, x, P.q), f.mulc.w[limb], f.mulc.ws[limb], P.q);
+        } else {
+            v = mul_shoup(sub_mod(a, x, P.q), f.mulc.w[limb], f.mulc.ws[limb], P.q);
+            const uint64_t *ad = r == 0 ? f.add0 : f.add1;
+            if (ad) {
+                const uint64_t *base = ad + bi * f.add_ct + (long long)t * nn;
+                const long long src = (r == 0 && f.add_galois != 1)
+                                          ? (long long)auto_index((uint32_t)n, f.add_galois, log_n)
+                                          : n;
+                v = add_mod(v, base[src], P.q);
+            }
+        }
+        f.out[bi * f.out_ct + r * f.out_ps + off] = v;
+    }
+}
+
 // One pass of the NTT.  COL = column pass (sub-transforms strided by C),
 // else row pass (contiguous chunks).  Grid: x = sub-transform groups of
-// one limb, y = limb of the batch (poly fastest, so one prime's twiddles
-// are reused across consecutive CTAs).
-template <int LOG_T, bool INV, bool COL>
-__global__ void __launch_bounds__(256) ntt_pass_kernel(LimbBatch b, NttTables tb, int log_n) {
+// one limb, y = (limb, poly) of the batch (poly fastest, so one prime's
+// twiddles are reused across consecutive CTAs).  Butterflies sharing a
+// twiddle are grouped so each distinct twiddle is one 16-byte load.
+// IO selects the fused load of the FIRST pass (forward: column pass,
+// inverse: row pass) or the fused store of the LAST pass (forward: row pass,
+// inverse: column pass); the intermediate always lives at the batch's own
+// limb storage (b.ptr).
+template <int LOG_T, bool INV, bool COL, int IO>
+__global__ void __launch_bounds__(256, 3)
+    ntt_pass_kernel(LimbBatch b, NttTables tb, int log_n, const __grid_constant__ FuseArgs f) {
     using S = NttShape<LOG_T>;
     constexpr int T = S::T, E = S::E, TPS = S::TPS, LE1 = S::LE1, LE2 = S::LE2;
+    constexpr bool FIRST = (COL != INV);  // forward column / inverse row pass
+    constexpr int LD = FIRST ? IO : LD_PLAIN;
+    constexpr int ST = FIRST ? ST_PLAIN : IO;
     extern __shared__ uint64_t smem[];
 
     const int n = 1 << log_n;
     const int CB = blockDim.x / TPS;  // sub-transforms per CTA
     const int y = blockIdx.y;
     const int limb = y / b.n_polys, poly = y - limb * b.n_polys;
-    const int pid = batch_pid(b, limb);
-    uint64_t *data = b.ptr + (long long)poly * b.poly_stride + (long long)limb * n;
+    const int bi = poly / b.ppc, r = poly - bi * b.ppc;
+    int t, pid;
+    if (!limb_map(b, r, limb, t, pid)) return;
+    uint64_t *data =
+        b.ptr + (long long)bi * b.ct_stride + (long long)r * b.poly_stride + (long long)t * n;
     const PrimeConst pc = tb.pc[pid];
     const uint64_t q = pc.q, two_q = pc.two_q;
-    const uint64_t *tw = (INV ? tb.itw : tb.tw) + (long long)pid * n;
-    const uint64_t *tws = (INV ? tb.itws : tb.tws) + (long long)pid * n;
+    const ulonglong2 *tw = (INV ? tb.itw : tb.tw) + (long long)pid * n;
+    const uint64_t *lsrc = data;  // LD_PLAIN / LD_AUTO source limb
+    if constexpr (FIRST && (LD == LD_PLAIN || LD == LD_AUTO)) {
+        if (f.src) lsrc = f.src + (long long)bi * f.src_ct + (long long)r * f.src_ps + (long long)t * n;
+    }
 
     const int tid = threadIdx.x;
     int sb, u;  // local sub-transform and thread-within-sub-transform
@@ -116,55 +331,32 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(LimbBatch b, NttTables tb
         u = tid % TPS;
     }
     const int sub = blockIdx.x * CB + sb;  // column index (COL) or chunk index
-    const int C = n >> LOG_T;               // COL: #columns ; ROW: T == C
-    // element c of this sub-transform lives at data[addr(c)]
+    const int C = n >> LOG_T;               // COL: #columns ; ROW: #rows (chunks)
     auto gaddr = [&](int c) -> long long {
         return COL ? (long long)c * C + sub : (long long)sub * T + c;
     };
-    const int R = n >> LOG_T;  // ROW pass: number of rows (chunks)
-    const int base = COL ? 1 : (R + sub);
-    auto tw_at = [&](int stage, int c, uint64_t &w, uint64_t &ws) {
-        int idx = (base << stage) + (c >> (LOG_T - stage));
-        w = __ldg(tw + idx);
-        ws = __ldg(tws + idx);
-    };
+    const int base = COL ? 1 : (C + sub);
     auto sidx = [&](int c) -> int {
         return COL ? c * CB + sb : row_sidx<LOG_T>(sb, c);
+    };
+    auto load = [&](int c) -> uint64_t {
+        if constexpr (FIRST) return fused_load<LD>(f, tb.pc, bi, r, t, pc, gaddr(c), log_n, lsrc);
+        else return data[gaddr(c)];
     };
 
     uint64_t x[E];
     if (!INV) {
         // ---- round 1: strided ownership c = u + TPS e, strides T/2 .. TPS
 #pragma unroll
-        for (int e = 0; e < E; e++) x[e] = data[gaddr(u + TPS * e)];
-#pragma unroll
-        for (int s = 0; s < LE1; s++) {
-            const int half = E >> (s + 1);
-#pragma unroll
-            for (int e = 0; e < E; e++) {
-                if (e & half) continue;
-                uint64_t w, ws;
-                tw_at(s, u + TPS * e, w, ws);
-                ct_bfly(x[e], x[e + half], w, ws, q, two_q);
-            }
-        }
+        for (int e = 0; e < E; e++) x[e] = load(u + TPS * e);
+        FwdR1<E, LE1>::run(x, tw, base, q, two_q);
 #pragma unroll
         for (int e = 0; e < E; e++) smem[sidx(u + TPS * e)] = x[e];
         __syncthreads();
         // ---- round 2: contiguous ownership c = u E + e, strides TPS/2 .. 1
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = smem[sidx(u * E + e)];
-#pragma unroll
-        for (int s = 0; s < LE2; s++) {
-            const int half = TPS >> (s + 1);
-#pragma unroll
-            for (int e = 0; e < E; e++) {
-                if (e & half) continue;
-                uint64_t w, ws;
-                tw_at(LE1 + s, u * E + e, w, ws);
-                ct_bfly(x[e], x[e + half], w, ws, q, two_q);
-            }
-        }
+        FwdR2<E, TPS, LE1, LE2>::run(x, tw, base, u, q, two_q);
         if (COL) {
 #pragma unroll
             for (int e = 0; e < E; e++) data[gaddr(u * E + e)] = x[e];  // [0,4q)
@@ -180,7 +372,10 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(LimbBatch b, NttTables tb
             }
             __syncthreads();
 #pragma unroll
-            for (int e = 0; e < E; e++) data[gaddr(u + TPS * e)] = smem[sidx(u + TPS * e)];
+            for (int e = 0; e < E; e++) {
+                const int c = u + TPS * e;
+                fused_store<ST>(f, bi, r, t, limb, pc, gaddr(c), log_n, smem[sidx(c)], data);
+            }
         }
     } else {
         // ---- round 1: contiguous ownership, strides 1 .. E/2
@@ -189,23 +384,12 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(LimbBatch b, NttTables tb
             for (int e = 0; e < E; e++) x[e] = data[gaddr(u * E + e)];
         } else {
 #pragma unroll
-            for (int e = 0; e < E; e++) smem[sidx(u + TPS * e)] = data[gaddr(u + TPS * e)];
+            for (int e = 0; e < E; e++) smem[sidx(u + TPS * e)] = load(u + TPS * e);
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < E; e++) x[e] = smem[sidx(u * E + e)];
         }
-#pragma unroll
-        for (int s = 0; s < LE1; s++) {
-            const int half = 1 << s;  // stride in elements == in registers
-            const int stage = LOG_T - 1 - s;
-#pragma unroll
-            for (int e = 0; e < E; e++) {
-                if (e & half) continue;
-                uint64_t w, ws;
-                tw_at(stage, u * E + e, w, ws);
-                gs_bfly(x[e], x[e + half], w, ws, q, two_q);
-            }
-        }
+        InvR1<E, LOG_T, LE1>::run(x, tw, base, u, q, two_q);
         if (!COL) __syncthreads();
 #pragma unroll
         for (int e = 0; e < E; e++) smem[sidx(u * E + e)] = x[e];
@@ -213,23 +397,16 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(LimbBatch b, NttTables tb
         // ---- round 2: strided ownership c = u + TPS e, strides E .. T/2
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = smem[sidx(u + TPS * e)];
-#pragma unroll
-        for (int s = 0; s < LE2; s++) {
-            const int half = (E / TPS) << s;  // register stride
-            const int stage = LE2 - 1 - s;
-#pragma unroll
-            for (int e = 0; e < E; e++) {
-                if (e & half) continue;
-                uint64_t w, ws;
-                tw_at(stage, u + TPS * e, w, ws);
-                gs_bfly(x[e], x[e + half], w, ws, q, two_q);
-            }
-        }
+        InvR2<E, TPS, LE2>::run(x, tw, base, q, two_q);
         if (COL) {
-            // last pass of the inverse: * N^-1, canonical
+            // last pass of the inverse: * N^-1 (or the fused per-limb scale), canonical
+            uint64_t m = pc.ninv, ms = pc.ninv_shoup;
+            if constexpr (ST == ST_SCALE) {
+                m = f.mulc.w[limb];
+                ms = f.mulc.ws[limb];
+            }
 #pragma unroll
-            for (int e = 0; e < E; e++)
-                data[gaddr(u + TPS * e)] = mul_shoup(x[e], pc.ninv, pc.ninv_shoup, q);
+            for (int e = 0; e < E; e++) data[gaddr(u + TPS * e)] = mul_shoup(x[e], m, ms, q);
         } else {
 #pragma unroll
             for (int e = 0; e < E; e++) data[gaddr(u + TPS * e)] = x[e];  // [0,2q)

@@ -190,3 +190,65 @@ def test_sampling_and_keygen(pair):
     call(gb, "srk_keygen", ptr(gb._sk_ntt), ptr(tsg), ptr(te),
          p.seed, 9, ptr(key), gb.workspace(), gb.stream())
     assert np.array_equal(host(gb, key), orc.keygen(sk, sg, e, p.seed, 9))
+
+
+def _key(p, seed):
+    rng = np.random.default_rng(seed)
+    n_all = len(p.all_primes)
+    key = np.empty((p.dnum, 2, n_all, p.ring_degree), dtype=np.uint64)
+    for i, q in enumerate(p.all_primes):
+        key[:, :, i, :] = rng.integers(0, q, (p.dnum, 2, p.ring_degree), dtype=np.uint64)
+    return key
+
+
+def test_batched_ops_match_oracle(pair):
+    """Batched C-ABI forms (chunked internally by 8) == per-ciphertext oracle."""
+    import ctypes
+
+    p, gb, orc = pair
+    B = 10 if p.log_n < 16 else 3
+    lvl = p.max_level
+    n = p.ring_degree
+    ps = (lvl + 1) * n
+    a = rand_limbs(p, (B, 2), lvl, 40)
+    b = rand_limbs(p, (B, 2), lvl, 41)
+    key = _key(p, 42)
+    ta, tb, tk = dev(gb, a), dev(gb, b), dev(gb, key)
+    g = pow(5, 5, 2 * n)
+    out = gb.empty_ct(lvl, polys=2 * B)
+    call(gb, "srk_rotate_batch", ptr(ta), 2 * ps, ptr(tk), ptr(out), 2 * ps, B, lvl, g,
+         gb.workspace(), gb.stream())
+    got = host(gb, out).reshape(B, 2, lvl + 1, n)
+    for i in range(B):
+        assert np.array_equal(got[i], orc.rotate_raw(a[i], key, g, lvl)), i
+    # hoisted: two rotations per ciphertext share the base extension and equal single rotations
+    g2 = pow(5, 9, 2 * n)
+    o1, o2 = gb.empty_ct(lvl, polys=2 * B), gb.empty_ct(lvl, polys=2 * B)
+    keys = (ctypes.c_void_p * 2)(ptr(tk), ptr(tk))
+    gal = (ctypes.c_uint64 * 2)(g, g2)
+    outs = (ctypes.c_void_p * 2)(ptr(o1), ptr(o2))
+    call(gb, "srk_rotate_hoisted", ptr(ta), 2 * ps, B, 2, keys, gal, outs, 2 * ps, lvl,
+         gb.workspace(), gb.stream())
+    h1 = host(gb, o1).reshape(B, 2, lvl + 1, n)
+    h2 = host(gb, o2).reshape(B, 2, lvl + 1, n)
+    assert np.array_equal(h1, got)
+    for i in range(B):
+        assert np.array_equal(h2[i], orc.rotate_raw(a[i], key, g2, lvl)), i
+    # relinearised products, with and without the rescale
+    for resc in (0, 1):
+        ol = lvl - resc
+        out = gb.empty_ct(ol, polys=2 * B)
+        call(gb, "srk_mul_relin_batch", ptr(ta), ptr(tb), 2 * ps, ptr(tk), ptr(out), 2 * (ol + 1) * n, B,
+             lvl, resc, gb.workspace(), gb.stream())
+        got = host(gb, out).reshape(B, 2, ol + 1, n)
+        for i in range(B):
+            want = orc.mul_relin(a[i], b[i], key, lvl)
+            if resc:
+                want = orc.rescale(want, lvl)
+            assert np.array_equal(got[i], want), (resc, i)
+    out = gb.empty_ct(lvl - 1, polys=2 * B)
+    call(gb, "srk_rescale_batch", ptr(ta), 2 * ps, ptr(out), 2 * lvl * n, B, lvl, gb.workspace(),
+         gb.stream())
+    got = host(gb, out).reshape(B, 2, lvl, n)
+    for i in range(B):
+        assert np.array_equal(got[i], orc.rescale(a[i], lvl)), i

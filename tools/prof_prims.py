@@ -14,7 +14,7 @@ for _ in range(2):
         step.ntt(step.x, False)
         step.ntt(step.x, True)
     elif what == "keyswitch":
-        step.keyswitch_batch()
+        step.relin_batch()
     elif what == "step":
         step.step()
 torch.cuda.synchronize()
