@@ -165,13 +165,13 @@ static int build_plan(srk_ctx *c, BconvPlan &pl, const std::vector<int> &src_pid
     TRY(dupload(c, &pl.hinv, hv));
     TRY(dupload(c, &pl.dst_slot, dst_slots));
     TRY(dupload(c, &pl.dst_pid, dst_pids));
-    if (exact) {
-        std::vector<uint64_t> corr(nd);
+    if (exact) {  // table [v][t] = v * [prod src]_{q_t}, v = 0..n_src
+        std::vector<uint64_t> corr((size_t)(ns + 1) * nd);
         for (int t = 0; t < nd; t++) {
             const uint64_t p = c->primes[dst_pids[t]];
             uint64_t v = 1;
             for (int m = 0; m < ns; m++) v = hmul(v, c->primes[src_pids[m]] % p, p);
-            corr[t] = v;
+            for (int k = 0; k <= ns; k++) corr[(size_t)k * nd + t] = hmul((uint64_t)k, v, p);
         }
         TRY(dupload(c, &pl.dst_corr, corr));
     }
@@ -339,7 +339,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
 // words of scratch (x N) each op needs for a chunk of B ciphertexts at level l
 static size_t ks_limbs(const srk_ctx *c, int level, int B) {
     const size_t nl = level + 1, ne = nl + c->n_p, beta = (nl + c->alpha - 1) / c->alpha;
-    return (size_t)B * (nl + beta * ne + 2 * ne + 2 * nl);
+    return (size_t)B * (nl + beta * ne + 2 * ne + 2 * nl + 1);  // + rounding bytes
 }
 static size_t rescale_limbs(int level, int B) { return (size_t)B * (2 + 2 * (size_t)level); }
 static size_t relin_limbs(const srk_ctx *c, int level, int B) {
@@ -745,6 +745,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
     uint64_t *ext = dc + (long long)B * nl * n;        // [B][beta][ne]
     uint64_t *acc = ext + (long long)B * beta * ne * n;  // [B][2][ne]
     uint64_t *conv = acc + (long long)B * 2 * ne * n;    // [B][2][nl]
+    uint8_t *vround = (uint8_t *)(conv + (long long)B * 2 * nl * n);  // [B][2][N] bytes
     // 1. INTT with the ModUp scale folded in
     {
         FuseArgs f = no_fuse();
@@ -825,7 +826,12 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             b.off_b = c->n_q;
             TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, s));
         }
-        // 6. ModDown: NTT(conversion) with the combine in its store
+        // 6. ModDown: rounding term once per coefficient, then NTT(conversion)
+        //    with the combine in its store
+        k_moddown_v<<<grid_for(2ll * B * n), 256, 0, s>>>(acc + (long long)nl * n, 2ll * ne * n,
+                                                          (long long)ne * n, K, c->n_q, vround,
+                                                          c->d_pc, c->log_n, B);
+        LAUNCHED();
         {
             FuseArgs f = no_fuse();
             f.src = acc + (long long)nl * n;
@@ -836,6 +842,8 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             f.mat = pd.mat;
             f.mat_ld = pd.n_dst;
             f.corr = pd.dst_corr;
+            f.corr_ld = pd.n_dst;
+            f.vround = vround;
             f.out = ko.out;
             f.out_ct = ko.out_ct;
             f.out_ps = ko.out_ps;

@@ -152,7 +152,7 @@ __global__ void k_automorph(const uint64_t *__restrict__ a, uint64_t *__restrict
 // ---------------------------------------------------------------------
 // hybrid key switching, batched over B ciphertexts
 // ---------------------------------------------------------------------
-#define SRK_MAX_DIGITS 16
+#define SRK_MAX_DIGITS 64
 
 // ModUp base conversion for every digit of every ciphertext:
 //   ext[b][j][slot_t] = sum_{i in G_j} y_i * mat_j[i][t]  mod p_t
@@ -203,7 +203,10 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
 // key-switch inner product (optionally composed with X -> X^galois):
 //   acc[b][r][t][n] = sum_j E_j[t][pi(n)] * key[j][r][pid(t)][n]
 // E_j[t] = d[b][t] for t in digit j's own limbs G_j (NTT form input), else
-// ext[b][j][t].  pi = identity when galois == 1.
+// ext[b][j][t].  pi = identity when galois == 1.  Each thread owns one
+// (t, n) for every ciphertext of the batch, so each key word is read once
+// per batch (the key is the dominant HBM stream of a key switch).
+#define SRK_KS_MAXB 8
 struct KsInnerArgs {
     const uint64_t *d;
     long long d_ct;
@@ -219,29 +222,65 @@ struct KsInnerArgs {
 __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInnerArgs a,
                                                   const PrimeConst *__restrict__ pc, int log_n) {
     const long long n = 1ll << log_n;
-    const long long per_ct = (long long)a.ne * n;
-    const long long total = per_ct * a.batch;
+    const long long total = (long long)a.ne * n;
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
-        const int b = (int)(x / per_ct);
-        const long long xi = x - b * per_ct;
-        const int t = (int)(xi >> log_n);
-        const long long off = xi & (n - 1);
+        const int t = (int)(x >> log_n);
+        const long long off = x & (n - 1);
         const long long src = a.galois == 1 ? off : (long long)auto_index((uint32_t)off, a.galois, log_n);
         const int pid = t <= a.level ? t : t + (a.L - a.level);
         const int jt = t < a.nl ? t / a.alpha : -1;
-        U128 a0 = {0, 0}, a1 = {0, 0};
+        U128 a0[SRK_KS_MAXB], a1[SRK_KS_MAXB];
+#pragma unroll
+        for (int b = 0; b < SRK_KS_MAXB; b++) a0[b] = a1[b] = U128{0, 0};
         for (int j = 0; j < a.beta; j++) {
-            const uint64_t e = j == jt ? a.d[b * a.d_ct + (long long)t * n + src]
-                                       : a.ext[b * a.ext_ct + j * a.ext_dig + (long long)t * n + src];
             const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + pid) * n + off;
-            mac(a0, e, __ldg(kj));
-            mac(a1, e, __ldg(kj + (long long)a.n_primes * n));
+            const uint64_t k0 = __ldg(kj), k1 = __ldg(kj + (long long)a.n_primes * n);
+            const uint64_t *e = j == jt ? a.d + (long long)t * n + src
+                                        : a.ext + j * a.ext_dig + (long long)t * n + src;
+            const long long es = j == jt ? a.d_ct : a.ext_ct;
+#pragma unroll
+            for (int b = 0; b < SRK_KS_MAXB; b++) {
+                if (b < a.batch) {
+                    const uint64_t v = e[b * es];
+                    mac(a0[b], v, k0);
+                    mac(a1[b], v, k1);
+                }
+            }
         }
         const PrimeConst P = pc[pid];
-        uint64_t *o = a.acc + b * a.acc_ct + (long long)t * n + off;
-        o[0] = reduce_u128(a0, P);
-        o[per_ct] = reduce_u128(a1, P);
+#pragma unroll
+        for (int b = 0; b < SRK_KS_MAXB; b++) {
+            if (b < a.batch) {
+                uint64_t *o = a.acc + b * a.acc_ct + (long long)t * n + off;
+                o[0] = reduce_u128(a0[b], P);
+                o[total] = reduce_u128(a1[b], P);
+            }
+        }
+    }
+}
+
+// exact ModDown rounding term per coefficient: v = round(sum_k z_k / p_k)
+// (64.64 fixed point, f_k = z_k R1 + hi(z_k R0), R = floor(2^128 / p_k));
+// z: B*2 polys (ct stride z_ct, poly stride z_ps) of K limbs; v: [B*2][N]
+__global__ void k_moddown_v(const uint64_t *__restrict__ z, long long z_ct, long long z_ps, int K,
+                            int pid0, uint8_t *__restrict__ v, const PrimeConst *__restrict__ pc,
+                            int log_n, int batch) {
+    const long long n = 1ll << log_n;
+    const long long total = 2ll * batch * n;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long p = x >> log_n;
+        const long long off = x & (n - 1);
+        const uint64_t *zp = z + (p >> 1) * z_ct + (p & 1) * z_ps + off;
+        U128 frac = {0, 1ull << 63};
+        for (int k = 0; k < K; k++) {
+            const uint64_t zk = zp[k * n];
+            const PrimeConst Q = pc[pid0 + k];
+            U128 fr = {0, zk * Q.ratio_hi + mulhi64(zk, Q.ratio_lo)};
+            add_to(frac, fr);
+        }
+        v[x] = (uint8_t)frac.hi;
     }
 }
 

@@ -87,7 +87,9 @@ struct FuseArgs {
     int n_src, src_pid0;     // LD_BCONV: z limbs under primes src_pid0 ..
     const uint64_t *mat;     // LD_BCONV: [n_src][mat_ld] conversion constants
     int mat_ld;
-    const uint64_t *corr;    // LD_BCONV: [prod src primes]_{q_t} for exact rounding
+    const uint64_t *corr;    // LD_BCONV: [v * prod src primes]_{q_t}, table [v][corr_ld]
+    int corr_ld;
+    const uint8_t *vround;   // LD_BCONV: v = round(sum z_k / p_k) per (b, r, n), k_moddown_v
     uint64_t top_q;          // LD_SPREAD: modulus of the limb being spread
     // stores: out(b, r, t) from the transform result x and
     //   ST_MODDOWN: add_r + (acc - x) * mulc          (add0 gathered if add_galois != 1)
@@ -148,78 +150,111 @@ __device__ __forceinline__ int row_sidx(int sb, int c) {
     return sb * (S::T + S::T / S::E) + c + (c >> S::LE1);
 }
 
+// Reduction-free butterflies for primes below 2^46 (all scaling primes):
+// forward outputs grow by at most 2q per stage (T in [0, 2q)), so 16 stages
+// stay below 34q; inverse sums at most double per stage, and the difference
+// is offset by M = q << k (a multiple of q above any operand at step k), so
+// 16 steps stay below 2^16 q < 2^62.  Only the final pass reduces.
+#define SRK_SMALL_Q (1ull << 46)
+
+__device__ __forceinline__ void ct_bfly_small(uint64_t &x, uint64_t &y, uint64_t w, uint64_t ws,
+                                              uint64_t q, uint64_t two_q) {
+    uint64_t T = mul_shoup_lazy(y, w, ws, q);
+    y = x - T + two_q;
+    x = x + T;
+}
+
+__device__ __forceinline__ void gs_bfly_small(uint64_t &x, uint64_t &y, uint64_t w, uint64_t ws,
+                                              uint64_t q, uint64_t m) {
+    uint64_t D = x - y + m;
+    x = x + y;
+    y = mul_shoup_lazy(D, w, ws, q);
+}
+
 // Register-resident radix-2 stages, unrolled at compile time through
 // template recursion so x[] never spills to local memory.
 //   tw_group(g) -> twiddle for butterfly group g of the stage;
 //   group g covers x[g*2*HALF .. g*2*HALF + 2*HALF), pairs (e, e + HALF).
-template <int E, int HALF, int NG, bool GS, typename TwFn>
+// SMALL: reduction-free variants; m = inverse difference offset (q << step)
+template <int E, int HALF, int NG, bool GS, bool SMALL, typename TwFn>
 __device__ __forceinline__ void reg_stage(uint64_t (&x)[E], TwFn tw_group, uint64_t q,
-                                          uint64_t two_q) {
+                                          uint64_t two_q, uint64_t m) {
 #pragma unroll
     for (int g = 0; g < NG; g++) {
         const ulonglong2 w = tw_group(g);
 #pragma unroll
         for (int k = 0; k < HALF; k++) {
-            if (GS)
-                gs_bfly(x[g * 2 * HALF + k], x[g * 2 * HALF + k + HALF], w.x, w.y, q, two_q);
-            else
-                ct_bfly(x[g * 2 * HALF + k], x[g * 2 * HALF + k + HALF], w.x, w.y, q, two_q);
+            uint64_t &a = x[g * 2 * HALF + k];
+            uint64_t &b = x[g * 2 * HALF + k + HALF];
+            if (GS) {
+                if (SMALL)
+                    gs_bfly_small(a, b, w.x, w.y, q, m);
+                else
+                    gs_bfly(a, b, w.x, w.y, q, two_q);
+            } else {
+                if (SMALL)
+                    ct_bfly_small(a, b, w.x, w.y, q, two_q);
+                else
+                    ct_bfly(a, b, w.x, w.y, q, two_q);
+            }
         }
     }
 }
 
 // forward round 1: stages s = 0..LE1-1, half = E >> (s+1), 2^s groups,
 // twiddle (base << s) + g
-template <int E, int LE1, int S = 0>
+template <int E, int LE1, bool SM, int S = 0>
 struct FwdR1 {
     static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
                                                uint64_t q, uint64_t two_q) {
         if constexpr (S < LE1) {
-            reg_stage<E, (E >> (S + 1)), (1 << S), false>(
-                x, [&](int g) { return __ldg(tw + ((base << S) + g)); }, q, two_q);
-            FwdR1<E, LE1, S + 1>::run(x, tw, base, q, two_q);
+            reg_stage<E, (E >> (S + 1)), (1 << S), false, SM>(
+                x, [&](int g) { return __ldg(tw + ((base << S) + g)); }, q, two_q, 0);
+            FwdR1<E, LE1, SM, S + 1>::run(x, tw, base, q, two_q);
         }
     }
 };
 // forward round 2: stages LE1+s, half = TPS >> (s+1), ng = E/(2 half),
 // twiddle (base << (LE1+s)) + u ng + g
-template <int E, int TPS, int LE1, int LE2, int S = 0>
+template <int E, int TPS, int LE1, int LE2, bool SM, int S = 0>
 struct FwdR2 {
     static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
                                                int u, uint64_t q, uint64_t two_q) {
         if constexpr (S < LE2) {
             constexpr int half = TPS >> (S + 1), ng = E / (2 * half);
-            reg_stage<E, half, ng, false>(
-                x, [&](int g) { return __ldg(tw + ((base << (LE1 + S)) + u * ng + g)); }, q, two_q);
-            FwdR2<E, TPS, LE1, LE2, S + 1>::run(x, tw, base, u, q, two_q);
+            reg_stage<E, half, ng, false, SM>(
+                x, [&](int g) { return __ldg(tw + ((base << (LE1 + S)) + u * ng + g)); }, q, two_q, 0);
+            FwdR2<E, TPS, LE1, LE2, SM, S + 1>::run(x, tw, base, u, q, two_q);
         }
     }
 };
 // inverse round 1: register stride half = 2^s, stage LOG_T-1-s, ng = E/(2 half),
 // twiddle (base << stage) + u ng + g
-template <int E, int LOG_T, int LE1, int S = 0>
+template <int E, int LOG_T, int LE1, bool SM, int S = 0>
 struct InvR1 {
     static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
-                                               int u, uint64_t q, uint64_t two_q) {
+                                               int u, uint64_t q, uint64_t two_q, int k0) {
         if constexpr (S < LE1) {
             constexpr int half = 1 << S, ng = E / (2 * half), stage = LOG_T - 1 - S;
-            reg_stage<E, half, ng, true>(
-                x, [&](int g) { return __ldg(tw + ((base << stage) + u * ng + g)); }, q, two_q);
-            InvR1<E, LOG_T, LE1, S + 1>::run(x, tw, base, u, q, two_q);
+            reg_stage<E, half, ng, true, SM>(
+                x, [&](int g) { return __ldg(tw + ((base << stage) + u * ng + g)); }, q, two_q,
+                q << (k0 + S));
+            InvR1<E, LOG_T, LE1, SM, S + 1>::run(x, tw, base, u, q, two_q, k0);
         }
     }
 };
 // inverse round 2: register stride half = (E/TPS) << s, stage LE2-1-s,
 // 2^stage groups, twiddle (base << stage) + g
-template <int E, int TPS, int LE2, int S = 0>
+template <int E, int TPS, int LE2, bool SM, int S = 0>
 struct InvR2 {
     static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
-                                               uint64_t q, uint64_t two_q) {
+                                               uint64_t q, uint64_t two_q, int k0) {
         if constexpr (S < LE2) {
             constexpr int half = (E / TPS) << S, stage = LE2 - 1 - S;
-            reg_stage<E, half, (1 << stage), true>(
-                x, [&](int g) { return __ldg(tw + ((base << stage) + g)); }, q, two_q);
-            InvR2<E, TPS, LE2, S + 1>::run(x, tw, base, q, two_q);
+            reg_stage<E, half, (1 << stage), true, SM>(
+                x, [&](int g) { return __ldg(tw + ((base << stage) + g)); }, q, two_q,
+                q << (k0 + S));
+            InvR2<E, TPS, LE2, SM, S + 1>::run(x, tw, base, q, two_q, k0);
         }
     }
 };
@@ -238,19 +273,13 @@ __device__ __forceinline__ uint64_t fused_load(const FuseArgs &f, const PrimeCon
         // centred representative of v mod top_q, reduced mod this prime
         return v > (f.top_q >> 1) ? sub_mod(reduce64(v, P), reduce64(f.top_q, P), P.q)
                                   : reduce64(v, P);
-    } else {  // LD_BCONV with exact rounding
+    } else {  // LD_BCONV with exact rounding (v precomputed once per coefficient)
         const uint64_t *z = f.src + bi * f.src_ct + r * f.src_ps + n;
         const long long nn = 1ll << log_n;
-        U128 acc = {0, 0}, frac = {0, 1ull << 63};
-        for (int k = 0; k < f.n_src; k++) {
-            const uint64_t zk = z[k * nn];
-            const PrimeConst Q = pcs[f.src_pid0 + k];
-            mac(acc, zk, __ldg(f.mat + (long long)k * f.mat_ld + t));
-            U128 fr = {0, zk * Q.ratio_hi + mulhi64(zk, Q.ratio_lo)};
-            add_to(frac, fr);
-        }
-        const uint64_t v = frac.hi;  // round(sum z_k / p_k)
-        return sub_mod(reduce_u128(acc, P), mul_mod(v, __ldg(f.corr + t), P), P.q);
+        U128 acc = {0, 0};
+        for (int k = 0; k < f.n_src; k++) mac(acc, z[k * nn], __ldg(f.mat + (long long)k * f.mat_ld + t));
+        const int v = f.vround[((long long)bi * 2 + r) * nn + n];
+        return sub_mod(reduce_u128(acc, P), __ldg(f.corr + v * f.corr_ld + t), P.q);
     }
 }
 
@@ -315,6 +344,7 @@ __global__ void __launch_bounds__(256, 3)
         b.ptr + (long long)bi * b.ct_stride + (long long)r * b.poly_stride + (long long)t * n;
     const PrimeConst pc = tb.pc[pid];
     const uint64_t q = pc.q, two_q = pc.two_q;
+    const bool small = q < SRK_SMALL_Q;  // uniform per CTA (one limb per CTA)
     const ulonglong2 *tw = (INV ? tb.itw : tb.tw) + (long long)pid * n;
     const uint64_t *lsrc = data;  // LD_PLAIN / LD_AUTO source limb
     if constexpr (FIRST && (LD == LD_PLAIN || LD == LD_AUTO)) {
@@ -349,14 +379,20 @@ __global__ void __launch_bounds__(256, 3)
         // ---- round 1: strided ownership c = u + TPS e, strides T/2 .. TPS
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = load(u + TPS * e);
-        FwdR1<E, LE1>::run(x, tw, base, q, two_q);
+        if (small)
+            FwdR1<E, LE1, true>::run(x, tw, base, q, two_q);
+        else
+            FwdR1<E, LE1, false>::run(x, tw, base, q, two_q);
 #pragma unroll
         for (int e = 0; e < E; e++) smem[sidx(u + TPS * e)] = x[e];
         __syncthreads();
         // ---- round 2: contiguous ownership c = u E + e, strides TPS/2 .. 1
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = smem[sidx(u * E + e)];
-        FwdR2<E, TPS, LE1, LE2>::run(x, tw, base, u, q, two_q);
+        if (small)
+            FwdR2<E, TPS, LE1, LE2, true>::run(x, tw, base, u, q, two_q);
+        else
+            FwdR2<E, TPS, LE1, LE2, false>::run(x, tw, base, u, q, two_q);
         if (COL) {
 #pragma unroll
             for (int e = 0; e < E; e++) data[gaddr(u * E + e)] = x[e];  // [0,4q)
@@ -366,7 +402,11 @@ __global__ void __launch_bounds__(256, 3)
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 uint64_t v = x[e];
-                v = v >= two_q ? v - two_q : v;
+                if (small) {  // v < 34 q: one Barrett step (floor(2^64/q)) then one subtraction
+                    v -= mulhi64(v, pc.ratio_hi) * q;
+                } else {
+                    v = v >= two_q ? v - two_q : v;
+                }
                 v = v >= q ? v - q : v;
                 smem[sidx(u * E + e)] = v;
             }
@@ -389,7 +429,12 @@ __global__ void __launch_bounds__(256, 3)
 #pragma unroll
             for (int e = 0; e < E; e++) x[e] = smem[sidx(u * E + e)];
         }
-        InvR1<E, LOG_T, LE1>::run(x, tw, base, u, q, two_q);
+        // step numbers of the inverse: row pass 0.., column pass log_n - LOG_T ..
+        const int k0 = COL ? log_n - LOG_T : 0;
+        if (small)
+            InvR1<E, LOG_T, LE1, true>::run(x, tw, base, u, q, two_q, k0);
+        else
+            InvR1<E, LOG_T, LE1, false>::run(x, tw, base, u, q, two_q, k0);
         if (!COL) __syncthreads();
 #pragma unroll
         for (int e = 0; e < E; e++) smem[sidx(u * E + e)] = x[e];
@@ -397,7 +442,10 @@ __global__ void __launch_bounds__(256, 3)
         // ---- round 2: strided ownership c = u + TPS e, strides E .. T/2
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = smem[sidx(u + TPS * e)];
-        InvR2<E, TPS, LE2>::run(x, tw, base, q, two_q);
+        if (small)
+            InvR2<E, TPS, LE2, true>::run(x, tw, base, q, two_q, k0 + LE1);
+        else
+            InvR2<E, TPS, LE2, false>::run(x, tw, base, q, two_q, k0 + LE1);
         if (COL) {
             // last pass of the inverse: * N^-1 (or the fused per-limb scale), canonical
             uint64_t m = pc.ninv, ms = pc.ninv_shoup;
