@@ -135,12 +135,24 @@ int srk_square(srk_ctx *ctx, const uint64_t *s, uint64_t *out, int n_limbs, void
 /* switching key sfrom -> s; e: int64[dnum][N] device */
 int srk_keygen(srk_ctx *ctx, const uint64_t *s_ntt, const uint64_t *sfrom_ntt, const int64_t *e,
                uint64_t seed, uint64_t key_id, uint64_t *key, void *ws, void *stream);
+/* Rotation keys are consumed in "rotation layout": the switching key
+ * sigma_g(s) -> s with every limb permuted by sigma_g^-1, so the key-switch
+ * inner product streams coalesced and sigma_g is applied while ModDown reads
+ * the accumulator.  srk_keygen_galois produces that layout directly;
+ * srk_permute_key converts a standard-layout key in place (tmp: 2*n_primes
+ * limbs of device scratch).  srk_rotate* expect rotation-layout keys. */
+int srk_keygen_galois(srk_ctx *ctx, const uint64_t *s_ntt, const int64_t *e, uint64_t seed,
+                      uint64_t key_id, uint64_t galois, uint64_t *key, void *ws, void *stream);
+int srk_permute_key(srk_ctx *ctx, uint64_t *key, uint64_t galois, void *tmp, void *stream);
 /* m, e: int64[N] device; out: uint64[2][level+1][N] */
 int srk_encrypt(srk_ctx *ctx, const int64_t *m, const uint64_t *s_ntt, const int64_t *e,
                 uint64_t seed, uint64_t seq, uint64_t *out, int level, void *ws, void *stream);
 /* m_out: int64[N] device, centred coefficients of c0 + c1 s mod q_0 */
 int srk_decrypt_limb0(srk_ctx *ctx, const uint64_t *ct, const uint64_t *s_ntt, int64_t *m_out,
                       int level, void *ws, void *stream);
+/* multi-GPU fix-up after an int64 all-reduce of n_polys polys of level+1
+ * limbs (values < 2^63): reduce every limb mod its prime in place */
+int srk_reduce_mod(srk_ctx *ctx, uint64_t *data, int n_polys, int level, void *stream);
 /* pt_out: uint64[level+1][N] = NTT(coeffs mod q_i) */
 int srk_encode_plain(srk_ctx *ctx, const int64_t *coeffs, uint64_t *pt_out, int level,
                      void *stream);

@@ -262,6 +262,24 @@ class OracleBackend:
     def rotate(self, a, galois, level):
         return self.o.rotate_raw(a, self.galois_key(galois), galois, level)
 
+    # collectives (paper_2412_15126_b200/shard.py) over gloo
+    def as_tensor(self, data):
+        import torch
+
+        return torch.from_numpy(np.ascontiguousarray(data).view(np.int64).copy())
+
+    def zeros_tensor(self, level):
+        import torch
+
+        return torch.zeros((2, level + 1, self.n), dtype=torch.int64)
+
+    def from_tensor(self, t, level):
+        return t.numpy().view(np.uint64).copy()
+
+    def reduce_mod_tensor(self, t, level):
+        q = np.array(self.params.q_primes[: level + 1], dtype=np.uint64)[None, :, None]
+        return t.numpy().view(np.uint64) % q
+
 
 def oracle_engine(params):
     """The product's engine bookkeeping over the CPU oracle backend (tests only)."""

@@ -57,9 +57,13 @@ EXPORTS = {
     "srk_small_to_ntt": [c_void_p, _u64p, _u64p, c_int, c_int, c_void_p],
     "srk_square": [c_void_p, _u64p, _u64p, c_int, c_void_p],
     "srk_keygen": [c_void_p, _u64p, _u64p, _u64p, c_uint64, c_uint64, _u64p, c_void_p, c_void_p],
+    "srk_keygen_galois": [c_void_p, _u64p, _u64p, c_uint64, c_uint64, c_uint64, _u64p, c_void_p,
+                          c_void_p],
+    "srk_permute_key": [c_void_p, _u64p, c_uint64, c_void_p, c_void_p],
     "srk_encrypt": [c_void_p, _u64p, _u64p, _u64p, c_uint64, c_uint64, _u64p, c_int, c_void_p,
                     c_void_p],
     "srk_decrypt_limb0": [c_void_p, _u64p, _u64p, _u64p, c_int, c_void_p, c_void_p],
+    "srk_reduce_mod": [c_void_p, _u64p, c_int, c_int, c_void_p],
     "srk_encode_plain": [c_void_p, _u64p, _u64p, c_int, c_void_p],
 }
 _RESTYPES = {"srk_last_error": ctypes.c_char_p, "srk_workspace_bytes": c_size_t,

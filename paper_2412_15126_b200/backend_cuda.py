@@ -144,11 +144,14 @@ class CudaBackend:
         with self._key_lock:
             k = self._keys.get(kid)
             if k is None:
-                np_all = len(self.params.all_primes)
-                sg = torch.empty_like(self._sk_ntt)
-                self._call("srk_automorph", _ptr(self._sk_ntt), _ptr(sg), np_all, galois,
-                           self.stream())
-                k = self._keygen(kid, sg)
+                # rotation layout: sigma_g(s) -> s switching key, limbs permuted by sigma_g^-1
+                p = self.params
+                np_all = len(p.all_primes)
+                e = sample_error(p, (2, kid), p.dnum)
+                e_dev = torch.from_numpy(e).to(self.device)
+                k = torch.empty((p.dnum, 2, np_all, self.n), dtype=torch.int64, device=self.device)
+                self._call("srk_keygen_galois", _ptr(self._sk_ntt), _ptr(e_dev), p.seed, kid, galois,
+                           _ptr(k), self.workspace(), self.stream())
                 self._keys[kid] = k
             return k
 
@@ -222,3 +225,17 @@ class CudaBackend:
 
     def mod_drop(self, a, src_level: int, level: int) -> torch.Tensor:
         return a[:, : level + 1, :].contiguous()
+
+    # collectives (shard.py): limbs travel as int64 tensors on this device
+    def as_tensor(self, data) -> torch.Tensor:
+        return data.clone()
+
+    def zeros_tensor(self, level: int) -> torch.Tensor:
+        return torch.zeros((2, level + 1, self.n), dtype=torch.int64, device=self.device)
+
+    def from_tensor(self, t, level: int) -> torch.Tensor:
+        return t
+
+    def reduce_mod_tensor(self, t, level: int) -> torch.Tensor:
+        self._call("srk_reduce_mod", _ptr(t), 2, level, self.stream())
+        return t

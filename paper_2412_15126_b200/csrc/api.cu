@@ -339,7 +339,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
 // words of scratch (x N) each op needs for a chunk of B ciphertexts at level l
 static size_t ks_limbs(const srk_ctx *c, int level, int B) {
     const size_t nl = level + 1, ne = nl + c->n_p, beta = (nl + c->alpha - 1) / c->alpha;
-    return (size_t)B * (nl + beta * ne + 2 * ne + 2 * nl + 1);  // + rounding bytes
+    return (size_t)B * (nl + beta * ne + 2 * ne + 2 * nl + 2 * c->n_p + 1);  // + z, rounding bytes
 }
 static size_t rescale_limbs(int level, int B) { return (size_t)B * (2 + 2 * (size_t)level); }
 static size_t relin_limbs(const srk_ctx *c, int level, int B) {
@@ -351,7 +351,7 @@ extern "C" size_t srk_workspace_bytes(const srk_ctx *c) {
     const int L = c->L;
     size_t limbs = std::max({relin_limbs(c, L, SRK_WS_BATCH), ks_limbs(c, L, SRK_WS_BATCH) + 4 * (L + 1),
                              rescale_limbs(L, SRK_WS_BATCH) + 2 * (size_t)(L + 1) * SRK_WS_BATCH,
-                             (size_t)2 * c->n_primes, (size_t)2 * (L + 1)});
+                             (size_t)4 * c->n_primes, (size_t)2 * (L + 1)});
     return limbs * c->n * sizeof(uint64_t) + 256;
 }
 
@@ -745,7 +745,8 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
     uint64_t *ext = dc + (long long)B * nl * n;        // [B][beta][ne]
     uint64_t *acc = ext + (long long)B * beta * ne * n;  // [B][2][ne]
     uint64_t *conv = acc + (long long)B * 2 * ne * n;    // [B][2][nl]
-    uint8_t *vround = (uint8_t *)(conv + (long long)B * 2 * nl * n);  // [B][2][N] bytes
+    uint64_t *zb = conv + (long long)B * 2 * nl * n;    // [B][2][K] special limbs, coef
+    uint8_t *vround = (uint8_t *)(zb + (long long)B * 2 * K * n);  // [B][2][N] bytes
     // 1. INTT with the ModUp scale folded in
     {
         FuseArgs f = no_fuse();
@@ -817,26 +818,29 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         ka.batch = B;
         k_ks_inner<<<grid_for((long long)B * ne * n), 256, 0, s>>>(ka, c->d_pc, c->log_n);
         LAUNCHED();
-        // 5. INTT of the special limbs, (P/p_k)^-1 folded in
+        // 5. INTT of the special limbs read through sigma_g, (P/p_k)^-1 folded in -> zb
         {
             FuseArgs f = no_fuse();
             f.mulc = c->lc_moddown_scale;
-            LimbBatch b = cbatch(acc + (long long)nl * n, B, 2, 2ll * ne * n, (long long)ne * n, K, 0);
-            b.split = 0;
-            b.off_b = c->n_q;
-            TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, s));
-        }
-        // 6. ModDown: rounding term once per coefficient, then NTT(conversion)
-        //    with the combine in its store
-        k_moddown_v<<<grid_for(2ll * B * n), 256, 0, s>>>(acc + (long long)nl * n, 2ll * ne * n,
-                                                          (long long)ne * n, K, c->n_q, vround,
-                                                          c->d_pc, c->log_n, B);
-        LAUNCHED();
-        {
-            FuseArgs f = no_fuse();
             f.src = acc + (long long)nl * n;
             f.src_ct = 2ll * ne * n;
             f.src_ps = (long long)ne * n;
+            f.galois = ko.galois;
+            LimbBatch b = cbatch(zb, B, 2, 2ll * K * n, (long long)K * n, K, 0);
+            b.split = 0;
+            b.off_b = c->n_q;
+            TRY(ntt_run(c, b, true, f, ko.galois == 1 ? LD_PLAIN : LD_AUTO, ST_SCALE, s));
+        }
+        // 6. ModDown: rounding term once per coefficient, then NTT(conversion)
+        //    with the combine in its store
+        k_moddown_v<<<grid_for(2ll * B * n), 256, 0, s>>>(zb, 2ll * K * n, (long long)K * n, K,
+                                                          c->n_q, vround, c->d_pc, c->log_n, B);
+        LAUNCHED();
+        {
+            FuseArgs f = no_fuse();
+            f.src = zb;
+            f.src_ct = 2ll * K * n;
+            f.src_ps = (long long)K * n;
             f.n_src = K;
             f.src_pid0 = c->n_q;
             f.mat = pd.mat;
@@ -850,6 +854,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             f.acc = acc;
             f.acc_ct = 2ll * ne * n;
             f.acc_ps = (long long)ne * n;
+            f.acc_galois = ko.galois;
             f.add0 = ko.add0;
             f.add1 = ko.add1;
             f.add_ct = ko.add_ct;
@@ -1022,6 +1027,45 @@ extern "C" int srk_keygen(srk_ctx *c, const uint64_t *s_ntt, const uint64_t *sfr
     return SRK_OK;
 }
 
+// key (dnum x 2 x n_primes limbs) <- sigma_g^-1(key), limb by limb, via tmp (2 x n_primes limbs)
+extern "C" int srk_permute_key(srk_ctx *c, uint64_t *key, uint64_t galois, void *tmp_ws,
+                               void *stream) {
+    if (!(galois & 1)) return fail(SRK_EINVAL, "Galois element must be odd");
+    const long long np = c->n_primes, n = c->n;
+    const uint64_t two_n = 2ull * c->n;
+    // inverse of g in (Z/2N)^*: g^(N/2 - 1) has order dividing N/2 ... use g^(phi-1), phi = N
+    uint64_t ginv = 1, b = galois % two_n, e = (uint64_t)c->n - 1;
+    while (e) {
+        if (e & 1) ginv = ginv * b % two_n;
+        b = b * b % two_n;
+        e >>= 1;
+    }
+    uint64_t *tmp = (uint64_t *)tmp_ws;
+    for (int j = 0; j < c->dnum; j++) {
+        uint64_t *kj = key + (long long)j * 2 * np * n;
+        k_automorph<<<grid_for(2 * np * n), 256, 0, S(stream)>>>(kj, tmp, 2 * np, ginv, c->log_n);
+        LAUNCHED();
+        CU(cudaMemcpyAsync(kj, tmp, sizeof(uint64_t) * 2 * np * n, cudaMemcpyDeviceToDevice, S(stream)));
+    }
+    return SRK_OK;
+}
+
+// Galois key for X -> X^g in the rotation layout: every limb of the
+// switching key sigma_g(s) -> s permuted by sigma_g^-1 (see k_ks_inner)
+extern "C" int srk_keygen_galois(srk_ctx *c, const uint64_t *s_ntt, const int64_t *e, uint64_t seed,
+                                 uint64_t key_id, uint64_t galois, uint64_t *key, void *ws,
+                                 void *stream) {
+    if (!(galois & 1)) return fail(SRK_EINVAL, "Galois element must be odd");
+    const long long np = c->n_primes, n = c->n;
+    uint64_t *sg = (uint64_t *)ws;           // sigma_g(s)
+    uint64_t *tmp = sg + np * n;             // one key digit
+    k_automorph<<<grid_for(np * n), 256, 0, S(stream)>>>(s_ntt, sg, np, galois, c->log_n);
+    LAUNCHED();
+    // ws after sg: keygen needs np limbs of scratch -> place it after tmp region
+    TRY(srk_keygen(c, s_ntt, sg, e, seed, key_id, key, tmp + 2 * np * n, stream));
+    return srk_permute_key(c, key, galois, tmp, stream);
+}
+
 extern "C" int srk_encrypt(srk_ctx *c, const int64_t *m, const uint64_t *s_ntt, const int64_t *e,
                            uint64_t seed, uint64_t seq, uint64_t *out, int level, void *ws,
                            void *stream) {
@@ -1047,6 +1091,14 @@ extern "C" int srk_decrypt_limb0(srk_ctx *c, const uint64_t *ct, const uint64_t 
     LAUNCHED();
     TRY(ntt_batch(c, qbatch(t, 1, 0, 1, 0), true, S(stream)));
     k_center_limb0<<<grid_for(c->n), 256, 0, S(stream)>>>(t, m_out, c->d_pc, c->log_n);
+    LAUNCHED();
+    return SRK_OK;
+}
+
+extern "C" int srk_reduce_mod(srk_ctx *c, uint64_t *data, int n_polys, int level, void *stream) {
+    TRY(check_level(c, level));
+    const long long total = (long long)n_polys * (level + 1) * c->n;
+    k_reduce_mod<<<grid_for(total), 256, 0, S(stream)>>>(data, c->d_pc, c->log_n, level + 1, total);
     LAUNCHED();
     return SRK_OK;
 }

@@ -200,12 +200,15 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
     }
 }
 
-// key-switch inner product (optionally composed with X -> X^galois):
-//   acc[b][r][t][n] = sum_j E_j[t][pi(n)] * key[j][r][pid(t)][n]
+// key-switch inner product:
+//   acc[b][r][t][n] = sum_j E_j[t][n] * key[j][r][pid(t)][n]
 // E_j[t] = d[b][t] for t in digit j's own limbs G_j (NTT form input), else
-// ext[b][j][t].  pi = identity when galois == 1.  Each thread owns one
-// (t, n) for every ciphertext of the batch, so each key word is read once
-// per batch (the key is the dominant HBM stream of a key switch).
+// ext[b][j][t].  For a rotation by X -> X^g the key is stored permuted by
+// sigma_g^-1 (srk_keygen_galois), so acc here is sigma_g^-1 of the rotated
+// accumulator and the ModDown reads it back through sigma_g: the streams in
+// this kernel stay coalesced.  Each thread owns one (t, n) for every
+// ciphertext of the batch, so each key word is read once per batch (the
+// key is the dominant HBM stream of a key switch).
 #define SRK_KS_MAXB 8
 struct KsInnerArgs {
     const uint64_t *d;
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
          x += (long long)gridDim.x * blockDim.x) {
         const int t = (int)(x >> log_n);
         const long long off = x & (n - 1);
-        const long long src = a.galois == 1 ? off : (long long)auto_index((uint32_t)off, a.galois, log_n);
+        const long long src = off;
         const int pid = t <= a.level ? t : t + (a.L - a.level);
         const int jt = t < a.nl ? t / a.alpha : -1;
         U128 a0[SRK_KS_MAXB], a1[SRK_KS_MAXB];
@@ -379,6 +382,14 @@ __global__ void k_center_limb0(const uint64_t *__restrict__ t, int64_t *__restri
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
          x += (long long)gridDim.x * blockDim.x)
         m[x] = t[x] > (q >> 1) ? -(int64_t)(q - t[x]) : (int64_t)t[x];
+}
+
+// cross-rank modular sum fix-up: limbs hold plain int64 sums (< 2^63)
+__global__ void k_reduce_mod(uint64_t *__restrict__ a, const PrimeConst *__restrict__ pc,
+                             int log_n, int nl, long long total) {
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x)
+        a[x] = reduce64(a[x], pc[(x >> log_n) % nl]);
 }
 
 // square (NTT domain) of s over all primes: relinearisation source key

@@ -99,6 +99,7 @@ struct FuseArgs {
     long long out_ct, out_ps;
     const uint64_t *acc;
     long long acc_ct, acc_ps;
+    uint64_t acc_galois;     // ST_MODDOWN: read acc through X -> X^acc_galois (1 = none)
     const uint64_t *add0, *add1;
     long long add_ct;
     uint64_t add_galois;
@@ -293,7 +294,10 @@ __device__ __forceinline__ void fused_store(const FuseArgs &f, int bi, int r, in
     } else {
         const long long nn = 1ll << log_n;
         const long long off = (long long)t * nn + n;
-        uint64_t a = f.acc[bi * f.acc_ct + r * f.acc_ps + off];
+        const long long aoff = (ST == ST_MODDOWN && f.acc_galois != 1)
+                                   ? (long long)t * nn + auto_index((uint32_t)n, f.acc_galois, log_n)
+                                   : off;
+        uint64_t a = f.acc[bi * f.acc_ct + r * f.acc_ps + aoff];
         uint64_t v;
         if constexpr (ST == ST_RESCALE) {
             if (f.pre_mode == 1) a = mul_shoup(a, f.pre.w[limb], f.pre.ws[limb], P.q);
@@ -324,7 +328,7 @@ __device__ __forceinline__ void fused_store(const FuseArgs &f, int bi, int r, in
 // inverse: column pass); the intermediate always lives at the batch's own
 // limb storage (b.ptr).
 template <int LOG_T, bool INV, bool COL, int IO>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 4)
     ntt_pass_kernel(LimbBatch b, NttTables tb, int log_n, const __grid_constant__ FuseArgs f) {
     using S = NttShape<LOG_T>;
     constexpr int T = S::T, E = S::E, TPS = S::TPS, LE1 = S::LE1, LE2 = S::LE2;

@@ -207,6 +207,14 @@ class CKKSEngineCore:
         k = int(round(p.scales[level] * p.q_primes[level + 1] / p.scales[ct.level]))
         return self.backend.mul_const_rescale(ct.data, ct.level, self._residues(k, level + 1), level + 1)
 
+    def at_level(self, ct: Ciphertext, level: int) -> Ciphertext:
+        """``ct`` brought down to ``level`` (scale-preserving; not counted, like the min rule)."""
+        return self._emit(self._align(ct, level), level, ct.rot_chain)
+
+    def wrap(self, data, level: int, rot_chain: int = 0) -> Ciphertext:
+        """Ciphertext around backend limbs produced outside the engine (collectives)."""
+        return self._emit(data, level, rot_chain)
+
     @staticmethod
     def _as_constant(p):
         """Return the float if ``p`` is a scalar or a constant vector, else None."""

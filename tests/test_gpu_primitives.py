@@ -51,6 +51,13 @@ def ptr(t):
     return t.data_ptr()
 
 
+def rot_layout(gb, key, galois):
+    """Device copy of a standard-layout switching key in rotation layout."""
+    k = dev(gb, key)
+    call(gb, "srk_permute_key", ptr(k), galois, gb.workspace(), gb.stream())
+    return k
+
+
 def levels_for(p):
     return sorted({p.max_level, max(1, p.max_level // 2), 1})
 
@@ -165,7 +172,8 @@ def test_keyswitch_and_relin(pair):
     assert np.array_equal(host(gb, out), orc.mul_relin(a, b, key, lvl))
     g = pow(5, 3, 2 * p.ring_degree)
     out = gb.empty_ct(lvl)
-    call(gb, "srk_rotate", ptr(ta), ptr(kd), ptr(out), lvl, g, gb.workspace(), gb.stream())
+    kr = rot_layout(gb, key, g)
+    call(gb, "srk_rotate", ptr(ta), ptr(kr), ptr(out), lvl, g, gb.workspace(), gb.stream())
     assert np.array_equal(host(gb, out), orc.rotate_raw(a, key, g, lvl))
 
 
@@ -216,7 +224,8 @@ def test_batched_ops_match_oracle(pair):
     ta, tb, tk = dev(gb, a), dev(gb, b), dev(gb, key)
     g = pow(5, 5, 2 * n)
     out = gb.empty_ct(lvl, polys=2 * B)
-    call(gb, "srk_rotate_batch", ptr(ta), 2 * ps, ptr(tk), ptr(out), 2 * ps, B, lvl, g,
+    tr = rot_layout(gb, key, g)
+    call(gb, "srk_rotate_batch", ptr(ta), 2 * ps, ptr(tr), ptr(out), 2 * ps, B, lvl, g,
          gb.workspace(), gb.stream())
     got = host(gb, out).reshape(B, 2, lvl + 1, n)
     for i in range(B):
@@ -224,7 +233,8 @@ def test_batched_ops_match_oracle(pair):
     # hoisted: two rotations per ciphertext share the base extension and equal single rotations
     g2 = pow(5, 9, 2 * n)
     o1, o2 = gb.empty_ct(lvl, polys=2 * B), gb.empty_ct(lvl, polys=2 * B)
-    keys = (ctypes.c_void_p * 2)(ptr(tk), ptr(tk))
+    tr2 = rot_layout(gb, key, g2)
+    keys = (ctypes.c_void_p * 2)(ptr(tr), ptr(tr2))
     gal = (ctypes.c_uint64 * 2)(g, g2)
     outs = (ctypes.c_void_p * 2)(ptr(o1), ptr(o2))
     call(gb, "srk_rotate_hoisted", ptr(ta), 2 * ps, B, 2, keys, gal, outs, 2 * ps, lvl,
