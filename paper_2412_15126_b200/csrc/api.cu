@@ -816,8 +816,18 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         ka.alpha = alpha;
         ka.beta = beta;
         ka.batch = B;
-        k_ks_inner<<<grid_for((long long)B * ne * n), 256, 0, s>>>(ka, c->d_pc, c->log_n);
-        LAUNCHED();
+        {
+            const long long tot = (long long)ne * n;
+            if (beta <= 4)
+                k_ks_inner<4><<<grid_for(tot), 256, 0, s>>>(ka, c->d_pc, c->log_n);
+            else if (beta <= 8)
+                k_ks_inner<8><<<grid_for(tot), 256, 0, s>>>(ka, c->d_pc, c->log_n);
+            else if (beta <= 16)
+                k_ks_inner<16><<<grid_for(tot), 256, 0, s>>>(ka, c->d_pc, c->log_n);
+            else
+                k_ks_inner<64><<<grid_for(tot), 256, 0, s>>>(ka, c->d_pc, c->log_n);
+            LAUNCHED();
+        }
         // 5. INTT of the special limbs read through sigma_g, (P/p_k)^-1 folded in -> zb
         {
             FuseArgs f = no_fuse();

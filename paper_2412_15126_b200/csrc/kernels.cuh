@@ -209,7 +209,6 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
 // this kernel stay coalesced.  Each thread owns one (t, n) for every
 // ciphertext of the batch, so each key word is read once per batch (the
 // key is the dominant HBM stream of a key switch).
-#define SRK_KS_MAXB 8
 struct KsInnerArgs {
     const uint64_t *d;
     long long d_ct;
@@ -222,6 +221,7 @@ struct KsInnerArgs {
     int n_primes, nl, ne, level, L, alpha, beta, batch;
 };
 
+template <int MAXD>
 __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInnerArgs a,
                                                   const PrimeConst *__restrict__ pc, int log_n) {
     const long long n = 1ll << log_n;
@@ -230,35 +230,34 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
          x += (long long)gridDim.x * blockDim.x) {
         const int t = (int)(x >> log_n);
         const long long off = x & (n - 1);
-        const long long src = off;
         const int pid = t <= a.level ? t : t + (a.L - a.level);
         const int jt = t < a.nl ? t / a.alpha : -1;
-        U128 a0[SRK_KS_MAXB], a1[SRK_KS_MAXB];
+        // this (t, n)'s key words, one pair per digit, read once for the whole batch
+        uint64_t k0[MAXD], k1[MAXD];
 #pragma unroll
-        for (int b = 0; b < SRK_KS_MAXB; b++) a0[b] = a1[b] = U128{0, 0};
-        for (int j = 0; j < a.beta; j++) {
-            const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + pid) * n + off;
-            const uint64_t k0 = __ldg(kj), k1 = __ldg(kj + (long long)a.n_primes * n);
-            const uint64_t *e = j == jt ? a.d + (long long)t * n + src
-                                        : a.ext + j * a.ext_dig + (long long)t * n + src;
-            const long long es = j == jt ? a.d_ct : a.ext_ct;
-#pragma unroll
-            for (int b = 0; b < SRK_KS_MAXB; b++) {
-                if (b < a.batch) {
-                    const uint64_t v = e[b * es];
-                    mac(a0[b], v, k0);
-                    mac(a1[b], v, k1);
-                }
+        for (int j = 0; j < MAXD; j++) {
+            if (j < a.beta) {
+                const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + pid) * n + off;
+                k0[j] = __ldg(kj);
+                k1[j] = __ldg(kj + (long long)a.n_primes * n);
             }
         }
         const PrimeConst P = pc[pid];
+        const uint64_t *ext = a.ext + (long long)t * n + off;
+        const uint64_t *dd = a.d + (long long)t * n + off;
+        for (int b = 0; b < a.batch; b++) {
+            U128 a0 = {0, 0}, a1 = {0, 0};
 #pragma unroll
-        for (int b = 0; b < SRK_KS_MAXB; b++) {
-            if (b < a.batch) {
-                uint64_t *o = a.acc + b * a.acc_ct + (long long)t * n + off;
-                o[0] = reduce_u128(a0[b], P);
-                o[total] = reduce_u128(a1[b], P);
+            for (int j = 0; j < MAXD; j++) {
+                if (j < a.beta) {
+                    const uint64_t e = j == jt ? dd[b * a.d_ct] : ext[b * a.ext_ct + j * a.ext_dig];
+                    mac(a0, e, k0[j]);
+                    mac(a1, e, k1[j]);
+                }
             }
+            uint64_t *o = a.acc + b * a.acc_ct + (long long)t * n + off;
+            o[0] = reduce_u128(a0, P);
+            o[total] = reduce_u128(a1, P);
         }
     }
 }

@@ -274,14 +274,25 @@ __device__ __forceinline__ uint64_t fused_load(const FuseArgs &f, const PrimeCon
         // centred representative of v mod top_q, reduced mod this prime
         return v > (f.top_q >> 1) ? sub_mod(reduce64(v, P), reduce64(f.top_q, P), P.q)
                                   : reduce64(v, P);
-    } else {  // LD_BCONV with exact rounding (v precomputed once per coefficient)
-        const uint64_t *z = f.src + bi * f.src_ct + r * f.src_ps + n;
-        const long long nn = 1ll << log_n;
-        U128 acc = {0, 0};
-        for (int k = 0; k < f.n_src; k++) mac(acc, z[k * nn], __ldg(f.mat + (long long)k * f.mat_ld + t));
-        const int v = f.vround[((long long)bi * 2 + r) * nn + n];
-        return sub_mod(reduce_u128(acc, P), __ldg(f.corr + v * f.corr_ld + t), P.q);
+    } else {  // LD_BCONV: handled by bconv_load (needs per-thread hoisted constants)
+        return 0;
     }
+}
+
+// ModDown conversion with exact rounding (v precomputed once per coefficient):
+//   sum_k z_k[n] * mat[k][t] - corr[v(n)][t]   mod q_t
+// mat column / corr table for this limb are hoisted into registers by the caller.
+#define SRK_MAX_SPECIAL 16
+__device__ __forceinline__ uint64_t bconv_load(const FuseArgs &f, const uint64_t *z,
+                                               const uint8_t *vr, const uint64_t (&m)[SRK_MAX_SPECIAL],
+                                               const PrimeConst &P, long long n, int log_n, int t) {
+    const long long nn = 1ll << log_n;
+    U128 acc = {0, 0};
+#pragma unroll
+    for (int k = 0; k < SRK_MAX_SPECIAL; k++)
+        if (k < f.n_src) mac(acc, z[k * nn + n], m[k]);
+    const int v = vr[n];
+    return sub_mod(reduce_u128(acc, P), __ldg(f.corr + v * f.corr_ld + t), P.q);
 }
 
 // last-pass element store; x canonical in [0, q)
@@ -373,8 +384,19 @@ __global__ void __launch_bounds__(256, 4)
     auto sidx = [&](int c) -> int {
         return COL ? c * CB + sb : row_sidx<LOG_T>(sb, c);
     };
+    uint64_t bm[SRK_MAX_SPECIAL];
+    const uint64_t *bz = nullptr;
+    const uint8_t *bvr = nullptr;
+    if constexpr (FIRST && LD == LD_BCONV) {
+#pragma unroll
+        for (int k = 0; k < SRK_MAX_SPECIAL; k++)
+            bm[k] = k < f.n_src ? __ldg(f.mat + (long long)k * f.mat_ld + t) : 0;
+        bz = f.src + (long long)bi * f.src_ct + (long long)r * f.src_ps;
+        bvr = f.vround + ((long long)bi * 2 + r) * n;
+    }
     auto load = [&](int c) -> uint64_t {
-        if constexpr (FIRST) return fused_load<LD>(f, tb.pc, bi, r, t, pc, gaddr(c), log_n, lsrc);
+        if constexpr (FIRST && LD == LD_BCONV) return bconv_load(f, bz, bvr, bm, pc, gaddr(c), log_n, t);
+        else if constexpr (FIRST) return fused_load<LD>(f, tb.pc, bi, r, t, pc, gaddr(c), log_n, lsrc);
         else return data[gaddr(c)];
     };
 

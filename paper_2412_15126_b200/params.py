@@ -256,6 +256,7 @@ PRESETS = {
     # small rings for CPU tests
     "toy": dict(log_n=10, levels=12, special=4, special_bits=60, dnum=4, hamming_weight=32),
     "toy_deep": dict(log_n=11, levels=40, special=6, special_bits=60, dnum=6, hamming_weight=32),
+    "toy_sort": dict(log_n=11, levels=48, special=7, special_bits=60, dnum=6, hamming_weight=32),
 }
 
 

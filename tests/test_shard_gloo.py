@@ -12,7 +12,7 @@ import torch.multiprocessing as mp
 import paper_2412_15126_b200 as M
 from paper_2412_15126_b200.params import preset
 
-KCFG = M.KernelConfig(mode="composite", composite=(3, 2), indicator_composite=(3, 2))
+KCFG = M.KernelConfig(mode="composite", composite=(3, 2), indicator_composite=(4, 2))
 VALUES = np.random.default_rng(5).choice(256, 40, replace=False) / 256  # 3 blocks of 16
 
 
@@ -32,7 +32,7 @@ def _worker(rank, world, port, what, out_dir):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    eng = oracle_engine(preset("toy_deep"))
+    eng = oracle_engine(preset("toy_sort"))
     bv = M.block_split(eng, VALUES)
     comm = Comm()
     if what == "rank":
@@ -46,7 +46,7 @@ def _worker(rank, world, port, what, out_dir):
 def _single(what):
     from oracle.oracle import oracle_engine
 
-    eng = oracle_engine(preset("toy_deep"))
+    eng = oracle_engine(preset("toy_sort"))
     bv = M.block_split(eng, VALUES)
     if what == "rank":
         res = M.multi_rank(eng, bv, KCFG)
@@ -71,4 +71,4 @@ def test_two_rank_shards_are_bit_identical(tmp_path, what):
 
         assert np.array_equal(np.rint(vals), fractional_ranks(VALUES))
     else:
-        assert np.abs(vals - np.sort(VALUES)).max() < 1e-3
+        assert np.abs(vals - np.sort(VALUES)).max() < 5e-3
