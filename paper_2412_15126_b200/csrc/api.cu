@@ -400,7 +400,7 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
         bb.split = b.split - l0;
         bb.off_a = b.off_a + l0;
         bb.off_b = b.off_b + l0;
-        if (ff.src && (IO == LD_PLAIN || IO == LD_AUTO)) ff.src += (long long)l0 * c->n;
+        if (ff.src && (IO == LD_PLAIN || IO == LD_AUTO) && COL == INV) ff.src += (long long)l0 * c->n;
         if (ff.out) ff.out += (long long)l0 * c->n;
         if (ff.acc) ff.acc += (long long)l0 * c->n;
         if (ff.add0) ff.add0 += (long long)l0 * c->n;
@@ -457,7 +457,14 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
         if (!inverse) {
             switch (ld) {
                 case LD_PLAIN: TRY((pass_t<false, true, LD_PLAIN>(c, log_r, b, l0, nlc, f, s))); break;
-                case LD_BCONV: TRY((pass_t<false, true, LD_BCONV>(c, log_r, b, l0, nlc, f, s))); break;
+                case LD_BCONV:
+                    if (f.n_src <= 4)
+                        TRY((pass_t<false, true, LD_BCONV>(c, log_r, b, l0, nlc, f, s)));
+                    else if (f.n_src <= 8)
+                        TRY((pass_t<false, true, LD_BCONV8>(c, log_r, b, l0, nlc, f, s)));
+                    else
+                        TRY((pass_t<false, true, LD_BCONV16>(c, log_r, b, l0, nlc, f, s)));
+                    break;
                 case LD_SPREAD: TRY((pass_t<false, true, LD_SPREAD>(c, log_r, b, l0, nlc, f, s))); break;
                 default: return fail(SRK_EINVAL, "bad forward load mode");
             }
@@ -817,7 +824,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         ka.beta = beta;
         ka.batch = B;
         {
-            const long long tot = (long long)ne * n;
+            const long long tot = (long long)ne * n / 2;
             if (beta <= 4)
                 k_ks_inner<4><<<grid_for(tot), 256, 0, s>>>(ka, c->d_pc, c->log_n);
             else if (beta <= 8)

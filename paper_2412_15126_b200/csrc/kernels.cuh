@@ -224,40 +224,44 @@ struct KsInnerArgs {
 template <int MAXD>
 __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInnerArgs a,
                                                   const PrimeConst *__restrict__ pc, int log_n) {
+    // two consecutive coefficients per thread: 16-byte loads/stores throughout
     const long long n = 1ll << log_n;
     const long long total = (long long)a.ne * n;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
-         x += (long long)gridDim.x * blockDim.x) {
+    for (long long x = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; x < total;
+         x += (long long)gridDim.x * blockDim.x * 2) {
         const int t = (int)(x >> log_n);
         const long long off = x & (n - 1);
         const int pid = t <= a.level ? t : t + (a.L - a.level);
         const int jt = t < a.nl ? t / a.alpha : -1;
-        // this (t, n)'s key words, one pair per digit, read once for the whole batch
-        uint64_t k0[MAXD], k1[MAXD];
+        ulonglong2 k0[MAXD], k1[MAXD];
 #pragma unroll
         for (int j = 0; j < MAXD; j++) {
             if (j < a.beta) {
                 const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + pid) * n + off;
-                k0[j] = __ldg(kj);
-                k1[j] = __ldg(kj + (long long)a.n_primes * n);
+                k0[j] = __ldg(reinterpret_cast<const ulonglong2 *>(kj));
+                k1[j] = __ldg(reinterpret_cast<const ulonglong2 *>(kj + (long long)a.n_primes * n));
             }
         }
         const PrimeConst P = pc[pid];
         const uint64_t *ext = a.ext + (long long)t * n + off;
         const uint64_t *dd = a.d + (long long)t * n + off;
         for (int b = 0; b < a.batch; b++) {
-            U128 a0 = {0, 0}, a1 = {0, 0};
+            U128 a0x = {0, 0}, a0y = {0, 0}, a1x = {0, 0}, a1y = {0, 0};
 #pragma unroll
             for (int j = 0; j < MAXD; j++) {
                 if (j < a.beta) {
-                    const uint64_t e = j == jt ? dd[b * a.d_ct] : ext[b * a.ext_ct + j * a.ext_dig];
-                    mac(a0, e, k0[j]);
-                    mac(a1, e, k1[j]);
+                    const ulonglong2 e = *reinterpret_cast<const ulonglong2 *>(
+                        j == jt ? dd + b * a.d_ct : ext + b * a.ext_ct + j * a.ext_dig);
+                    mac(a0x, e.x, k0[j].x);
+                    mac(a0y, e.y, k0[j].y);
+                    mac(a1x, e.x, k1[j].x);
+                    mac(a1y, e.y, k1[j].y);
                 }
             }
             uint64_t *o = a.acc + b * a.acc_ct + (long long)t * n + off;
-            o[0] = reduce_u128(a0, P);
-            o[total] = reduce_u128(a1, P);
+            *reinterpret_cast<ulonglong2 *>(o) = make_ulonglong2(reduce_u128(a0x, P), reduce_u128(a0y, P));
+            *reinterpret_cast<ulonglong2 *>(o + total) =
+                make_ulonglong2(reduce_u128(a1x, P), reduce_u128(a1y, P));
         }
     }
 }

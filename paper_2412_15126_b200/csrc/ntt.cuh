@@ -75,7 +75,14 @@ __device__ __forceinline__ uint32_t auto_index(uint32_t k, uint64_t g, int log_n
 }
 
 // Fused first-pass loads / last-pass stores (see ntt_pass_kernel).
-enum { LD_PLAIN = 0, LD_BCONV = 1, LD_SPREAD = 2, LD_AUTO = 3 };
+enum { LD_PLAIN = 0, LD_BCONV = 1, LD_SPREAD = 2, LD_AUTO = 3, LD_BCONV8 = 4, LD_BCONV16 = 5 };
+// ModDown conversion load, bucketed by the number of special primes it reads
+__host__ __device__ constexpr bool is_bconv(int ld) {
+    return ld == LD_BCONV || ld == LD_BCONV8 || ld == LD_BCONV16;
+}
+__host__ __device__ constexpr int bconv_maxk(int ld) {
+    return ld == LD_BCONV ? 4 : (ld == LD_BCONV8 ? 8 : 16);
+}
 enum { ST_PLAIN = 0, ST_MODDOWN = 1, ST_RESCALE = 2, ST_SCALE = 3 };
 
 struct FuseArgs {
@@ -157,6 +164,9 @@ __device__ __forceinline__ int row_sidx(int sb, int c) {
 // is offset by M = q << k (a multiple of q above any operand at step k), so
 // 16 steps stay below 2^16 q < 2^62.  Only the final pass reduces.
 #define SRK_SMALL_Q (1ull << 46)
+#ifndef SRK_NTT_MINB
+#define SRK_NTT_MINB 3  // CTAs per SM the register budget is sized for
+#endif
 
 __device__ __forceinline__ void ct_bfly_small(uint64_t &x, uint64_t &y, uint64_t w, uint64_t ws,
                                               uint64_t q, uint64_t two_q) {
@@ -274,7 +284,7 @@ __device__ __forceinline__ uint64_t fused_load(const FuseArgs &f, const PrimeCon
         // centred representative of v mod top_q, reduced mod this prime
         return v > (f.top_q >> 1) ? sub_mod(reduce64(v, P), reduce64(f.top_q, P), P.q)
                                   : reduce64(v, P);
-    } else {  // LD_BCONV: handled by bconv_load (needs per-thread hoisted constants)
+    } else {  // ModDown conversion: handled by bconv_load (per-thread hoisted constants)
         return 0;
     }
 }
@@ -282,14 +292,14 @@ __device__ __forceinline__ uint64_t fused_load(const FuseArgs &f, const PrimeCon
 // ModDown conversion with exact rounding (v precomputed once per coefficient):
 //   sum_k z_k[n] * mat[k][t] - corr[v(n)][t]   mod q_t
 // mat column / corr table for this limb are hoisted into registers by the caller.
-#define SRK_MAX_SPECIAL 16
+template <int MAXK>
 __device__ __forceinline__ uint64_t bconv_load(const FuseArgs &f, const uint64_t *z,
-                                               const uint8_t *vr, const uint64_t (&m)[SRK_MAX_SPECIAL],
+                                               const uint8_t *vr, const uint64_t (&m)[MAXK],
                                                const PrimeConst &P, long long n, int log_n, int t) {
     const long long nn = 1ll << log_n;
     U128 acc = {0, 0};
 #pragma unroll
-    for (int k = 0; k < SRK_MAX_SPECIAL; k++)
+    for (int k = 0; k < MAXK; k++)
         if (k < f.n_src) mac(acc, z[k * nn + n], m[k]);
     const int v = vr[n];
     return sub_mod(reduce_u128(acc, P), __ldg(f.corr + v * f.corr_ld + t), P.q);
@@ -339,7 +349,7 @@ __device__ __forceinline__ void fused_store(const FuseArgs &f, int bi, int r, in
 // inverse: column pass); the intermediate always lives at the batch's own
 // limb storage (b.ptr).
 template <int LOG_T, bool INV, bool COL, int IO>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, SRK_NTT_MINB)
     ntt_pass_kernel(LimbBatch b, NttTables tb, int log_n, const __grid_constant__ FuseArgs f) {
     using S = NttShape<LOG_T>;
     constexpr int T = S::T, E = S::E, TPS = S::TPS, LE1 = S::LE1, LE2 = S::LE2;
@@ -384,18 +394,19 @@ __global__ void __launch_bounds__(256, 4)
     auto sidx = [&](int c) -> int {
         return COL ? c * CB + sb : row_sidx<LOG_T>(sb, c);
     };
-    uint64_t bm[SRK_MAX_SPECIAL];
+    constexpr int MAXK = bconv_maxk(LD);
+    uint64_t bm[MAXK];
     const uint64_t *bz = nullptr;
     const uint8_t *bvr = nullptr;
-    if constexpr (FIRST && LD == LD_BCONV) {
+    if constexpr (FIRST && is_bconv(LD)) {
 #pragma unroll
-        for (int k = 0; k < SRK_MAX_SPECIAL; k++)
+        for (int k = 0; k < MAXK; k++)
             bm[k] = k < f.n_src ? __ldg(f.mat + (long long)k * f.mat_ld + t) : 0;
         bz = f.src + (long long)bi * f.src_ct + (long long)r * f.src_ps;
         bvr = f.vround + ((long long)bi * 2 + r) * n;
     }
     auto load = [&](int c) -> uint64_t {
-        if constexpr (FIRST && LD == LD_BCONV) return bconv_load(f, bz, bvr, bm, pc, gaddr(c), log_n, t);
+        if constexpr (FIRST && is_bconv(LD)) return bconv_load<MAXK>(f, bz, bvr, bm, pc, gaddr(c), log_n, t);
         else if constexpr (FIRST) return fused_load<LD>(f, tb.pc, bi, r, t, pc, gaddr(c), log_n, lsrc);
         else return data[gaddr(c)];
     };
