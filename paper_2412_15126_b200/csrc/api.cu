@@ -785,7 +785,24 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             maxd = std::max(maxd, pl.n_dst);
         }
         dim3 grid((unsigned)((n + 255) / 256), B * beta, (maxd + SRK_MODUP_TCH - 1) / SRK_MODUP_TCH);
-        k_modup<<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n);
+        switch (alpha) {
+            case 1: k_modup<1><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 2: k_modup<2><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 3: k_modup<3><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 4: k_modup<4><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 5: k_modup<5><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 6: k_modup<6><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 7: k_modup<7><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 8: k_modup<8><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 9: k_modup<9><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 10: k_modup<10><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 11: k_modup<11><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 12: k_modup<12><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 13: k_modup<13><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 14: k_modup<14><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            case 15: k_modup<15><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            default: k_modup<16><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+        }
         LAUNCHED();
     }
     // 3. NTT of all ModUp targets
@@ -824,15 +841,15 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         ka.beta = beta;
         ka.batch = B;
         {
-            const long long tot = (long long)ne * n / 2;
-            if (beta <= 4)
-                k_ks_inner<4><<<grid_for(tot), 256, 0, s>>>(ka, c->d_pc, c->log_n);
-            else if (beta <= 8)
-                k_ks_inner<8><<<grid_for(tot), 256, 0, s>>>(ka, c->d_pc, c->log_n);
-            else if (beta <= 16)
-                k_ks_inner<16><<<grid_for(tot), 256, 0, s>>>(ka, c->d_pc, c->log_n);
-            else
-                k_ks_inner<64><<<grid_for(tot), 256, 0, s>>>(ka, c->d_pc, c->log_n);
+            const long long tiles = (long long)ne * n / SRK_KS_TILE;
+            const size_t smem = (size_t)beta * 2 * SRK_KS_TILE * 8;
+            const int blocks = (int)std::min<long long>(tiles, 148 * 8);
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_ks_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+                attr = true;
+            }
+            k_ks_inner<<<blocks, SRK_KS_TILE, smem, s>>>(ka, c->d_pc, c->log_n);
             LAUNCHED();
         }
         // 5. INTT of the special limbs read through sigma_g, (P/p_k)^-1 folded in -> zb

@@ -172,6 +172,9 @@ struct ModUpArgs {
 
 #define SRK_MODUP_TCH 8
 
+// GS = exact digit size (compile-time: no predicated MACs); digits smaller
+// than GS (the last one at some levels) fall back to the runtime loop
+template <int GS>
 __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs a,
                                                const PrimeConst *__restrict__ pc, int log_n) {
     const long long n = 1ll << log_n;
@@ -186,16 +189,22 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
     const uint64_t *mat = a.mat[j];
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
          x += (long long)gridDim.x * blockDim.x) {
-        uint64_t y[16];
+        if (gs == GS) {
+            uint64_t y[GS];
 #pragma unroll
-        for (int i = 0; i < 16; i++)
-            if (i < gs) y[i] = src[(long long)i * n + x];
-        for (int t = t0; t < t1; t++) {
-            U128 acc = {0, 0};
+            for (int i = 0; i < GS; i++) y[i] = src[(long long)i * n + x];
+            for (int t = t0; t < t1; t++) {
+                U128 acc = {0, 0};
 #pragma unroll
-            for (int i = 0; i < 16; i++)
-                if (i < gs) mac(acc, y[i], __ldg(mat + i * nd + t));
-            dst[(long long)__ldg(a.slot[j] + t) * n + x] = reduce_u128(acc, pc[__ldg(a.pid[j] + t)]);
+                for (int i = 0; i < GS; i++) mac(acc, y[i], __ldg(mat + i * nd + t));
+                dst[(long long)__ldg(a.slot[j] + t) * n + x] = reduce_u128(acc, pc[__ldg(a.pid[j] + t)]);
+            }
+        } else {
+            for (int t = t0; t < t1; t++) {
+                U128 acc = {0, 0};
+                for (int i = 0; i < gs; i++) mac(acc, src[(long long)i * n + x], __ldg(mat + i * nd + t));
+                dst[(long long)__ldg(a.slot[j] + t) * n + x] = reduce_u128(acc, pc[__ldg(a.pid[j] + t)]);
+            }
         }
     }
 }
@@ -221,47 +230,43 @@ struct KsInnerArgs {
     int n_primes, nl, ne, level, L, alpha, beta, batch;
 };
 
-template <int MAXD>
-__global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInnerArgs a,
-                                                  const PrimeConst *__restrict__ pc, int log_n) {
-    // two consecutive coefficients per thread: 16-byte loads/stores throughout
+// CTA = one limb t x 256 consecutive coefficients; the tile's key words
+// (beta digits x 2 outputs) are staged once in shared memory and reused for
+// every ciphertext of the batch, so registers stay low (high occupancy hides
+// the HBM latency of the ext / d streams).
+#define SRK_KS_TILE 256
+__global__ void __launch_bounds__(SRK_KS_TILE) k_ks_inner(const __grid_constant__ KsInnerArgs a,
+                                                          const PrimeConst *__restrict__ pc, int log_n) {
+    extern __shared__ uint64_t skey[];  // [beta][2][TILE]
     const long long n = 1ll << log_n;
     const long long total = (long long)a.ne * n;
-    for (long long x = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; x < total;
-         x += (long long)gridDim.x * blockDim.x * 2) {
+    const long long tiles = total / SRK_KS_TILE;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const long long x = tile * SRK_KS_TILE + threadIdx.x;
         const int t = (int)(x >> log_n);
         const long long off = x & (n - 1);
         const int pid = t <= a.level ? t : t + (a.L - a.level);
         const int jt = t < a.nl ? t / a.alpha : -1;
-        ulonglong2 k0[MAXD], k1[MAXD];
-#pragma unroll
-        for (int j = 0; j < MAXD; j++) {
-            if (j < a.beta) {
-                const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + pid) * n + off;
-                k0[j] = __ldg(reinterpret_cast<const ulonglong2 *>(kj));
-                k1[j] = __ldg(reinterpret_cast<const ulonglong2 *>(kj + (long long)a.n_primes * n));
-            }
+        __syncthreads();
+        for (int j = 0; j < a.beta; j++) {
+            const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + pid) * n + off;
+            skey[(2 * j) * SRK_KS_TILE + threadIdx.x] = __ldg(kj);
+            skey[(2 * j + 1) * SRK_KS_TILE + threadIdx.x] = __ldg(kj + (long long)a.n_primes * n);
         }
+        __syncthreads();
         const PrimeConst P = pc[pid];
         const uint64_t *ext = a.ext + (long long)t * n + off;
         const uint64_t *dd = a.d + (long long)t * n + off;
         for (int b = 0; b < a.batch; b++) {
-            U128 a0x = {0, 0}, a0y = {0, 0}, a1x = {0, 0}, a1y = {0, 0};
-#pragma unroll
-            for (int j = 0; j < MAXD; j++) {
-                if (j < a.beta) {
-                    const ulonglong2 e = *reinterpret_cast<const ulonglong2 *>(
-                        j == jt ? dd + b * a.d_ct : ext + b * a.ext_ct + j * a.ext_dig);
-                    mac(a0x, e.x, k0[j].x);
-                    mac(a0y, e.y, k0[j].y);
-                    mac(a1x, e.x, k1[j].x);
-                    mac(a1y, e.y, k1[j].y);
-                }
+            U128 a0 = {0, 0}, a1 = {0, 0};
+            for (int j = 0; j < a.beta; j++) {
+                const uint64_t e = j == jt ? dd[b * a.d_ct] : ext[b * a.ext_ct + j * a.ext_dig];
+                mac(a0, e, skey[(2 * j) * SRK_KS_TILE + threadIdx.x]);
+                mac(a1, e, skey[(2 * j + 1) * SRK_KS_TILE + threadIdx.x]);
             }
             uint64_t *o = a.acc + b * a.acc_ct + (long long)t * n + off;
-            *reinterpret_cast<ulonglong2 *>(o) = make_ulonglong2(reduce_u128(a0x, P), reduce_u128(a0y, P));
-            *reinterpret_cast<ulonglong2 *>(o + total) =
-                make_ulonglong2(reduce_u128(a1x, P), reduce_u128(a1y, P));
+            o[0] = reduce_u128(a0, P);
+            o[total] = reduce_u128(a1, P);
         }
     }
 }

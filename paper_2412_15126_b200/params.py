@@ -256,6 +256,8 @@ PRESETS = {
     # small rings for CPU tests
     "toy": dict(log_n=10, levels=12, special=4, special_bits=60, dnum=4, hamming_weight=32),
     "toy_deep": dict(log_n=11, levels=40, special=6, special_bits=60, dnum=6, hamming_weight=32),
+    # ring 2^12 with room for the golden Chebyshev circuits (2048 slots)
+    "ring12": dict(log_n=12, levels=34, special=6, special_bits=60, dnum=5, hamming_weight=64),
     "toy_sort": dict(log_n=11, levels=48, special=7, special_bits=60, dnum=6, hamming_weight=32),
 }
 

@@ -1,0 +1,119 @@
+"""Pipelines on the B200 engine: full-pipeline bit-exactness against the CPU
+oracle, the reference's golden circuits after decryption, and the BASELINE
+configurations' results (ranks / argmin / argmax / k-th / sort order)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2412_15126_b200 as M
+from oracle.circuits import circuits
+from oracle.plain import fractional_ranks
+from oracle.slotsim import SimParams, SlotSim
+from paper_2412_15126_b200.params import preset
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = {c["name"]: c for c in json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                                             "circuits.json")))["cases"]}
+# slot-level tolerance vs the reference simulator on the same circuit (CKKS noise
+# amplified by the degree-d Chebyshev recursion), checked per circuit
+CHEB_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def eng12(require_cuda):
+    return M.B200Engine(preset("ring12"))
+
+
+def test_full_pipeline_limbs_bit_exact_vs_oracle(require_cuda):
+    """Every op of a composite-mode rank (rotations, products, plaintext masks,
+    level alignments) yields the same limbs on the GPU as on the CPU oracle."""
+    from oracle.oracle import oracle_engine
+
+    p = preset("toy_deep")
+    gpu, cpu = M.B200Engine(p), oracle_engine(p)
+    v = np.array([0.30, 0.10, 0.80, 0.55, 0.20, 0.95, 0.65, 0.40])
+    cfg = M.KernelConfig(mode="composite", composite=(3, 2))
+    rg = M.rank(gpu, gpu.encrypt(v), 8, cfg).ranks
+    rc = M.rank(cpu, cpu.encrypt(v), 8, cfg).ranks
+    assert rg.level == rc.level
+    assert np.array_equal(gpu.backend.to_host(rg.data), rc.data)
+    assert gpu.cost_snapshot() == cpu.cost_snapshot()
+
+
+@pytest.mark.parametrize("name", sorted(c["name"] for c in circuits() if c["gpu"]))
+def test_golden_circuit_on_gpu(eng12, name):
+    c = next(c for c in circuits() if c["name"] == name)
+    g = GOLDEN[name]
+    assert eng12.params.slot_count == c["slot_count"]
+    eng12.cost_reset()
+    out = np.asarray(c["fn"](eng12, M, c["kernel"]))[: c["keep"]]
+    want = np.array(g["output"])
+    assert np.abs(out - want).max() < CHEB_TOL, np.abs(out - want).max()
+    rep = eng12.cost_snapshot().__dict__
+    assert {k: v for k, v in rep.items() if k != "levels_consumed"} == \
+        {k: v for k, v in g["cost"].items() if k != "levels_consumed"}
+    assert eng12.rotation_offsets() == g["trace"]
+
+
+def test_cfg1_rank_n16(require_cuda):
+    """BASELINE config 1: 16 grid values k/64 on ring 2^12 (2048 slots), composite sign."""
+    v = np.random.default_rng(0).choice(64, 16, replace=False) / 64
+    eng = M.B200Engine(preset("cfg1"))
+    cfg = M.KernelConfig(mode="composite", composite=(3, 2))
+    r = M.read_row(eng, M.rank(eng, eng.encrypt(v), 16, cfg).ranks, 16)
+    assert np.array_equal(np.rint(r), fractional_ranks(v))
+    sim = SlotSim(SimParams(2048, 22))
+    rs = M.read_row(sim, M.rank(sim, sim.encrypt(v), 16, cfg).ranks, 16)
+    assert np.abs(r - rs).max() < 1e-4
+    assert eng.cost_snapshot().rotations == 16  # log2(16) x 4 (ReplR, TransR, ReplC, SumR)
+
+
+def test_cfg3_rank_n128(require_cuda):
+    v = np.random.default_rng(0).choice(1024, 128, replace=False) / 1024
+    eng = M.B200Engine(preset("cfg3"))
+    cfg = M.KernelConfig(mode="composite", composite=(4, 2))
+    r = M.read_row(eng, M.rank(eng, eng.encrypt(v), 128, cfg).ranks, 128)
+    assert np.array_equal(np.rint(r), fractional_ranks(v))
+    sim = SlotSim(SimParams(32768, 29))
+    rs = M.read_row(sim, M.rank(sim, sim.encrypt(v), 128, cfg).ranks, 128)
+    assert np.abs(r - rs).max() < 1e-3
+    assert eng.cost_snapshot().rotations == 28
+
+
+@pytest.fixture(scope="module")
+def eng_long(require_cuda):
+    return M.B200Engine(preset("long"))
+
+
+def test_cfg4_order_statistic_masks(eng_long):
+    v = np.random.default_rng(1).choice(1024, 128, replace=False) / 1024
+    cfg = M.KernelConfig(mode="composite", composite=(4, 2), tie_margin=2.0 ** -11)
+    ct = eng_long.encrypt(v)
+    order = np.argsort(v)
+    for q, idx in ((M.StatisticQuery("min"), order[0]), (M.StatisticQuery("max"), order[-1]),
+                   (M.StatisticQuery("kth", k=64), order[63])):
+        m = M.read_row(eng_long, M.order_statistic_mask(eng_long, ct, 128, q, cfg), 128)
+        assert int(np.argmax(m)) == int(idx)
+        assert np.abs(m - np.eye(128)[idx]).max() < 0.05
+
+
+def test_cfg4_min_value(eng_long):
+    v = np.random.default_rng(2).choice(1024, 16, replace=False) / 1024
+    cfg = M.KernelConfig(mode="composite", composite=(3, 2), tie_margin=2.0 ** -9,
+                         goldschmidt_iters=4)
+    val = eng_long.decrypt(M.order_statistic_value(eng_long, eng_long.encrypt(v), 16,
+                                                    M.StatisticQuery("min"), cfg))[0]
+    assert abs(val - v.min()) < 1e-3
+
+
+def test_multi_sort_n256(eng_long):
+    v = np.random.default_rng(3).choice(2048, 256, replace=False) / 2048
+    cfg = M.SortConfig(kernel=M.KernelConfig(mode="composite", composite=(5, 2),
+                                             indicator_composite=(5, 2)), tie_correction=False)
+    out = M.block_merge(eng_long, M.multi_sort(eng_long, M.block_split(eng_long, v), cfg))
+    assert np.array_equal(np.argsort(out), np.arange(256))
+    assert np.abs(out - np.sort(v)).max() < 1e-3
