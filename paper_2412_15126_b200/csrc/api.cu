@@ -400,7 +400,7 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
         bb.split = b.split - l0;
         bb.off_a = b.off_a + l0;
         bb.off_b = b.off_b + l0;
-        if (ff.src && (IO == LD_PLAIN || IO == LD_AUTO) && COL == INV) ff.src += (long long)l0 * c->n;
+        if (ff.src && (IO == LD_PLAIN || IO == LD_AUTO) && COL != INV) ff.src += (long long)l0 * c->n;
         if (ff.out) ff.out += (long long)l0 * c->n;
         if (ff.acc) ff.acc += (long long)l0 * c->n;
         if (ff.add0) ff.add0 += (long long)l0 * c->n;
