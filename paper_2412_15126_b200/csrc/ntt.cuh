@@ -498,3 +498,199 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
         }
     }
 }
+
+// ---------------------------------------------------------------------------
+// Persistent, double-buffered NTT pass (plain loads).  Each CTA walks tiles
+// blockIdx.x, +gridDim.x, ...; while one tile is transformed out of shared
+// memory the next one streams in with cp.async (16-B, L1-bypassing), so the
+// HBM latency is hidden behind the butterflies of the previous tile.  Used for
+// every pass whose input is a plain copy of limbs (all second passes, and
+// first passes with LD_PLAIN); fused gathers/conversions keep ntt_pass_kernel.
+// Row-pass tiles are padded by 2 words per E so 16-B cp.async stays aligned.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int LOG_T>
+__device__ __forceinline__ int row_sidx2(int sb, int c) {
+    using S = NttShape<LOG_T>;
+    return sb * (S::T + 2 * S::T / S::E) + c + 2 * (c >> S::LE1);
+}
+
+template <int LOG_T, bool COL>
+__host__ __device__ constexpr int pipe_tile_words(int cb) {
+    return COL ? cb * (1 << LOG_T)
+               : cb * ((1 << LOG_T) + 2 * (1 << LOG_T) / NttShape<LOG_T>::E);
+}
+
+template <int LOG_T, bool INV, bool COL, int IO>
+__global__ void __launch_bounds__(256, 3)
+    ntt_pass_pipe(LimbBatch b, NttTables tb, int log_n, const __grid_constant__ FuseArgs f,
+                  int n_tiles, int tiles_x) {
+    using S = NttShape<LOG_T>;
+    constexpr int T = S::T, E = S::E, TPS = S::TPS, LE1 = S::LE1, LE2 = S::LE2;
+    constexpr bool FIRST = (COL != INV);
+    constexpr int ST = FIRST ? ST_PLAIN : IO;
+    extern __shared__ __align__(16) uint64_t smem[];
+
+    const int n = 1 << log_n;
+    const int CB = blockDim.x / TPS;
+    const int TW = pipe_tile_words<LOG_T, COL>(CB);
+    const int C = n >> LOG_T;
+    const int tid = threadIdx.x;
+    int sb, u;
+    if (COL) {
+        sb = tid % CB;
+        u = tid / CB;
+    } else {
+        sb = tid / TPS;
+        u = tid % TPS;
+    }
+    auto sidx = [&](int c) -> int { return COL ? c * CB + sb : row_sidx2<LOG_T>(sb, c); };
+
+    // tile -> (limb data pointer, load source pointer, sub-transform group)
+    struct Tile {
+        uint64_t *data;
+        const uint64_t *src;
+        int pid, bi, r, t, limb, sub0;
+        bool ok;
+    };
+    auto tile_of = [&](int tile) -> Tile {
+        Tile z;
+        const int y = tile / tiles_x, xg = tile - y * tiles_x;
+        z.limb = y / b.n_polys;
+        const int poly = y - z.limb * b.n_polys;
+        z.bi = poly / b.ppc;
+        z.r = poly - z.bi * b.ppc;
+        z.ok = limb_map(b, z.r, z.limb, z.t, z.pid);
+        z.data = b.ptr + (long long)z.bi * b.ct_stride + (long long)z.r * b.poly_stride + (long long)z.t * n;
+        z.src = z.data;
+        if (FIRST && f.src)
+            z.src = f.src + (long long)z.bi * f.src_ct + (long long)z.r * f.src_ps + (long long)z.t * n;
+        z.sub0 = xg * CB;
+        return z;
+    };
+    // 16-B chunks of a tile: COL: CB columns x T rows (row segments of CB words);
+    // ROW: CB chunks of T contiguous words
+    auto issue = [&](const Tile &z, uint64_t *dst) {
+        if (!z.ok) return;
+        constexpr int W = 2;  // words per 16-B chunk
+        const int per_row = COL ? CB / W : T / W;
+        const int total = COL ? T * per_row : CB * per_row;
+        for (int k = tid; k < total; k += blockDim.x) {
+            const int row = k / per_row, w = (k - row * per_row) * W;
+            if (COL) {
+                cp_async16(dst + row * CB + w, z.src + (long long)row * C + z.sub0 + w);
+            } else {
+                cp_async16(dst + row_sidx2<LOG_T>(row, w), z.src + (long long)(z.sub0 + row) * T + w);
+            }
+        }
+    };
+
+    int tile = blockIdx.x;
+    if (tile < n_tiles) issue(tile_of(tile), smem);
+    cp_async_commit();
+    for (int it = 0; tile < n_tiles; it++, tile += gridDim.x) {
+        const int nxt = tile + gridDim.x;
+        if (nxt < n_tiles) issue(tile_of(nxt), smem + ((it + 1) & 1) * TW);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const Tile z = tile_of(tile);
+        uint64_t *cur = smem + (it & 1) * TW;
+        if (z.ok) {
+            const PrimeConst pc = tb.pc[z.pid];
+            const uint64_t q = pc.q, two_q = pc.two_q;
+            const bool small = q < SRK_SMALL_Q;
+            const ulonglong2 *tw = (INV ? tb.itw : tb.tw) + (long long)z.pid * n;
+            const int sub = z.sub0 + sb;
+            const int base = COL ? 1 : (C + sub);
+            auto gaddr = [&](int c) -> long long {
+                return COL ? (long long)c * C + sub : (long long)sub * T + c;
+            };
+            uint64_t x[E];
+            if (!INV) {
+#pragma unroll
+                for (int e = 0; e < E; e++) x[e] = cur[sidx(u + TPS * e)];
+                if (small)
+                    FwdR1<E, LE1, true>::run(x, tw, base, q, two_q);
+                else
+                    FwdR1<E, LE1, false>::run(x, tw, base, q, two_q);
+#pragma unroll
+                for (int e = 0; e < E; e++) cur[sidx(u + TPS * e)] = x[e];
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; e++) x[e] = cur[sidx(u * E + e)];
+                if (small)
+                    FwdR2<E, TPS, LE1, LE2, true>::run(x, tw, base, u, q, two_q);
+                else
+                    FwdR2<E, TPS, LE1, LE2, false>::run(x, tw, base, u, q, two_q);
+                if (COL) {
+#pragma unroll
+                    for (int e = 0; e < E; e++) z.data[gaddr(u * E + e)] = x[e];
+                } else {
+                    __syncthreads();
+#pragma unroll
+                    for (int e = 0; e < E; e++) {
+                        uint64_t v = x[e];
+                        if (small)
+                            v -= mulhi64(v, pc.ratio_hi) * q;
+                        else
+                            v = v >= two_q ? v - two_q : v;
+                        v = v >= q ? v - q : v;
+                        cur[sidx(u * E + e)] = v;
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (int e = 0; e < E; e++) {
+                        const int c = u + TPS * e;
+                        fused_store<ST>(f, z.bi, z.r, z.t, z.limb, pc, gaddr(c), log_n, cur[sidx(c)],
+                                        z.data);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; e++) x[e] = cur[sidx(u * E + e)];
+                const int k0 = COL ? log_n - LOG_T : 0;
+                if (small)
+                    InvR1<E, LOG_T, LE1, true>::run(x, tw, base, u, q, two_q, k0);
+                else
+                    InvR1<E, LOG_T, LE1, false>::run(x, tw, base, u, q, two_q, k0);
+#pragma unroll
+                for (int e = 0; e < E; e++) cur[sidx(u * E + e)] = x[e];
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; e++) x[e] = cur[sidx(u + TPS * e)];
+                if (small)
+                    InvR2<E, TPS, LE2, true>::run(x, tw, base, q, two_q, k0 + LE1);
+                else
+                    InvR2<E, TPS, LE2, false>::run(x, tw, base, q, two_q, k0 + LE1);
+                if (COL) {
+                    uint64_t m = pc.ninv, ms = pc.ninv_shoup;
+                    if constexpr (ST == ST_SCALE) {
+                        m = f.mulc.w[z.limb];
+                        ms = f.mulc.ws[z.limb];
+                    }
+#pragma unroll
+                    for (int e = 0; e < E; e++) z.data[gaddr(u + TPS * e)] = mul_shoup(x[e], m, ms, q);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < E; e++) z.data[gaddr(u + TPS * e)] = x[e];
+                }
+            }
+        } else {
+            __syncthreads();  // keep the barrier count uniform across the CTA
+            if (!INV && !COL) {
+                __syncthreads();
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+}

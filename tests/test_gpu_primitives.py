@@ -262,3 +262,38 @@ def test_batched_ops_match_oracle(pair):
     got = host(gb, out).reshape(B, 2, lvl, n)
     for i in range(B):
         assert np.array_equal(got[i], orc.rescale(a[i], lvl)), i
+
+
+@pytest.mark.parametrize("chunk,pipe", [("4", "1"), ("4", "0"), ("1000", "0")])
+@pytest.mark.parametrize("name", ["toy", "cfg1"])
+def test_ntt_chunking_and_kernel_variants(name, chunk, pipe, require_cuda, monkeypatch):
+    """Force multi-chunk NTT launches and both pass kernels (persistent
+    double-buffered / one-tile-per-CTA): limbs must not change."""
+    from oracle.oracle import OracleCKKS
+    from paper_2412_15126_b200.backend_cuda import CudaBackend
+
+    monkeypatch.setenv("SRK_NTT_CHUNK", chunk)
+    monkeypatch.setenv("SRK_NTT_PIPE", pipe)
+    p = preset(name)
+    gb, orc = CudaBackend(p), OracleCKKS(p)
+    B, lvl, n = 9, p.max_level, p.ring_degree
+    ps = (lvl + 1) * n
+    a = rand_limbs(p, (B, 2), lvl, 50)
+    key = _key(p, 51)
+    g = pow(5, 7, 2 * n)
+    ta, tr = dev(gb, a), rot_layout(gb, key, g)
+    out = gb.empty_ct(lvl, polys=2 * B)
+    call(gb, "srk_rotate_batch", ptr(ta), 2 * ps, ptr(tr), ptr(out), 2 * ps, B, lvl, g,
+         gb.workspace(), gb.stream())
+    got = host(gb, out).reshape(B, 2, lvl + 1, n)
+    for i in (0, B - 1):
+        assert np.array_equal(got[i], orc.rotate_raw(a[i], key, g, lvl)), i
+    t = dev(gb, a)
+    call(gb, "srk_ntt", ptr(t), 2 * B, ps, lvl + 1, 0, 0, gb.stream())
+    call(gb, "srk_ntt", ptr(t), 2 * B, ps, lvl + 1, 0, 1, gb.stream())
+    assert np.array_equal(host(gb, t), a)
+    out = gb.empty_ct(lvl - 1, polys=2 * B)
+    call(gb, "srk_rescale_batch", ptr(ta), 2 * ps, ptr(out), 2 * lvl * n, B, lvl, gb.workspace(),
+         gb.stream())
+    got = host(gb, out).reshape(B, 2, lvl, n)
+    assert np.array_equal(got[B - 1], orc.rescale(a[B - 1], lvl))
