@@ -14,7 +14,8 @@ from ctypes import c_int, c_longlong, c_size_t, c_uint64, c_void_p, POINTER
 
 __all__ = ["lib", "LIB_PATH", "check", "SrkError", "EXPORTS"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslotrank_b200.so")
+LIB_PATH = os.environ.get("SRK_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                     "libslotrank_b200.so")
 
 _u64p = c_void_p  # device or host pointers passed as integers
 

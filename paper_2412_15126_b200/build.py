@@ -36,14 +36,15 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
-        cmd = [NVCC, *FLAGS, os.path.join(CSRC, "api.cu"), "-o", OUT + ".tmp"]
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    if force or out != OUT or needs_build():
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], os.path.join(CSRC, "api.cu"), "-o",
+               out + ".tmp"]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)
-        os.replace(OUT + ".tmp", OUT)
-    return OUT
+        os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

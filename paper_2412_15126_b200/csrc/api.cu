@@ -118,7 +118,7 @@ struct srk_ctx {
     LimbConsts lc_pmod;               // P mod prime_i (all primes)
     std::vector<LimbConsts> lc_qlinv; // [level]: q_level^-1 mod q_i
     int ntt_chunk = 128;              // limbs per L2-resident NTT chunk
-    bool ntt_pipe = true;             // persistent double-buffered passes
+    bool ntt_pipe = false;            // persistent double-buffered passes (SRK_NTT_PIPE=1)
 };
 
 template <typename T>
@@ -383,6 +383,9 @@ static FuseArgs no_fuse() {
     memset(&f, 0, sizeof f);
     f.galois = 1;
     f.add_galois = 1;
+    f.acc_galois = 1;
+    f.out_galois = 1;
+    f.out_galois_inv = 1;
     return f;
 }
 
@@ -754,6 +757,18 @@ extern "C" int srk_mul_plain_rescale(srk_ctx *c, const uint64_t *a, const uint64
 // out[o]: ct stride out_ct, c0 at +0, c1 at +out_ps.  add0 (gathered through
 // g when add_galois_is_g) and add1 are optional per-ciphertext addends.
 // ---------------------------------------------------------------------
+static uint64_t galois_inverse(const srk_ctx *c, uint64_t g) {
+    // (Z/2N)^* has order N, so g^-1 = g^(N-1) mod 2N
+    const uint64_t two_n = 2ull * c->n;
+    uint64_t r = 1, b = g % two_n, e = (uint64_t)c->n - 1;
+    while (e) {
+        if (e & 1) r = r * b % two_n;
+        b = b * b % two_n;
+        e >>= 1;
+    }
+    return r;
+}
+
 struct KsOut {
     uint64_t *out;
     long long out_ct, out_ps;
@@ -881,11 +896,10 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             f.src = acc + (long long)nl * n;
             f.src_ct = 2ll * ne * n;
             f.src_ps = (long long)ne * n;
-            f.galois = ko.galois;
             LimbBatch b = cbatch(zb, B, 2, 2ll * K * n, (long long)K * n, K, 0);
             b.split = 0;
             b.off_b = c->n_q;
-            TRY(ntt_run(c, b, true, f, ko.galois == 1 ? LD_PLAIN : LD_AUTO, ST_SCALE, s));
+            TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, s));
         }
         // 6. ModDown: rounding term once per coefficient, then NTT(conversion)
         //    with the combine in its store
@@ -910,11 +924,15 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             f.acc = acc;
             f.acc_ct = 2ll * ne * n;
             f.acc_ps = (long long)ne * n;
-            f.acc_galois = ko.galois;
+            // rotation: everything above ran in sigma_g^-1 space (rotation-layout key);
+            // exact ModDown commutes with sigma_g, so out = sigma_g(add + ModDown(acc'))
+            f.acc_galois = 1;
             f.add0 = ko.add0;
             f.add1 = ko.add1;
             f.add_ct = ko.add_ct;
-            f.add_galois = ko.gather_add0 ? ko.galois : 1;
+            f.add_galois = 1;
+            f.out_galois = ko.galois;
+            f.out_galois_inv = galois_inverse(c, ko.galois);
             f.mulc = c->lc_pinv;
             TRY(ntt_run(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), false, f,
                         LD_BCONV, ST_MODDOWN, s));
@@ -1082,6 +1100,7 @@ extern "C" int srk_keygen(srk_ctx *c, const uint64_t *s_ntt, const uint64_t *sfr
     }
     return SRK_OK;
 }
+
 
 // key (dnum x 2 x n_primes limbs) <- sigma_g^-1(key), limb by limb, via tmp (2 x n_primes limbs)
 extern "C" int srk_permute_key(srk_ctx *c, uint64_t *key, uint64_t galois, void *tmp_ws,

@@ -110,6 +110,8 @@ struct FuseArgs {
     const uint64_t *add0, *add1;
     long long add_ct;
     uint64_t add_galois;
+    uint64_t out_galois;     // ST_MODDOWN: write sigma_{out_galois}(result) (1 = identity);
+    uint64_t out_galois_inv; //   rows of T elements map to rows, staged through smem
     int pre_mode;            // 0 none, 1 per-limb constant, 2 plaintext
     const uint64_t *pt;      // [limbs][N]
     LimbConsts mulc;
@@ -339,6 +341,54 @@ __device__ __forceinline__ void fused_store(const FuseArgs &f, int bi, int r, in
     }
 }
 
+// Final phase of a forward row pass whose canonical results sit in smem
+// (sidx layout).  Plain/fused stores write each element in place; with
+// ST_MODDOWN and out_galois != 1 the combined values are first written back
+// to smem, then every row (chunk) is emitted permuted:
+//   out[m] = w[pi(m)],  pi = X -> X^out_galois on NTT slots,
+// which maps chunk sub to chunk d = pi^-1(sub*T) / T as a whole, so both the
+// reads (acc, add) and the writes stay coalesced.
+template <int LOG_T, int ST, typename SIdx>
+__device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm, SIdx sidx, int bi,
+                                                int r, int t, int limb, const PrimeConst &pc,
+                                                int sub, int u, int log_n, uint64_t *data) {
+    using S = NttShape<LOG_T>;
+    constexpr int T = S::T, E = S::E, TPS = S::TPS;
+    if constexpr (ST == ST_MODDOWN) {
+        if (f.out_galois != 1) {
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const int c = u + TPS * e;
+                const long long n = (long long)sub * T + c;
+                const long long nn = 1ll << log_n;
+                const long long off = (long long)t * nn + n;
+                uint64_t v = mul_shoup(sub_mod(f.acc[bi * f.acc_ct + r * f.acc_ps + off], sm[sidx(c)], pc.q),
+                                       f.mulc.w[limb], f.mulc.ws[limb], pc.q);
+                const uint64_t *ad = r == 0 ? f.add0 : f.add1;
+                if (ad) v = add_mod(v, ad[bi * f.add_ct + off], pc.q);
+                sm[sidx(c)] = v;
+            }
+            __syncthreads();
+            const long long nn = 1ll << log_n;
+            const int d = (int)(auto_index((uint32_t)((long long)sub * T), f.out_galois_inv, log_n) >> LOG_T);
+            uint64_t *o = f.out + bi * f.out_ct + r * f.out_ps + (long long)t * nn + (long long)d * T;
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const int c = u + TPS * e;
+                const int p = (int)(auto_index((uint32_t)((long long)d * T + c), f.out_galois, log_n) -
+                                    (uint32_t)sub * T);
+                o[c] = sm[sidx(p)];
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int c = u + TPS * e;
+        fused_store<ST>(f, bi, r, t, limb, pc, (long long)sub * T + c, log_n, sm[sidx(c)], data);
+    }
+}
+
 // One pass of the NTT.  COL = column pass (sub-transforms strided by C),
 // else row pass (contiguous chunks).  Grid: x = sub-transform groups of
 // one limb, y = (limb, poly) of the batch (poly fastest, so one prime's
@@ -448,11 +498,7 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
                 smem[sidx(u * E + e)] = v;
             }
             __syncthreads();
-#pragma unroll
-            for (int e = 0; e < E; e++) {
-                const int c = u + TPS * e;
-                fused_store<ST>(f, bi, r, t, limb, pc, gaddr(c), log_n, smem[sidx(c)], data);
-            }
+            row_final_store<LOG_T, ST>(f, smem, sidx, bi, r, t, limb, pc, sub, u, log_n, data);
         }
     } else {
         // ---- round 1: contiguous ownership, strides 1 .. E/2
@@ -646,12 +692,8 @@ __global__ void __launch_bounds__(256, 3)
                         cur[sidx(u * E + e)] = v;
                     }
                     __syncthreads();
-#pragma unroll
-                    for (int e = 0; e < E; e++) {
-                        const int c = u + TPS * e;
-                        fused_store<ST>(f, z.bi, z.r, z.t, z.limb, pc, gaddr(c), log_n, cur[sidx(c)],
-                                        z.data);
-                    }
+                    row_final_store<LOG_T, ST>(f, cur, sidx, z.bi, z.r, z.t, z.limb, pc, sub, u, log_n,
+                                               z.data);
                 }
             } else {
 #pragma unroll
@@ -688,6 +730,7 @@ __global__ void __launch_bounds__(256, 3)
             if (!INV && !COL) {
                 __syncthreads();
                 __syncthreads();
+                if (ST == ST_MODDOWN && f.out_galois != 1) __syncthreads();
             }
         }
         __syncthreads();
