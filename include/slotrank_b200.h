@@ -118,6 +118,17 @@ int srk_mul_relin_batch(srk_ctx *ctx, const uint64_t *a, const uint64_t *b, long
 int srk_rotate_batch(srk_ctx *ctx, const uint64_t *a, long long a_ct, const uint64_t *gkey,
                      uint64_t *out, long long out_ct, int batch, int level, uint64_t galois,
                      void *ws, void *stream);
+/* elementwise / plaintext ops over `batch` packed ciphertexts [batch][2][level+1][N] */
+int srk_addsub_batch(srk_ctx *ctx, const uint64_t *a, const uint64_t *b, uint64_t *out, int batch,
+                     int level, int op, void *stream);
+/* pt != NULL: plaintexts at stride pt_ct words (0 = shared); else constant k_res */
+int srk_add_plain_batch(srk_ctx *ctx, const uint64_t *a, const uint64_t *pt, long long pt_ct,
+                        const uint64_t *k_res, uint64_t *out, int batch, int level, void *stream);
+int srk_mul_const_rescale_batch(srk_ctx *ctx, const uint64_t *a, long long a_ct, int src_limbs,
+                                const uint64_t *k_res, uint64_t *out, int batch, int level, void *ws,
+                                void *stream);
+int srk_mul_plain_rescale_batch(srk_ctx *ctx, const uint64_t *a, const uint64_t *pt, long long pt_ct,
+                                uint64_t *out, int batch, int level, void *ws, void *stream);
 /* n_rot rotations of each of `batch` ciphertexts sharing one base extension
  * per ciphertext (hoisting); gkeys / galois / outs are HOST arrays (of device
  * pointers); rotation r of ciphertext b lands at outs[r] + b * out_ct */

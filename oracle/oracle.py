@@ -161,6 +161,25 @@ class OracleCKKS:
         return key
 
 
+def _batched(fn):
+    """Run a single-ciphertext oracle op over a batch (leading axis) element by element."""
+
+    def wrapper(self, a, *args, batch=None, each=False, **kw):
+        if batch is None:
+            return fn(self, a, *args, **kw)
+        outs = []
+        for i in range(batch):
+            rest = list(args)
+            if rest and isinstance(rest[0], np.ndarray) and rest[0].ndim == a.ndim:
+                rest[0] = rest[0][i]  # second ciphertext operand (add/sub/mul)
+            elif each and rest and isinstance(rest[0], np.ndarray):
+                rest[0] = rest[0][i]  # per-ciphertext plaintext
+            outs.append(fn(self, np.ascontiguousarray(a[i]), *rest, **kw))
+        return np.stack(outs)
+
+    return wrapper
+
+
 class OracleBackend:
     """CPU restatement of ``CudaBackend``'s surface (numpy uint64 arrays)."""
 
@@ -226,17 +245,20 @@ class OracleBackend:
     def encode_plain(self, coeffs, level):
         return self.o.small_to_ntt(coeffs, range(level + 1))
 
+    @_batched
     def addsub(self, a, b, level, op):
         out = np.empty((2, level + 1, self.n), dtype=_u64)
         self.o.L.orc_addsub(self.o.ctx, _p(a), _p(b) if b is not None else _p(a), _p(out), level, op)
         return out
 
+    @_batched
     def add_const(self, a, residues, level):
         out = np.empty_like(a)
         k = np.array([int(r) for r in residues], dtype=_u64)
         self.o.L.orc_add_const(self.o.ctx, _p(a), _p(k), _p(out), level)
         return out
 
+    @_batched
     def add_plain(self, a, pt, level):
         out = a.copy()
         q = np.array(self.params.q_primes[: level + 1], dtype=_u64)[:, None]
@@ -244,23 +266,36 @@ class OracleBackend:
         out[0] = np.where(s >= q, s - q, s)
         return out
 
+    @_batched
     def mul_const_rescale(self, a, src_level, residues, level):
         k = np.array([int(r) for r in residues], dtype=_u64)
         tmp = np.empty((2, level + 1, self.n), dtype=_u64)
         self.o.L.orc_mul_const(self.o.ctx, _p(a), src_level + 1, _p(k), _p(tmp), level)
         return self.o.rescale(tmp, level)
 
+    @_batched
     def mul_plain_rescale(self, a, pt, level):
         tmp = np.empty_like(a)
         self.o.L.orc_mul_plain(self.o.ctx, _p(a), _p(pt), _p(tmp), level)
         return self.o.rescale(tmp, level)
 
+    @_batched
     def mul_relin_rescale(self, a, b, level):
         prod = self.o.mul_relin(a, b, self.relin_key(), level)
         return self.o.rescale(prod, level)
 
+    @_batched
     def rotate(self, a, galois, level):
         return self.o.rotate_raw(a, self.galois_key(galois), galois, level)
+
+    def stack(self, datas):
+        return np.stack(datas)
+
+    def index(self, data, i):
+        return np.ascontiguousarray(data[i])
+
+    def stack_plain(self, pts):
+        return np.stack(pts)
 
     # collectives (paper_2412_15126_b200/shard.py) over gloo
     def as_tensor(self, data):

@@ -181,46 +181,66 @@ class CudaBackend:
         self._call("srk_encode_plain", _ptr(c), _ptr(pt), level, self.stream())
         return pt
 
-    def addsub(self, a, b, level: int, op: int) -> torch.Tensor:
-        out = self.empty_ct(level)
-        self._call("srk_addsub", _ptr(a), _ptr(b) if b is not None else 0, _ptr(out), level, op,
+    # batched ciphertexts: data [B][2][level+1][N]; batch=None -> [2][level+1][N]
+    def _out(self, level: int, batch) -> torch.Tensor:
+        shape = (2, level + 1, self.n) if batch is None else (batch, 2, level + 1, self.n)
+        return torch.empty(shape, dtype=torch.int64, device=self.device)
+
+    def stack(self, datas) -> torch.Tensor:
+        return torch.stack(datas)
+
+    def index(self, data, i: int) -> torch.Tensor:
+        return data[i]
+
+    def stack_plain(self, pts) -> torch.Tensor:
+        return torch.stack(pts)
+
+    def addsub(self, a, b, level: int, op: int, batch=None) -> torch.Tensor:
+        out = self._out(level, batch)
+        self._call("srk_addsub_batch", _ptr(a), _ptr(b) if b is not None else 0, _ptr(out), batch or 1,
+                   level, op, self.stream())
+        return out
+
+    def add_const(self, a, residues, level: int, batch=None) -> torch.Tensor:
+        out = self._out(level, batch)
+        self._call("srk_add_plain_batch", _ptr(a), 0, 0, _u64_array(residues), _ptr(out), batch or 1,
+                   level, self.stream())
+        return out
+
+    def add_plain(self, a, pt, level: int, batch=None, each=False) -> torch.Tensor:
+        out = self._out(level, batch)
+        pt_ct = (level + 1) * self.n if each else 0
+        self._call("srk_add_plain_batch", _ptr(a), _ptr(pt), pt_ct, None, _ptr(out), batch or 1, level,
                    self.stream())
         return out
 
-    def add_const(self, a, residues, level: int) -> torch.Tensor:
-        out = self.empty_ct(level)
-        self._call("srk_add_const", _ptr(a), _u64_array(residues), _ptr(out), level, self.stream())
-        return out
-
-    def add_plain(self, a, pt, level: int) -> torch.Tensor:
-        out = self.empty_ct(level)
-        self._call("srk_add_plain", _ptr(a), _ptr(pt), _ptr(out), level, self.stream())
-        return out
-
-    def mul_const_rescale(self, a, src_level: int, residues, level: int) -> torch.Tensor:
+    def mul_const_rescale(self, a, src_level: int, residues, level: int, batch=None) -> torch.Tensor:
         """rescale(view_level(a) * k): output at level-1."""
-        out = self.empty_ct(level - 1)
-        self._call("srk_mul_const_rescale", _ptr(a), src_level + 1, _u64_array(residues),
-                   _ptr(out), level, self.workspace(), self.stream())
+        out = self._out(level - 1, batch)
+        self._call("srk_mul_const_rescale_batch", _ptr(a), 2 * (src_level + 1) * self.n, src_level + 1,
+                   _u64_array(residues), _ptr(out), batch or 1, level, self.workspace(), self.stream())
         return out
 
-    def mul_plain_rescale(self, a, pt, level: int) -> torch.Tensor:
-        out = self.empty_ct(level - 1)
-        self._call("srk_mul_plain_rescale", _ptr(a), _ptr(pt), _ptr(out), level,
+    def mul_plain_rescale(self, a, pt, level: int, batch=None, each=False) -> torch.Tensor:
+        out = self._out(level - 1, batch)
+        pt_ct = (level + 1) * self.n if each else 0
+        self._call("srk_mul_plain_rescale_batch", _ptr(a), _ptr(pt), pt_ct, _ptr(out), batch or 1, level,
                    self.workspace(), self.stream())
         return out
 
-    def mul_relin_rescale(self, a, b, level: int) -> torch.Tensor:
-        out = self.empty_ct(level - 1)
-        self._call("srk_mul_relin_rescale", _ptr(a), _ptr(b), _ptr(self.relin_key()), _ptr(out),
-                   level, self.workspace(), self.stream())
+    def mul_relin_rescale(self, a, b, level: int, batch=None) -> torch.Tensor:
+        out = self._out(level - 1, batch)
+        ct = 2 * (level + 1) * self.n
+        self._call("srk_mul_relin_batch", _ptr(a), _ptr(b), ct, _ptr(self.relin_key()), _ptr(out),
+                   2 * level * self.n, batch or 1, level, 1, self.workspace(), self.stream())
         return out
 
-    def rotate(self, a, galois: int, level: int) -> torch.Tensor:
+    def rotate(self, a, galois: int, level: int, batch=None) -> torch.Tensor:
         key = self.galois_key(galois)
-        out = self.empty_ct(level)
-        self._call("srk_rotate", _ptr(a), _ptr(key), _ptr(out), level, galois, self.workspace(),
-                   self.stream())
+        out = self._out(level, batch)
+        ct = 2 * (level + 1) * self.n
+        self._call("srk_rotate_batch", _ptr(a), ct, _ptr(key), _ptr(out), ct, batch or 1, level, galois,
+                   self.workspace(), self.stream())
         return out
 
     def mod_drop(self, a, src_level: int, level: int) -> torch.Tensor:

@@ -577,7 +577,8 @@ extern "C" int srk_addsub(srk_ctx *c, const uint64_t *a, const uint64_t *b, uint
     TRY(check_level(c, level));
     if (op < 0 || op > 2) return fail(SRK_EINVAL, "bad op");
     const long long total = 2ll * (level + 1) * c->n;
-    k_addsub<<<grid_for(total, 2), 256, 0, S(stream)>>>(a, b, out, c->d_pc, c->log_n, level + 1, op);
+    k_addsub<<<grid_for(total, 2), 256, 0, S(stream)>>>(a, b, out, c->d_pc, c->log_n, level + 1, op,
+                                                        total);
     LAUNCHED();
     return SRK_OK;
 }
@@ -592,13 +593,24 @@ static LimbConsts host_consts(const srk_ctx *c, const uint64_t *k_res, int nl) {
     return lc;
 }
 
+extern "C" int srk_addsub_batch(srk_ctx *c, const uint64_t *a, const uint64_t *b, uint64_t *out,
+                                int batch, int level, int op, void *stream) {
+    TRY(check_level(c, level));
+    if (op < 0 || op > 2 || batch < 1) return fail(SRK_EINVAL, "bad op or batch");
+    const long long total = 2ll * batch * (level + 1) * c->n;
+    k_addsub<<<grid_for(total, 2), 256, 0, S(stream)>>>(a, b, out, c->d_pc, c->log_n, level + 1, op,
+                                                        total);
+    LAUNCHED();
+    return SRK_OK;
+}
+
 extern "C" int srk_add_const(srk_ctx *c, const uint64_t *a, const uint64_t *k_res, uint64_t *out,
                              int level, void *stream) {
     TRY(check_level(c, level));
     LimbConsts lc = host_consts(c, k_res, level + 1);
     const long long total = 2ll * (level + 1) * c->n;
-    k_add_plain<<<grid_for(total, 2), 256, 0, S(stream)>>>(a, nullptr, lc, out, c->d_pc, c->log_n,
-                                                           level + 1);
+    k_add_plain<<<grid_for(total, 2), 256, 0, S(stream)>>>(a, nullptr, 0, lc, out, c->d_pc, c->log_n,
+                                                           level + 1, 1);
     LAUNCHED();
     return SRK_OK;
 }
@@ -609,8 +621,27 @@ extern "C" int srk_add_plain(srk_ctx *c, const uint64_t *a, const uint64_t *pt, 
     LimbConsts lc;
     memset(&lc, 0, sizeof lc);
     const long long total = 2ll * (level + 1) * c->n;
-    k_add_plain<<<grid_for(total, 2), 256, 0, S(stream)>>>(a, pt, lc, out, c->d_pc, c->log_n,
-                                                           level + 1);
+    k_add_plain<<<grid_for(total, 2), 256, 0, S(stream)>>>(a, pt, 0, lc, out, c->d_pc, c->log_n,
+                                                           level + 1, 1);
+    LAUNCHED();
+    return SRK_OK;
+}
+
+// batched add of a constant (pt == NULL, residues k_res) or plaintexts pt
+// (stride pt_ct words, 0 = one plaintext for all) to poly 0 of every ciphertext
+extern "C" int srk_add_plain_batch(srk_ctx *c, const uint64_t *a, const uint64_t *pt, long long pt_ct,
+                                   const uint64_t *k_res, uint64_t *out, int batch, int level,
+                                   void *stream) {
+    TRY(check_level(c, level));
+    LimbConsts lc;
+    memset(&lc, 0, sizeof lc);
+    if (!pt) {
+        if (!k_res) return fail(SRK_EINVAL, "need a plaintext or constant residues");
+        lc = host_consts(c, k_res, level + 1);
+    }
+    const long long total = 2ll * batch * (level + 1) * c->n;
+    k_add_plain<<<grid_for(total, 2), 256, 0, S(stream)>>>(a, pt, pt_ct, lc, out, c->d_pc, c->log_n,
+                                                           level + 1, batch);
     LAUNCHED();
     return SRK_OK;
 }
@@ -658,7 +689,7 @@ extern "C" int srk_tensor(srk_ctx *c, const uint64_t *a, const uint64_t *b, uint
 // ---------------------------------------------------------------------
 static int rescale_impl(srk_ctx *c, const uint64_t *a, long long a_ct, long long a_ps,
                         const uint64_t *pt, const LimbConsts *k, uint64_t *out, long long out_ct,
-                        int level, int B, uint64_t *ws, cudaStream_t s) {
+                        int level, int B, uint64_t *ws, cudaStream_t s, long long pt_ct = 0) {
     if (level < 1) return fail(SRK_EINVAL, "cannot rescale a level-0 ciphertext");
     const long long n = c->n;
     uint64_t *top = ws;              // [B][2][N]
@@ -667,7 +698,7 @@ static int rescale_impl(srk_ctx *c, const uint64_t *a, long long a_ct, long long
     FuseArgs f = no_fuse();
     LimbBatch bt = cbatch(top, B, 2, 2 * n, n, 1, level);
     if (mode == 2) {
-        k_rescale_top<<<grid_for(2ll * B * n), 256, 0, s>>>(a, a_ct, a_ps, pt, top, c->d_pc,
+        k_rescale_top<<<grid_for(2ll * B * n), 256, 0, s>>>(a, a_ct, a_ps, pt, pt_ct, top, c->d_pc,
                                                              c->log_n, level, B);
         LAUNCHED();
         TRY(ntt_run(c, bt, true, f, LD_PLAIN, ST_PLAIN, s));
@@ -696,6 +727,7 @@ static int rescale_impl(srk_ctx *c, const uint64_t *a, long long a_ct, long long
     g.acc_ps = a_ps;
     g.pre_mode = mode;
     g.pt = pt;
+    g.pt_ct = pt_ct;
     if (k) g.pre = *k;
     g.mulc = c->lc_qlinv[level];
     LimbBatch bq = cbatch(tb, B, 2, 2ll * level * n, (long long)level * n, level, 0);
@@ -734,6 +766,34 @@ extern "C" int srk_mul_const_rescale(srk_ctx *c, const uint64_t *a, int src_limb
     const long long ps = (long long)src_limbs * c->n;
     return rescale_impl(c, a, 2 * ps, ps, nullptr, &lc, out, 2ll * level * c->n, level, 1,
                         (uint64_t *)ws, S(stream));
+}
+
+// batch versions: a at ct stride a_ct read as a level-`level` view (src_limbs
+// limbs per poly); outputs packed [batch][2][level][N]
+extern "C" int srk_mul_const_rescale_batch(srk_ctx *c, const uint64_t *a, long long a_ct, int src_limbs,
+                                           const uint64_t *k_res, uint64_t *out, int batch, int level,
+                                           void *ws, void *stream) {
+    TRY(check_level(c, level));
+    if (src_limbs < level + 1) return fail(SRK_EINVAL, "source has fewer limbs than level+1");
+    LimbConsts lc = host_consts(c, k_res, level + 1);
+    const long long ps = (long long)src_limbs * c->n, oct = 2ll * level * c->n;
+    FOR_CHUNKS(batch, b0, nb) {
+        TRY(rescale_impl(c, a + b0 * a_ct, a_ct, ps, nullptr, &lc, out + b0 * oct, oct, level, nb,
+                         (uint64_t *)ws, S(stream)));
+    }
+    return SRK_OK;
+}
+
+extern "C" int srk_mul_plain_rescale_batch(srk_ctx *c, const uint64_t *a, const uint64_t *pt,
+                                           long long pt_ct, uint64_t *out, int batch, int level,
+                                           void *ws, void *stream) {
+    TRY(check_level(c, level));
+    const long long ps = (long long)(level + 1) * c->n, oct = 2ll * level * c->n;
+    FOR_CHUNKS(batch, b0, nb) {
+        TRY(rescale_impl(c, a + b0 * 2 * ps, 2 * ps, ps, pt + b0 * pt_ct, nullptr, out + b0 * oct, oct,
+                         level, nb, (uint64_t *)ws, S(stream), pt_ct));
+    }
+    return SRK_OK;
 }
 
 extern "C" int srk_mul_plain_rescale(srk_ctx *c, const uint64_t *a, const uint64_t *pt,

@@ -17,9 +17,7 @@
 // op 0: a+b, 1: a-b, 2: -a
 __global__ void k_addsub(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
                          uint64_t *__restrict__ out, const PrimeConst *__restrict__ pc, int log_n,
-                         int nl, int op) {
-    const long long n = 1ll << log_n;
-    const long long total = 2ll * nl * n;
+                         int nl, int op, long long total) {
     for (long long x = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; x < total;
          x += (long long)gridDim.x * blockDim.x * 2) {
         const int limb = (int)((x >> log_n) % nl);
@@ -43,22 +41,25 @@ __global__ void k_addsub(const uint64_t *__restrict__ a, const uint64_t *__restr
     }
 }
 
-// out = a + (poly0: pt or const k[limb]); poly1 copied.  pt == nullptr -> const
+// out = a + (poly0: pt or const k[limb]); poly1 copied.  pt == nullptr -> const.
+// a/out: [batch][2][nl][N]; pt: [nl][N] per ciphertext at stride pt_ct (0 = shared)
 __global__ void k_add_plain(const uint64_t *__restrict__ a, const uint64_t *__restrict__ pt,
-                            LimbConsts k, uint64_t *__restrict__ out,
-                            const PrimeConst *__restrict__ pc, int log_n, int nl) {
+                            long long pt_ct, LimbConsts k, uint64_t *__restrict__ out,
+                            const PrimeConst *__restrict__ pc, int log_n, int nl, int batch) {
     const long long n = 1ll << log_n;
-    const long long total = 2ll * nl * n;
+    const long long per = 2ll * nl * n;
+    const long long total = per * batch;
     for (long long x = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; x < total;
          x += (long long)gridDim.x * blockDim.x * 2) {
-        const long long limb_all = x >> log_n;
+        const long long b = x / per, xi = x - b * per;
+        const long long limb_all = xi >> log_n;
         ulonglong2 va = *reinterpret_cast<const ulonglong2 *>(a + x);
         if (limb_all < nl) {
             const int limb = (int)limb_all;
             const uint64_t q = pc[limb].q;
             ulonglong2 vb;
             if (pt) {
-                vb = *reinterpret_cast<const ulonglong2 *>(pt + x);
+                vb = *reinterpret_cast<const ulonglong2 *>(pt + b * pt_ct + xi);
             } else {
                 vb.x = vb.y = k.w[limb];
             }
@@ -120,7 +121,7 @@ __global__ void k_tensor(const uint64_t *__restrict__ a, const uint64_t *__restr
 // top[b][p] = a[b][p][level] * pt[level]   (rescale of a ct x pt product:
 // the dropped limb of the product, before its INTT)
 __global__ void k_rescale_top(const uint64_t *__restrict__ a, long long a_ct, long long a_ps,
-                              const uint64_t *__restrict__ pt, uint64_t *__restrict__ top,
+                              const uint64_t *__restrict__ pt, long long pt_ct, uint64_t *__restrict__ top,
                               const PrimeConst *__restrict__ pc, int log_n, int level, int batch) {
     const long long n = 1ll << log_n;
     const PrimeConst P = pc[level];
@@ -130,7 +131,7 @@ __global__ void k_rescale_top(const uint64_t *__restrict__ a, long long a_ct, lo
         const int b = (int)(bp >> 1), p = (int)(bp & 1);
         const long long off = x & (n - 1);
         top[x] = mul_mod(a[b * a_ct + p * a_ps + (long long)level * n + off],
-                         pt[(long long)level * n + off], P);
+                         pt[b * pt_ct + (long long)level * n + off], P);
     }
 }
 

@@ -113,7 +113,8 @@ struct FuseArgs {
     uint64_t out_galois;     // ST_MODDOWN: write sigma_{out_galois}(result) (1 = identity);
     uint64_t out_galois_inv; //   rows of T elements map to rows, staged through smem
     int pre_mode;            // 0 none, 1 per-limb constant, 2 plaintext
-    const uint64_t *pt;      // [limbs][N]
+    const uint64_t *pt;      // [limbs][N] per ciphertext at stride pt_ct (0 = shared)
+    long long pt_ct;
     LimbConsts mulc;
     LimbConsts pre;
 };
@@ -324,7 +325,7 @@ __device__ __forceinline__ void fused_store(const FuseArgs &f, int bi, int r, in
         uint64_t v;
         if constexpr (ST == ST_RESCALE) {
             if (f.pre_mode == 1) a = mul_shoup(a, f.pre.w[limb], f.pre.ws[limb], P.q);
-            if (f.pre_mode == 2) a = mul_mod(a, __ldg(f.pt + off), P);
+            if (f.pre_mode == 2) a = mul_mod(a, __ldg(f.pt + bi * f.pt_ct + off), P);
             v = mul_shoup(sub_mod(a, x, P.q), f.mulc.w[limb], f.mulc.ws[limb], P.q);
         } else {
             v = mul_shoup(sub_mod(a, x, P.q), f.mulc.w[limb], f.mulc.ws[limb], P.q);

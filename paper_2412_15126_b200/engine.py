@@ -83,18 +83,26 @@ class DepthBudgetError(EngineError):
 
 
 class Ciphertext:
-    """Device limbs + remaining level + rotation-chain tag.  Immutable by contract."""
+    """Device limbs + remaining level + rotation-chain tag.  Immutable by contract.
 
-    __slots__ = ("data", "level", "rot_chain", "params")
+    ``batch`` is None for one ciphertext (limbs [2][level+1][N]) or B for a
+    stack of B ciphertexts evaluated in lock step (limbs [B][2][level+1][N]):
+    every engine op then runs as ONE batched kernel sequence and is counted B
+    times, exactly as B separate calls would be (``CKKSEngineCore.stack``).
+    """
 
-    def __init__(self, data, level: int, rot_chain: int, params: CKKSParams):
+    __slots__ = ("data", "level", "rot_chain", "params", "batch")
+
+    def __init__(self, data, level: int, rot_chain: int, params: CKKSParams, batch: int | None = None):
         self.data = data
         self.level = level
         self.rot_chain = rot_chain
         self.params = params
+        self.batch = batch
 
     def __repr__(self):
-        return f"Ciphertext(level={self.level}, ring=2^{self.params.log_n}, rot_chain={self.rot_chain})"
+        b = "" if self.batch is None else f", batch={self.batch}"
+        return f"Ciphertext(level={self.level}, ring=2^{self.params.log_n}, rot_chain={self.rot_chain}{b})"
 
 
 @dataclass(frozen=True)
@@ -189,12 +197,40 @@ class CKKSEngineCore:
                     f"ciphertext parameters {c.params.name} do not match engine {self.params.name}"
                 )
 
-    def _emit(self, data, level: int, rot_chain: int) -> Ciphertext:
+    def _emit(self, data, level: int, rot_chain: int, batch: int | None = None) -> Ciphertext:
         consumed = self.params.max_level - level
         with self._lock:
             if consumed > self._levels:
                 self._levels = consumed
-        return Ciphertext(data, level, rot_chain, self.params)
+        return Ciphertext(data, level, rot_chain, self.params, batch)
+
+    @staticmethod
+    def _nb(*cts) -> int | None:
+        """Common batch size of the operands (None = single ciphertexts)."""
+        sizes = {c.batch for c in cts}
+        if len(sizes) != 1:
+            raise ValueError(f"mixed batch sizes {sorted(map(str, sizes))}")
+        return sizes.pop()
+
+    # ------------------------------------------------------------------
+    # batches of ciphertexts evaluated in lock step
+    # ------------------------------------------------------------------
+    def stack(self, cts) -> Ciphertext:
+        """One batched ciphertext from single ones (aligned to their min level)."""
+        cts = list(cts)
+        self._check(*cts)
+        if any(c.batch is not None for c in cts):
+            raise ValueError("stack takes single ciphertexts")
+        level = min(c.level for c in cts)
+        datas = [self._align(c, level) for c in cts]
+        return self._emit(self.backend.stack(datas), level, max(c.rot_chain for c in cts), len(cts))
+
+    def unstack(self, ct: Ciphertext) -> list:
+        """Single ciphertexts viewing the limbs of a batched one."""
+        if ct.batch is None:
+            return [ct]
+        return [Ciphertext(self.backend.index(ct.data, i), ct.level, ct.rot_chain, self.params)
+                for i in range(ct.batch)]
 
     def _residues(self, k: int, level: int) -> list[int]:
         return [k % q for q in self.params.q_primes[: level + 1]]
@@ -205,11 +241,12 @@ class CKKSEngineCore:
             return ct.data
         p = self.params
         k = int(round(p.scales[level] * p.q_primes[level + 1] / p.scales[ct.level]))
-        return self.backend.mul_const_rescale(ct.data, ct.level, self._residues(k, level + 1), level + 1)
+        return self.backend.mul_const_rescale(ct.data, ct.level, self._residues(k, level + 1), level + 1,
+                                              batch=ct.batch)
 
     def at_level(self, ct: Ciphertext, level: int) -> Ciphertext:
         """``ct`` brought down to ``level`` (scale-preserving; not counted, like the min rule)."""
-        return self._emit(self._align(ct, level), level, ct.rot_chain)
+        return self._emit(self._align(ct, level), level, ct.rot_chain, ct.batch)
 
     def wrap(self, data, level: int, rot_chain: int = 0) -> Ciphertext:
         """Ciphertext around backend limbs produced outside the engine (collectives)."""
@@ -226,6 +263,25 @@ class CKKSEngineCore:
         if arr.size and arr.min() == arr.max():
             return float(arr.flat[0])
         return None
+
+    def _batch_plain(self, p, batch):
+        """('const', c) | ('vec', vector) | ('each', [B, slots] array) for plaintext p."""
+        if batch is not None and not np.isscalar(p):
+            arr = np.asarray(p, dtype=np.float64)
+            if arr.ndim == 2:
+                if arr.shape != (batch, self.params.slot_count):
+                    raise ValueError(f"per-ciphertext plaintexts must be [{batch}, {self.params.slot_count}]")
+                return "each", arr
+        c = self._as_constant(p)
+        if c is not None:
+            if isinstance(p, np.ndarray) and p.size != self.params.slot_count:
+                self.plain(p)
+            return "const", c
+        return "vec", self.plain(p)
+
+    def _encode_each(self, arr: np.ndarray, scale: float, level: int):
+        return self.backend.stack_plain([self._encode_cached(np.ascontiguousarray(v), scale, level)
+                                         for v in arr])
 
     def _encode_cached(self, vec: np.ndarray, scale: float, level: int):
         if vec.flags.writeable:
@@ -271,7 +327,10 @@ class CKKSEngineCore:
         return Ciphertext(data, level, 0, p)
 
     def decrypt(self, ct: Ciphertext) -> np.ndarray:
+        """Slot vector (or [B, slots] for a batched ciphertext)."""
         self._check(ct)
+        if ct.batch is not None:
+            return np.stack([self.decrypt(c) for c in self.unstack(ct)])
         coeffs = self.backend.decrypt_limb0(ct.data, ct.level)
         return self.encoder.decode(coeffs.astype(np.float64) / self.params.scales[ct.level])
 
@@ -291,11 +350,12 @@ class CKKSEngineCore:
     # ------------------------------------------------------------------
     def _addsub(self, x: Ciphertext, y: Ciphertext, op: int) -> Ciphertext:
         self._check(x, y)
+        nb = self._nb(x, y)
         level = min(x.level, y.level)
-        data = self.backend.addsub(self._align(x, level), self._align(y, level), level, op)
+        data = self.backend.addsub(self._align(x, level), self._align(y, level), level, op, batch=nb)
         with self._lock:
-            self._adds += 1
-        return self._emit(data, level, max(x.rot_chain, y.rot_chain))
+            self._adds += nb or 1
+        return self._emit(data, level, max(x.rot_chain, y.rot_chain), nb)
 
     def add(self, x: Ciphertext, y: Ciphertext) -> Ciphertext:
         return self._addsub(x, y, 0)
@@ -305,75 +365,80 @@ class CKKSEngineCore:
 
     def negate(self, x: Ciphertext) -> Ciphertext:
         self._check(x)
-        data = self.backend.addsub(x.data, None, x.level, 2)
-        return self._emit(data, x.level, x.rot_chain)
+        data = self.backend.addsub(x.data, None, x.level, 2, batch=x.batch)
+        return self._emit(data, x.level, x.rot_chain, x.batch)
 
     def add_plain(self, x: Ciphertext, p) -> Ciphertext:
+        """x + p; for a batched x, p may also be a [B, slots] array (one plaintext each)."""
         self._check(x)
-        level = x.level
-        c = self._as_constant(p)
-        if c is not None:
-            if isinstance(p, np.ndarray) and p.size != self.params.slot_count:
-                self.plain(p)  # raises the reference's ValueError
-            k = int(round(c * self.params.scales[level]))
-            data = self.backend.add_const(x.data, self._residues(k, level), level)
+        level, nb = x.level, x.batch
+        kind, val = self._batch_plain(p, nb)
+        if kind == "const":
+            k = int(round(val * self.params.scales[level]))
+            data = self.backend.add_const(x.data, self._residues(k, level), level, batch=nb)
+        elif kind == "vec":
+            pt = self._encode_cached(val, self.params.scales[level], level)
+            data = self.backend.add_plain(x.data, pt, level, batch=nb)
         else:
-            vec = self.plain(p)
-            pt = self._encode_cached(vec, self.params.scales[level], level)
-            data = self.backend.add_plain(x.data, pt, level)
+            pts = self._encode_each(val, self.params.scales[level], level)
+            data = self.backend.add_plain(x.data, pts, level, batch=nb, each=True)
         with self._lock:
-            self._adds += 1
-        return self._emit(data, level, x.rot_chain)
+            self._adds += nb or 1
+        return self._emit(data, level, x.rot_chain, nb)
 
     def mul(self, x: Ciphertext, y: Ciphertext, site: str = "mul") -> Ciphertext:
         self._check(x, y)
+        nb = self._nb(x, y)
         level = min(x.level, y.level)
         if level < 1:
             raise DepthBudgetError(site, level)
         a = self._align(x, level)
         b = a if y is x else self._align(y, level)
-        data = self.backend.mul_relin_rescale(a, b, level)
+        data = self.backend.mul_relin_rescale(a, b, level, batch=nb)
         with self._lock:
-            self._ctct += 1
-        return self._emit(data, level - 1, max(x.rot_chain, y.rot_chain))
+            self._ctct += nb or 1
+        return self._emit(data, level - 1, max(x.rot_chain, y.rot_chain), nb)
 
     supports_mul_plain_level = True
 
     def mul_plain(self, x: Ciphertext, p, site: str = "mul_plain", level: int | None = None) -> Ciphertext:
         """x * p, one level down -- or, for a scalar p and ``level`` < x.level - 1,
         straight to ``level`` in the same single rescale (the simulator's
-        mul_plain followed by the min-level rule of a later add)."""
+        mul_plain followed by the min-level rule of a later add).  A batched x
+        may take a [B, slots] array of per-ciphertext plaintexts."""
         self._check(x)
         if x.level < 1:
             raise DepthBudgetError(site, x.level)
         pr = self.params
-        c = self._as_constant(p)
+        nb = x.batch
+        kind, val = self._batch_plain(p, nb)
         if level is not None and level < x.level - 1:
-            if c is None:
+            if kind != "const":
                 raise ValueError("mul_plain(level=...) takes a scalar plaintext")
             if level < 0:
                 raise DepthBudgetError(site, x.level, x.level - level)
             # drop to level+1 limbs, multiply by round(c * scales[level] q_{level+1} / scales[x]),
             # rescale by q_{level+1}  -> scale scales[level]
-            k = int(round(c * pr.scales[level] * pr.q_primes[level + 1] / pr.scales[x.level]))
-            data = self.backend.mul_const_rescale(x.data, x.level, self._residues(k, level + 1), level + 1)
+            k = int(round(val * pr.scales[level] * pr.q_primes[level + 1] / pr.scales[x.level]))
+            data = self.backend.mul_const_rescale(x.data, x.level, self._residues(k, level + 1), level + 1,
+                                                  batch=nb)
             with self._lock:
-                self._ctpt += 1
-            return self._emit(data, level, x.rot_chain)
+                self._ctpt += nb or 1
+            return self._emit(data, level, x.rot_chain, nb)
         level = x.level
         pt_scale = pr.scales[level - 1] * pr.q_primes[level] / pr.scales[level]
-        if c is not None:
-            if isinstance(p, np.ndarray) and p.size != pr.slot_count:
-                self.plain(p)
-            k = int(round(c * pt_scale))
-            data = self.backend.mul_const_rescale(x.data, level, self._residues(k, level), level)
+        if kind == "const":
+            k = int(round(val * pt_scale))
+            data = self.backend.mul_const_rescale(x.data, level, self._residues(k, level), level, batch=nb)
+        elif kind == "vec":
+            pt = self._encode_cached(val, pt_scale, level)
+            data = self.backend.mul_plain_rescale(x.data, pt, level, batch=nb)
         else:
-            vec = self.plain(p)
-            pt = self._encode_cached(vec, pt_scale, level)
-            data = self.backend.mul_plain_rescale(x.data, pt, level)
+            pts = self._encode_each(val, pt_scale, level)
+            data = self.backend.mul_plain_rescale(x.data, pts, level, batch=nb, each=True)
         with self._lock:
-            self._ctpt += 1
-        return self._emit(data, level - 1, x.rot_chain)
+            self._ctpt += nb or 1
+        return self._emit(data, level - 1, x.rot_chain, nb)
 
     def rotate(self, x: Ciphertext, k: int) -> Ciphertext:
         """Cyclic rotation of the slot vector; k > 0 rotates left (``engine.py:234``)."""
@@ -383,14 +448,14 @@ class CKKSEngineCore:
         if k_eff == 0:
             return x
         galois = pow(5, k_eff, 2 * self.params.ring_degree)
-        data = self.backend.rotate(x.data, galois, x.level)
+        data = self.backend.rotate(x.data, galois, x.level, batch=x.batch)
         chain = x.rot_chain + 1
         with self._lock:
-            self._rotations += 1
+            self._rotations += x.batch or 1
             if chain > self._critical:
                 self._critical = chain
-            self.trace.append(("rotate", k_eff))
-        return self._emit(data, x.level, chain)
+            self.trace.extend([("rotate", k_eff)] * (x.batch or 1))
+        return self._emit(data, x.level, chain, x.batch)
 
     def ideal_map(self, fn, *cts: Ciphertext, levels: int = 0, site: str = "ideal_map") -> Ciphertext:
         """Only constant slot functions have an encrypted realisation.

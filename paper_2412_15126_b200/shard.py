@@ -26,6 +26,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 from .chebyshev import KernelConfig, equality_from_compare, with_input_range
 from .matrix import MatrixLayout, replicate, sum_axis, transpose_vector
 from .ranking import (
@@ -34,13 +36,15 @@ from .ranking import (
     _triangle_mask,
     _prefix_vector,
     block_pairs,
-    compare_block_pair,
+    compare_block_pairs,
     finish_block_rank,
     lower_partial,
     replicated_blocks,
     upper_partial,
 )
-from .sorting import SortConfig, place_block
+from .chebyshev import indicator_kernel
+from .ranking import batched
+from .sorting import SortConfig, _neg_rank_targets, common_level, place_block
 
 __all__ = ["Comm", "multi_rank_sharded", "multi_sort_sharded"]
 
@@ -114,8 +118,7 @@ def multi_rank_sharded(engine, bv: BlockVector, cfg: KernelConfig, comm: Comm, *
     rows, cols = replicated_blocks(engine, bv, layout)
     pairs = block_pairs(count)
     mine = [p for idx, p in enumerate(pairs) if comm.owner(idx) == comm.rank]
-    comparisons = {p: compare_block_pair(engine, p, rows, cols, cfg, layout, count, valid_last)
-                   for p in mine}
+    comparisons = compare_block_pairs(engine, mine, rows, cols, cfg, layout, count, valid_last)
     equalities = {p: equality_from_compare(engine, c) for p, c in comparisons.items()} if tie_correction else {}
     blocks = []
     for i in range(count):
@@ -185,15 +188,32 @@ def multi_sort_sharded(engine, bv: BlockVector, cfg: SortConfig, comm: Comm) -> 
     window = with_input_range(cfg.kernel, -float(b * count), float(b * count))
     units = [(i, j) for i in range(count) for j in range(count)]
     mine = [u for idx, u in enumerate(units) if comm.owner(idx) == comm.rank]
+    rank_blocks = common_level(engine, ranking.ranks.blocks)
     needed = sorted({j for _, j in mine})
-    spreads = {j: replicate(engine, ranking.ranks.blocks[j], layout, "row") for j in needed}
+    if batched(engine) and len(needed) > 1:
+        spread_list = engine.unstack(replicate(engine, engine.stack([rank_blocks[j] for j in needed]),
+                                               layout, "row"))
+        spreads = dict(zip(needed, spread_list))
+    else:
+        spreads = {j: replicate(engine, rank_blocks[j], layout, "row") for j in needed}
+    placed_all = {}
+    if batched(engine) and len(mine) > 1:
+        targets = np.stack([_neg_rank_targets(layout.slot_count, b, "row", b * i + 1) for i, _ in mine])
+        shifted = engine.add_plain(engine.stack([spreads[j] for _, j in mine]), targets)
+        sel = indicator_kernel(engine, shifted, -0.5, 0.5, window, boundary="open")
+        for _ in range(len(mine) - 1):
+            engine.note_indicator_eval()
+        prod = engine.mul(sel, engine.stack([ranking.row_replicated[j] for _, j in mine]), site="sort-place")
+        placed_all = dict(zip(mine, engine.unstack(prod)))
     out = []
     for i in range(count):
         acc = None
         for (ii, j) in mine:
             if ii != i:
                 continue
-            placed = place_block(engine, spreads[j], ranking.row_replicated[j], i, layout, window)
+            placed = placed_all.get((ii, j))
+            if placed is None:
+                placed = place_block(engine, spreads[j], ranking.row_replicated[j], i, layout, window)
             acc = placed if acc is None else engine.add(acc, placed)
         acc = _sum_across(engine, acc, comm)
         owner = comm.owner(i)
