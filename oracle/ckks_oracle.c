@@ -324,21 +324,19 @@ void orc_automorph(const orc_ctx *c, const uint64_t *a, uint64_t *out, int n_lim
 
 static inline uint32_t auto_index(uint32_t k, uint64_t g, int log_n);
 
-/* d: uint64[level+1][N] NTT form.  key: uint64[dnum][2][n_q+n_p][N].
- * out0/out1: uint64[level+1][N] NTT form, <(out0,out1),(1,s)> ~ sigma_g(d) * s_from,
- * where sigma_g (X -> X^galois, galois = 1: identity) is applied to the
- * ModUp-extended digits -- i.e. after base extension, so several rotations
- * of one ciphertext can share the extension (hoisting). */
-void orc_keyswitch_g(const orc_ctx *c, const uint64_t *d, const uint64_t *key, uint64_t *out0,
-                     uint64_t *out1, int level, uint64_t galois) {
+/* Base-extend d (uint64[level+1][N], NTT form) digit by digit and take the
+ * inner product with the switching key: acc[r] over the extended basis
+ * Q_level u P (uint64[2][level+1+K][N]).  galois != 1 applies X -> X^galois
+ * to the extended digits (after base extension, so rotations of one
+ * ciphertext can share it). */
+static void ks_inner_acc(const orc_ctx *c, const uint64_t *d, const uint64_t *key, int level,
+                         uint64_t galois, uint64_t *acc) {
     const int n = c->n, nl = level + 1, K = c->n_p, ne = nl + K, np_all = c->n_primes;
     const int alpha = c->alpha, beta = (nl + alpha - 1) / alpha;
     uint64_t *dc = (uint64_t *)malloc(sizeof(uint64_t) * nl * n);
     memcpy(dc, d, sizeof(uint64_t) * nl * n);
     for (int i = 0; i < nl; i++) intt_limb(c, dc + (size_t)i * n, i);
-
-    uint64_t *acc[2];
-    for (int r = 0; r < 2; r++) acc[r] = (uint64_t *)calloc((size_t)ne * n, sizeof(uint64_t));
+    memset(acc, 0, sizeof(uint64_t) * 2 * ne * n);
     uint64_t *ext = (uint64_t *)malloc(sizeof(uint64_t) * ne * n);
 
     for (int jd = 0; jd < beta; jd++) {
@@ -393,7 +391,7 @@ void orc_keyswitch_g(const orc_ctx *c, const uint64_t *d, const uint64_t *key, u
             const uint64_t p = c->prime[pid];
             for (int r = 0; r < 2; r++) {
                 const uint64_t *kk = key + (((size_t)jd * 2 + r) * np_all + pid) * n;
-                uint64_t *ac = acc[r] + (size_t)t * n;
+                uint64_t *ac = acc + ((size_t)r * ne + t) * n;
                 const uint64_t *e = ext + (size_t)t * n;
                 for (int j = 0; j < n; j++) ac[j] = addmod(ac[j], mulmod(e[j], kk[j], p), p);
             }
@@ -401,62 +399,120 @@ void orc_keyswitch_g(const orc_ctx *c, const uint64_t *d, const uint64_t *key, u
     }
     free(ext);
     free(dc);
+}
 
-    /* ModDown: out_i = (acc_i - conv_P->q_i(acc_P)) * P^-1 */
-    for (int r = 0; r < 2; r++) {
-        uint64_t *a = acc[r];
-        uint64_t *z = (uint64_t *)malloc(sizeof(uint64_t) * K * n);
-        for (int k = 0; k < K; k++) {
-            const int pid = c->n_q + k;
-            const uint64_t p = c->prime[pid];
-            memcpy(z + (size_t)k * n, a + (size_t)(nl + k) * n, sizeof(uint64_t) * n);
-            intt_limb(c, z + (size_t)k * n, pid);
-            uint64_t phat = 1;
-            for (int m = 0; m < K; m++)
-                if (m != k) phat = mulmod(phat, c->prime[c->n_q + m] % p, p);
-            const uint64_t phinv = invmod(phat, p);
-            for (int j = 0; j < n; j++) z[(size_t)k * n + j] = mulmod(z[(size_t)k * n + j], phinv, p);
+/* Exact ModDown over a special basis S (ns limbs, prime ids sid[]):
+ * xs[k] (NTT form, under prime sid[k]); xq[i] (NTT form, i < no, prime i);
+ * out[i] = (xq_i - conv_S->q_i(xs)) * (prod S)^-1 mod q_i, with the centred
+ * conversion conv = sum_k z_k [S/s_k]_{q_i} - v [prod S]_{q_i},
+ * z_k = [x_k (S/s_k)^-1]_{s_k}, v = round(sum_k z_k / s_k) evaluated in 64.64
+ * fixed point (f_k = z_k R1 + hi(z_k R0), R = floor(2^128/s_k)) -- the same
+ * integer recipe as the GPU, so the rounding decision is bit-identical. */
+static void moddown_exact(const orc_ctx *c, const uint64_t *xq, int no, const uint64_t *xs, int ns,
+                          const int *sid, uint64_t *out) {
+    const int n = c->n;
+    uint64_t *z = (uint64_t *)malloc(sizeof(uint64_t) * ns * n);
+    for (int k = 0; k < ns; k++) {
+        const uint64_t p = c->prime[sid[k]];
+        memcpy(z + (size_t)k * n, xs + (size_t)k * n, sizeof(uint64_t) * n);
+        intt_limb(c, z + (size_t)k * n, sid[k]);
+        uint64_t shat = 1;
+        for (int m = 0; m < ns; m++)
+            if (m != k) shat = mulmod(shat, c->prime[sid[m]] % p, p);
+        const uint64_t shinv = invmod(shat, p);
+        for (int j = 0; j < n; j++) z[(size_t)k * n + j] = mulmod(z[(size_t)k * n + j], shinv, p);
+    }
+    uint64_t *vr = (uint64_t *)malloc(sizeof(uint64_t) * n);
+    for (int j = 0; j < n; j++) {
+        u128 frac = 0;
+        for (int k = 0; k < ns; k++) {
+            const uint64_t zk = z[(size_t)k * n + j];
+            const u128 R = (~(u128)0) / c->prime[sid[k]];
+            const uint64_t r1 = (uint64_t)(R >> 64), r0 = (uint64_t)R;
+            frac += (u128)(uint64_t)(zk * r1 + (uint64_t)(((u128)zk * r0) >> 64));
         }
-        uint64_t *dst = r ? out1 : out0;
+        vr[j] = (uint64_t)((frac + ((u128)1 << 63)) >> 64);
+    }
 #pragma omp parallel for
+    for (int i = 0; i < no; i++) {
+        const uint64_t q = c->prime[i];
+        uint64_t coef[ORC_MAX_PRIMES];
+        uint64_t smod = 1;
+        for (int k = 0; k < ns; k++) {
+            uint64_t v = 1;
+            for (int m = 0; m < ns; m++)
+                if (m != k) v = mulmod(v, c->prime[sid[m]] % q, q);
+            coef[k] = v;
+            smod = mulmod(smod, c->prime[sid[k]] % q, q);
+        }
+        const uint64_t sinv = invmod(smod, q);
+        uint64_t *t = (uint64_t *)malloc(sizeof(uint64_t) * n);
+        for (int j = 0; j < n; j++) {
+            u128 s = 0;
+            for (int k = 0; k < ns; k++) s += (u128)z[(size_t)k * n + j] * coef[k];
+            t[j] = submod((uint64_t)(s % q), mulmod(vr[j] % q, smod, q), q);
+        }
+        ntt_limb(c, t, i);
+        for (int j = 0; j < n; j++)
+            out[(size_t)i * n + j] = mulmod(submod(xq[(size_t)i * n + j], t[j], q), sinv, q);
+        free(t);
+    }
+    free(vr);
+    free(z);
+}
+
+/* out0/out1: uint64[level+1][N] NTT form, <(out0,out1),(1,s)> ~ sigma_g(d) * s_from
+ * (galois = 1: plain key switch).  Exact ModDown by P. */
+void orc_keyswitch_g(const orc_ctx *c, const uint64_t *d, const uint64_t *key, uint64_t *out0,
+                     uint64_t *out1, int level, uint64_t galois) {
+    const int n = c->n, nl = level + 1, K = c->n_p, ne = nl + K;
+    uint64_t *acc = (uint64_t *)malloc(sizeof(uint64_t) * 2 * ne * n);
+    ks_inner_acc(c, d, key, level, galois, acc);
+    int sid[ORC_MAX_PRIMES];
+    for (int k = 0; k < K; k++) sid[k] = c->n_q + k;
+    for (int r = 0; r < 2; r++) {
+        const uint64_t *a = acc + (size_t)r * ne * n;
+        moddown_exact(c, a, nl, a + (size_t)nl * n, K, sid, r ? out1 : out0);
+    }
+    free(acc);
+}
+
+/* HMult with the rescale fused into the key switch:
+ * X_r = acc_r + P d_r (d = tensor(a, b), acc = key switch accumulator of d2),
+ * out_r = round(X_r / (P q_level)) over Q_{level-1}: one exact ModDown over the
+ * special basis P u {q_level}.  Output at level-1. */
+void orc_mul_relin_rescale(const orc_ctx *c, const uint64_t *a, const uint64_t *b,
+                           const uint64_t *rlk, uint64_t *out, int level) {
+    const int n = c->n, nl = level + 1, K = c->n_p, ne = nl + K;
+    const size_t ps = (size_t)nl * n;
+    uint64_t *d = (uint64_t *)malloc(sizeof(uint64_t) * 3 * ps);
+    orc_tensor(c, a, b, d, level);
+    uint64_t *acc = (uint64_t *)malloc(sizeof(uint64_t) * 2 * ne * n);
+    ks_inner_acc(c, d + 2 * ps, rlk, level, 1, acc);
+    int sid[ORC_MAX_PRIMES];
+    for (int k = 0; k < K; k++) sid[k] = c->n_q + k;
+    sid[K] = level;
+    uint64_t *xs = (uint64_t *)malloc(sizeof(uint64_t) * (K + 1) * n);
+    uint64_t *xq = (uint64_t *)malloc(sizeof(uint64_t) * nl * n);
+    for (int r = 0; r < 2; r++) {
+        const uint64_t *ar = acc + (size_t)r * ne * n;
+        const uint64_t *dr = d + (size_t)r * ps;
+        /* X over Q_level: acc + P d ; over P: acc */
         for (int i = 0; i < nl; i++) {
             const uint64_t q = c->prime[i];
-            uint64_t coef[ORC_MAX_PRIMES];
-            uint64_t pmod = 1;
-            for (int k = 0; k < K; k++) {
-                uint64_t v = 1;
-                for (int m = 0; m < K; m++)
-                    if (m != k) v = mulmod(v, c->prime[c->n_q + m] % q, q);
-                coef[k] = v;
-                pmod = mulmod(pmod, c->prime[c->n_q + k] % q, q);
-            }
-            const uint64_t pinv = invmod(pmod, q);
-            uint64_t *t = (uint64_t *)malloc(sizeof(uint64_t) * n);
-            /* exact (rounded) conversion: subtract v*P, v = round(sum_k z_k / p_k)
-             * evaluated in 64.64 fixed point with f_k = z_k*R1 + hi(z_k*R0),
-             * R = floor(2^128 / p_k) -- the same integer recipe as the GPU */
-            const uint64_t pq = pmod;
-            for (int j = 0; j < n; j++) {
-                u128 s = 0, frac = 0;
-                for (int k = 0; k < K; k++) {
-                    const uint64_t zk = z[(size_t)k * n + j];
-                    const uint64_t pk = c->prime[c->n_q + k];
-                    const u128 R = (~(u128)0) / pk;
-                    const uint64_t r1 = (uint64_t)(R >> 64), r0 = (uint64_t)R;
-                    frac += (u128)(uint64_t)(zk * r1 + (uint64_t)(((u128)zk * r0) >> 64));
-                    s += (u128)zk * coef[k];
-                }
-                const uint64_t v = (uint64_t)((frac + ((u128)1 << 63)) >> 64);
-                t[j] = submod((uint64_t)(s % q), mulmod(v % q, pq, q), q);
-            }
-            ntt_limb(c, t, i);
+            uint64_t pm = 1;
+            for (int k = 0; k < K; k++) pm = mulmod(pm, c->prime[c->n_q + k] % q, q);
             for (int j = 0; j < n; j++)
-                dst[(size_t)i * n + j] = mulmod(submod(a[(size_t)i * n + j], t[j], q), pinv, q);
-            free(t);
+                xq[(size_t)i * n + j] = addmod(ar[(size_t)i * n + j], mulmod(dr[(size_t)i * n + j], pm, q), q);
         }
-        free(z);
-        free(acc[r]);
+        memcpy(xs, ar + (size_t)nl * n, sizeof(uint64_t) * K * n);
+        memcpy(xs + (size_t)K * n, xq + (size_t)level * n, sizeof(uint64_t) * n);
+        moddown_exact(c, xq, level, xs, K + 1, sid, out + (size_t)r * level * n);
     }
+    free(xq);
+    free(xs);
+    free(acc);
+    free(d);
 }
 
 void orc_keyswitch(const orc_ctx *c, const uint64_t *d, const uint64_t *key, uint64_t *out0,

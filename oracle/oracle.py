@@ -56,6 +56,7 @@ def lib():
                 "orc_automorph": ([P, P, P, c_int, c_uint64], None),
                 "orc_keyswitch": ([P, P, P, P, P, c_int], None),
                 "orc_mul_relin": ([P, P, P, P, P, c_int], None),
+                "orc_mul_relin_rescale": ([P, P, P, P, P, c_int], None),
                 "orc_rotate": ([P, P, P, P, c_int, c_uint64], None),
                 "orc_uniform_poly": ([P, P, c_int, P, c_uint64, c_uint64], None),
                 "orc_small_to_ntt": ([P, P, P, c_int, P], None),
@@ -128,6 +129,12 @@ class OracleCKKS:
     def mul_relin(self, a, b, rlk, level):
         out = np.empty((2, level + 1, self.n), dtype=_u64)
         self.L.orc_mul_relin(self.ctx, _p(a), _p(b), _p(rlk), _p(out), level)
+        return out
+
+    def mul_relin_rescale(self, a, b, rlk, level):
+        """HMult + relinearisation with the rescale fused into the ModDown."""
+        out = np.empty((2, level, self.n), dtype=_u64)
+        self.L.orc_mul_relin_rescale(self.ctx, _p(a), _p(b), _p(rlk), _p(out), level)
         return out
 
     def automorph(self, a, galois):
@@ -281,8 +288,8 @@ class OracleBackend:
 
     @_batched
     def mul_relin_rescale(self, a, b, level):
-        prod = self.o.mul_relin(a, b, self.relin_key(), level)
-        return self.o.rescale(prod, level)
+        return self.o.mul_relin_rescale(np.ascontiguousarray(a), np.ascontiguousarray(b), self.relin_key(),
+                                        level)
 
     @_batched
     def rotate(self, a, galois, level):

@@ -112,6 +112,9 @@ struct srk_ctx {
     // modup[level][digit], moddown[level]
     std::vector<std::vector<BconvPlan>> modup;
     std::vector<BconvPlan> moddown;
+    std::vector<BconvPlan> moddown_rs;        // [level]: P u {q_level} -> q_0..q_{level-1}
+    std::vector<LimbConsts> lc_rs_scale;      // [level]: N^-1 (S/s_k)^-1 mod s_k, S = P q_level
+    std::vector<LimbConsts> lc_rs_mulc;       // [level]: (P q_level)^-1 mod q_i
     std::vector<LimbConsts> lc_modup_scale;  // [level]: N^-1 (Q_j/q_i)^-1 mod q_i (INTT fold)
     LimbConsts lc_moddown_scale;      // N^-1 (P/p_k)^-1 mod p_k (INTT fold)
     LimbConsts lc_pinv;               // P^-1 mod q_i
@@ -265,6 +268,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     // base-conversion plans
     c->modup.resize(n_q);
     c->moddown.resize(n_q);
+    c->moddown_rs.resize(n_q);
     std::vector<uint64_t> qv(c->primes);
     for (int l = 0; l < n_q; l++) {
         const int nl = l + 1, ne = nl + n_p;
@@ -288,6 +292,15 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
             pid.push_back(i);
         }
         if ((rc = build_plan(c, c->moddown[l], src, slot, pid, true))) { srk_ctx_destroy(c); return rc; }
+        if (l >= 1) {  // fused HMult rescale: special basis P u {q_l}, targets q_0..q_{l-1}
+            std::vector<int> src2(src), slot2, pid2;
+            src2.push_back(l);
+            for (int i = 0; i < l; i++) {
+                slot2.push_back(i);
+                pid2.push_back(i);
+            }
+            if ((rc = build_plan(c, c->moddown_rs[l], src2, slot2, pid2, true))) { srk_ctx_destroy(c); return rc; }
+        }
     }
     // P^-1 mod q_i, P mod prime_i, q_l^-1 mod q_i
     std::vector<uint64_t> pinv(n_q), pmod(np);
@@ -309,6 +322,31 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
             qq[k] = p;
         }
         fill_consts(c->lc_moddown_scale, w, qq);
+    }
+    c->lc_rs_scale.resize(n_q);
+    c->lc_rs_mulc.resize(n_q);
+    for (int l = 1; l < n_q; l++) {
+        std::vector<int> sid;
+        for (int k = 0; k < n_p; k++) sid.push_back(n_q + k);
+        sid.push_back(l);
+        std::vector<uint64_t> w(sid.size()), qq(sid.size());
+        for (size_t k = 0; k < sid.size(); k++) {
+            const uint64_t p = primes[sid[k]];
+            uint64_t h = 1;
+            for (size_t m = 0; m < sid.size(); m++)
+                if (m != k) h = hmul(h, primes[sid[m]] % p, p);
+            w[k] = hmul(hinv((uint64_t)n, p), hinv(h, p), p);
+            qq[k] = p;
+        }
+        fill_consts(c->lc_rs_scale[l], w, qq);
+        std::vector<uint64_t> mc(l), q2(l);
+        for (int i = 0; i < l; i++) {
+            uint64_t s = pmod[i];
+            s = hmul(s, primes[l] % primes[i], primes[i]);
+            mc[i] = hinv(s, primes[i]);
+            q2[i] = primes[i];
+        }
+        fill_consts(c->lc_rs_mulc[l], mc, q2);
     }
     c->lc_modup_scale.resize(n_q);
     for (int l = 0; l < n_q; l++) {
@@ -343,7 +381,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
 // words of scratch (x N) each op needs for a chunk of B ciphertexts at level l
 static size_t ks_limbs(const srk_ctx *c, int level, int B) {
     const size_t nl = level + 1, ne = nl + c->n_p, beta = (nl + c->alpha - 1) / c->alpha;
-    return (size_t)B * (nl + beta * ne + 2 * ne + 2 * nl + 2 * c->n_p + 1);  // + z, rounding bytes
+    return (size_t)B * (nl + beta * ne + 2 * ne + 2 * nl + 2 * (c->n_p + 1) + 1);  // + z, rounding bytes
 }
 static size_t rescale_limbs(int level, int B) { return (size_t)B * (2 + 2 * (size_t)level); }
 static size_t relin_limbs(const srk_ctx *c, int level, int B) {
@@ -420,6 +458,8 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
             ff.mulc.ws[k] = f.mulc.ws[k + l0];
             ff.pre.w[k] = f.pre.w[k + l0];
             ff.pre.ws[k] = f.pre.ws[k + l0];
+            ff.addc.w[k] = f.addc.w[k + l0];
+            ff.addc.ws[k] = f.addc.ws[k + l0];
         }
     }
     bb.n_limbs = nlc;
@@ -839,8 +879,13 @@ struct KsOut {
     bool gather_add0;
 };
 
+// rescale_d: fused HMult rescale -- outs[0].add0/add1 are d0/d1 (ct stride
+// add_ct, poly stride = level+1 limbs) and the output is
+// round((acc + P d) / (P q_level)) at level-1 (bit-identical to ModDown then
+// rescale: consecutive roundings by odd moduli compose exactly)
 static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const KsOut *outs,
-                          int n_out, int level, int B, uint64_t *ws, cudaStream_t s) {
+                          int n_out, int level, int B, uint64_t *ws, cudaStream_t s,
+                          bool rescale_d = false) {
     const long long n = c->n;
     const int nl = level + 1, K = c->n_p, ne = nl + K;
     const int alpha = c->alpha, beta = (nl + alpha - 1) / alpha;
@@ -849,8 +894,9 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
     uint64_t *ext = dc + (long long)B * nl * n;        // [B][beta][ne]
     uint64_t *acc = ext + (long long)B * beta * ne * n;  // [B][2][ne]
     uint64_t *conv = acc + (long long)B * 2 * ne * n;    // [B][2][nl]
-    uint64_t *zb = conv + (long long)B * 2 * nl * n;    // [B][2][K] special limbs, coef
-    uint8_t *vround = (uint8_t *)(zb + (long long)B * 2 * K * n);  // [B][2][N] bytes
+    uint64_t *zb = conv + (long long)B * 2 * nl * n;    // [B][2][K(+1)] special limbs, coef
+    uint8_t *vround = (uint8_t *)(zb + (long long)B * 2 * (K + 1) * n);  // [B][2][N] bytes
+    if (rescale_d && level < 1) return fail(SRK_EINVAL, "cannot rescale a level-0 ciphertext");
     // 1. INTT with the ModUp scale folded in
     {
         FuseArgs f = no_fuse();
@@ -949,7 +995,54 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             k_ks_inner<<<blocks, SRK_KS_TILE, smem, s>>>(ka, c->d_pc, c->log_n);
             LAUNCHED();
         }
-        // 5. INTT of the special limbs read through sigma_g, (P/p_k)^-1 folded in -> zb
+        if (rescale_d) {
+            // 5'. special basis S = P u {q_l}: X_S = (acc_P, acc_l + P d_l), INTT with
+            //     N^-1 (S/s_k)^-1 folded in; rounding term over K+1 limbs
+            const int ns = K + 1;
+            const uint64_t pm = c->lc_pmod.w[level], pms = c->lc_pmod.ws[level];
+            k_prep_special<<<grid_for(2ll * B * ns * n), 256, 0, s>>>(
+                acc, 2ll * ne * n, (long long)ne * n, ko.add0, ko.add_ct, (long long)nl * n, zb, pm, pms,
+                c->d_pc, c->log_n, level, K, B);
+            LAUNCHED();
+            FuseArgs f = no_fuse();
+            f.mulc = c->lc_rs_scale[level];
+            LimbBatch b = cbatch(zb, B, 2, 2ll * ns * n, (long long)ns * n, ns, 0);
+            b.split = K;
+            b.off_a = c->n_q;
+            b.off_b = level - K;
+            TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, s));
+            k_moddown_v<<<grid_for(2ll * B * n), 256, 0, s>>>(zb, 2ll * ns * n, (long long)ns * n, K,
+                                                              c->n_q, ns, level, vround, c->d_pc, c->log_n, B);
+            LAUNCHED();
+            // 6'. NTT(conversion S -> q_0..q_{l-1}) with out = (acc - conv) (P q_l)^-1 + d q_l^-1
+            const BconvPlan &pr = c->moddown_rs[level];
+            FuseArgs g = no_fuse();
+            g.src = zb;
+            g.src_ct = 2ll * ns * n;
+            g.src_ps = (long long)ns * n;
+            g.n_src = ns;
+            g.mat = pr.mat;
+            g.mat_ld = pr.n_dst;
+            g.corr = pr.dst_corr;
+            g.corr_ld = pr.n_dst;
+            g.vround = vround;
+            g.out = ko.out;
+            g.out_ct = ko.out_ct;
+            g.out_ps = ko.out_ps;
+            g.acc = acc;
+            g.acc_ct = 2ll * ne * n;
+            g.acc_ps = (long long)ne * n;
+            g.add0 = ko.add0;
+            g.add1 = ko.add1;
+            g.add_ct = ko.add_ct;
+            g.add_scaled = 1;
+            g.addc = c->lc_qlinv[level];
+            g.mulc = c->lc_rs_mulc[level];
+            TRY(ntt_run(c, cbatch(conv, B, 2, 2ll * level * n, (long long)level * n, level, 0), false, g,
+                        LD_BCONV, ST_MODDOWN, s));
+            continue;
+        }
+        // 5. INTT of the special limbs, (P/p_k)^-1 folded in -> zb
         {
             FuseArgs f = no_fuse();
             f.mulc = c->lc_moddown_scale;
@@ -964,7 +1057,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         // 6. ModDown: rounding term once per coefficient, then NTT(conversion)
         //    with the combine in its store
         k_moddown_v<<<grid_for(2ll * B * n), 256, 0, s>>>(zb, 2ll * K * n, (long long)K * n, K,
-                                                          c->n_q, vround, c->d_pc, c->log_n, B);
+                                                          c->n_q, K, 0, vround, c->d_pc, c->log_n, B);
         LAUNCHED();
         {
             FuseArgs f = no_fuse();
@@ -1022,12 +1115,13 @@ static int mul_relin_chunk(srk_ctx *c, const uint64_t *a, const uint64_t *b, lon
                                               c->log_n, level + 1);
         LAUNCHED();
     }
-    uint64_t *dst = rescale ? prod : out;
-    const long long dst_ct = rescale ? 2 * ps : out_ct;
-    KsOut o = {dst, dst_ct, ps, rlk, 1, d, d + ps, 3 * ps, false};
-    TRY(keyswitch_impl(c, d + 2 * ps, 3 * ps, &o, 1, level, B, rest, s));
-    if (!rescale) return SRK_OK;
-    return rescale_impl(c, prod, 2 * ps, ps, nullptr, nullptr, out, out_ct, level, B, rest, s);
+    (void)prod;
+    if (rescale) {  // HMult rescale fused into the key switch's ModDown
+        KsOut o = {out, out_ct, (long long)level * n, rlk, 1, d, d + ps, 3 * ps, false};
+        return keyswitch_impl(c, d + 2 * ps, 3 * ps, &o, 1, level, B, rest, s, true);
+    }
+    KsOut o = {out, out_ct, ps, rlk, 1, d, d + ps, 3 * ps, false};
+    return keyswitch_impl(c, d + 2 * ps, 3 * ps, &o, 1, level, B, rest, s);
 }
 
 extern "C" int srk_mul_relin(srk_ctx *c, const uint64_t *a, const uint64_t *b,

@@ -275,9 +275,10 @@ __global__ void __launch_bounds__(SRK_KS_TILE) k_ks_inner(const __grid_constant_
 // exact ModDown rounding term per coefficient: v = round(sum_k z_k / p_k)
 // (64.64 fixed point, f_k = z_k R1 + hi(z_k R0), R = floor(2^128 / p_k));
 // z: B*2 polys (ct stride z_ct, poly stride z_ps) of K limbs; v: [B*2][N]
+// (limb k < K under prime pid0 + k; limb K, if present, under prime pid_last)
 __global__ void k_moddown_v(const uint64_t *__restrict__ z, long long z_ct, long long z_ps, int K,
-                            int pid0, uint8_t *__restrict__ v, const PrimeConst *__restrict__ pc,
-                            int log_n, int batch) {
+                            int pid0, int n_src, int pid_last, uint8_t *__restrict__ v,
+                            const PrimeConst *__restrict__ pc, int log_n, int batch) {
     const long long n = 1ll << log_n;
     const long long total = 2ll * batch * n;
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
@@ -286,9 +287,9 @@ __global__ void k_moddown_v(const uint64_t *__restrict__ z, long long z_ct, long
         const long long off = x & (n - 1);
         const uint64_t *zp = z + (p >> 1) * z_ct + (p & 1) * z_ps + off;
         U128 frac = {0, 1ull << 63};
-        for (int k = 0; k < K; k++) {
+        for (int k = 0; k < n_src; k++) {
             const uint64_t zk = zp[k * n];
-            const PrimeConst Q = pc[pid0 + k];
+            const PrimeConst Q = pc[k < K ? pid0 + k : pid_last];
             U128 fr = {0, zk * Q.ratio_hi + mulhi64(zk, Q.ratio_lo)};
             add_to(frac, fr);
         }
@@ -399,6 +400,36 @@ __global__ void k_reduce_mod(uint64_t *__restrict__ a, const PrimeConst *__restr
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x)
         a[x] = reduce64(a[x], pc[(x >> log_n) % nl]);
+}
+
+// special limbs of X = acc + P d for the fused HMult rescale:
+// zb[b][r][k] = acc[b][r][nl + k] (k < K), zb[b][r][K] = acc[b][r][l] + P d_r[l]  (mod q_l)
+__global__ void k_prep_special(const uint64_t *__restrict__ acc, long long acc_ct, long long acc_ps,
+                               const uint64_t *__restrict__ d, long long d_ct, long long d_ps,
+                               uint64_t *__restrict__ zb, uint64_t pmod_l, uint64_t pmod_l_shoup,
+                               const PrimeConst *__restrict__ pc, int log_n, int level, int K,
+                               int batch) {
+    const long long n = 1ll << log_n;
+    const int nl = level + 1;
+    const long long per = (long long)(K + 1) * n;
+    const long long total = 2ll * batch * per;
+    const uint64_t ql = pc[level].q;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long p = x / per, xi = x - p * per;
+        const int k = (int)(xi >> log_n);
+        const long long off = xi & (n - 1);
+        const long long b = p >> 1, r = p & 1;
+        const uint64_t *a = acc + b * acc_ct + r * acc_ps;
+        uint64_t v;
+        if (k < K) {
+            v = a[(long long)(nl + k) * n + off];
+        } else {
+            const uint64_t dv = d[b * d_ct + r * d_ps + (long long)level * n + off];
+            v = add_mod(a[(long long)level * n + off], mul_shoup(dv, pmod_l, pmod_l_shoup, ql), ql);
+        }
+        zb[x] = v;
+    }
 }
 
 // square (NTT domain) of s over all primes: relinearisation source key

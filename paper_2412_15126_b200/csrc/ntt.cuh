@@ -117,6 +117,8 @@ struct FuseArgs {
     long long pt_ct;
     LimbConsts mulc;
     LimbConsts pre;
+    LimbConsts addc;         // ST_MODDOWN: add_r scaled by addc (when add_scaled)
+    int add_scaled;
 };
 
 struct NttTables {
@@ -335,7 +337,9 @@ __device__ __forceinline__ void fused_store(const FuseArgs &f, int bi, int r, in
                 const long long src = (r == 0 && f.add_galois != 1)
                                           ? (long long)auto_index((uint32_t)n, f.add_galois, log_n)
                                           : n;
-                v = add_mod(v, base[src], P.q);
+                uint64_t av = base[src];
+                if (f.add_scaled) av = mul_shoup(av, f.addc.w[limb], f.addc.ws[limb], P.q);
+                v = add_mod(v, av, P.q);
             }
         }
         f.out[bi * f.out_ct + r * f.out_ps + off] = v;
@@ -366,7 +370,11 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
                 uint64_t v = mul_shoup(sub_mod(f.acc[bi * f.acc_ct + r * f.acc_ps + off], sm[sidx(c)], pc.q),
                                        f.mulc.w[limb], f.mulc.ws[limb], pc.q);
                 const uint64_t *ad = r == 0 ? f.add0 : f.add1;
-                if (ad) v = add_mod(v, ad[bi * f.add_ct + off], pc.q);
+                if (ad) {
+                    uint64_t av = ad[bi * f.add_ct + off];
+                    if (f.add_scaled) av = mul_shoup(av, f.addc.w[limb], f.addc.ws[limb], pc.q);
+                    v = add_mod(v, av, pc.q);
+                }
                 sm[sidx(c)] = v;
             }
             __syncthreads();

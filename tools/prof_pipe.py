@@ -1,0 +1,34 @@
+"""Pipeline driver for ncu launch lists: rank N=128 (cfg3) or multi_sort N=256 (long)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2412_15126_b200 as M  # noqa: E402
+from paper_2412_15126_b200.params import preset  # noqa: E402
+
+what = sys.argv[1] if len(sys.argv) > 1 else "rank"
+if what == "rank":
+    eng = M.B200Engine(preset("cfg3"))
+    v = np.random.default_rng(0).choice(1024, 128, replace=False) / 1024
+    cfg = M.KernelConfig(mode="composite", composite=(4, 2))
+    ct = eng.encrypt(v)
+    run = lambda: M.rank(eng, ct, 128, cfg).ranks  # noqa: E731
+else:
+    eng = M.B200Engine(preset("long"))
+    v = np.random.default_rng(0).choice(2048, 256, replace=False) / 2048
+    cfg = M.SortConfig(kernel=M.KernelConfig(mode="composite", composite=(6, 2), indicator_composite=(6, 2)),
+                       tie_correction=False)
+    bv = M.block_split(eng, v)
+    run = lambda: M.multi_sort(eng, bv, cfg)  # noqa: E731
+run()
+torch.cuda.synchronize()
+k0 = eng.backend.lib.srk_kernel_launches()
+t = time.perf_counter()
+run()
+torch.cuda.synchronize()
+print(what, "wall", time.perf_counter() - t, "kernels", eng.backend.lib.srk_kernel_launches() - k0,
+      eng.cost_snapshot())
