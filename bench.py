@@ -192,6 +192,30 @@ class PrimitiveStep:
                 2 * L * self.p.ring_degree, self.n_ct, L, self.ws, s)
 
 
+def bench_config(p):
+    parts, _ = algorithmic_bytes(p)
+    return {"workload": "cfg2 primitive step: fwd NTT + INTT + 64 HMult/relin + 64x15 "
+                        "power-of-two rotations + 64 rescale",
+            "ciphertexts_per_gpu": N_CT, "ring": p.ring_degree, "q_limbs": len(p.q_primes),
+            "p_limbs": len(p.p_primes), "dnum": p.dnum,
+            "algorithmic_gb_per_step": round(sum(parts.values()) / GB, 3),
+            "l2": "inputs 1.9 GiB per operand set >> 126 MB L2 (no flush needed)"}
+
+
+# integer-pipe roof of the NTT: a radix-2 64-bit Shoup butterfly is
+# 11.3 IMAD (fma pipe, 64 lanes/clk/SM) per the SASS of ntt_pass_kernel
+IMAD_PER_BUTTERFLY = 11.3
+
+
+def int_roofline(p, n_limbs, ms, sm_mhz):
+    bfly = n_limbs * (p.ring_degree // 2) * p.log_n
+    achieved = bfly / (ms * 1e-3) / 1e12
+    peak = 148 * 64 * (sm_mhz or 1965.0) * 1e6 / IMAD_PER_BUTTERFLY / 1e12
+    return {"bound": "int (IMAD pipe)", "achieved": round(achieved, 3), "peak": round(peak, 3),
+            "unit": "T butterflies/s", "frac": round(achieved / peak, 4),
+            "model": f"{IMAD_PER_BUTTERFLY} IMAD per butterfly (SASS), 148 SMs x 64 IMAD/clk x sm clock"}
+
+
 def time_region(torch, fn, reps, barrier=None):
     """CUDA-event time of ``reps`` calls of fn (ms per call), synchronized both sides."""
     torch.cuda.synchronize()
@@ -353,12 +377,7 @@ def gpu_arm(args):
             "vs_baseline": None,
             "dtype": "u64 (RNS limbs mod 40/60-bit primes)",
             "data": "synthetic: uniform limbs mod each prime, seeded (BASELINE cfg 2)",
-            "config": {"workload": "cfg2 primitive step: fwd NTT + INTT + 64 HMult/relin + 64x15 "
-                                   "power-of-two rotations + 64 rescale",
-                       "ciphertexts_per_gpu": N_CT, "ring": p.ring_degree, "q_limbs": len(p.q_primes),
-                       "p_limbs": len(p.p_primes), "dnum": p.dnum,
-                       "algorithmic_gb_per_step": round(step_bytes / GB, 3),
-                       "l2": "inputs 1.9 GiB per operand set >> 126 MB L2 (no flush needed)"},
+            "config": bench_config(p),
             "gpu_launches": int(kernels),
             "api_calls_per_step": launches,
             "roofline": {"bound": "hbm", "kernel": "forward NTT (ntt_pass_kernel x2 per chunk)",
@@ -366,6 +385,8 @@ def gpu_arm(args):
                          "frac": round(ntt_gbs / peak, 4), "traffic": None,
                          "algorithmic_bytes": parts["ntt_fwd"], "ms": round(ntt_ms, 4),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+            "roofline_int": int_roofline(p, N_CT * 2 * len(p.q_primes), ntt_ms,
+                                         clk.summary().get("sm_mhz")),
             "roofline_keyswitch": {"bound": "hbm", "unit_of_work": "64 x HMult+relinearise (no rescale)", "achieved": round(ks_gbs, 1), "peak": peak,
                                    "unit": "GB/s", "frac": round(ks_gbs / peak, 4),
                                    "algorithmic_bytes": ks_bytes, "ms": round(ks_ms, 4)},
@@ -442,6 +463,8 @@ def cpu_baseline(args, threads=None):
 
 
 def reference_arm(args):
+    from paper_2412_15126_b200.params import preset
+
     rank_id = int(os.environ.get("RANK", "0"))
     if rank_id != 0:
         return
@@ -459,7 +482,7 @@ def reference_arm(args):
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64 (RNS limbs mod 40/60-bit primes)", "data": "synthetic (BASELINE cfg 2)",
-        "config": {"workload": "cfg2 primitive step (bounded sample per step, see cpu_baseline.sample)"},
+        "config": bench_config(preset("cfg2")),
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": res["cores"], "kind": "port",
                          "sample": res["sample"]},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
