@@ -263,7 +263,17 @@ def run_pipelines(torch, quick=False):
     exact = bool(np.array_equal(np.rint(res), fractional_ranks(v128)))
     out["rank_n128_s"] = {"latency_s": dt, "exact_ranks": exact,
                           "max_rank_err": float(np.abs(res - fractional_ranks(v128)).max()),
-                          "cost": eng.cost_snapshot().__dict__, "params": "cfg3"}
+                          "cost": eng.cost_snapshot().__dict__, "params": "cfg3",
+                          "kernel": "composite g3^4 o f3^2"}
+    # the reference's own comparison: Chebyshev interpolant, degree 1024
+    ccfg = KernelConfig(mode="chebyshev", degree=1024)
+    rank(eng, ct, 128, ccfg)
+    eng.cost_reset()
+    dt, res = timed(lambda: read_row(eng, rank(eng, ct, 128, ccfg).ranks, 128), reps=2)
+    out["rank_n128_chebyshev_d1024_s"] = {
+        "latency_s": dt, "exact_ranks": bool(np.array_equal(np.rint(res), fractional_ranks(v128))),
+        "max_rank_err": float(np.abs(res - fractional_ranks(v128)).max()),
+        "cost": eng.cost_snapshot().__dict__, "params": "cfg3", "kernel": "chebyshev d=1024 (reference)"}
     del eng
     torch.cuda.empty_cache()
     if quick:

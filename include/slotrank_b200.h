@@ -161,6 +161,11 @@ int srk_encrypt(srk_ctx *ctx, const int64_t *m, const uint64_t *s_ntt, const int
 /* m_out: int64[N] device, centred coefficients of c0 + c1 s mod q_0 */
 int srk_decrypt_limb0(srk_ctx *ctx, const uint64_t *ct, const uint64_t *s_ntt, int64_t *m_out,
                       int level, void *ws, void *stream);
+/* BSGS leaf sum before its single rescale: out = sum_i k[i] * terms[i] over
+ * limbs 0..level (terms: HOST array of device pointers, term_limbs: HOST
+ * limbs per poly of each term, k: DEVICE residues [n_terms][level+1]) */
+int srk_lincomb(srk_ctx *ctx, const uint64_t *const *terms, const int *term_limbs, int n_terms,
+                const uint64_t *k, uint64_t *out, int batch, int level, void *stream);
 /* multi-GPU fix-up after an int64 all-reduce of n_polys polys of level+1
  * limbs (values < 2^63): reduce every limb mod its prime in place */
 int srk_reduce_mod(srk_ctx *ctx, uint64_t *data, int n_polys, int level, void *stream);

@@ -295,6 +295,28 @@ class OracleBackend:
     def rotate(self, a, galois, level):
         return self.o.rotate_raw(a, self.galois_key(galois), galois, level)
 
+    @_batched
+    def rescale(self, a, level):
+        return self.o.rescale(np.ascontiguousarray(a), level)
+
+    def lincomb(self, terms, term_levels, residues, level, batch=None):
+        """sum_i k_i T_i over limbs 0..level, term by term (mul_const + add)."""
+        if batch is not None:
+            return np.stack([self.lincomb([t[i] for t in terms], term_levels, residues, level)
+                             for i in range(batch)])
+        acc = None
+        for t, lv, res in zip(terms, term_levels, residues):
+            k = np.array([int(r) for r in res], dtype=_u64)
+            prod = np.empty((2, level + 1, self.n), dtype=_u64)
+            self.o.L.orc_mul_const(self.o.ctx, _p(np.ascontiguousarray(t)), lv + 1, _p(k), _p(prod), level)
+            if acc is None:
+                acc = prod
+            else:
+                nxt = np.empty_like(acc)
+                self.o.L.orc_addsub(self.o.ctx, _p(acc), _p(prod), _p(nxt), level, 0)
+                acc = nxt
+        return acc
+
     def stack(self, datas):
         return np.stack(datas)
 

@@ -235,6 +235,24 @@ class CudaBackend:
                    2 * level * self.n, batch or 1, level, 1, self.workspace(), self.stream())
         return out
 
+    def rescale(self, a, level: int, batch=None) -> torch.Tensor:
+        out = self._out(level - 1, batch)
+        self._call("srk_rescale_batch", _ptr(a), 2 * (level + 1) * self.n, _ptr(out),
+                   2 * level * self.n, batch or 1, level, self.workspace(), self.stream())
+        return out
+
+    def lincomb(self, terms, term_levels, residues, level: int, batch=None) -> torch.Tensor:
+        """sum_i k_i T_i over limbs 0..level (no rescale); residues: [n_terms][level+1] ints."""
+        n_t = len(terms)
+        out = self._out(level, batch)
+        k = np.array([[int(r) for r in row] for row in residues], dtype=np.uint64).view(np.int64)
+        k_dev = torch.from_numpy(k).to(self.device, non_blocking=True)
+        ptrs = (ctypes.c_void_p * n_t)(*[_ptr(t) for t in terms])
+        limbs = (ctypes.c_int * n_t)(*[lv + 1 for lv in term_levels])
+        self._call("srk_lincomb", ptrs, limbs, n_t, _ptr(k_dev), _ptr(out), batch or 1, level,
+                   self.stream())
+        return out
+
     def rotate(self, a, galois: int, level: int, batch=None) -> torch.Tensor:
         key = self.galois_key(galois)
         out = self._out(level, batch)

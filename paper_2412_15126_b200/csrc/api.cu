@@ -1324,6 +1324,34 @@ extern "C" int srk_decrypt_limb0(srk_ctx *c, const uint64_t *ct, const uint64_t 
     return SRK_OK;
 }
 
+// out = sum_i k[i] * terms[i] over the first level+1 limbs (no rescale);
+// terms: host array of device pointers, term_limbs: limbs per poly of each
+// term (>= level+1), k: DEVICE [n_terms][level+1] residues, batch packed
+// ciphertexts per term (ct stride 2 * term_limbs * N), out [batch][2][level+1][N]
+extern "C" int srk_lincomb(srk_ctx *c, const uint64_t *const *terms, const int *term_limbs,
+                           int n_terms, const uint64_t *k, uint64_t *out, int batch, int level,
+                           void *stream) {
+    TRY(check_level(c, level));
+    if (n_terms < 1 || n_terms > SRK_LC_MAX) return fail(SRK_EINVAL, "1..64 terms");
+    LinCombArgs la;
+    memset(&la, 0, sizeof la);
+    for (int i = 0; i < n_terms; i++) {
+        if (term_limbs[i] < level + 1) return fail(SRK_EINVAL, "term below the output level");
+        la.term[i] = terms[i];
+        la.term_ps[i] = (long long)term_limbs[i] * c->n;
+        la.term_ct[i] = 2ll * term_limbs[i] * c->n;
+    }
+    la.n_terms = n_terms;
+    la.nl = level + 1;
+    la.batch = batch;
+    la.k = k;
+    la.out = out;
+    const long long total = 2ll * batch * (level + 1) * c->n;
+    k_lincomb<<<grid_for(total), 256, 0, S(stream)>>>(la, c->d_pc, c->log_n);
+    LAUNCHED();
+    return SRK_OK;
+}
+
 extern "C" int srk_reduce_mod(srk_ctx *c, uint64_t *data, int n_polys, int level, void *stream) {
     TRY(check_level(c, level));
     const long long total = (long long)n_polys * (level + 1) * c->n;

@@ -432,6 +432,44 @@ __global__ void k_prep_special(const uint64_t *__restrict__ acc, long long acc_c
     }
 }
 
+// linear combination of ciphertexts (the BSGS leaf sum), before its rescale:
+//   out[b][r][j] = sum_i k[i][j] * T_i[b][r][j]   mod q_j,  j < nl
+// T_i read as its first nl limbs (terms may sit at higher levels); k: device
+// [n_terms][nl] residues; U128 accumulation, one reduction per output word
+#define SRK_LC_MAX 64
+struct LinCombArgs {
+    const uint64_t *term[SRK_LC_MAX];
+    long long term_ps[SRK_LC_MAX];  // poly stride (words) of each term
+    long long term_ct[SRK_LC_MAX];  // ciphertext stride for batches
+    int n_terms, nl, batch;
+    const uint64_t *k;
+    uint64_t *out;
+};
+
+__global__ void k_lincomb(const __grid_constant__ LinCombArgs a, const PrimeConst *__restrict__ pc,
+                          int log_n) {
+    const long long n = 1ll << log_n;
+    const long long per = 2ll * a.nl * n;
+    const long long total = per * a.batch;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long b = x / per, xi = x - b * per;
+        const long long lr = xi >> log_n;
+        const int r = (int)(lr / a.nl), j = (int)(lr - (long long)r * a.nl);
+        const long long off = xi & (n - 1);
+        U128 acc = {0, 0};
+        for (int i = 0; i < a.n_terms; i++) {
+            const uint64_t v = a.term[i][b * a.term_ct[i] + r * a.term_ps[i] + (long long)j * n + off];
+            mac(acc, v, __ldg(a.k + (long long)i * a.nl + j));
+            if ((i & 7) == 7) {  // keep the 128-bit sum bounded: reduce every 8 products
+                U128 red = {0, reduce_u128(acc, pc[j])};
+                acc = red;
+            }
+        }
+        a.out[x] = reduce_u128(acc, pc[j]);
+    }
+}
+
 // square (NTT domain) of s over all primes: relinearisation source key
 __global__ void k_square(const uint64_t *__restrict__ s, uint64_t *__restrict__ out,
                          const PrimeConst *__restrict__ pc, int log_n, int n_limbs) {

@@ -440,6 +440,34 @@ class CKKSEngineCore:
             self._ctpt += nb or 1
         return self._emit(data, level - 1, x.rot_chain, nb)
 
+    def linear_combination(self, terms, site: str = "lincomb") -> Ciphertext:
+        """sum_i c_i * ct_i with ONE rescale (the BSGS leaf sum).
+
+        Counted as the reference counts the unfused form -- len(terms)
+        plaintext multiplications and len(terms)-1 additions -- and lands at
+        min(level_i) - 1 like it.  Each term is multiplied by the integer
+        round(c_i scales[o] q_{o+1} / scales[l_i]) on its first o+2 limbs, the
+        products are summed (U128, one reduction per word) and rescaled once.
+        """
+        cts = [t for t, _ in terms]
+        self._check(*cts)
+        nb = self._nb(*cts)
+        lo = min(t.level for t in cts)
+        if lo < 1:
+            raise DepthBudgetError(site, lo)
+        o = lo - 1
+        pr = self.params
+        res = []
+        for ct, c in terms:
+            k = int(round(float(c) * pr.scales[o] * pr.q_primes[o + 1] / pr.scales[ct.level]))
+            res.append(self._residues(k, o + 1))
+        summed = self.backend.lincomb([t.data for t in cts], [t.level for t in cts], res, o + 1, batch=nb)
+        data = self.backend.rescale(summed, o + 1, batch=nb)
+        with self._lock:
+            self._ctpt += len(terms) * (nb or 1)
+            self._adds += (len(terms) - 1) * (nb or 1)
+        return self._emit(data, o, max(t.rot_chain for t in cts), nb)
+
     def rotate(self, x: Ciphertext, k: int) -> Ciphertext:
         """Cyclic rotation of the slot vector; k > 0 rotates left (``engine.py:234``)."""
         self._check(x)
