@@ -43,14 +43,28 @@ def _mul_plain_at(engine, x, c: float, level: int, site: str):
     return engine.mul_plain(x, c, site=site)
 
 
+def _three_products(engine, y, u3, u7, site):
+    """(y*y, u3*y, u7*y): one lock-step batch on engines that stack ciphertexts."""
+    concat = getattr(engine, "concat", None)
+    if concat is None:
+        return (engine.mul(y, y, site=f"{site}-quad"), engine.mul(u3, y, site=f"{site}-x3"),
+                engine.mul(u7, y, site=f"{site}-x3"))
+    b = y.batch or 1
+    prod = engine.mul(concat([y, u3, u7]), concat([y, y, y]), site=f"{site}-quad")
+    if y.batch is None:
+        return tuple(engine.unstack(prod))
+    singles = engine.unstack(prod)
+    return tuple(engine.stack(singles[i * b:(i + 1) * b]) for i in range(3))
+
+
 def odd_poly_eval(engine, x, coeffs, site: str = "composite"):
     """a1 x + a3 x^3 + a5 x^5 + a7 x^7 on ``x`` in depth 3 (coeffs = (a1, a3, a5, a7))."""
     a1, a3, a5, a7 = (float(c) for c in coeffs)
     lvl = x.level
     y = engine.mul(x, x, site=f"{site}-sq")
-    z = engine.mul(y, y, site=f"{site}-quad")
-    t3 = engine.mul(engine.mul_plain(x, a3, site=f"{site}-c3"), y, site=f"{site}-x3")
-    t7 = engine.mul(engine.mul_plain(x, a7, site=f"{site}-c7"), y, site=f"{site}-x3")
+    u3 = engine.mul_plain(x, a3, site=f"{site}-c3")
+    u7 = engine.mul_plain(x, a7, site=f"{site}-c7")
+    z, t3, t7 = _three_products(engine, y, u3, u7, site)
     w = _mul_plain_at(engine, x, a5, lvl - 2, f"{site}-c5")
     t57 = engine.mul(engine.add(w, t7), z, site=f"{site}-x5")
     t1 = _mul_plain_at(engine, x, a1, lvl - 3, f"{site}-c1")

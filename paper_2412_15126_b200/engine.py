@@ -232,6 +232,13 @@ class CKKSEngineCore:
         return [Ciphertext(self.backend.index(ct.data, i), ct.level, ct.rot_chain, self.params)
                 for i in range(ct.batch)]
 
+    def concat(self, cts) -> Ciphertext:
+        """One batch from single and/or batched ciphertexts (in order)."""
+        singles = []
+        for c in cts:
+            singles.extend(self.unstack(c))
+        return self.stack(singles)
+
     def _residues(self, k: int, level: int) -> list[int]:
         return [k % q for q in self.params.q_primes[: level + 1]]
 

@@ -121,7 +121,7 @@ def test_batched_pipeline_equals_loop():
     e1 = oracle_engine(p)
     r1 = M.multi_sort(e1, M.block_split(e1, v), M.SortConfig(kernel=kc, tie_correction=False))
     e2 = oracle_engine(p)
-    e2.stack = None  # force the sequential reference structure
+    e2.stack = e2.concat = None  # force the sequential reference structure
     r2 = M.multi_sort(e2, M.block_split(e2, v), M.SortConfig(kernel=kc, tie_correction=False))
     assert all(np.array_equal(a.data, b.data) for a, b in zip(r1.blocks, r2.blocks))
     assert e1.cost_snapshot() == e2.cost_snapshot()
