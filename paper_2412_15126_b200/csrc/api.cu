@@ -121,7 +121,6 @@ struct srk_ctx {
     LimbConsts lc_pmod;               // P mod prime_i (all primes)
     std::vector<LimbConsts> lc_qlinv; // [level]: q_level^-1 mod q_i
     int ntt_chunk = 128;              // limbs per L2-resident NTT chunk
-    bool ntt_pipe = false;            // persistent double-buffered passes (SRK_NTT_PIPE=1)
 };
 
 template <typename T>
@@ -220,7 +219,6 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     c->n_primes = n_q + n_p;
     c->primes.assign(primes, primes + c->n_primes);
     if (const char *e = getenv("SRK_NTT_CHUNK")) c->ntt_chunk = std::max(1, atoi(e));
-    if (const char *e = getenv("SRK_NTT_PIPE")) c->ntt_pipe = atoi(e) != 0;
     if (c->alpha > 16 || n_p > 16) {
         srk_ctx_destroy(c);
         return fail(SRK_EINVAL, "digit size and special prime count must be <= 16");
@@ -463,24 +461,6 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
         }
     }
     bb.n_limbs = nlc;
-    constexpr bool FIRST = (COL != INV);
-    // plain-input passes go through the persistent double-buffered kernel
-    if (c->ntt_pipe && (!FIRST || IO == LD_PLAIN)) {
-        const int tiles_x = subs / cb;
-        const int n_tiles = tiles_x * nlc * b.n_polys;
-        const size_t psm = 2 * (size_t)pipe_tile_words<LOG_T, COL>(cb) * 8;
-        static bool pattr = false;
-        if (!pattr) {
-            cudaFuncSetAttribute(ntt_pass_pipe<LOG_T, INV, COL, IO>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
-            pattr = true;
-        }
-        const int blocks = std::min(n_tiles, 148 * 3);
-        ntt_pass_pipe<LOG_T, INV, COL, IO><<<blocks, threads, psm, s>>>(bb, tables(c), c->log_n, ff,
-                                                                          n_tiles, tiles_x);
-        LAUNCHED();
-        return SRK_OK;
-    }
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(ntt_pass_kernel<LOG_T, INV, COL, IO>,

@@ -187,28 +187,90 @@ __device__ __forceinline__ void gs_bfly_small(uint64_t &x, uint64_t &y, uint64_t
     y = mul_shoup_lazy(D, w, ws, q);
 }
 
+// ---------------------------------------------------------------------------
+// FP64 path for primes below 2^41 (every scaling prime).  B200's FP64 pipe is
+// full rate and independent of the IMAD pipe the integer butterflies saturate;
+// a 64-bit Shoup product costs ~17 IMAD slots, the FP64 one 6 full-rate ops:
+//   hi = y w;  lo = fma(y, w, -hi)            (y w == hi + lo exactly)
+//   t  = fma(hi, 1/q, 1.5*2^52) - 1.5*2^52   (nearest integer, no FRND)
+//   r  = fma(-t, q, hi) + lo                  (exact: y w - t q, |r| < q)
+// valid while |y| < 2^51 (so hi/q < 2^51) and w < q < 2^41.  Values live as
+// signed integer-valued doubles in the same 64-bit registers/smem words:
+// forward outputs grow by < q per stage (16 stages < 17 q); inverse sums
+// double per stage, so the second pass starts with a centred reduction.
+// u64 <-> f64 conversions use the 2^52 magic-number trick (LOP + DADD).
+// ---------------------------------------------------------------------------
+#define SRK_F64_Q (1ull << 41)
+#define SRK_F64_MAGIC 6755399441055744.0  // 1.5 * 2^52
+#define SRK_F64_TWO52 4503599627370496.0  // 2^52
+
+__device__ __forceinline__ double f64_of_u64(uint64_t v) {  // v < 2^52
+    return __longlong_as_double((long long)(v | 0x4330000000000000ull)) - SRK_F64_TWO52;
+}
+__device__ __forceinline__ uint64_t u64_of_f64(double d) {  // 0 <= d < 2^52, integral
+    return (uint64_t)__double_as_longlong(d + SRK_F64_TWO52) & 0xFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ double modmul_f64(double y, double w, double q, double qinv) {
+    const double hi = y * w;
+    const double lo = fma(y, w, -hi);
+    const double t = fma(hi, qinv, SRK_F64_MAGIC) - SRK_F64_MAGIC;
+    return fma(-t, q, hi) + lo;
+}
+// centred representative in [-q/2, q/2] of an integer-valued |v| < 2^51
+__device__ __forceinline__ double centre_f64(double v, double q, double qinv) {
+    const double t = fma(v, qinv, SRK_F64_MAGIC) - SRK_F64_MAGIC;
+    return fma(-t, q, v);
+}
+__device__ __forceinline__ uint64_t canon_u64_of_f64(double v, double q, double qinv) {
+    double r = centre_f64(v, q, qinv);
+    r = r < 0.0 ? r + q : r;
+    return u64_of_f64(r);
+}
+__device__ __forceinline__ void ct_bfly_f64(uint64_t &xb, uint64_t &yb, double w, double q,
+                                            double qinv) {
+    const double x = __longlong_as_double((long long)xb), y = __longlong_as_double((long long)yb);
+    const double t = modmul_f64(y, w, q, qinv);
+    xb = (uint64_t)__double_as_longlong(x + t);
+    yb = (uint64_t)__double_as_longlong(x - t);
+}
+__device__ __forceinline__ void gs_bfly_f64(uint64_t &xb, uint64_t &yb, double w, double q,
+                                            double qinv) {
+    const double x = __longlong_as_double((long long)xb), y = __longlong_as_double((long long)yb);
+    xb = (uint64_t)__double_as_longlong(x + y);
+    yb = (uint64_t)__double_as_longlong(modmul_f64(x - y, w, q, qinv));
+}
+
 // Register-resident radix-2 stages, unrolled at compile time through
 // template recursion so x[] never spills to local memory.
 //   tw_group(g) -> twiddle for butterfly group g of the stage;
 //   group g covers x[g*2*HALF .. g*2*HALF + 2*HALF), pairs (e, e + HALF).
-// SMALL: reduction-free variants; m = inverse difference offset (q << step)
-template <int E, int HALF, int NG, bool GS, bool SMALL, typename TwFn>
+// SM: 0 = Harvey lazy (any prime < 2^62), 1 = reduction-free integer (q < 2^46),
+// 2 = FP64 (q < 2^41); m = inverse difference offset (q << step) for SM 1
+struct F64Q {
+    double q, qinv;
+};
+template <int E, int HALF, int NG, bool GS, int SM, typename TwFn>
 __device__ __forceinline__ void reg_stage(uint64_t (&x)[E], TwFn tw_group, uint64_t q,
-                                          uint64_t two_q, uint64_t m) {
+                                          uint64_t two_q, uint64_t m, F64Q fq) {
 #pragma unroll
     for (int g = 0; g < NG; g++) {
         const ulonglong2 w = tw_group(g);
+        const double wf = SM == 2 ? f64_of_u64(w.x) : 0.0;
 #pragma unroll
         for (int k = 0; k < HALF; k++) {
             uint64_t &a = x[g * 2 * HALF + k];
             uint64_t &b = x[g * 2 * HALF + k + HALF];
             if (GS) {
-                if (SMALL)
+                if (SM == 2)
+                    gs_bfly_f64(a, b, wf, fq.q, fq.qinv);
+                else if (SM == 1)
                     gs_bfly_small(a, b, w.x, w.y, q, m);
                 else
                     gs_bfly(a, b, w.x, w.y, q, two_q);
             } else {
-                if (SMALL)
+                if (SM == 2)
+                    ct_bfly_f64(a, b, wf, fq.q, fq.qinv);
+                else if (SM == 1)
                     ct_bfly_small(a, b, w.x, w.y, q, two_q);
                 else
                     ct_bfly(a, b, w.x, w.y, q, two_q);
@@ -219,58 +281,60 @@ __device__ __forceinline__ void reg_stage(uint64_t (&x)[E], TwFn tw_group, uint6
 
 // forward round 1: stages s = 0..LE1-1, half = E >> (s+1), 2^s groups,
 // twiddle (base << s) + g
-template <int E, int LE1, bool SM, int S = 0>
+template <int E, int LE1, int SM, int S = 0>
 struct FwdR1 {
     static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
-                                               uint64_t q, uint64_t two_q) {
+                                               uint64_t q, uint64_t two_q, F64Q fq = {}) {
         if constexpr (S < LE1) {
             reg_stage<E, (E >> (S + 1)), (1 << S), false, SM>(
-                x, [&](int g) { return __ldg(tw + ((base << S) + g)); }, q, two_q, 0);
-            FwdR1<E, LE1, SM, S + 1>::run(x, tw, base, q, two_q);
+                x, [&](int g) { return __ldg(tw + ((base << S) + g)); }, q, two_q, 0, fq);
+            FwdR1<E, LE1, SM, S + 1>::run(x, tw, base, q, two_q, fq);
         }
     }
 };
 // forward round 2: stages LE1+s, half = TPS >> (s+1), ng = E/(2 half),
 // twiddle (base << (LE1+s)) + u ng + g
-template <int E, int TPS, int LE1, int LE2, bool SM, int S = 0>
+template <int E, int TPS, int LE1, int LE2, int SM, int S = 0>
 struct FwdR2 {
     static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
-                                               int u, uint64_t q, uint64_t two_q) {
+                                               int u, uint64_t q, uint64_t two_q, F64Q fq = {}) {
         if constexpr (S < LE2) {
             constexpr int half = TPS >> (S + 1), ng = E / (2 * half);
             reg_stage<E, half, ng, false, SM>(
-                x, [&](int g) { return __ldg(tw + ((base << (LE1 + S)) + u * ng + g)); }, q, two_q, 0);
-            FwdR2<E, TPS, LE1, LE2, SM, S + 1>::run(x, tw, base, u, q, two_q);
+                x, [&](int g) { return __ldg(tw + ((base << (LE1 + S)) + u * ng + g)); }, q, two_q, 0,
+                fq);
+            FwdR2<E, TPS, LE1, LE2, SM, S + 1>::run(x, tw, base, u, q, two_q, fq);
         }
     }
 };
 // inverse round 1: register stride half = 2^s, stage LOG_T-1-s, ng = E/(2 half),
 // twiddle (base << stage) + u ng + g
-template <int E, int LOG_T, int LE1, bool SM, int S = 0>
+template <int E, int LOG_T, int LE1, int SM, int S = 0>
 struct InvR1 {
     static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
-                                               int u, uint64_t q, uint64_t two_q, int k0) {
+                                               int u, uint64_t q, uint64_t two_q, int k0,
+                                               F64Q fq = {}) {
         if constexpr (S < LE1) {
             constexpr int half = 1 << S, ng = E / (2 * half), stage = LOG_T - 1 - S;
             reg_stage<E, half, ng, true, SM>(
                 x, [&](int g) { return __ldg(tw + ((base << stage) + u * ng + g)); }, q, two_q,
-                q << (k0 + S));
-            InvR1<E, LOG_T, LE1, SM, S + 1>::run(x, tw, base, u, q, two_q, k0);
+                q << (k0 + S), fq);
+            InvR1<E, LOG_T, LE1, SM, S + 1>::run(x, tw, base, u, q, two_q, k0, fq);
         }
     }
 };
 // inverse round 2: register stride half = (E/TPS) << s, stage LE2-1-s,
 // 2^stage groups, twiddle (base << stage) + g
-template <int E, int TPS, int LE2, bool SM, int S = 0>
+template <int E, int TPS, int LE2, int SM, int S = 0>
 struct InvR2 {
     static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
-                                               uint64_t q, uint64_t two_q, int k0) {
+                                               uint64_t q, uint64_t two_q, int k0, F64Q fq = {}) {
         if constexpr (S < LE2) {
             constexpr int half = (E / TPS) << S, stage = LE2 - 1 - S;
             reg_stage<E, half, (1 << stage), true, SM>(
                 x, [&](int g) { return __ldg(tw + ((base << stage) + g)); }, q, two_q,
-                q << (k0 + S));
-            InvR2<E, TPS, LE2, SM, S + 1>::run(x, tw, base, q, two_q, k0);
+                q << (k0 + S), fq);
+            InvR2<E, TPS, LE2, SM, S + 1>::run(x, tw, base, q, two_q, k0, fq);
         }
     }
 };
@@ -470,40 +534,57 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
         else return data[gaddr(c)];
     };
 
+    // arithmetic mode, uniform per CTA: 2 = FP64 (q < 2^41), 1 = reduction-free
+    // integer (q < 2^46), 0 = Harvey lazy integer
+    const int mode = q < SRK_F64_Q ? 2 : (small ? 1 : 0);
+    const F64Q fq = {(double)q, 1.0 / (double)q};
+    // first-pass loads are canonical u64; FP64 limbs convert on load
+    auto load_m = [&](int c) -> uint64_t {
+        const uint64_t v = load(c);
+        return mode == 2 ? (uint64_t)__double_as_longlong(f64_of_u64(v)) : v;
+    };
     uint64_t x[E];
     if (!INV) {
         // ---- round 1: strided ownership c = u + TPS e, strides T/2 .. TPS
 #pragma unroll
-        for (int e = 0; e < E; e++) x[e] = load(u + TPS * e);
-        if (small)
-            FwdR1<E, LE1, true>::run(x, tw, base, q, two_q);
+        for (int e = 0; e < E; e++) x[e] = FIRST ? load_m(u + TPS * e) : data[gaddr(u + TPS * e)];
+        if (mode == 2)
+            FwdR1<E, LE1, 2>::run(x, tw, base, q, two_q, fq);
+        else if (mode == 1)
+            FwdR1<E, LE1, 1>::run(x, tw, base, q, two_q);
         else
-            FwdR1<E, LE1, false>::run(x, tw, base, q, two_q);
+            FwdR1<E, LE1, 0>::run(x, tw, base, q, two_q);
 #pragma unroll
         for (int e = 0; e < E; e++) smem[sidx(u + TPS * e)] = x[e];
         __syncthreads();
         // ---- round 2: contiguous ownership c = u E + e, strides TPS/2 .. 1
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = smem[sidx(u * E + e)];
-        if (small)
-            FwdR2<E, TPS, LE1, LE2, true>::run(x, tw, base, u, q, two_q);
+        if (mode == 2)
+            FwdR2<E, TPS, LE1, LE2, 2>::run(x, tw, base, u, q, two_q, fq);
+        else if (mode == 1)
+            FwdR2<E, TPS, LE1, LE2, 1>::run(x, tw, base, u, q, two_q);
         else
-            FwdR2<E, TPS, LE1, LE2, false>::run(x, tw, base, u, q, two_q);
+            FwdR2<E, TPS, LE1, LE2, 0>::run(x, tw, base, u, q, two_q);
         if (COL) {
 #pragma unroll
-            for (int e = 0; e < E; e++) data[gaddr(u * E + e)] = x[e];  // [0,4q)
+            for (int e = 0; e < E; e++) data[gaddr(u * E + e)] = x[e];  // lazy / FP64 bits
         } else {
             // final pass: canonical values, staged through smem for coalescing
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 uint64_t v = x[e];
-                if (small) {  // v < 34 q: one Barrett step (floor(2^64/q)) then one subtraction
-                    v -= mulhi64(v, pc.ratio_hi) * q;
+                if (mode == 2) {
+                    v = canon_u64_of_f64(__longlong_as_double((long long)v), fq.q, fq.qinv);
                 } else {
-                    v = v >= two_q ? v - two_q : v;
+                    if (mode == 1) {  // v < 34 q: one Barrett step (floor(2^64/q)) then one subtraction
+                        v -= mulhi64(v, pc.ratio_hi) * q;
+                    } else {
+                        v = v >= two_q ? v - two_q : v;
+                    }
+                    v = v >= q ? v - q : v;
                 }
-                v = v >= q ? v - q : v;
                 smem[sidx(u * E + e)] = v;
             }
             __syncthreads();
@@ -512,21 +593,30 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
     } else {
         // ---- round 1: contiguous ownership, strides 1 .. E/2
         if (COL) {
+            // second pass: FP64 sums doubled every stage of the first -> re-centre
 #pragma unroll
-            for (int e = 0; e < E; e++) x[e] = data[gaddr(u * E + e)];
+            for (int e = 0; e < E; e++) {
+                uint64_t v = data[gaddr(u * E + e)];
+                if (mode == 2)
+                    v = (uint64_t)__double_as_longlong(
+                        centre_f64(__longlong_as_double((long long)v), fq.q, fq.qinv));
+                x[e] = v;
+            }
         } else {
 #pragma unroll
-            for (int e = 0; e < E; e++) smem[sidx(u + TPS * e)] = load(u + TPS * e);
+            for (int e = 0; e < E; e++) smem[sidx(u + TPS * e)] = load_m(u + TPS * e);
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < E; e++) x[e] = smem[sidx(u * E + e)];
         }
         // step numbers of the inverse: row pass 0.., column pass log_n - LOG_T ..
         const int k0 = COL ? log_n - LOG_T : 0;
-        if (small)
-            InvR1<E, LOG_T, LE1, true>::run(x, tw, base, u, q, two_q, k0);
+        if (mode == 2)
+            InvR1<E, LOG_T, LE1, 2>::run(x, tw, base, u, q, two_q, k0, fq);
+        else if (mode == 1)
+            InvR1<E, LOG_T, LE1, 1>::run(x, tw, base, u, q, two_q, k0);
         else
-            InvR1<E, LOG_T, LE1, false>::run(x, tw, base, u, q, two_q, k0);
+            InvR1<E, LOG_T, LE1, 0>::run(x, tw, base, u, q, two_q, k0);
         if (!COL) __syncthreads();
 #pragma unroll
         for (int e = 0; e < E; e++) smem[sidx(u * E + e)] = x[e];
@@ -534,10 +624,12 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
         // ---- round 2: strided ownership c = u + TPS e, strides E .. T/2
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = smem[sidx(u + TPS * e)];
-        if (small)
-            InvR2<E, TPS, LE2, true>::run(x, tw, base, q, two_q, k0 + LE1);
+        if (mode == 2)
+            InvR2<E, TPS, LE2, 2>::run(x, tw, base, q, two_q, k0 + LE1, fq);
+        else if (mode == 1)
+            InvR2<E, TPS, LE2, 1>::run(x, tw, base, q, two_q, k0 + LE1);
         else
-            InvR2<E, TPS, LE2, false>::run(x, tw, base, q, two_q, k0 + LE1);
+            InvR2<E, TPS, LE2, 0>::run(x, tw, base, q, two_q, k0 + LE1);
         if (COL) {
             // last pass of the inverse: * N^-1 (or the fused per-limb scale), canonical
             uint64_t m = pc.ninv, ms = pc.ninv_shoup;
@@ -545,204 +637,19 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
                 m = f.mulc.w[limb];
                 ms = f.mulc.ws[limb];
             }
+            if (mode == 2) {
+                const double mf = f64_of_u64(m);
 #pragma unroll
-            for (int e = 0; e < E; e++) data[gaddr(u + TPS * e)] = mul_shoup(x[e], m, ms, q);
-        } else {
-#pragma unroll
-            for (int e = 0; e < E; e++) data[gaddr(u + TPS * e)] = x[e];  // [0,2q)
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Persistent, double-buffered NTT pass (plain loads).  Each CTA walks tiles
-// blockIdx.x, +gridDim.x, ...; while one tile is transformed out of shared
-// memory the next one streams in with cp.async (16-B, L1-bypassing), so the
-// HBM latency is hidden behind the butterflies of the previous tile.  Used for
-// every pass whose input is a plain copy of limbs (all second passes, and
-// first passes with LD_PLAIN); fused gathers/conversions keep ntt_pass_kernel.
-// Row-pass tiles are padded by 2 words per E so 16-B cp.async stays aligned.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-template <int LOG_T>
-__device__ __forceinline__ int row_sidx2(int sb, int c) {
-    using S = NttShape<LOG_T>;
-    return sb * (S::T + 2 * S::T / S::E) + c + 2 * (c >> S::LE1);
-}
-
-template <int LOG_T, bool COL>
-__host__ __device__ constexpr int pipe_tile_words(int cb) {
-    return COL ? cb * (1 << LOG_T)
-               : cb * ((1 << LOG_T) + 2 * (1 << LOG_T) / NttShape<LOG_T>::E);
-}
-
-template <int LOG_T, bool INV, bool COL, int IO>
-__global__ void __launch_bounds__(256, 3)
-    ntt_pass_pipe(LimbBatch b, NttTables tb, int log_n, const __grid_constant__ FuseArgs f,
-                  int n_tiles, int tiles_x) {
-    using S = NttShape<LOG_T>;
-    constexpr int T = S::T, E = S::E, TPS = S::TPS, LE1 = S::LE1, LE2 = S::LE2;
-    constexpr bool FIRST = (COL != INV);
-    constexpr int ST = FIRST ? ST_PLAIN : IO;
-    extern __shared__ __align__(16) uint64_t smem[];
-
-    const int n = 1 << log_n;
-    const int CB = blockDim.x / TPS;
-    const int TW = pipe_tile_words<LOG_T, COL>(CB);
-    const int C = n >> LOG_T;
-    const int tid = threadIdx.x;
-    int sb, u;
-    if (COL) {
-        sb = tid % CB;
-        u = tid / CB;
-    } else {
-        sb = tid / TPS;
-        u = tid % TPS;
-    }
-    auto sidx = [&](int c) -> int { return COL ? c * CB + sb : row_sidx2<LOG_T>(sb, c); };
-
-    // tile -> (limb data pointer, load source pointer, sub-transform group)
-    struct Tile {
-        uint64_t *data;
-        const uint64_t *src;
-        int pid, bi, r, t, limb, sub0;
-        bool ok;
-    };
-    auto tile_of = [&](int tile) -> Tile {
-        Tile z;
-        const int y = tile / tiles_x, xg = tile - y * tiles_x;
-        z.limb = y / b.n_polys;
-        const int poly = y - z.limb * b.n_polys;
-        z.bi = poly / b.ppc;
-        z.r = poly - z.bi * b.ppc;
-        z.ok = limb_map(b, z.r, z.limb, z.t, z.pid);
-        z.data = b.ptr + (long long)z.bi * b.ct_stride + (long long)z.r * b.poly_stride + (long long)z.t * n;
-        z.src = z.data;
-        if (FIRST && f.src)
-            z.src = f.src + (long long)z.bi * f.src_ct + (long long)z.r * f.src_ps + (long long)z.t * n;
-        z.sub0 = xg * CB;
-        return z;
-    };
-    // 16-B chunks of a tile: COL: CB columns x T rows (row segments of CB words);
-    // ROW: CB chunks of T contiguous words
-    auto issue = [&](const Tile &z, uint64_t *dst) {
-        if (!z.ok) return;
-        constexpr int W = 2;  // words per 16-B chunk
-        const int per_row = COL ? CB / W : T / W;
-        const int total = COL ? T * per_row : CB * per_row;
-        for (int k = tid; k < total; k += blockDim.x) {
-            const int row = k / per_row, w = (k - row * per_row) * W;
-            if (COL) {
-                cp_async16(dst + row * CB + w, z.src + (long long)row * C + z.sub0 + w);
-            } else {
-                cp_async16(dst + row_sidx2<LOG_T>(row, w), z.src + (long long)(z.sub0 + row) * T + w);
-            }
-        }
-    };
-
-    int tile = blockIdx.x;
-    if (tile < n_tiles) issue(tile_of(tile), smem);
-    cp_async_commit();
-    for (int it = 0; tile < n_tiles; it++, tile += gridDim.x) {
-        const int nxt = tile + gridDim.x;
-        if (nxt < n_tiles) issue(tile_of(nxt), smem + ((it + 1) & 1) * TW);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-        const Tile z = tile_of(tile);
-        uint64_t *cur = smem + (it & 1) * TW;
-        if (z.ok) {
-            const PrimeConst pc = tb.pc[z.pid];
-            const uint64_t q = pc.q, two_q = pc.two_q;
-            const bool small = q < SRK_SMALL_Q;
-            const ulonglong2 *tw = (INV ? tb.itw : tb.tw) + (long long)z.pid * n;
-            const int sub = z.sub0 + sb;
-            const int base = COL ? 1 : (C + sub);
-            auto gaddr = [&](int c) -> long long {
-                return COL ? (long long)c * C + sub : (long long)sub * T + c;
-            };
-            uint64_t x[E];
-            if (!INV) {
-#pragma unroll
-                for (int e = 0; e < E; e++) x[e] = cur[sidx(u + TPS * e)];
-                if (small)
-                    FwdR1<E, LE1, true>::run(x, tw, base, q, two_q);
-                else
-                    FwdR1<E, LE1, false>::run(x, tw, base, q, two_q);
-#pragma unroll
-                for (int e = 0; e < E; e++) cur[sidx(u + TPS * e)] = x[e];
-                __syncthreads();
-#pragma unroll
-                for (int e = 0; e < E; e++) x[e] = cur[sidx(u * E + e)];
-                if (small)
-                    FwdR2<E, TPS, LE1, LE2, true>::run(x, tw, base, u, q, two_q);
-                else
-                    FwdR2<E, TPS, LE1, LE2, false>::run(x, tw, base, u, q, two_q);
-                if (COL) {
-#pragma unroll
-                    for (int e = 0; e < E; e++) z.data[gaddr(u * E + e)] = x[e];
-                } else {
-                    __syncthreads();
-#pragma unroll
-                    for (int e = 0; e < E; e++) {
-                        uint64_t v = x[e];
-                        if (small)
-                            v -= mulhi64(v, pc.ratio_hi) * q;
-                        else
-                            v = v >= two_q ? v - two_q : v;
-                        v = v >= q ? v - q : v;
-                        cur[sidx(u * E + e)] = v;
-                    }
-                    __syncthreads();
-                    row_final_store<LOG_T, ST>(f, cur, sidx, z.bi, z.r, z.t, z.limb, pc, sub, u, log_n,
-                                               z.data);
-                }
+                for (int e = 0; e < E; e++)
+                    data[gaddr(u + TPS * e)] = canon_u64_of_f64(
+                        modmul_f64(__longlong_as_double((long long)x[e]), mf, fq.q, fq.qinv), fq.q, fq.qinv);
             } else {
 #pragma unroll
-                for (int e = 0; e < E; e++) x[e] = cur[sidx(u * E + e)];
-                const int k0 = COL ? log_n - LOG_T : 0;
-                if (small)
-                    InvR1<E, LOG_T, LE1, true>::run(x, tw, base, u, q, two_q, k0);
-                else
-                    InvR1<E, LOG_T, LE1, false>::run(x, tw, base, u, q, two_q, k0);
-#pragma unroll
-                for (int e = 0; e < E; e++) cur[sidx(u * E + e)] = x[e];
-                __syncthreads();
-#pragma unroll
-                for (int e = 0; e < E; e++) x[e] = cur[sidx(u + TPS * e)];
-                if (small)
-                    InvR2<E, TPS, LE2, true>::run(x, tw, base, q, two_q, k0 + LE1);
-                else
-                    InvR2<E, TPS, LE2, false>::run(x, tw, base, q, two_q, k0 + LE1);
-                if (COL) {
-                    uint64_t m = pc.ninv, ms = pc.ninv_shoup;
-                    if constexpr (ST == ST_SCALE) {
-                        m = f.mulc.w[z.limb];
-                        ms = f.mulc.ws[z.limb];
-                    }
-#pragma unroll
-                    for (int e = 0; e < E; e++) z.data[gaddr(u + TPS * e)] = mul_shoup(x[e], m, ms, q);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < E; e++) z.data[gaddr(u + TPS * e)] = x[e];
-                }
+                for (int e = 0; e < E; e++) data[gaddr(u + TPS * e)] = mul_shoup(x[e], m, ms, q);
             }
         } else {
-            __syncthreads();  // keep the barrier count uniform across the CTA
-            if (!INV && !COL) {
-                __syncthreads();
-                __syncthreads();
-                if (ST == ST_MODDOWN && f.out_galois != 1) __syncthreads();
-            }
+#pragma unroll
+            for (int e = 0; e < E; e++) data[gaddr(u + TPS * e)] = x[e];  // lazy / FP64 bits
         }
-        __syncthreads();
     }
-    cp_async_wait<0>();
 }

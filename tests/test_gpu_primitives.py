@@ -264,16 +264,14 @@ def test_batched_ops_match_oracle(pair):
         assert np.array_equal(got[i], orc.rescale(a[i], lvl)), i
 
 
-@pytest.mark.parametrize("chunk,pipe", [("4", "1"), ("4", "0"), ("1000", "0")])
+@pytest.mark.parametrize("chunk", ["4", "1000"])
 @pytest.mark.parametrize("name", ["toy", "cfg1"])
-def test_ntt_chunking_and_kernel_variants(name, chunk, pipe, require_cuda, monkeypatch):
-    """Force multi-chunk NTT launches and both pass kernels (persistent
-    double-buffered / one-tile-per-CTA): limbs must not change."""
+def test_ntt_chunking_and_kernel_variants(name, chunk, require_cuda, monkeypatch):
+    """Force multi-chunk NTT launches: limbs must not change."""
     from oracle.oracle import OracleCKKS
     from paper_2412_15126_b200.backend_cuda import CudaBackend
 
     monkeypatch.setenv("SRK_NTT_CHUNK", chunk)
-    monkeypatch.setenv("SRK_NTT_PIPE", pipe)
     p = preset(name)
     gb, orc = CudaBackend(p), OracleCKKS(p)
     B, lvl, n = 9, p.max_level, p.ring_degree
