@@ -964,15 +964,20 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         ka.beta = beta;
         ka.batch = B;
         {
-            const long long tiles = (long long)ne * n / SRK_KS_TILE;
-            const size_t smem = (size_t)beta * 2 * SRK_KS_TILE * 8;
-            const int blocks = (int)std::min<long long>(tiles, 148 * 8);
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_ks_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-                attr = true;
+            const int blocks = grid_for((long long)ne * n);
+            switch (beta) {
+                case 1: k_ks_inner<1><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n); break;
+                case 2: k_ks_inner<2><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n); break;
+                case 3: k_ks_inner<3><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n); break;
+                case 4: k_ks_inner<4><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n); break;
+                default:
+                    if (beta <= 8)
+                        k_ks_inner<8><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n);
+                    else if (beta <= 16)
+                        k_ks_inner<16><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n);
+                    else
+                        k_ks_inner<64><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n);
             }
-            k_ks_inner<<<blocks, SRK_KS_TILE, smem, s>>>(ka, c->d_pc, c->log_n);
             LAUNCHED();
         }
         if (rescale_d) {

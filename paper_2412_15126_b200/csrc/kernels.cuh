@@ -231,43 +231,62 @@ struct KsInnerArgs {
     int n_primes, nl, ne, level, L, alpha, beta, batch;
 };
 
-// CTA = one limb t x 256 consecutive coefficients; the tile's key words
-// (beta digits x 2 outputs) are staged once in shared memory and reused for
-// every ciphertext of the batch, so registers stay low (high occupancy hides
-// the HBM latency of the ext / d streams).
-#define SRK_KS_TILE 256
-__global__ void __launch_bounds__(SRK_KS_TILE) k_ks_inner(const __grid_constant__ KsInnerArgs a,
-                                                          const PrimeConst *__restrict__ pc, int log_n) {
-    extern __shared__ uint64_t skey[];  // [beta][2][TILE]
+// Thread = one coefficient of one limb t, for every ciphertext of the batch:
+// its beta x 2 key words are loaded once and kept in registers; ciphertexts
+// are processed two at a time so 2 x beta independent ext loads are in flight
+// before the MACs need them (the kernel is HBM-latency bound otherwise).
+template <int MAXD>
+__global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInnerArgs a,
+                                                  const PrimeConst *__restrict__ pc, int log_n) {
     const long long n = 1ll << log_n;
     const long long total = (long long)a.ne * n;
-    const long long tiles = total / SRK_KS_TILE;
-    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const long long x = tile * SRK_KS_TILE + threadIdx.x;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
         const int t = (int)(x >> log_n);
         const long long off = x & (n - 1);
         const int pid = t <= a.level ? t : t + (a.L - a.level);
         const int jt = t < a.nl ? t / a.alpha : -1;
-        __syncthreads();
-        for (int j = 0; j < a.beta; j++) {
-            const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + pid) * n + off;
-            skey[(2 * j) * SRK_KS_TILE + threadIdx.x] = __ldg(kj);
-            skey[(2 * j + 1) * SRK_KS_TILE + threadIdx.x] = __ldg(kj + (long long)a.n_primes * n);
+        uint64_t k0[MAXD], k1[MAXD];
+#pragma unroll
+        for (int j = 0; j < MAXD; j++) {
+            if (j < a.beta) {
+                const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + pid) * n + off;
+                k0[j] = __ldg(kj);
+                k1[j] = __ldg(kj + (long long)a.n_primes * n);
+            }
         }
-        __syncthreads();
         const PrimeConst P = pc[pid];
         const uint64_t *ext = a.ext + (long long)t * n + off;
         const uint64_t *dd = a.d + (long long)t * n + off;
-        for (int b = 0; b < a.batch; b++) {
-            U128 a0 = {0, 0}, a1 = {0, 0};
-            for (int j = 0; j < a.beta; j++) {
-                const uint64_t e = j == jt ? dd[b * a.d_ct] : ext[b * a.ext_ct + j * a.ext_dig];
-                mac(a0, e, skey[(2 * j) * SRK_KS_TILE + threadIdx.x]);
-                mac(a1, e, skey[(2 * j + 1) * SRK_KS_TILE + threadIdx.x]);
+        for (int b = 0; b < a.batch; b += 2) {
+            const bool two = b + 1 < a.batch;
+            uint64_t e0[MAXD], e1[MAXD];
+#pragma unroll
+            for (int j = 0; j < MAXD; j++) {
+                if (j < a.beta) {
+                    const uint64_t *p = j == jt ? dd + b * a.d_ct : ext + b * a.ext_ct + j * a.ext_dig;
+                    const long long st = j == jt ? a.d_ct : a.ext_ct;
+                    e0[j] = p[0];
+                    e1[j] = two ? p[st] : 0;
+                }
+            }
+            U128 a0 = {0, 0}, a1 = {0, 0}, c0 = {0, 0}, c1 = {0, 0};
+#pragma unroll
+            for (int j = 0; j < MAXD; j++) {
+                if (j < a.beta) {
+                    mac(a0, e0[j], k0[j]);
+                    mac(a1, e0[j], k1[j]);
+                    mac(c0, e1[j], k0[j]);
+                    mac(c1, e1[j], k1[j]);
+                }
             }
             uint64_t *o = a.acc + b * a.acc_ct + (long long)t * n + off;
             o[0] = reduce_u128(a0, P);
             o[total] = reduce_u128(a1, P);
+            if (two) {
+                o[a.acc_ct] = reduce_u128(c0, P);
+                o[a.acc_ct + total] = reduce_u128(c1, P);
+            }
         }
     }
 }
