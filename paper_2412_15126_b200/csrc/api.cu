@@ -121,6 +121,7 @@ struct srk_ctx {
     LimbConsts lc_pmod;               // P mod prime_i (all primes)
     std::vector<LimbConsts> lc_qlinv; // [level]: q_level^-1 mod q_i
     int ntt_chunk = 128;              // limbs per L2-resident NTT chunk
+    bool fused_moddown = true;        // conversion inside the NTT load (SRK_MODDOWN_FUSED=0: separate)
 };
 
 template <typename T>
@@ -219,6 +220,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     c->n_primes = n_q + n_p;
     c->primes.assign(primes, primes + c->n_primes);
     if (const char *e = getenv("SRK_NTT_CHUNK")) c->ntt_chunk = std::max(1, atoi(e));
+    if (const char *e = getenv("SRK_MODDOWN_FUSED")) c->fused_moddown = atoi(e) != 0;
     if (c->alpha > 16 || n_p > 16) {
         srk_ctx_destroy(c);
         return fail(SRK_EINVAL, "digit size and special prime count must be <= 16");
@@ -849,6 +851,29 @@ static uint64_t galois_inverse(const srk_ctx *c, uint64_t g) {
     return r;
 }
 
+// forward NTT of the ModDown conversion with the combine fused into its store:
+// either the conversion fused into the first pass's loads (LD_BCONV) or a
+// streaming conversion kernel into the NTT buffer first (then a plain load)
+static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int nout, cudaStream_t s) {
+    if (c->fused_moddown) return ntt_run(c, bq, false, g, LD_BCONV, ST_MODDOWN, s);
+    const long long n = c->n;
+    dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + 7) / 8);
+    const uint64_t *z = g.src;
+    if (g.n_src <= 4)
+        k_moddown_conv<4><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat, g.mat_ld,
+                                               g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
+    else if (g.n_src <= 8)
+        k_moddown_conv<8><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat, g.mat_ld,
+                                               g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
+    else
+        k_moddown_conv<16><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat, g.mat_ld,
+                                                g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
+    LAUNCHED();
+    FuseArgs h = g;
+    h.src = nullptr;  // first pass reads the conversion in place
+    return ntt_run(c, bq, false, h, LD_PLAIN, ST_MODDOWN, s);
+}
+
 struct KsOut {
     uint64_t *out;
     long long out_ct, out_ps;
@@ -1023,8 +1048,8 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             g.add_scaled = 1;
             g.addc = c->lc_qlinv[level];
             g.mulc = c->lc_rs_mulc[level];
-            TRY(ntt_run(c, cbatch(conv, B, 2, 2ll * level * n, (long long)level * n, level, 0), false, g,
-                        LD_BCONV, ST_MODDOWN, s));
+            TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * level * n, (long long)level * n, level, 0), g, B,
+                            level, s));
             continue;
         }
         // 5. INTT of the special limbs, (P/p_k)^-1 folded in -> zb
@@ -1072,8 +1097,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             f.out_galois = ko.galois;
             f.out_galois_inv = galois_inverse(c, ko.galois);
             f.mulc = c->lc_pinv;
-            TRY(ntt_run(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), false, f,
-                        LD_BCONV, ST_MODDOWN, s));
+            TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), f, B, nl, s));
         }
     }
     return SRK_OK;

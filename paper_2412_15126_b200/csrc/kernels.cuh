@@ -291,6 +291,42 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
     }
 }
 
+// ModDown conversion as a streaming kernel (alternative to the fused NTT load):
+//   conv[b][r][t][n] = sum_k z_k[n] mat[k][t] - corr[v(n)][t]  mod q_t
+// one thread per coefficient and chunk of 8 targets: the K z-words and v are
+// loaded once and reused for every target of the chunk.
+template <int MAXK>
+__global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict__ z, long long z_ct,
+                                                      long long z_ps, int n_src,
+                                                      const uint8_t *__restrict__ vround,
+                                                      const uint64_t *__restrict__ mat, int n_dst,
+                                                      const uint64_t *__restrict__ corr,
+                                                      uint64_t *__restrict__ conv, long long c_ct,
+                                                      long long c_ps, const PrimeConst *__restrict__ pc,
+                                                      int log_n) {
+    const long long n = 1ll << log_n;
+    const int p = blockIdx.y;  // (b, r)
+    const int b = p >> 1, r = p & 1;
+    const int t0 = blockIdx.z * 8, t1 = min(n_dst, t0 + 8);
+    const uint64_t *zp = z + b * z_ct + r * z_ps;
+    uint64_t *cp = conv + b * c_ct + r * c_ps;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
+         x += (long long)gridDim.x * blockDim.x) {
+        uint64_t zz[MAXK];
+#pragma unroll
+        for (int k = 0; k < MAXK; k++) zz[k] = k < n_src ? zp[k * n + x] : 0;
+        const int v = vround[(long long)p * n + x];
+        for (int t = t0; t < t1; t++) {
+            U128 acc = {0, 0};
+#pragma unroll
+            for (int k = 0; k < MAXK; k++)
+                if (k < n_src) mac(acc, zz[k], __ldg(mat + k * n_dst + t));
+            const PrimeConst P = pc[t];
+            cp[(long long)t * n + x] = sub_mod(reduce_u128(acc, P), __ldg(corr + v * n_dst + t), P.q);
+        }
+    }
+}
+
 // exact ModDown rounding term per coefficient: v = round(sum_k z_k / p_k)
 // (64.64 fixed point, f_k = z_k R1 + hi(z_k R0), R = floor(2^128 / p_k));
 // z: B*2 polys (ct stride z_ct, poly stride z_ps) of K limbs; v: [B*2][N]
