@@ -121,7 +121,10 @@ struct srk_ctx {
     LimbConsts lc_pmod;               // P mod prime_i (all primes)
     std::vector<LimbConsts> lc_qlinv; // [level]: q_level^-1 mod q_i
     int ntt_chunk = 128;              // limbs per L2-resident NTT chunk
-    bool fused_moddown = true;        // conversion inside the NTT load (SRK_MODDOWN_FUSED=0: separate)
+    // ModDown forward NTT: 0 = conversion and combine in separate streaming
+    // kernels, 1 = both fused into the NTT, 2 = conversion separate, combine
+    // fused into the NTT store (default; fastest on B200, see profiles/)
+    int moddown_mode = 2;
 };
 
 template <typename T>
@@ -220,7 +223,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     c->n_primes = n_q + n_p;
     c->primes.assign(primes, primes + c->n_primes);
     if (const char *e = getenv("SRK_NTT_CHUNK")) c->ntt_chunk = std::max(1, atoi(e));
-    if (const char *e = getenv("SRK_MODDOWN_FUSED")) c->fused_moddown = atoi(e) != 0;
+    if (const char *e = getenv("SRK_MODDOWN_MODE")) c->moddown_mode = atoi(e);
     if (c->alpha > 16 || n_p > 16) {
         srk_ctx_destroy(c);
         return fail(SRK_EINVAL, "digit size and special prime count must be <= 16");
@@ -855,7 +858,7 @@ static uint64_t galois_inverse(const srk_ctx *c, uint64_t g) {
 // either the conversion fused into the first pass's loads (LD_BCONV) or a
 // streaming conversion kernel into the NTT buffer first (then a plain load)
 static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int nout, cudaStream_t s) {
-    if (c->fused_moddown) return ntt_run(c, bq, false, g, LD_BCONV, ST_MODDOWN, s);
+    if (c->moddown_mode == 1) return ntt_run(c, bq, false, g, LD_BCONV, ST_MODDOWN, s);
     const long long n = c->n;
     dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + 7) / 8);
     const uint64_t *z = g.src;
@@ -871,7 +874,31 @@ static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int n
     LAUNCHED();
     FuseArgs h = g;
     h.src = nullptr;  // first pass reads the conversion in place
-    return ntt_run(c, bq, false, h, LD_PLAIN, ST_MODDOWN, s);
+    if (c->moddown_mode == 2) return ntt_run(c, bq, false, h, LD_PLAIN, ST_MODDOWN, s);
+    TRY(ntt_run(c, bq, false, no_fuse(), LD_PLAIN, ST_PLAIN, s));
+    CombineArgs ca;
+    memset(&ca, 0, sizeof ca);
+    ca.conv = bq.ptr;
+    ca.conv_ct = bq.ct_stride;
+    ca.conv_ps = bq.poly_stride;
+    ca.acc = g.acc;
+    ca.acc_ct = g.acc_ct;
+    ca.acc_ps = g.acc_ps;
+    ca.add0 = g.add0;
+    ca.add1 = g.add1;
+    ca.add_ct = g.add_ct;
+    ca.out = g.out;
+    ca.out_ct = g.out_ct;
+    ca.out_ps = g.out_ps;
+    ca.galois = g.out_galois;
+    ca.nl = nout;
+    ca.batch = B;
+    ca.add_scaled = g.add_scaled;
+    ca.mulc = g.mulc;
+    ca.addc = g.addc;
+    k_moddown_combine<<<grid_for(2ll * B * nout * n), 256, 0, s>>>(ca, c->d_pc, c->log_n);
+    LAUNCHED();
+    return SRK_OK;
 }
 
 struct KsOut {

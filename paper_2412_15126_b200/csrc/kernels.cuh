@@ -327,6 +327,49 @@ __global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict
     }
 }
 
+// ModDown combine as a streaming kernel (alternative to the fused NTT store):
+//   w = (acc - conv) mulc + add (addc if add_scaled);  out[m] = w[pi(m)],
+// pi = X -> X^galois on NTT slots (identity for galois == 1)
+struct CombineArgs {
+    const uint64_t *conv;
+    long long conv_ct, conv_ps;
+    const uint64_t *acc;
+    long long acc_ct, acc_ps;
+    const uint64_t *add0, *add1;
+    long long add_ct;
+    uint64_t *out;
+    long long out_ct, out_ps;
+    uint64_t galois;
+    int nl, batch, add_scaled;
+    LimbConsts mulc, addc;
+};
+
+__global__ void k_moddown_combine(const __grid_constant__ CombineArgs a, const PrimeConst *__restrict__ pc,
+                                  int log_n) {
+    const long long n = 1ll << log_n;
+    const long long per = (long long)a.nl * n;
+    const long long total = 2ll * a.batch * per;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long p = x / per, xi = x - p * per;
+        const long long b = p >> 1, r = p & 1;
+        const int i = (int)(xi >> log_n);
+        const long long m = xi & (n - 1);
+        const long long src = a.galois == 1 ? m : (long long)auto_index((uint32_t)m, a.galois, log_n);
+        const long long o = (long long)i * n + src;
+        const PrimeConst P = pc[i];
+        uint64_t v = sub_mod(a.acc[b * a.acc_ct + r * a.acc_ps + o], a.conv[b * a.conv_ct + r * a.conv_ps + o], P.q);
+        v = mul_shoup(v, a.mulc.w[i], a.mulc.ws[i], P.q);
+        const uint64_t *ad = r == 0 ? a.add0 : a.add1;
+        if (ad) {
+            uint64_t av = ad[b * a.add_ct + o];
+            if (a.add_scaled) av = mul_shoup(av, a.addc.w[i], a.addc.ws[i], P.q);
+            v = add_mod(v, av, P.q);
+        }
+        a.out[b * a.out_ct + r * a.out_ps + (long long)i * n + m] = v;
+    }
+}
+
 // exact ModDown rounding term per coefficient: v = round(sum_k z_k / p_k)
 // (64.64 fixed point, f_k = z_k R1 + hi(z_k R0), R = floor(2^128 / p_k));
 // z: B*2 polys (ct stride z_ct, poly stride z_ps) of K limbs; v: [B*2][N]
