@@ -122,9 +122,11 @@ struct srk_ctx {
     std::vector<LimbConsts> lc_qlinv; // [level]: q_level^-1 mod q_i
     int ntt_chunk = 128;              // limbs per L2-resident NTT chunk
     // ModDown forward NTT: 0 = conversion and combine in separate streaming
-    // kernels, 1 = both fused into the NTT, 2 = conversion separate, combine
-    // fused into the NTT store (default; fastest on B200, see profiles/)
-    int moddown_mode = 2;
+    // kernels (default: fastest on B200 -- the NTT passes are latency-bound and
+    // extra loads in them cost more than the streams; profiles/r01), 1 = both
+    // fused into the NTT, 2 = conversion separate, combine fused into the store
+    int moddown_mode = 0;
+    int rescale_fused = 0;            // same trade-off for the rescale (SRK_RESCALE_FUSED=1)
 };
 
 template <typename T>
@@ -224,6 +226,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     c->primes.assign(primes, primes + c->n_primes);
     if (const char *e = getenv("SRK_NTT_CHUNK")) c->ntt_chunk = std::max(1, atoi(e));
     if (const char *e = getenv("SRK_MODDOWN_MODE")) c->moddown_mode = atoi(e);
+    if (const char *e = getenv("SRK_RESCALE_FUSED")) c->rescale_fused = atoi(e);
     if (c->alpha > 16 || n_p > 16) {
         srk_ctx_destroy(c);
         return fail(SRK_EINVAL, "digit size and special prime count must be <= 16");
@@ -756,7 +759,16 @@ static int rescale_impl(srk_ctx *c, const uint64_t *a, long long a_ct, long long
     if (k) g.pre = *k;
     g.mulc = c->lc_qlinv[level];
     LimbBatch bq = cbatch(tb, B, 2, 2ll * level * n, (long long)level * n, level, 0);
-    return ntt_run(c, bq, false, g, LD_SPREAD, ST_RESCALE, s);
+    if (c->rescale_fused) return ntt_run(c, bq, false, g, LD_SPREAD, ST_RESCALE, s);
+    // streaming spread -> plain NTT -> streaming combine
+    k_rescale_spread<<<grid_for(2ll * B * level * n), 256, 0, s>>>(top, tb, c->d_pc, c->log_n, level, B);
+    LAUNCHED();
+    TRY(ntt_run(c, bq, false, no_fuse(), LD_PLAIN, ST_PLAIN, s));
+    k_rescale_combine<<<grid_for(2ll * B * level * n), 256, 0, s>>>(
+        a, a_ct, a_ps, pt, pt_ct, k ? *k : LimbConsts{}, mode, tb, c->lc_qlinv[level], out, out_ct,
+        c->d_pc, c->log_n, level, B);
+    LAUNCHED();
+    return SRK_OK;
 }
 
 // chunk a batch of B into SRK_WS_BATCH pieces

@@ -135,6 +135,47 @@ __global__ void k_rescale_top(const uint64_t *__restrict__ a, long long a_ct, lo
     }
 }
 
+// t[b][p][i] = centred(top[b][p]) mod q_i for i < level  (streaming rescale spread)
+__global__ void k_rescale_spread(const uint64_t *__restrict__ top, uint64_t *__restrict__ t,
+                                 const PrimeConst *__restrict__ pc, int log_n, int level, int batch) {
+    const long long n = 1ll << log_n;
+    const long long per = (long long)level * n;
+    const long long total = 2ll * batch * per;
+    const uint64_t ql = pc[level].q;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long p = x / per, xi = x - p * per;
+        const int i = (int)(xi >> log_n);
+        const PrimeConst P = pc[i];
+        const uint64_t v = top[p * n + (xi & (n - 1))];
+        t[x] = v > (ql >> 1) ? sub_mod(reduce64(v, P), reduce64(ql, P), P.q) : reduce64(v, P);
+    }
+}
+
+// out[b][p][i] = (a[b][p][i] * pre_i - t[b][p][i]) * q_l^-1   (streaming rescale combine)
+__global__ void k_rescale_combine(const uint64_t *__restrict__ a, long long a_ct, long long a_ps,
+                                  const uint64_t *__restrict__ pt, long long pt_ct, LimbConsts k,
+                                  int mode, const uint64_t *__restrict__ t, LimbConsts qlinv,
+                                  uint64_t *__restrict__ out, long long out_ct,
+                                  const PrimeConst *__restrict__ pc, int log_n, int level, int batch) {
+    const long long n = 1ll << log_n;
+    const long long per = (long long)level * n;
+    const long long total = 2ll * batch * per;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long p = x / per, xi = x - p * per;
+        const long long b = p >> 1, r = p & 1;
+        const int i = (int)(xi >> log_n);
+        const long long off = xi & (n - 1);
+        const PrimeConst P = pc[i];
+        uint64_t v = a[b * a_ct + r * a_ps + (long long)i * n + off];
+        if (mode == 1) v = mul_shoup(v, k.w[i], k.ws[i], P.q);
+        if (mode == 2) v = mul_mod(v, pt[b * pt_ct + (long long)i * n + off], P);
+        v = sub_mod(v, t[x], P.q);
+        out[b * out_ct + r * per + (long long)i * n + off] = mul_shoup(v, qlinv.w[i], qlinv.ws[i], P.q);
+    }
+}
+
 // ---------------------------------------------------------------------
 // Galois automorphism in the NTT domain (gather, one permutation per limb)
 // ---------------------------------------------------------------------
