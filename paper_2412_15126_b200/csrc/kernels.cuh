@@ -235,20 +235,7 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
             uint64_t y[GS];
 #pragma unroll
             for (int i = 0; i < GS; i++) y[i] = src[(long long)i * n + x];
-            // two targets per step: independent MAC / reduction chains interleave
-            int t = t0;
-            for (; t + 1 < t1; t += 2) {
-                U128 acc0 = {0, 0}, acc1 = {0, 0};
-#pragma unroll
-                for (int i = 0; i < GS; i++) {
-                    mac(acc0, y[i], __ldg(mat + i * nd + t));
-                    mac(acc1, y[i], __ldg(mat + i * nd + t + 1));
-                }
-                dst[(long long)__ldg(a.slot[j] + t) * n + x] = reduce_u128(acc0, pc[__ldg(a.pid[j] + t)]);
-                dst[(long long)__ldg(a.slot[j] + t + 1) * n + x] =
-                    reduce_u128(acc1, pc[__ldg(a.pid[j] + t + 1)]);
-            }
-            if (t < t1) {
+            for (int t = t0; t < t1; t++) {
                 U128 acc = {0, 0};
 #pragma unroll
                 for (int i = 0; i < GS; i++) mac(acc, y[i], __ldg(mat + i * nd + t));
@@ -370,18 +357,13 @@ __global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict
 #pragma unroll
         for (int k = 0; k < MAXK; k++) zz[k] = k < n_src ? zp[k * n + x] : 0;
         const int v = vround[(long long)p * n + x];
-        // all 8 targets of the chunk unrolled: independent reduction chains interleave
+        for (int t = t0; t < t1; t++) {
+            U128 acc = {0, 0};
 #pragma unroll
-        for (int tt = 0; tt < 8; tt++) {
-            const int t = t0 + tt;
-            if (t < t1) {
-                U128 acc = {0, 0};
-#pragma unroll
-                for (int k = 0; k < MAXK; k++)
-                    if (k < n_src) mac(acc, zz[k], __ldg(mat + k * n_dst + t));
-                const PrimeConst P = pc[t];
-                cp[(long long)t * n + x] = sub_mod(reduce_u128(acc, P), __ldg(corr + v * n_dst + t), P.q);
-            }
+            for (int k = 0; k < MAXK; k++)
+                if (k < n_src) mac(acc, zz[k], __ldg(mat + k * n_dst + t));
+            const PrimeConst P = pc[t];
+            cp[(long long)t * n + x] = sub_mod(reduce_u128(acc, P), __ldg(corr + v * n_dst + t), P.q);
         }
     }
 }
