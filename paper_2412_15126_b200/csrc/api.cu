@@ -440,6 +440,9 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
     const int subs = c->n >> LOG_T;  // sub-transforms per limb
     int cb = 256 / SH::TPS;
     if (cb > subs) cb = subs;
+    // small batches (single-ciphertext ops): narrower tiles so the grid covers
+    // several waves of the 148 SMs instead of ~1 wave plus a long tail
+    while (cb > 4 && (long long)(subs / cb) * nlc * b.n_polys < 148 * 3 * 4) cb >>= 1;
     const int threads = cb * SH::TPS;
     const size_t smem = COL ? (size_t)cb * SH::T * 8 : (size_t)cb * (SH::T + SH::T / SH::E) * 8;
     // shift the batch to start at limb l0 (mode 0: pointer + prime offsets; mode 1 keeps the
