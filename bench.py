@@ -230,6 +230,42 @@ def time_region(torch, fn, reps, barrier=None):
     return a.elapsed_time(b) / reps
 
 
+def _event_time(torch, fn, dist=None):
+    """Seconds between CUDA events around fn on the current stream (max over ranks)."""
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    r = fn()
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / 1e3], device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), r
+
+
+def run_sharded_sort(torch, dist):
+    """Config 5 on every rank: multi_sort of N=1024 sharded over the world (shard.py)."""
+    from paper_2412_15126_b200 import (B200Engine, KernelConfig, SortConfig, block_merge, block_split)
+    from paper_2412_15126_b200.params import preset
+    from paper_2412_15126_b200.shard import Comm, multi_sort_sharded
+
+    eng = B200Engine(preset("long"))
+    v1024 = np.random.default_rng(0).choice(8192, 1024, replace=False) / 8192
+    scfg = SortConfig(kernel=KernelConfig(mode="composite", composite=(6, 2), indicator_composite=(6, 2)),
+                      tie_correction=False)
+    bv = block_split(eng, v1024)
+    comm = Comm()
+    multi_sort_sharded(eng, bv, scfg, comm)  # warm-up: keys, plaintext cache
+    dt, res = _event_time(torch, lambda: multi_sort_sharded(eng, bv, scfg, comm), dist)
+    srt = block_merge(eng, res)
+    return {"latency_s": dt, "order_ok": bool(np.array_equal(np.argsort(srt), np.arange(1024))),
+            "max_abs_err": float(np.abs(srt - np.sort(v1024)).max()), "params": "long",
+            "gpus": comm.world, "sharding": "block pairs + placements round-robin, NCCL all-reduce"}
+
+
 def run_pipelines(torch, quick=False):
     """BASELINE pipeline latencies (seconds) on cuda:current, decrypted results checked."""
     from oracle.plain import fractional_ranks  # result-level checker only
@@ -362,10 +398,16 @@ def gpu_arm(args):
     e2e_ms = float(te.item())
 
     pipelines = None
-    if rank_id == 0 and not args.no_pipelines:
+    if not args.no_pipelines:
         del step
         torch.cuda.empty_cache()
-        pipelines = run_pipelines(torch, quick=args.quick)
+        if rank_id == 0:
+            pipelines = run_pipelines(torch, quick=args.quick or world > 1)
+        if world > 1:
+            dist.barrier()
+            sharded = run_sharded_sort(torch, dist) if not args.quick else None
+            if rank_id == 0 and sharded is not None:
+                pipelines["sort_n1024_s"] = sharded
 
     if rank_id == 0:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(

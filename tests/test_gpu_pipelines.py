@@ -119,9 +119,10 @@ def test_multi_sort_n256(eng_long):
     assert np.abs(out - np.sort(v)).max() < 1e-3
 
 
-def test_tie_corrected_rank_and_sort(eng12):
+def test_tie_corrected_rank_and_sort(eng12, eng_long):
     """Ties: corrected ranks are a permutation (reference ranking.py:203-232), and
-    the tie-corrected sort returns the sorted multiset (composite kernels)."""
+    the tie-corrected sort returns the sorted multiset (composite kernels; the
+    sort needs ~38 levels, so it runs on the long chain)."""
     from oracle.plain import corrected_ranks
 
     v = np.array([0.5, 0.25, 0.5, 0.75, 0.25, 0.5, 0.125, 1.0,
@@ -129,16 +130,16 @@ def test_tie_corrected_rank_and_sort(eng12):
     cfg = M.KernelConfig(mode="composite", composite=(3, 2), indicator_composite=(3, 2))
     r = M.read_row(eng12, M.rank_corrected(eng12, eng12.encrypt(v), 16, cfg).ranks, 16)
     assert np.array_equal(np.rint(r), corrected_ranks(v))
-    out = M.read_row(eng12, M.sort(eng12, eng12.encrypt(v), 16, M.SortConfig(kernel=cfg)), 16)
+    out = M.read_row(eng_long, M.sort(eng_long, eng_long.encrypt(v), 16, M.SortConfig(kernel=cfg)), 16)
     assert np.abs(out - np.sort(v)).max() < 1e-3
 
 
 def test_chebyshev_sort_matches_reference_simulator(eng12):
     """The reference's own Chebyshev sort circuit on the GPU vs the slot oracle."""
     v = np.array([0.15, 0.55, 0.35, 0.95, 0.05, 0.75, 0.25, 0.85])
-    cfg = M.SortConfig(kernel=M.KernelConfig(mode="chebyshev", degree=128), tie_correction=False)
+    cfg = M.SortConfig(kernel=M.KernelConfig(mode="chebyshev", degree=512), tie_correction=False)
     out = M.read_row(eng12, M.sort(eng12, eng12.encrypt(v), 8, cfg), 8)
     sim = SlotSim(SimParams(eng12.params.slot_count, eng12.params.max_level))
     ref = M.read_row(sim, M.sort(sim, sim.encrypt(v), 8, cfg), 8)
     assert np.abs(out - ref).max() < 1e-4
-    assert np.array_equal(np.argsort(out), np.argsort(np.sort(v)))
+    assert np.abs(out - np.sort(v)).max() < 1e-3
