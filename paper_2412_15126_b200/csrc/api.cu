@@ -127,6 +127,7 @@ struct srk_ctx {
     // fused into the NTT, 2 = conversion separate, combine fused into the store
     int moddown_mode = 0;
     int rescale_fused = 0;            // same trade-off for the rescale (SRK_RESCALE_FUSED=1)
+    int ks_fused = 1;                 // Q-limb inner product fused into the combine (SRK_KS_FUSED=0: off)
 };
 
 template <typename T>
@@ -227,6 +228,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     if (const char *e = getenv("SRK_NTT_CHUNK")) c->ntt_chunk = std::max(1, atoi(e));
     if (const char *e = getenv("SRK_MODDOWN_MODE")) c->moddown_mode = atoi(e);
     if (const char *e = getenv("SRK_RESCALE_FUSED")) c->rescale_fused = atoi(e);
+    if (const char *e = getenv("SRK_KS_FUSED")) c->ks_fused = atoi(e);
     if (c->alpha > 16 || n_p > 16) {
         srk_ctx_destroy(c);
         return fail(SRK_EINVAL, "digit size and special prime count must be <= 16");
@@ -872,7 +874,8 @@ static uint64_t galois_inverse(const srk_ctx *c, uint64_t g) {
 // forward NTT of the ModDown conversion with the combine fused into its store:
 // either the conversion fused into the first pass's loads (LD_BCONV) or a
 // streaming conversion kernel into the NTT buffer first (then a plain load)
-static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int nout, cudaStream_t s) {
+static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int nout, cudaStream_t s,
+                       bool combine = true) {
     if (c->moddown_mode == 1) return ntt_run(c, bq, false, g, LD_BCONV, ST_MODDOWN, s);
     const long long n = c->n;
     dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + 7) / 8);
@@ -891,6 +894,7 @@ static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int n
     h.src = nullptr;  // first pass reads the conversion in place
     if (c->moddown_mode == 2) return ntt_run(c, bq, false, h, LD_PLAIN, ST_MODDOWN, s);
     TRY(ntt_run(c, bq, false, no_fuse(), LD_PLAIN, ST_PLAIN, s));
+    if (!combine) return SRK_OK;
     CombineArgs ca;
     memset(&ca, 0, sizeof ca);
     ca.conv = bq.ptr;
@@ -1009,6 +1013,8 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         TRY(ntt_run(c, b, false, no_fuse(), LD_PLAIN, ST_PLAIN, s));
     }
     const BconvPlan &pd = c->moddown[level];
+    // the ciphertext-modulus limbs' inner product is fused into the combine
+    const bool ks_fused = !rescale_d && c->moddown_mode == 0 && c->ks_fused;
     for (int o = 0; o < n_out; o++) {
         const KsOut &ko = outs[o];
         // 4. inner product (+ automorphism)
@@ -1030,8 +1036,9 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         ka.alpha = alpha;
         ka.beta = beta;
         ka.batch = B;
+        ka.t0 = ks_fused ? nl : 0;
         {
-            const int blocks = grid_for((long long)ne * n);
+            const int blocks = grid_for((long long)(ne - ka.t0) * n);
             switch (beta) {
                 case 1: k_ks_inner<1><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n); break;
                 case 2: k_ks_inner<2><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n); break;
@@ -1139,7 +1146,50 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             f.out_galois = ko.galois;
             f.out_galois_inv = galois_inverse(c, ko.galois);
             f.mulc = c->lc_pinv;
-            TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), f, B, nl, s));
+            TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), f, B, nl, s,
+                            !ks_fused));
+            if (ks_fused) {
+                // 7. out = sigma_g(add + (sum_j e_j key_j - conv) P^-1) over q_0..q_l
+                KsCombineArgs kc;
+                memset(&kc, 0, sizeof kc);
+                kc.d = d;
+                kc.d_ct = d_ct;
+                kc.ext = ext;
+                kc.ext_ct = (long long)beta * ne * n;
+                kc.ext_dig = (long long)ne * n;
+                kc.key = ko.key;
+                kc.conv = conv;
+                kc.conv_ct = 2ll * nl * n;
+                kc.conv_ps = (long long)nl * n;
+                kc.add0 = ko.add0;
+                kc.add1 = ko.add1;
+                kc.add_ct = ko.add_ct;
+                kc.out = ko.out;
+                kc.out_ct = ko.out_ct;
+                kc.out_ps = ko.out_ps;
+                kc.galois = ko.galois;
+                kc.n_primes = c->n_primes;
+                kc.nl = nl;
+                kc.alpha = alpha;
+                kc.beta = beta;
+                kc.batch = B;
+                kc.mulc = c->lc_pinv;
+                const int blocks = grid_for((long long)nl * n);
+                switch (beta) {
+                    case 1: k_ks_combine<1><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+                    case 2: k_ks_combine<2><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+                    case 3: k_ks_combine<3><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+                    case 4: k_ks_combine<4><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+                    default:
+                        if (beta <= 8)
+                            k_ks_combine<8><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
+                        else if (beta <= 16)
+                            k_ks_combine<16><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
+                        else
+                            k_ks_combine<64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
+                }
+                LAUNCHED();
+            }
         }
     }
     return SRK_OK;

@@ -270,6 +270,7 @@ struct KsInnerArgs {
     long long acc_ct;
     uint64_t galois;
     int n_primes, nl, ne, level, L, alpha, beta, batch;
+    int t0;  // first extended-basis limb to produce (nl: special limbs only)
 };
 
 // Thread = one coefficient of one limb t, for every ciphertext of the batch:
@@ -280,10 +281,11 @@ template <int MAXD>
 __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInnerArgs a,
                                                   const PrimeConst *__restrict__ pc, int log_n) {
     const long long n = 1ll << log_n;
-    const long long total = (long long)a.ne * n;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+    const long long total = (long long)a.ne * n;  // acc poly stride
+    const long long work = (long long)(a.ne - a.t0) * n;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < work;
          x += (long long)gridDim.x * blockDim.x) {
-        const int t = (int)(x >> log_n);
+        const int t = a.t0 + (int)(x >> log_n);
         const long long off = x & (n - 1);
         const int pid = t <= a.level ? t : t + (a.L - a.level);
         const int jt = t < a.nl ? t / a.alpha : -1;
@@ -408,6 +410,100 @@ __global__ void k_moddown_combine(const __grid_constant__ CombineArgs a, const P
             v = add_mod(v, av, P.q);
         }
         a.out[b * a.out_ct + r * a.out_ps + (long long)i * n + m] = v;
+    }
+}
+
+// Key-switch inner product of the ciphertext-modulus limbs fused into the
+// ModDown combine (the special limbs' inner product ran first through
+// k_ks_inner with t0 = nl, was INTT'd and converted):
+//   out[b][r][i][m] = (sum_j e_j key_r_j - conv[b][r]) P^-1 (+ add_r)  at src = sigma(m)
+// so the 2 x nl accumulator limbs are never written or re-read.  Thread = one
+// coefficient of one limb for every ciphertext of the batch (keys in
+// registers); all reads are at the sigma-gathered index, which keeps each
+// aligned 2^k block of m inside an aligned 2^k block of src (coalesced).
+struct KsCombineArgs {
+    const uint64_t *d;
+    long long d_ct;
+    const uint64_t *ext;
+    long long ext_ct, ext_dig;
+    const uint64_t *key;
+    const uint64_t *conv;
+    long long conv_ct, conv_ps;
+    const uint64_t *add0, *add1;
+    long long add_ct;
+    uint64_t *out;
+    long long out_ct, out_ps;
+    uint64_t galois;
+    int n_primes, nl, alpha, beta, batch;
+    LimbConsts mulc;
+};
+
+template <int MAXD>
+__global__ void __launch_bounds__(256) k_ks_combine(const __grid_constant__ KsCombineArgs a,
+                                                    const PrimeConst *__restrict__ pc, int log_n) {
+    const long long n = 1ll << log_n;
+    const long long work = (long long)a.nl * n;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < work;
+         x += (long long)gridDim.x * blockDim.x) {
+        const int t = (int)(x >> log_n);
+        const long long m = x & (n - 1);
+        const long long src = a.galois == 1 ? m : (long long)auto_index((uint32_t)m, a.galois, log_n);
+        const int jt = t / a.alpha;
+        uint64_t k0[MAXD], k1[MAXD];
+#pragma unroll
+        for (int j = 0; j < MAXD; j++) {
+            if (j < a.beta) {
+                const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + t) * n + src;
+                k0[j] = __ldg(kj);
+                k1[j] = __ldg(kj + (long long)a.n_primes * n);
+            }
+        }
+        const PrimeConst P = pc[t];
+        const uint64_t w = a.mulc.w[t], ws = a.mulc.ws[t];
+        const long long o = (long long)t * n + src;
+        for (int b = 0; b < a.batch; b += 2) {
+            const bool two = b + 1 < a.batch;
+            uint64_t e0[MAXD], e1[MAXD];
+#pragma unroll
+            for (int j = 0; j < MAXD; j++) {
+                if (j < a.beta) {
+                    const uint64_t *p = j == jt ? a.d + b * a.d_ct + o : a.ext + b * a.ext_ct + j * a.ext_dig + o;
+                    const long long st = j == jt ? a.d_ct : a.ext_ct;
+                    e0[j] = p[0];
+                    e1[j] = two ? p[st] : 0;
+                }
+            }
+            const uint64_t *cv = a.conv + b * a.conv_ct + o;
+            const uint64_t cv00 = cv[0], cv01 = cv[a.conv_ps];
+            const uint64_t cv10 = two ? cv[a.conv_ct] : 0, cv11 = two ? cv[a.conv_ct + a.conv_ps] : 0;
+            uint64_t ad00 = 0, ad01 = 0, ad10 = 0, ad11 = 0;
+            if (a.add0) {
+                ad00 = a.add0[b * a.add_ct + o];
+                ad10 = two ? a.add0[(b + 1) * a.add_ct + o] : 0;
+            }
+            if (a.add1) {
+                ad01 = a.add1[b * a.add_ct + o];
+                ad11 = two ? a.add1[(b + 1) * a.add_ct + o] : 0;
+            }
+            U128 s0 = {0, 0}, s1 = {0, 0}, u0 = {0, 0}, u1 = {0, 0};
+#pragma unroll
+            for (int j = 0; j < MAXD; j++) {
+                if (j < a.beta) {
+                    mac(s0, e0[j], k0[j]);
+                    mac(s1, e0[j], k1[j]);
+                    mac(u0, e1[j], k0[j]);
+                    mac(u1, e1[j], k1[j]);
+                }
+            }
+            uint64_t *op = a.out + b * a.out_ct + (long long)t * n + m;
+            op[0] = add_mod(mul_shoup(sub_mod(reduce_u128(s0, P), cv00, P.q), w, ws, P.q), ad00, P.q);
+            op[a.out_ps] = add_mod(mul_shoup(sub_mod(reduce_u128(s1, P), cv01, P.q), w, ws, P.q), ad01, P.q);
+            if (two) {
+                op[a.out_ct] = add_mod(mul_shoup(sub_mod(reduce_u128(u0, P), cv10, P.q), w, ws, P.q), ad10, P.q);
+                op[a.out_ct + a.out_ps] =
+                    add_mod(mul_shoup(sub_mod(reduce_u128(u1, P), cv11, P.q), w, ws, P.q), ad11, P.q);
+            }
+        }
     }
 }
 

@@ -295,3 +295,43 @@ def test_ntt_chunking_and_kernel_variants(name, chunk, require_cuda, monkeypatch
          gb.stream())
     got = host(gb, out).reshape(B, 2, lvl, n)
     assert np.array_equal(got[B - 1], orc.rescale(a[B - 1], lvl))
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+@pytest.mark.parametrize("name", ["toy", "cfg1"])
+def test_keyswitch_fused_combine_paths(name, fused, require_cuda, monkeypatch):
+    """SRK_KS_FUSED=1 (inner product fused into the ModDown combine) and =0
+    (separate k_ks_inner + combine) give the oracle's limbs for rotate,
+    hoisted rotate and relinearise (odd batch: the two-at-a-time tail)."""
+    import ctypes
+
+    from oracle.oracle import OracleCKKS
+    from paper_2412_15126_b200.backend_cuda import CudaBackend
+
+    monkeypatch.setenv("SRK_KS_FUSED", fused)
+    p = preset(name)
+    gb, orc = CudaBackend(p), OracleCKKS(p)
+    B, lvl, n = 3, p.max_level - 1, p.ring_degree
+    ps = (lvl + 1) * n
+    a = rand_limbs(p, (B, 2), lvl, 60)
+    b = rand_limbs(p, (B, 2), lvl, 61)
+    key = _key(p, 62)
+    ta, tb, tk = dev(gb, a), dev(gb, b), dev(gb, key)
+    g1, g2 = pow(5, 3, 2 * n), pow(5, 2 * n // 4 - 1, 2 * n)
+    r1, r2 = rot_layout(gb, key, g1), rot_layout(gb, key, g2)
+    o1, o2 = gb.empty_ct(lvl, polys=2 * B), gb.empty_ct(lvl, polys=2 * B)
+    keys = (ctypes.c_void_p * 2)(ptr(r1), ptr(r2))
+    gal = (ctypes.c_uint64 * 2)(g1, g2)
+    outs = (ctypes.c_void_p * 2)(ptr(o1), ptr(o2))
+    call(gb, "srk_rotate_hoisted", ptr(ta), 2 * ps, B, 2, keys, gal, outs, 2 * ps, lvl,
+         gb.workspace(), gb.stream())
+    for o, g in ((o1, g1), (o2, g2)):
+        got = host(gb, o).reshape(B, 2, lvl + 1, n)
+        for i in (0, B - 1):
+            assert np.array_equal(got[i], orc.rotate_raw(a[i], key, g, lvl)), (g, i)
+    out = gb.empty_ct(lvl, polys=2 * B)
+    call(gb, "srk_mul_relin_batch", ptr(ta), ptr(tb), 2 * ps, ptr(tk), ptr(out), 2 * ps, B, lvl, 0,
+         gb.workspace(), gb.stream())
+    got = host(gb, out).reshape(B, 2, lvl + 1, n)
+    for i in range(B):
+        assert np.array_equal(got[i], orc.mul_relin(a[i], b[i], key, lvl)), i
