@@ -95,6 +95,7 @@ static inline uint32_t hbrv(uint32_t x, int bits) {
 // ---------------------------------------------------------------------
 struct BconvPlan {
     uint64_t *mat = nullptr;   // [n_src][n_dst]
+    ulonglong2 *mat2 = nullptr;  // [n_src][n_dst] {m, floor(m 2^64 / q_t)} (Shoup)
     uint64_t *hinv = nullptr;  // [2][n_src]
     int *dst_slot = nullptr;
     int *dst_pid = nullptr;
@@ -173,6 +174,13 @@ static int build_plan(srk_ctx *c, BconvPlan &pl, const std::vector<int> &src_pid
     pl.n_dst = nd;
     pl.src_pid0 = src_pids[0];
     TRY(dupload(c, &pl.mat, mat));
+    std::vector<ulonglong2> mat2((size_t)ns * nd);
+    for (int i = 0; i < ns; i++)
+        for (int t = 0; t < nd; t++) {
+            const uint64_t m = mat[(size_t)i * nd + t];
+            mat2[(size_t)i * nd + t] = make_ulonglong2(m, shoup(m, c->primes[dst_pids[t]]));
+        }
+    TRY(dupload(c, &pl.mat2, mat2));
     TRY(dupload(c, &pl.hinv, hv));
     TRY(dupload(c, &pl.dst_slot, dst_slots));
     TRY(dupload(c, &pl.dst_pid, dst_pids));
@@ -881,13 +889,13 @@ static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int n
     dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + 7) / 8);
     const uint64_t *z = g.src;
     if (g.n_src <= 4)
-        k_moddown_conv<4><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat, g.mat_ld,
+        k_moddown_conv<4><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2, g.mat_ld,
                                                g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
     else if (g.n_src <= 8)
-        k_moddown_conv<8><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat, g.mat_ld,
+        k_moddown_conv<8><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2, g.mat_ld,
                                                g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
     else
-        k_moddown_conv<16><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat, g.mat_ld,
+        k_moddown_conv<16><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2, g.mat_ld,
                                                 g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
     LAUNCHED();
     FuseArgs h = g;
@@ -1081,6 +1089,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             g.src_ps = (long long)ns * n;
             g.n_src = ns;
             g.mat = pr.mat;
+            g.mat2 = pr.mat2;
             g.mat_ld = pr.n_dst;
             g.corr = pr.dst_corr;
             g.corr_ld = pr.n_dst;
@@ -1126,6 +1135,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             f.n_src = K;
             f.src_pid0 = c->n_q;
             f.mat = pd.mat;
+            f.mat2 = pd.mat2;
             f.mat_ld = pd.n_dst;
             f.corr = pd.dst_corr;
             f.corr_ld = pd.n_dst;

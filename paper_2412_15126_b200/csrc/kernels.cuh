@@ -337,12 +337,15 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
 // ModDown conversion as a streaming kernel (alternative to the fused NTT load):
 //   conv[b][r][t][n] = sum_k z_k[n] mat[k][t] - corr[v(n)][t]  mod q_t
 // one thread per coefficient and chunk of 8 targets: the K z-words and v are
-// loaded once and reused for every target of the chunk.
+// loaded once and reused for every target of the chunk.  Each term is a
+// Shoup product (mat2 = {m, floor(m 2^64 / q_t)}) in [0, 2q), folded into a
+// [0, 2q) running sum -- about half the instructions of a 128-bit MAC chain
+// plus one two-word Barrett reduction.
 template <int MAXK>
 __global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict__ z, long long z_ct,
                                                       long long z_ps, int n_src,
                                                       const uint8_t *__restrict__ vround,
-                                                      const uint64_t *__restrict__ mat, int n_dst,
+                                                      const ulonglong2 *__restrict__ mat2, int n_dst,
                                                       const uint64_t *__restrict__ corr,
                                                       uint64_t *__restrict__ conv, long long c_ct,
                                                       long long c_ps, const PrimeConst *__restrict__ pc,
@@ -360,19 +363,21 @@ __global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict
         for (int k = 0; k < MAXK; k++) zz[k] = k < n_src ? zp[k * n + x] : 0;
         const int v = vround[(long long)p * n + x];
         for (int t = t0; t < t1; t++) {
-            U128 acc = {0, 0};
+            const uint64_t q = pc[t].q, two_q = 2 * q;
+            uint64_t acc = 0;
 #pragma unroll
             for (int k = 0; k < MAXK; k++)
-                if (k < n_src) mac(acc, zz[k], __ldg(mat + k * n_dst + t));
-            const PrimeConst P = pc[t];
-            cp[(long long)t * n + x] = sub_mod(reduce_u128(acc, P), __ldg(corr + v * n_dst + t), P.q);
+                if (k < n_src) {
+                    const ulonglong2 mw = __ldg(mat2 + k * n_dst + t);
+                    acc += mul_shoup_lazy(zz[k], mw.x, mw.y, q);
+                    acc = acc >= two_q ? acc - two_q : acc;
+                }
+            acc = acc >= q ? acc - q : acc;
+            cp[(long long)t * n + x] = sub_mod(acc, __ldg(corr + v * n_dst + t), q);
         }
     }
 }
 
-// ModDown combine as a streaming kernel (alternative to the fused NTT store):
-//   w = (acc - conv) mulc + add (addc if add_scaled);  out[m] = w[pi(m)],
-// pi = X -> X^galois on NTT slots (identity for galois == 1)
 struct CombineArgs {
     const uint64_t *conv;
     long long conv_ct, conv_ps;

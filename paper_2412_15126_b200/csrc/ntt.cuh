@@ -93,6 +93,7 @@ struct FuseArgs {
     uint64_t galois;         // LD_AUTO: X -> X^galois gather
     int n_src, src_pid0;     // LD_BCONV: z limbs under primes src_pid0 ..
     const uint64_t *mat;     // LD_BCONV: [n_src][mat_ld] conversion constants
+    const ulonglong2 *mat2;  // the same with Shoup companions (streaming conversion)
     int mat_ld;
     const uint64_t *corr;    // LD_BCONV: [v * prod src primes]_{q_t}, table [v][corr_ld]
     int corr_ld;
