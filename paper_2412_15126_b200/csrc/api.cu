@@ -1186,17 +1186,17 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
                 kc.mulc = c->lc_pinv;
                 const int blocks = grid_for((long long)nl * n);
                 switch (beta) {
-                    case 1: k_ks_combine<1><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-                    case 2: k_ks_combine<2><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-                    case 3: k_ks_combine<3><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-                    case 4: k_ks_combine<4><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+                    case 1: k_ks_combine<1, true><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+                    case 2: k_ks_combine<2, true><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+                    case 3: k_ks_combine<3, true><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+                    case 4: k_ks_combine<4, true><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
                     default:
                         if (beta <= 8)
-                            k_ks_combine<8><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
+                            k_ks_combine<8, false><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
                         else if (beta <= 16)
-                            k_ks_combine<16><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
+                            k_ks_combine<16, false><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
                         else
-                            k_ks_combine<64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
+                            k_ks_combine<64, false><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
                 }
                 LAUNCHED();
             }

@@ -443,8 +443,12 @@ struct KsCombineArgs {
     LimbConsts mulc;
 };
 
-template <int MAXD>
-__global__ void __launch_bounds__(256) k_ks_combine(const __grid_constant__ KsCombineArgs a,
+#ifndef SRK_KSC_MINB
+#define SRK_KSC_MINB 3
+#endif
+// EXACT: beta == MAXD (no per-digit predicates)
+template <int MAXD, bool EXACT>
+__global__ void __launch_bounds__(256, SRK_KSC_MINB) k_ks_combine(const __grid_constant__ KsCombineArgs a,
                                                     const PrimeConst *__restrict__ pc, int log_n) {
     const long long n = 1ll << log_n;
     const long long work = (long long)a.nl * n;
@@ -457,7 +461,7 @@ __global__ void __launch_bounds__(256) k_ks_combine(const __grid_constant__ KsCo
         uint64_t k0[MAXD], k1[MAXD];
 #pragma unroll
         for (int j = 0; j < MAXD; j++) {
-            if (j < a.beta) {
+            if (EXACT || j < a.beta) {
                 const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + t) * n + src;
                 k0[j] = __ldg(kj);
                 k1[j] = __ldg(kj + (long long)a.n_primes * n);
@@ -471,7 +475,7 @@ __global__ void __launch_bounds__(256) k_ks_combine(const __grid_constant__ KsCo
             uint64_t e0[MAXD], e1[MAXD];
 #pragma unroll
             for (int j = 0; j < MAXD; j++) {
-                if (j < a.beta) {
+                if (EXACT || j < a.beta) {
                     const uint64_t *p = j == jt ? a.d + b * a.d_ct + o : a.ext + b * a.ext_ct + j * a.ext_dig + o;
                     const long long st = j == jt ? a.d_ct : a.ext_ct;
                     e0[j] = p[0];
@@ -493,7 +497,7 @@ __global__ void __launch_bounds__(256) k_ks_combine(const __grid_constant__ KsCo
             U128 s0 = {0, 0}, s1 = {0, 0}, u0 = {0, 0}, u1 = {0, 0};
 #pragma unroll
             for (int j = 0; j < MAXD; j++) {
-                if (j < a.beta) {
+                if (EXACT || j < a.beta) {
                     mac(s0, e0[j], k0[j]);
                     mac(s1, e0[j], k1[j]);
                     mac(u0, e1[j], k0[j]);
