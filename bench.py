@@ -230,6 +230,16 @@ def time_region(torch, fn, reps, barrier=None):
     return a.elapsed_time(b) / reps
 
 
+def ntt_traffic():
+    """DRAM bytes of one forward NTT of the bench batch from the committed ncu capture."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ntt_fwd_traffic.json")
+    try:
+        with open(path) as fh:
+            return int(json.load(fh)["dram_bytes"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def _event_time(torch, fn, dist=None):
     """Seconds between CUDA events around fn on the current stream (max over ranks)."""
     if dist is not None:
@@ -434,7 +444,8 @@ def gpu_arm(args):
             "api_calls_per_step": launches,
             "roofline": {"bound": "hbm", "kernel": "forward NTT (ntt_pass_kernel x2 per chunk)",
                          "achieved": round(ntt_gbs, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(ntt_gbs / peak, 4), "traffic": None,
+                         "frac": round(ntt_gbs / peak, 4), "traffic": ntt_traffic(),
+                         "traffic_source": "profiles/r01/ntt_fwd_traffic.json (ncu --set full, same workload)",
                          "algorithmic_bytes": parts["ntt_fwd"], "ms": round(ntt_ms, 4),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
             "roofline_int": int_roofline(p, N_CT * 2 * len(p.q_primes), ntt_ms,
