@@ -122,6 +122,7 @@ struct srk_ctx {
     LimbConsts lc_pmod;               // P mod prime_i (all primes)
     std::vector<LimbConsts> lc_qlinv; // [level]: q_level^-1 mod q_i
     int ntt_chunk = 128;              // limbs per L2-resident NTT chunk
+    int ntt_split = 1;                // FP64-only pass kernels for runs of < 2^41 primes (SRK_NTT_SPLIT)
     // ModDown forward NTT: 0 = conversion and combine in separate streaming
     // kernels (default: fastest on B200 -- the NTT passes are latency-bound and
     // extra loads in them cost more than the streams; profiles/r01), 1 = both
@@ -234,6 +235,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     c->n_primes = n_q + n_p;
     c->primes.assign(primes, primes + c->n_primes);
     if (const char *e = getenv("SRK_NTT_CHUNK")) c->ntt_chunk = std::max(1, atoi(e));
+    if (const char *e = getenv("SRK_NTT_SPLIT")) c->ntt_split = atoi(e);
     if (const char *e = getenv("SRK_MODDOWN_MODE")) c->moddown_mode = atoi(e);
     if (const char *e = getenv("SRK_RESCALE_FUSED")) c->rescale_fused = atoi(e);
     if (const char *e = getenv("SRK_KS_FUSED")) c->ks_fused = atoi(e);
@@ -443,9 +445,21 @@ static FuseArgs no_fuse() {
     return f;
 }
 
+template <int LOG_T, bool INV, bool COL, int IO, bool F64>
+static void launch_kernel(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
+                          const NttTables &tb, int log_n, const FuseArgs &ff) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(ntt_pass_kernel<LOG_T, INV, COL, IO, F64>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        attr_set = true;
+    }
+    ntt_pass_kernel<LOG_T, INV, COL, IO, F64><<<grid, threads, smem, s>>>(bb, tb, log_n, ff);
+}
+
 template <int LOG_T, bool INV, bool COL, int IO>
 static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const FuseArgs &f,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool f64) {
     using SH = NttShape<LOG_T>;
     const int subs = c->n >> LOG_T;  // sub-transforms per limb
     int cb = 256 / SH::TPS;
@@ -482,26 +496,27 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
         }
     }
     bb.n_limbs = nlc;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(ntt_pass_kernel<LOG_T, INV, COL, IO>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        attr_set = true;
-    }
     dim3 grid(subs / cb, nlc * b.n_polys);
-    ntt_pass_kernel<LOG_T, INV, COL, IO><<<grid, threads, smem, s>>>(bb, tables(c), c->log_n, ff);
+    bool done = false;
+    if constexpr (IO == 0 || IO == 3) {  // plain / automorphism loads, plain / scaled stores
+        if (f64) {
+            launch_kernel<LOG_T, INV, COL, IO, true>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
+            done = true;
+        }
+    }
+    if (!done) launch_kernel<LOG_T, INV, COL, IO, false>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
     LAUNCHED();
     return SRK_OK;
 }
 
 template <bool INV, bool COL, int IO>
 static int pass_t(const srk_ctx *c, int log_t, LimbBatch b, int l0, int nlc, const FuseArgs &f,
-                  cudaStream_t s) {
+                  cudaStream_t s, bool f64) {
     switch (log_t) {
-        case 5: return launch_pass<5, INV, COL, IO>(c, b, l0, nlc, f, s);
-        case 6: return launch_pass<6, INV, COL, IO>(c, b, l0, nlc, f, s);
-        case 7: return launch_pass<7, INV, COL, IO>(c, b, l0, nlc, f, s);
-        case 8: return launch_pass<8, INV, COL, IO>(c, b, l0, nlc, f, s);
+        case 5: return launch_pass<5, INV, COL, IO>(c, b, l0, nlc, f, s, f64);
+        case 6: return launch_pass<6, INV, COL, IO>(c, b, l0, nlc, f, s, f64);
+        case 7: return launch_pass<7, INV, COL, IO>(c, b, l0, nlc, f, s, f64);
+        case 8: return launch_pass<8, INV, COL, IO>(c, b, l0, nlc, f, s, f64);
         default: return fail(SRK_EINVAL, "unsupported NTT pass size 2^%d", log_t);
     }
 }
@@ -518,37 +533,50 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
     if (per > 65535 / b.n_polys) per = 65535 / b.n_polys;
     if (b.mode == 1 && per < b.n_limbs) per = b.n_limbs;  // slot map is absolute
     if ((long long)per * b.n_polys > 65535) return fail(SRK_EINVAL, "NTT batch too large");
-    for (int l0 = 0; l0 < b.n_limbs; l0 += per) {
-        const int nlc = std::min(per, b.n_limbs - l0);
+    // mode-0 batches: split chunks where the prime class changes, so runs of
+    // limbs under primes < 2^41 use the FP64-only pass kernels
+    auto f64_limb = [&](int i) {
+        const int pid = i + (i < b.split ? b.off_a : b.off_b);
+        return c->primes[pid] < SRK_F64_Q;
+    };
+    for (int l0 = 0, nlc = 0; l0 < b.n_limbs; l0 += nlc) {
+        nlc = std::min(per, b.n_limbs - l0);
+        bool f64 = false;
+        if (b.mode == 0 && c->ntt_split) {
+            f64 = f64_limb(l0);
+            int k = 1;
+            while (k < nlc && f64_limb(l0 + k) == f64) k++;
+            nlc = k;
+        }
         if (!inverse) {
             switch (ld) {
-                case LD_PLAIN: TRY((pass_t<false, true, LD_PLAIN>(c, log_r, b, l0, nlc, f, s))); break;
+                case LD_PLAIN: TRY((pass_t<false, true, LD_PLAIN>(c, log_r, b, l0, nlc, f, s, f64))); break;
                 case LD_BCONV:
                     if (f.n_src <= 4)
-                        TRY((pass_t<false, true, LD_BCONV>(c, log_r, b, l0, nlc, f, s)));
+                        TRY((pass_t<false, true, LD_BCONV>(c, log_r, b, l0, nlc, f, s, f64)));
                     else if (f.n_src <= 8)
-                        TRY((pass_t<false, true, LD_BCONV8>(c, log_r, b, l0, nlc, f, s)));
+                        TRY((pass_t<false, true, LD_BCONV8>(c, log_r, b, l0, nlc, f, s, f64)));
                     else
-                        TRY((pass_t<false, true, LD_BCONV16>(c, log_r, b, l0, nlc, f, s)));
+                        TRY((pass_t<false, true, LD_BCONV16>(c, log_r, b, l0, nlc, f, s, f64)));
                     break;
-                case LD_SPREAD: TRY((pass_t<false, true, LD_SPREAD>(c, log_r, b, l0, nlc, f, s))); break;
+                case LD_SPREAD: TRY((pass_t<false, true, LD_SPREAD>(c, log_r, b, l0, nlc, f, s, f64))); break;
                 default: return fail(SRK_EINVAL, "bad forward load mode");
             }
             switch (st) {
-                case ST_PLAIN: TRY((pass_t<false, false, ST_PLAIN>(c, log_c, b, l0, nlc, f, s))); break;
-                case ST_MODDOWN: TRY((pass_t<false, false, ST_MODDOWN>(c, log_c, b, l0, nlc, f, s))); break;
-                case ST_RESCALE: TRY((pass_t<false, false, ST_RESCALE>(c, log_c, b, l0, nlc, f, s))); break;
+                case ST_PLAIN: TRY((pass_t<false, false, ST_PLAIN>(c, log_c, b, l0, nlc, f, s, f64))); break;
+                case ST_MODDOWN: TRY((pass_t<false, false, ST_MODDOWN>(c, log_c, b, l0, nlc, f, s, f64))); break;
+                case ST_RESCALE: TRY((pass_t<false, false, ST_RESCALE>(c, log_c, b, l0, nlc, f, s, f64))); break;
                 default: return fail(SRK_EINVAL, "bad forward store mode");
             }
         } else {
             switch (ld) {
-                case LD_PLAIN: TRY((pass_t<true, false, LD_PLAIN>(c, log_c, b, l0, nlc, f, s))); break;
-                case LD_AUTO: TRY((pass_t<true, false, LD_AUTO>(c, log_c, b, l0, nlc, f, s))); break;
+                case LD_PLAIN: TRY((pass_t<true, false, LD_PLAIN>(c, log_c, b, l0, nlc, f, s, f64))); break;
+                case LD_AUTO: TRY((pass_t<true, false, LD_AUTO>(c, log_c, b, l0, nlc, f, s, f64))); break;
                 default: return fail(SRK_EINVAL, "bad inverse load mode");
             }
             switch (st) {
-                case ST_PLAIN: TRY((pass_t<true, true, ST_PLAIN>(c, log_r, b, l0, nlc, f, s))); break;
-                case ST_SCALE: TRY((pass_t<true, true, ST_SCALE>(c, log_r, b, l0, nlc, f, s))); break;
+                case ST_PLAIN: TRY((pass_t<true, true, ST_PLAIN>(c, log_r, b, l0, nlc, f, s, f64))); break;
+                case ST_SCALE: TRY((pass_t<true, true, ST_SCALE>(c, log_r, b, l0, nlc, f, s, f64))); break;
                 default: return fail(SRK_EINVAL, "bad inverse store mode");
             }
         }

@@ -472,7 +472,9 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
 // inverse: row pass) or the fused store of the LAST pass (forward: row pass,
 // inverse: column pass); the intermediate always lives at the batch's own
 // limb storage (b.ptr).
-template <int LOG_T, bool INV, bool COL, int IO>
+// F64: every limb of the launch is under a prime < 2^41, so only the FP64
+// arithmetic mode is compiled in (no integer-mode code, no register spills).
+template <int LOG_T, bool INV, bool COL, int IO, bool F64 = false>
 __global__ void __launch_bounds__(256, SRK_NTT_MINB)
     ntt_pass_kernel(LimbBatch b, NttTables tb, int log_n, const __grid_constant__ FuseArgs f) {
     using S = NttShape<LOG_T>;
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
 
     // arithmetic mode, uniform per CTA: 2 = FP64 (q < 2^41), 1 = reduction-free
     // integer (q < 2^46), 0 = Harvey lazy integer
-    const int mode = q < SRK_F64_Q ? 2 : (small ? 1 : 0);
+    const int mode = F64 ? 2 : (q < SRK_F64_Q ? 2 : (small ? 1 : 0));
     const F64Q fq = {(double)q, 1.0 / (double)q};
     // first-pass loads are canonical u64; FP64 limbs convert on load
     auto load_m = [&](int c) -> uint64_t {
