@@ -260,6 +260,9 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
         pc[i].ratio_lo = (uint64_t)ratio;
         pc[i].ninv = hinv((uint64_t)n, q);
         pc[i].ninv_shoup = shoup(pc[i].ninv, q);
+        const double qd = (double)q, qi = 1.0 / qd;
+        memcpy(&pc[i].qd_bits, &qd, 8);
+        memcpy(&pc[i].qinv_bits, &qi, 8);
     }
     if ((rc = dupload(c, &c->d_pc, pc))) { srk_ctx_destroy(c); return rc; }
     // twiddles

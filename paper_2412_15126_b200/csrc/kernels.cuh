@@ -470,6 +470,65 @@ __global__ void __launch_bounds__(256, SRK_KSC_MINB) k_ks_combine(const __grid_c
         const PrimeConst P = pc[t];
         const uint64_t w = a.mulc.w[t], ws = a.mulc.ws[t];
         const long long o = (long long)t * n + src;
+        if (P.q < SRK_F64_Q) {
+            // limbs under primes < 2^41: the whole inner product and combine on the
+            // FP64 pipe (exact FMA-split products, as in the NTT's FP64 mode); the
+            // integer path below stays for the 60-bit limbs
+            const double qd = __longlong_as_double((long long)P.qd_bits);
+            const double qi = __longlong_as_double((long long)P.qinv_bits);
+            const double wf = f64_of_u64(w);
+            double kf0[MAXD], kf1[MAXD];
+#pragma unroll
+            for (int j = 0; j < MAXD; j++) {
+                kf0[j] = (EXACT || j < a.beta) ? f64_of_u64(k0[j]) : 0.0;
+                kf1[j] = (EXACT || j < a.beta) ? f64_of_u64(k1[j]) : 0.0;
+            }
+            for (int b = 0; b < a.batch; b += 2) {
+                const bool two = b + 1 < a.batch;
+                double e0[MAXD], e1[MAXD];
+#pragma unroll
+                for (int j = 0; j < MAXD; j++) {
+                    if (EXACT || j < a.beta) {
+                        const uint64_t *p = j == jt ? a.d + b * a.d_ct + o : a.ext + b * a.ext_ct + j * a.ext_dig + o;
+                        const long long st = j == jt ? a.d_ct : a.ext_ct;
+                        e0[j] = f64_of_u64(p[0]);
+                        e1[j] = two ? f64_of_u64(p[st]) : 0.0;
+                    }
+                }
+                const uint64_t *cv = a.conv + b * a.conv_ct + o;
+                const double cv00 = f64_of_u64(cv[0]), cv01 = f64_of_u64(cv[a.conv_ps]);
+                const double cv10 = two ? f64_of_u64(cv[a.conv_ct]) : 0.0;
+                const double cv11 = two ? f64_of_u64(cv[a.conv_ct + a.conv_ps]) : 0.0;
+                double ad00 = 0, ad01 = 0, ad10 = 0, ad11 = 0;
+                if (a.add0) {
+                    ad00 = f64_of_u64(a.add0[b * a.add_ct + o]);
+                    ad10 = two ? f64_of_u64(a.add0[(b + 1) * a.add_ct + o]) : 0.0;
+                }
+                if (a.add1) {
+                    ad01 = f64_of_u64(a.add1[b * a.add_ct + o]);
+                    ad11 = two ? f64_of_u64(a.add1[(b + 1) * a.add_ct + o]) : 0.0;
+                }
+                // |each product| < q, |sum| < beta q, minus conv: < (beta + 1) q < 2^47
+                double s0 = -cv00, s1 = -cv01, u0 = -cv10, u1 = -cv11;
+#pragma unroll
+                for (int j = 0; j < MAXD; j++) {
+                    if (EXACT || j < a.beta) {
+                        s0 += modmul_f64(e0[j], kf0[j], qd, qi);
+                        s1 += modmul_f64(e0[j], kf1[j], qd, qi);
+                        u0 += modmul_f64(e1[j], kf0[j], qd, qi);
+                        u1 += modmul_f64(e1[j], kf1[j], qd, qi);
+                    }
+                }
+                uint64_t *op = a.out + b * a.out_ct + (long long)t * n + m;
+                op[0] = canon_u64_of_f64(modmul_f64(s0, wf, qd, qi) + ad00, qd, qi);
+                op[a.out_ps] = canon_u64_of_f64(modmul_f64(s1, wf, qd, qi) + ad01, qd, qi);
+                if (two) {
+                    op[a.out_ct] = canon_u64_of_f64(modmul_f64(u0, wf, qd, qi) + ad10, qd, qi);
+                    op[a.out_ct + a.out_ps] = canon_u64_of_f64(modmul_f64(u1, wf, qd, qi) + ad11, qd, qi);
+                }
+            }
+            continue;
+        }
         for (int b = 0; b < a.batch; b += 2) {
             const bool two = b + 1 < a.batch;
             uint64_t e0[MAXD], e1[MAXD];

@@ -24,7 +24,7 @@ struct PrimeConst {
     uint64_t two_q;   // 2q (lazy ranges)
     uint64_t ratio_hi, ratio_lo;  // floor(2^128 / q)
     uint64_t ninv, ninv_shoup;    // N^-1 mod q and its Shoup constant
-    uint64_t pad0, pad1;
+    uint64_t qd_bits, qinv_bits;  // (double) q and 1.0 / (double) q as bit patterns
 };
 
 SRK_HD uint64_t mulhi64(uint64_t a, uint64_t b) {
