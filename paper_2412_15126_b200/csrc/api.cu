@@ -959,6 +959,23 @@ static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int n
     return SRK_OK;
 }
 
+template <bool F64>
+static void launch_ks_combine(const KsCombineArgs &kc, int beta, int blocks, cudaStream_t s, const srk_ctx *c) {
+    switch (beta) {
+        case 1: k_ks_combine<1, true, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+        case 2: k_ks_combine<2, true, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+        case 3: k_ks_combine<3, true, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+        case 4: k_ks_combine<4, true, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
+        default:
+            if (beta <= 8)
+                k_ks_combine<8, false, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
+            else if (beta <= 16)
+                k_ks_combine<16, false, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
+            else
+                k_ks_combine<64, false, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
+    }
+}
+
 struct KsOut {
     uint64_t *out;
     long long out_ct, out_ps;
@@ -1215,21 +1232,20 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
                 kc.beta = beta;
                 kc.batch = B;
                 kc.mulc = c->lc_pinv;
-                const int blocks = grid_for((long long)nl * n);
-                switch (beta) {
-                    case 1: k_ks_combine<1, true><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-                    case 2: k_ks_combine<2, true><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-                    case 3: k_ks_combine<3, true><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-                    case 4: k_ks_combine<4, true><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-                    default:
-                        if (beta <= 8)
-                            k_ks_combine<8, false><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
-                        else if (beta <= 16)
-                            k_ks_combine<16, false><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
-                        else
-                            k_ks_combine<64, false><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
+                // runs of limbs of one prime class: FP64 instantiation for q < 2^41
+                for (int t0 = 0, t1 = 0; t0 < nl; t0 = t1) {
+                    const bool f64 = c->primes[t0] < SRK_F64_Q;
+                    t1 = t0 + 1;
+                    while (t1 < nl && (c->primes[t1] < SRK_F64_Q) == f64) t1++;
+                    kc.t0 = t0;
+                    kc.t1 = t1;
+                    const int blocks = grid_for((long long)(t1 - t0) * n);
+                    if (f64)
+                        launch_ks_combine<true>(kc, beta, blocks, s, c);
+                    else
+                        launch_ks_combine<false>(kc, beta, blocks, s, c);
+                    LAUNCHED();
                 }
-                LAUNCHED();
             }
         }
     }

@@ -440,6 +440,7 @@ struct KsCombineArgs {
     long long out_ct, out_ps;
     uint64_t galois;
     int n_primes, nl, alpha, beta, batch;
+    int t0, t1;  // limb range of this launch
     LimbConsts mulc;
 };
 
@@ -447,14 +448,20 @@ struct KsCombineArgs {
 #define SRK_KSC_MINB 3
 #endif
 // EXACT: beta == MAXD (no per-digit predicates)
-template <int MAXD, bool EXACT>
-__global__ void __launch_bounds__(256, SRK_KSC_MINB) k_ks_combine(const __grid_constant__ KsCombineArgs a,
-                                                    const PrimeConst *__restrict__ pc, int log_n) {
+#ifndef SRK_KSC_F64_MINB
+#define SRK_KSC_F64_MINB 4
+#endif
+// F64: every limb in [t0, t1) is under a prime < 2^41 (launched separately
+// from the integer limbs so the FP64 instantiation carries no integer code
+// and runs at higher occupancy -- the kernel is HBM-latency bound)
+template <int MAXD, bool EXACT, bool F64>
+__global__ void __launch_bounds__(256, F64 ? SRK_KSC_F64_MINB : SRK_KSC_MINB)
+    k_ks_combine(const __grid_constant__ KsCombineArgs a, const PrimeConst *__restrict__ pc, int log_n) {
     const long long n = 1ll << log_n;
-    const long long work = (long long)a.nl * n;
+    const long long work = (long long)(a.t1 - a.t0) * n;
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < work;
          x += (long long)gridDim.x * blockDim.x) {
-        const int t = (int)(x >> log_n);
+        const int t = a.t0 + (int)(x >> log_n);
         const long long m = x & (n - 1);
         const long long src = a.galois == 1 ? m : (long long)auto_index((uint32_t)m, a.galois, log_n);
         const int jt = t / a.alpha;
@@ -470,7 +477,7 @@ __global__ void __launch_bounds__(256, SRK_KSC_MINB) k_ks_combine(const __grid_c
         const PrimeConst P = pc[t];
         const uint64_t w = a.mulc.w[t], ws = a.mulc.ws[t];
         const long long o = (long long)t * n + src;
-        if (P.q < SRK_F64_Q) {
+        if (F64) {
             // limbs under primes < 2^41: the whole inner product and combine on the
             // FP64 pipe (exact FMA-split products, as in the NTT's FP64 mode); the
             // integer path below stays for the 60-bit limbs
