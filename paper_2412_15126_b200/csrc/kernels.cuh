@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(256, F64 ? SRK_KSC_F64_MINB : SRK_KSC_MINB)
         const PrimeConst P = pc[t];
         const uint64_t w = a.mulc.w[t], ws = a.mulc.ws[t];
         const long long o = (long long)t * n + src;
-        if (F64) {
+        if constexpr (F64) {
             // limbs under primes < 2^41: the whole inner product and combine on the
             // FP64 pipe (exact FMA-split products, as in the NTT's FP64 mode); the
             // integer path below stays for the 60-bit limbs
@@ -534,8 +534,7 @@ __global__ void __launch_bounds__(256, F64 ? SRK_KSC_F64_MINB : SRK_KSC_MINB)
                     op[a.out_ct + a.out_ps] = canon_u64_of_f64(modmul_f64(u1, wf, qd, qi) + ad11, qd, qi);
                 }
             }
-            continue;
-        }
+        } else {
         for (int b = 0; b < a.batch; b += 2) {
             const bool two = b + 1 < a.batch;
             uint64_t e0[MAXD], e1[MAXD];
@@ -578,6 +577,7 @@ __global__ void __launch_bounds__(256, F64 ? SRK_KSC_F64_MINB : SRK_KSC_MINB)
                 op[a.out_ct + a.out_ps] =
                     add_mod(mul_shoup(sub_mod(reduce_u128(u1, P), cv11, P.q), w, ws, P.q), ad11, P.q);
             }
+        }
         }
     }
 }
