@@ -540,7 +540,8 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
     // arithmetic mode, uniform per CTA: 2 = FP64 (q < 2^41), 1 = reduction-free
     // integer (q < 2^46), 0 = Harvey lazy integer
     const int mode = F64 ? 2 : (q < SRK_F64_Q ? 2 : (small ? 1 : 0));
-    const F64Q fq = {(double)q, 1.0 / (double)q};
+    // (double) q and 1 / (double) q precomputed per prime (no per-CTA division)
+    const F64Q fq = {__longlong_as_double((long long)pc.qd_bits), __longlong_as_double((long long)pc.qinv_bits)};
     // first-pass loads are canonical u64; FP64 limbs convert on load
     auto load_m = [&](int c) -> uint64_t {
         const uint64_t v = load(c);
