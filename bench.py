@@ -273,7 +273,7 @@ def run_sharded_sort(torch, dist):
     srt = block_merge(eng, res)
     return {"latency_s": dt, "order_ok": bool(np.array_equal(np.argsort(srt), np.arange(1024))),
             "max_abs_err": float(np.abs(srt - np.sort(v1024)).max()), "params": "long",
-            "gpus": comm.world, "sharding": "block pairs + placements round-robin, NCCL all-reduce"}
+            "gpus": comm.world, "sharding": f"block pairs + placements round-robin, {dist.get_backend()} all-reduce"}
 
 
 def run_pipelines(torch, quick=False):
@@ -359,10 +359,16 @@ def gpu_arm(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank_id = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank; SRK_DIST_BACKEND=gloo (host-side collectives) lets the
+    # N>1 path be exercised with several ranks sharing one GPU in a functional test
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SRK_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     barrier = (lambda: dist.barrier()) if world > 1 else None
 
     step = PrimitiveStep(torch, local)
