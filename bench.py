@@ -240,6 +240,20 @@ def ntt_traffic():
         return None
 
 
+def kernel_roofline():
+    """Per-kernel DRAM GB/s of one primitive step from the committed ncu capture."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
+                        "kernel_roofline_step64.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    return {"source": "profiles/r01/kernel_roofline_step64.json (" + d.get("note", "") + ")",
+            "kernels": [{k: e[k] for k in ("kernel", "time_share", "dram_gb_per_s", "frac_of_hbm")}
+                        for e in d["kernels"] if e["time_share"] >= 0.01]}
+
+
 def _event_time(torch, fn, dist=None):
     """Seconds between CUDA events around fn on the current stream (max over ranks)."""
     if dist is not None:
@@ -454,6 +468,7 @@ def gpu_arm(args):
                          "traffic_source": "profiles/r01/ntt_fwd_traffic.json (ncu --set full, same workload)",
                          "algorithmic_bytes": parts["ntt_fwd"], "ms": round(ntt_ms, 4),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+            "kernel_roofline": kernel_roofline(),
             "roofline_int": int_roofline(p, N_CT * 2 * len(p.q_primes), ntt_ms,
                                          clk.summary().get("sm_mhz")),
             "roofline_keyswitch": {"bound": "hbm", "unit_of_work": "64 x HMult+relinearise (no rescale)", "achieved": round(ks_gbs, 1), "peak": peak,
