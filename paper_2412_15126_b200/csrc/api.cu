@@ -919,15 +919,21 @@ static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int n
     const long long n = c->n;
     dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + 7) / 8);
     const uint64_t *z = g.src;
-    if (g.n_src <= 4)
-        k_moddown_conv<4><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2, g.mat_ld,
-                                               g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
-    else if (g.n_src <= 8)
-        k_moddown_conv<8><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2, g.mat_ld,
-                                               g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
-    else
-        k_moddown_conv<16><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2, g.mat_ld,
-                                                g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
+#define SRK_CONV_LAUNCH(MK, EX)                                                                         \
+    k_moddown_conv<MK, EX><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2, g.mat_ld, \
+                                                g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n)
+    switch (g.n_src) {
+        case 1: SRK_CONV_LAUNCH(1, true); break;
+        case 2: SRK_CONV_LAUNCH(2, true); break;
+        case 3: SRK_CONV_LAUNCH(3, true); break;
+        case 4: SRK_CONV_LAUNCH(4, true); break;
+        default:
+            if (g.n_src <= 8)
+                SRK_CONV_LAUNCH(8, false);
+            else
+                SRK_CONV_LAUNCH(16, false);
+    }
+#undef SRK_CONV_LAUNCH
     LAUNCHED();
     FuseArgs h = g;
     h.src = nullptr;  // first pass reads the conversion in place

@@ -341,7 +341,9 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
 // Shoup product (mat2 = {m, floor(m 2^64 / q_t)}) in [0, 2q), folded into a
 // [0, 2q) running sum -- about half the instructions of a 128-bit MAC chain
 // plus one two-word Barrett reduction.
-template <int MAXK>
+// EXACT: n_src == MAXK (no per-source guards: the constant loads and Shoup
+// products of a target are straight-line code)
+template <int MAXK, bool EXACT>
 __global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict__ z, long long z_ct,
                                                       long long z_ps, int n_src,
                                                       const uint8_t *__restrict__ vround,
@@ -360,14 +362,14 @@ __global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict
          x += (long long)gridDim.x * blockDim.x) {
         uint64_t zz[MAXK];
 #pragma unroll
-        for (int k = 0; k < MAXK; k++) zz[k] = k < n_src ? zp[k * n + x] : 0;
+        for (int k = 0; k < MAXK; k++) zz[k] = (EXACT || k < n_src) ? zp[k * n + x] : 0;
         const int v = vround[(long long)p * n + x];
         for (int t = t0; t < t1; t++) {
             const uint64_t q = pc[t].q, two_q = 2 * q;
             uint64_t acc = 0;
 #pragma unroll
             for (int k = 0; k < MAXK; k++)
-                if (k < n_src) {
+                if (EXACT || k < n_src) {
                     const ulonglong2 mw = __ldg(mat2 + k * n_dst + t);
                     acc += mul_shoup_lazy(zz[k], mw.x, mw.y, q);
                     acc = acc >= two_q ? acc - two_q : acc;
