@@ -130,6 +130,9 @@ struct srk_ctx {
     int moddown_mode = 0;
     int rescale_fused = 0;            // same trade-off for the rescale (SRK_RESCALE_FUSED=1)
     int ks_fused = 1;                 // Q-limb inner product fused into the combine (SRK_KS_FUSED=0: off)
+    int ks_streams = 2;               // hoisted outputs alternate over two streams (SRK_KS_STREAMS)
+    cudaStream_t side = nullptr;      // the second lane
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 template <typename T>
@@ -210,6 +213,9 @@ static void fill_consts(LimbConsts &lc, const std::vector<uint64_t> &w,
 extern "C" int srk_ctx_destroy(srk_ctx *c) {
     if (!c) return SRK_OK;
     cudaSetDevice(c->device);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (void *p : c->allocs) cudaFree(p);
     delete c;
     return SRK_OK;
@@ -239,6 +245,13 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     if (const char *e = getenv("SRK_MODDOWN_MODE")) c->moddown_mode = atoi(e);
     if (const char *e = getenv("SRK_RESCALE_FUSED")) c->rescale_fused = atoi(e);
     if (const char *e = getenv("SRK_KS_FUSED")) c->ks_fused = atoi(e);
+    if (const char *e = getenv("SRK_KS_STREAMS")) c->ks_streams = atoi(e);
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        srk_ctx_destroy(c);
+        return fail(SRK_ECUDA, "stream / event creation failed");
+    }
     if (c->alpha > 16 || n_p > 16) {
         srk_ctx_destroy(c);
         return fail(SRK_EINVAL, "digit size and special prime count must be <= 16");
@@ -402,7 +415,8 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
 // words of scratch (x N) each op needs for a chunk of B ciphertexts at level l
 static size_t ks_limbs(const srk_ctx *c, int level, int B) {
     const size_t nl = level + 1, ne = nl + c->n_p, beta = (nl + c->alpha - 1) / c->alpha;
-    return (size_t)B * (nl + beta * ne + 2 * ne + 2 * nl + 2 * (c->n_p + 1) + 1);  // + z, rounding bytes
+    // + two stream lanes of {acc, conversion, special limbs z, rounding bytes}
+    return (size_t)B * (nl + beta * ne + 2 * (2 * ne + 2 * nl + 2 * (c->n_p + 1) + 1));
 }
 static size_t rescale_limbs(int level, int B) { return (size_t)B * (2 + 2 * (size_t)level); }
 static size_t relin_limbs(const srk_ctx *c, int level, int B) {
@@ -1005,10 +1019,24 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
     if (beta > SRK_MAX_DIGITS) return fail(SRK_EINVAL, "too many digits");
     uint64_t *dc = ws;                                 // [B][nl]
     uint64_t *ext = dc + (long long)B * nl * n;        // [B][beta][ne]
-    uint64_t *acc = ext + (long long)B * beta * ne * n;  // [B][2][ne]
-    uint64_t *conv = acc + (long long)B * 2 * ne * n;    // [B][2][nl]
-    uint64_t *zb = conv + (long long)B * 2 * nl * n;    // [B][2][K(+1)] special limbs, coef
-    uint8_t *vround = (uint8_t *)(zb + (long long)B * 2 * (K + 1) * n);  // [B][2][N] bytes
+    // per-output scratch, one set per stream lane (outputs alternate between the
+    // caller's stream and the context's side stream so their small latency-bound
+    // kernels overlap the large ones)
+    uint64_t *lane_acc[2], *lane_conv[2], *lane_zb[2];
+    uint8_t *lane_vround[2];
+    {
+        uint64_t *q = ext + (long long)B * beta * ne * n;
+        for (int l = 0; l < 2; l++) {
+            lane_acc[l] = q;                                          // [B][2][ne]
+            lane_conv[l] = q + (long long)B * 2 * ne * n;             // [B][2][nl]
+            lane_zb[l] = lane_conv[l] + (long long)B * 2 * nl * n;    // [B][2][K(+1)] special limbs, coef
+            lane_vround[l] = (uint8_t *)(lane_zb[l] + (long long)B * 2 * (K + 1) * n);  // [B][2][N] bytes
+            q = (uint64_t *)lane_vround[l] + (long long)B * n;
+        }
+    }
+    const bool dual = n_out >= 2 && !rescale_d && c->ks_streams >= 2 && c->side;
+    cudaStream_t lane_s[2] = {s, dual ? c->side : s};
+
     if (rescale_d && level < 1) return fail(SRK_EINVAL, "cannot rescale a level-0 ciphertext");
     // 1. INTT with the ModUp scale folded in
     {
@@ -1077,8 +1105,16 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
     const BconvPlan &pd = c->moddown[level];
     // the ciphertext-modulus limbs' inner product is fused into the combine
     const bool ks_fused = !rescale_d && c->moddown_mode == 0 && c->ks_fused;
+    if (dual) {
+        CU(cudaEventRecord(c->ev_fork, s));
+        CU(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    }
     for (int o = 0; o < n_out; o++) {
         const KsOut &ko = outs[o];
+        const int lane = dual ? (o & 1) : 0;
+        cudaStream_t so = lane_s[lane];
+        uint64_t *acc = lane_acc[lane], *conv = lane_conv[lane], *zb = lane_zb[lane];
+        uint8_t *vround = lane_vround[lane];
         // 4. inner product (+ automorphism)
         KsInnerArgs ka;
         ka.d = d;
@@ -1102,17 +1138,17 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         {
             const int blocks = grid_for((long long)(ne - ka.t0) * n);
             switch (beta) {
-                case 1: k_ks_inner<1><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n); break;
-                case 2: k_ks_inner<2><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n); break;
-                case 3: k_ks_inner<3><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n); break;
-                case 4: k_ks_inner<4><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n); break;
+                case 1: k_ks_inner<1><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n); break;
+                case 2: k_ks_inner<2><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n); break;
+                case 3: k_ks_inner<3><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n); break;
+                case 4: k_ks_inner<4><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n); break;
                 default:
                     if (beta <= 8)
-                        k_ks_inner<8><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n);
+                        k_ks_inner<8><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n);
                     else if (beta <= 16)
-                        k_ks_inner<16><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n);
+                        k_ks_inner<16><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n);
                     else
-                        k_ks_inner<64><<<blocks, 256, 0, s>>>(ka, c->d_pc, c->log_n);
+                        k_ks_inner<64><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n);
             }
             LAUNCHED();
         }
@@ -1121,7 +1157,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             //     N^-1 (S/s_k)^-1 folded in; rounding term over K+1 limbs
             const int ns = K + 1;
             const uint64_t pm = c->lc_pmod.w[level], pms = c->lc_pmod.ws[level];
-            k_prep_special<<<grid_for(2ll * B * ns * n), 256, 0, s>>>(
+            k_prep_special<<<grid_for(2ll * B * ns * n), 256, 0, so>>>(
                 acc, 2ll * ne * n, (long long)ne * n, ko.add0, ko.add_ct, (long long)nl * n, zb, pm, pms,
                 c->d_pc, c->log_n, level, K, B);
             LAUNCHED();
@@ -1131,8 +1167,8 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             b.split = K;
             b.off_a = c->n_q;
             b.off_b = level - K;
-            TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, s));
-            k_moddown_v<<<grid_for(2ll * B * n), 256, 0, s>>>(zb, 2ll * ns * n, (long long)ns * n, K,
+            TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, so));
+            k_moddown_v<<<grid_for(2ll * B * n), 256, 0, so>>>(zb, 2ll * ns * n, (long long)ns * n, K,
                                                               c->n_q, ns, level, vround, c->d_pc, c->log_n, B);
             LAUNCHED();
             // 6'. NTT(conversion S -> q_0..q_{l-1}) with out = (acc - conv) (P q_l)^-1 + d q_l^-1
@@ -1161,7 +1197,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             g.addc = c->lc_qlinv[level];
             g.mulc = c->lc_rs_mulc[level];
             TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * level * n, (long long)level * n, level, 0), g, B,
-                            level, s));
+                            level, so));
             continue;
         }
         // 5. INTT of the special limbs, (P/p_k)^-1 folded in -> zb
@@ -1174,11 +1210,11 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             LimbBatch b = cbatch(zb, B, 2, 2ll * K * n, (long long)K * n, K, 0);
             b.split = 0;
             b.off_b = c->n_q;
-            TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, s));
+            TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, so));
         }
         // 6. ModDown: rounding term once per coefficient, then NTT(conversion)
         //    with the combine in its store
-        k_moddown_v<<<grid_for(2ll * B * n), 256, 0, s>>>(zb, 2ll * K * n, (long long)K * n, K,
+        k_moddown_v<<<grid_for(2ll * B * n), 256, 0, so>>>(zb, 2ll * K * n, (long long)K * n, K,
                                                           c->n_q, K, 0, vround, c->d_pc, c->log_n, B);
         LAUNCHED();
         {
@@ -1210,7 +1246,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             f.out_galois = ko.galois;
             f.out_galois_inv = galois_inverse(c, ko.galois);
             f.mulc = c->lc_pinv;
-            TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), f, B, nl, s,
+            TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), f, B, nl, so,
                             !ks_fused));
             if (ks_fused) {
                 // 7. out = sigma_g(add + (sum_j e_j key_j - conv) P^-1) over q_0..q_l
@@ -1247,13 +1283,17 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
                     kc.t1 = t1;
                     const int blocks = grid_for((long long)(t1 - t0) * n);
                     if (f64)
-                        launch_ks_combine<true>(kc, beta, blocks, s, c);
+                        launch_ks_combine<true>(kc, beta, blocks, so, c);
                     else
-                        launch_ks_combine<false>(kc, beta, blocks, s, c);
+                        launch_ks_combine<false>(kc, beta, blocks, so, c);
                     LAUNCHED();
                 }
             }
         }
+    }
+    if (dual) {
+        CU(cudaEventRecord(c->ev_join, c->side));
+        CU(cudaStreamWaitEvent(s, c->ev_join, 0));
     }
     return SRK_OK;
 }
