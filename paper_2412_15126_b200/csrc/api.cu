@@ -109,6 +109,7 @@ struct srk_ctx {
     std::vector<uint64_t> primes;
     PrimeConst *d_pc = nullptr;
     ulonglong2 *d_tw = nullptr, *d_itw = nullptr;  // {w, Shoup(w)} interleaved
+    double *d_twd = nullptr, *d_itwd = nullptr;     // w as double (FP64-mode limbs)
     std::vector<void *> allocs;
     // modup[level][digit], moddown[level]
     std::vector<std::vector<BconvPlan>> modup;
@@ -133,6 +134,12 @@ struct srk_ctx {
     int ks_streams = 2;               // hoisted outputs alternate over two streams (SRK_KS_STREAMS)
     cudaStream_t side = nullptr;      // the second lane
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // NTT chunk lanes: independent limb chunks of one NTT alternate between the
+    // caller's stream and nside[lane], so one chunk's pass tail overlaps the
+    // next chunk's passes (lane = 1 when called from the key-switch side lane)
+    int ntt_streams = 2;
+    cudaStream_t nside[2] = {nullptr, nullptr};
+    cudaEvent_t ev_nfork[2] = {nullptr, nullptr}, ev_njoin[2] = {nullptr, nullptr};
 };
 
 template <typename T>
@@ -216,6 +223,11 @@ extern "C" int srk_ctx_destroy(srk_ctx *c) {
     if (c->side) cudaStreamDestroy(c->side);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    for (int i = 0; i < 2; i++) {
+        if (c->nside[i]) cudaStreamDestroy(c->nside[i]);
+        if (c->ev_nfork[i]) cudaEventDestroy(c->ev_nfork[i]);
+        if (c->ev_njoin[i]) cudaEventDestroy(c->ev_njoin[i]);
+    }
     for (void *p : c->allocs) cudaFree(p);
     delete c;
     return SRK_OK;
@@ -246,11 +258,20 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     if (const char *e = getenv("SRK_RESCALE_FUSED")) c->rescale_fused = atoi(e);
     if (const char *e = getenv("SRK_KS_FUSED")) c->ks_fused = atoi(e);
     if (const char *e = getenv("SRK_KS_STREAMS")) c->ks_streams = atoi(e);
+    if (const char *e = getenv("SRK_NTT_STREAMS")) c->ntt_streams = atoi(e);
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
         srk_ctx_destroy(c);
         return fail(SRK_ECUDA, "stream / event creation failed");
+    }
+    for (int i = 0; i < 2; i++) {
+        if (cudaStreamCreateWithFlags(&c->nside[i], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_nfork[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_njoin[i], cudaEventDisableTiming) != cudaSuccess) {
+            srk_ctx_destroy(c);
+            return fail(SRK_ECUDA, "stream / event creation failed");
+        }
     }
     if (c->alpha > 16 || n_p > 16) {
         srk_ctx_destroy(c);
@@ -280,6 +301,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     if ((rc = dupload(c, &c->d_pc, pc))) { srk_ctx_destroy(c); return rc; }
     // twiddles
     std::vector<ulonglong2> tw((size_t)np * n), itw((size_t)np * n);
+    std::vector<double> twd((size_t)np * n), itwd((size_t)np * n);
     for (int i = 0; i < np; i++) {
         const uint64_t q = primes[i], psi = roots[i] % q, ipsi = hinv(psi, q);
         if (hpow(psi, (uint64_t)n, q) != q - 1) {
@@ -291,11 +313,14 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
             const size_t r = (size_t)i * n + hbrv((uint32_t)k, log_n);
             tw[r] = make_ulonglong2(p, shoup(p, q));
             itw[r] = make_ulonglong2(ip, shoup(ip, q));
+            twd[r] = (double)p;   // exact for the q < 2^41 limbs that use it
+            itwd[r] = (double)ip;
             p = hmul(p, psi, q);
             ip = hmul(ip, ipsi, q);
         }
     }
-    if ((rc = dupload(c, &c->d_tw, tw)) || (rc = dupload(c, &c->d_itw, itw))) {
+    if ((rc = dupload(c, &c->d_tw, tw)) || (rc = dupload(c, &c->d_itw, itw)) ||
+        (rc = dupload(c, &c->d_twd, twd)) || (rc = dupload(c, &c->d_itwd, itwd))) {
         srk_ctx_destroy(c);
         return rc;
     }
@@ -448,6 +473,8 @@ static NttTables tables(const srk_ctx *c) {
     t.pc = c->d_pc;
     t.tw = c->d_tw;
     t.itw = c->d_itw;
+    t.twd = c->d_twd;
+    t.itwd = c->d_itwd;
     return t;
 }
 
@@ -462,16 +489,28 @@ static FuseArgs no_fuse() {
     return f;
 }
 
-template <int LOG_T, bool INV, bool COL, int IO, bool F64>
-static void launch_kernel(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
-                          const NttTables &tb, int log_n, const FuseArgs &ff) {
+template <int LOG_T, bool INV, bool COL, int IO, bool F64, int LOGN>
+static void launch_kernel_n(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
+                            const NttTables &tb, int log_n, const FuseArgs &ff) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(ntt_pass_kernel<LOG_T, INV, COL, IO, F64>,
+        cudaFuncSetAttribute(ntt_pass_kernel<LOG_T, INV, COL, IO, F64, LOGN>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         attr_set = true;
     }
-    ntt_pass_kernel<LOG_T, INV, COL, IO, F64><<<grid, threads, smem, s>>>(bb, tb, log_n, ff);
+    ntt_pass_kernel<LOG_T, INV, COL, IO, F64, LOGN><<<grid, threads, smem, s>>>(bb, tb, log_n, ff);
+}
+// ring 2^16 (every BASELINE config past config 1): compile-time shape
+template <int LOG_T, bool INV, bool COL, int IO, bool F64>
+static void launch_kernel(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
+                          const NttTables &tb, int log_n, const FuseArgs &ff) {
+    if constexpr (LOG_T == 8) {
+        if (log_n == 16) {
+            launch_kernel_n<LOG_T, INV, COL, IO, F64, 16>(grid, threads, smem, s, bb, tb, log_n, ff);
+            return;
+        }
+    }
+    launch_kernel_n<LOG_T, INV, COL, IO, F64, 0>(grid, threads, smem, s, bb, tb, log_n, ff);
 }
 
 template <int LOG_T, bool INV, bool COL, int IO>
@@ -513,7 +552,7 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
         }
     }
     bb.n_limbs = nlc;
-    dim3 grid(subs / cb, nlc * b.n_polys);
+    dim3 grid(subs / cb, b.n_polys, nlc);
     bool done = false;
     if constexpr (IO == 0 || IO == 3) {  // plain / automorphism loads, plain / scaled stores
         if (f64) {
@@ -556,6 +595,11 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
         const int pid = i + (i < b.split ? b.off_a : b.off_b);
         return c->primes[pid] < SRK_F64_Q;
     };
+    struct Chunk {
+        int l0, nlc;
+        bool f64;
+    };
+    std::vector<Chunk> chunks;
     for (int l0 = 0, nlc = 0; l0 < b.n_limbs; l0 += nlc) {
         nlc = std::min(per, b.n_limbs - l0);
         bool f64 = false;
@@ -565,38 +609,55 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
             while (k < nlc && f64_limb(l0 + k) == f64) k++;
             nlc = k;
         }
+        chunks.push_back({l0, nlc, f64});
+    }
+    // independent chunks alternate between s and this lane's NTT side stream
+    const int lane = s == c->side ? 1 : 0;
+    const bool two = c->ntt_streams >= 2 && chunks.size() >= 2 && c->nside[lane];
+    if (two) {
+        CU(cudaEventRecord(c->ev_nfork[lane], s));
+        CU(cudaStreamWaitEvent(c->nside[lane], c->ev_nfork[lane], 0));
+    }
+    for (size_t ci = 0; ci < chunks.size(); ci++) {
+        const int l0 = chunks[ci].l0, nlc = chunks[ci].nlc;
+        const bool f64 = chunks[ci].f64;
+        cudaStream_t cs = (two && (ci & 1)) ? c->nside[lane] : s;
         if (!inverse) {
             switch (ld) {
-                case LD_PLAIN: TRY((pass_t<false, true, LD_PLAIN>(c, log_r, b, l0, nlc, f, s, f64))); break;
+                case LD_PLAIN: TRY((pass_t<false, true, LD_PLAIN>(c, log_r, b, l0, nlc, f, cs, f64))); break;
                 case LD_BCONV:
                     if (f.n_src <= 4)
-                        TRY((pass_t<false, true, LD_BCONV>(c, log_r, b, l0, nlc, f, s, f64)));
+                        TRY((pass_t<false, true, LD_BCONV>(c, log_r, b, l0, nlc, f, cs, f64)));
                     else if (f.n_src <= 8)
-                        TRY((pass_t<false, true, LD_BCONV8>(c, log_r, b, l0, nlc, f, s, f64)));
+                        TRY((pass_t<false, true, LD_BCONV8>(c, log_r, b, l0, nlc, f, cs, f64)));
                     else
-                        TRY((pass_t<false, true, LD_BCONV16>(c, log_r, b, l0, nlc, f, s, f64)));
+                        TRY((pass_t<false, true, LD_BCONV16>(c, log_r, b, l0, nlc, f, cs, f64)));
                     break;
-                case LD_SPREAD: TRY((pass_t<false, true, LD_SPREAD>(c, log_r, b, l0, nlc, f, s, f64))); break;
+                case LD_SPREAD: TRY((pass_t<false, true, LD_SPREAD>(c, log_r, b, l0, nlc, f, cs, f64))); break;
                 default: return fail(SRK_EINVAL, "bad forward load mode");
             }
             switch (st) {
-                case ST_PLAIN: TRY((pass_t<false, false, ST_PLAIN>(c, log_c, b, l0, nlc, f, s, f64))); break;
-                case ST_MODDOWN: TRY((pass_t<false, false, ST_MODDOWN>(c, log_c, b, l0, nlc, f, s, f64))); break;
-                case ST_RESCALE: TRY((pass_t<false, false, ST_RESCALE>(c, log_c, b, l0, nlc, f, s, f64))); break;
+                case ST_PLAIN: TRY((pass_t<false, false, ST_PLAIN>(c, log_c, b, l0, nlc, f, cs, f64))); break;
+                case ST_MODDOWN: TRY((pass_t<false, false, ST_MODDOWN>(c, log_c, b, l0, nlc, f, cs, f64))); break;
+                case ST_RESCALE: TRY((pass_t<false, false, ST_RESCALE>(c, log_c, b, l0, nlc, f, cs, f64))); break;
                 default: return fail(SRK_EINVAL, "bad forward store mode");
             }
         } else {
             switch (ld) {
-                case LD_PLAIN: TRY((pass_t<true, false, LD_PLAIN>(c, log_c, b, l0, nlc, f, s, f64))); break;
-                case LD_AUTO: TRY((pass_t<true, false, LD_AUTO>(c, log_c, b, l0, nlc, f, s, f64))); break;
+                case LD_PLAIN: TRY((pass_t<true, false, LD_PLAIN>(c, log_c, b, l0, nlc, f, cs, f64))); break;
+                case LD_AUTO: TRY((pass_t<true, false, LD_AUTO>(c, log_c, b, l0, nlc, f, cs, f64))); break;
                 default: return fail(SRK_EINVAL, "bad inverse load mode");
             }
             switch (st) {
-                case ST_PLAIN: TRY((pass_t<true, true, ST_PLAIN>(c, log_r, b, l0, nlc, f, s, f64))); break;
-                case ST_SCALE: TRY((pass_t<true, true, ST_SCALE>(c, log_r, b, l0, nlc, f, s, f64))); break;
+                case ST_PLAIN: TRY((pass_t<true, true, ST_PLAIN>(c, log_r, b, l0, nlc, f, cs, f64))); break;
+                case ST_SCALE: TRY((pass_t<true, true, ST_SCALE>(c, log_r, b, l0, nlc, f, cs, f64))); break;
                 default: return fail(SRK_EINVAL, "bad inverse store mode");
             }
         }
+    }
+    if (two) {
+        CU(cudaEventRecord(c->ev_njoin[lane], c->nside[lane]));
+        CU(cudaStreamWaitEvent(s, c->ev_njoin[lane], 0));
     }
     return SRK_OK;
 }

@@ -126,6 +126,8 @@ struct NttTables {
     const PrimeConst *pc;
     const ulonglong2 *tw;   // [n_primes][N] {psi^brv(k), Shoup}: one 16-B load per twiddle
     const ulonglong2 *itw;  // [n_primes][N] {psi^-brv(k), Shoup}
+    const double *twd;      // [n_primes][N] psi^brv(k) as an exact double (FP64 limbs:
+    const double *itwd;     //   one 8-B load, no u64 -> f64 conversion per twiddle)
 };
 
 template <int LOG_T>
@@ -222,10 +224,20 @@ __device__ __forceinline__ double centre_f64(double v, double q, double qinv) {
     const double t = fma(v, qinv, SRK_F64_MAGIC) - SRK_F64_MAGIC;
     return fma(-t, q, v);
 }
+// signed integer of an integer-valued double |r| < 2^51: r + 1.5*2^52 keeps
+// exponent 52, so its bit pattern is 0x4338000000000000 + r (one DADD + IADD)
+__device__ __forceinline__ long long i64_of_f64(double r) {
+    return __double_as_longlong(r + SRK_F64_MAGIC) - 0x4338000000000000ll;
+}
+// canonical [0, q) of an integer-valued double already in (-q, q)
+__device__ __forceinline__ uint64_t canon_u64_of_small_f64(double r, uint64_t q) {
+    const long long i = i64_of_f64(r);
+    return (uint64_t)(i < 0 ? i + (long long)q : i);
+}
 __device__ __forceinline__ uint64_t canon_u64_of_f64(double v, double q, double qinv) {
-    double r = centre_f64(v, q, qinv);
-    r = r < 0.0 ? r + q : r;
-    return u64_of_f64(r);
+    // centred r in [-q/2, q/2] (|r| < q with rounding slack); sign fix-up on the integer pipes
+    const long long i = i64_of_f64(centre_f64(v, q, qinv));
+    return (uint64_t)(i < 0 ? i + (long long)q : i);
 }
 __device__ __forceinline__ void ct_bfly_f64(uint64_t &xb, uint64_t &yb, double w, double q,
                                             double qinv) {
@@ -250,13 +262,21 @@ __device__ __forceinline__ void gs_bfly_f64(uint64_t &xb, uint64_t &yb, double w
 struct F64Q {
     double q, qinv;
 };
+struct TwPtr {
+    const ulonglong2 *w;  // {w, Shoup(w)} (integer modes)
+    const double *wd;     // w as double (FP64 mode)
+};
 template <int E, int HALF, int NG, bool GS, int SM, typename TwFn>
-__device__ __forceinline__ void reg_stage(uint64_t (&x)[E], TwFn tw_group, uint64_t q,
+__device__ __forceinline__ void reg_stage(uint64_t (&x)[E], TwPtr tp, TwFn tw_idx, uint64_t q,
                                           uint64_t two_q, uint64_t m, F64Q fq) {
 #pragma unroll
     for (int g = 0; g < NG; g++) {
-        const ulonglong2 w = tw_group(g);
-        const double wf = SM == 2 ? f64_of_u64(w.x) : 0.0;
+        ulonglong2 w = {0, 0};
+        double wf = 0.0;
+        if constexpr (SM == 2)
+            wf = __ldg(tp.wd + tw_idx(g));
+        else
+            w = __ldg(tp.w + tw_idx(g));
 #pragma unroll
         for (int k = 0; k < HALF; k++) {
             uint64_t &a = x[g * 2 * HALF + k];
@@ -284,11 +304,11 @@ __device__ __forceinline__ void reg_stage(uint64_t (&x)[E], TwFn tw_group, uint6
 // twiddle (base << s) + g
 template <int E, int LE1, int SM, int S = 0>
 struct FwdR1 {
-    static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
+    static __device__ __forceinline__ void run(uint64_t (&x)[E], TwPtr tw, int base,
                                                uint64_t q, uint64_t two_q, F64Q fq = {}) {
         if constexpr (S < LE1) {
             reg_stage<E, (E >> (S + 1)), (1 << S), false, SM>(
-                x, [&](int g) { return __ldg(tw + ((base << S) + g)); }, q, two_q, 0, fq);
+                x, tw, [&](int g) { return (base << S) + g; }, q, two_q, 0, fq);
             FwdR1<E, LE1, SM, S + 1>::run(x, tw, base, q, two_q, fq);
         }
     }
@@ -297,12 +317,12 @@ struct FwdR1 {
 // twiddle (base << (LE1+s)) + u ng + g
 template <int E, int TPS, int LE1, int LE2, int SM, int S = 0>
 struct FwdR2 {
-    static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
+    static __device__ __forceinline__ void run(uint64_t (&x)[E], TwPtr tw, int base,
                                                int u, uint64_t q, uint64_t two_q, F64Q fq = {}) {
         if constexpr (S < LE2) {
             constexpr int half = TPS >> (S + 1), ng = E / (2 * half);
             reg_stage<E, half, ng, false, SM>(
-                x, [&](int g) { return __ldg(tw + ((base << (LE1 + S)) + u * ng + g)); }, q, two_q, 0,
+                x, tw, [&](int g) { return (base << (LE1 + S)) + u * ng + g; }, q, two_q, 0,
                 fq);
             FwdR2<E, TPS, LE1, LE2, SM, S + 1>::run(x, tw, base, u, q, two_q, fq);
         }
@@ -312,13 +332,13 @@ struct FwdR2 {
 // twiddle (base << stage) + u ng + g
 template <int E, int LOG_T, int LE1, int SM, int S = 0>
 struct InvR1 {
-    static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
+    static __device__ __forceinline__ void run(uint64_t (&x)[E], TwPtr tw, int base,
                                                int u, uint64_t q, uint64_t two_q, int k0,
                                                F64Q fq = {}) {
         if constexpr (S < LE1) {
             constexpr int half = 1 << S, ng = E / (2 * half), stage = LOG_T - 1 - S;
             reg_stage<E, half, ng, true, SM>(
-                x, [&](int g) { return __ldg(tw + ((base << stage) + u * ng + g)); }, q, two_q,
+                x, tw, [&](int g) { return (base << stage) + u * ng + g; }, q, two_q,
                 q << (k0 + S), fq);
             InvR1<E, LOG_T, LE1, SM, S + 1>::run(x, tw, base, u, q, two_q, k0, fq);
         }
@@ -328,12 +348,12 @@ struct InvR1 {
 // 2^stage groups, twiddle (base << stage) + g
 template <int E, int TPS, int LE2, int SM, int S = 0>
 struct InvR2 {
-    static __device__ __forceinline__ void run(uint64_t (&x)[E], const ulonglong2 *tw, int base,
+    static __device__ __forceinline__ void run(uint64_t (&x)[E], TwPtr tw, int base,
                                                uint64_t q, uint64_t two_q, int k0, F64Q fq = {}) {
         if constexpr (S < LE2) {
             constexpr int half = (E / TPS) << S, stage = LE2 - 1 - S;
             reg_stage<E, half, (1 << stage), true, SM>(
-                x, [&](int g) { return __ldg(tw + ((base << stage) + g)); }, q, two_q,
+                x, tw, [&](int g) { return (base << stage) + g; }, q, two_q,
                 q << (k0 + S), fq);
             InvR2<E, TPS, LE2, SM, S + 1>::run(x, tw, base, q, two_q, k0, fq);
         }
@@ -474,9 +494,16 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
 // limb storage (b.ptr).
 // F64: every limb of the launch is under a prime < 2^41, so only the FP64
 // arithmetic mode is compiled in (no integer-mode code, no register spills).
-template <int LOG_T, bool INV, bool COL, int IO, bool F64 = false>
-__global__ void __launch_bounds__(256, SRK_NTT_MINB)
-    ntt_pass_kernel(LimbBatch b, NttTables tb, int log_n, const __grid_constant__ FuseArgs f) {
+// LOGN: compile-time log2 ring degree (0 = runtime log_n_arg), so the strided
+// element addresses of the 2^16 passes fold into immediate offsets.
+// Grid: x = sub-transform groups, y = poly, z = limb.
+#ifndef SRK_NTT_MINB_F64
+#define SRK_NTT_MINB_F64 4
+#endif
+template <int LOG_T, bool INV, bool COL, int IO, bool F64 = false, int LOGN = 0>
+__global__ void __launch_bounds__(256, F64 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB)
+    ntt_pass_kernel(LimbBatch b, NttTables tb, int log_n_arg, const __grid_constant__ FuseArgs f) {
+    const int log_n = LOGN ? LOGN : log_n_arg;
     using S = NttShape<LOG_T>;
     constexpr int T = S::T, E = S::E, TPS = S::TPS, LE1 = S::LE1, LE2 = S::LE2;
     constexpr bool FIRST = (COL != INV);  // forward column / inverse row pass
@@ -486,9 +513,9 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
 
     const int n = 1 << log_n;
     const int CB = blockDim.x / TPS;  // sub-transforms per CTA
-    const int y = blockIdx.y;
-    const int limb = y / b.n_polys, poly = y - limb * b.n_polys;
-    const int bi = poly / b.ppc, r = poly - bi * b.ppc;
+    const int limb = blockIdx.z, poly = blockIdx.y;
+    const int bi = b.ppc == 2 ? poly >> 1 : (b.ppc == 1 ? poly : poly / b.ppc);
+    const int r = poly - bi * b.ppc;
     int t, pid;
     if (!limb_map(b, r, limb, t, pid)) return;
     uint64_t *data =
@@ -496,7 +523,7 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
     const PrimeConst pc = tb.pc[pid];
     const uint64_t q = pc.q, two_q = pc.two_q;
     const bool small = q < SRK_SMALL_Q;  // uniform per CTA (one limb per CTA)
-    const ulonglong2 *tw = (INV ? tb.itw : tb.tw) + (long long)pid * n;
+    const TwPtr tw = {(INV ? tb.itw : tb.tw) + (long long)pid * n, (INV ? tb.itwd : tb.twd) + (long long)pid * n};
     const uint64_t *lsrc = data;  // LD_PLAIN / LD_AUTO source limb
     if constexpr (FIRST && (LD == LD_PLAIN || LD == LD_AUTO)) {
         if (f.src) lsrc = f.src + (long long)bi * f.src_ct + (long long)r * f.src_ps + (long long)t * n;
@@ -644,9 +671,9 @@ __global__ void __launch_bounds__(256, SRK_NTT_MINB)
             if (mode == 2) {
                 const double mf = f64_of_u64(m);
 #pragma unroll
-                for (int e = 0; e < E; e++)
-                    data[gaddr(u + TPS * e)] = canon_u64_of_f64(
-                        modmul_f64(__longlong_as_double((long long)x[e]), mf, fq.q, fq.qinv), fq.q, fq.qinv);
+                for (int e = 0; e < E; e++)  // modmul_f64 output is already in (-q, q)
+                    data[gaddr(u + TPS * e)] = canon_u64_of_small_f64(
+                        modmul_f64(__longlong_as_double((long long)x[e]), mf, fq.q, fq.qinv), q);
             } else {
 #pragma unroll
                 for (int e = 0; e < E; e++) data[gaddr(u + TPS * e)] = mul_shoup(x[e], m, ms, q);
