@@ -96,6 +96,8 @@ static inline uint32_t hbrv(uint32_t x, int bits) {
 struct BconvPlan {
     uint64_t *mat = nullptr;   // [n_src][n_dst]
     ulonglong2 *mat2 = nullptr;  // [n_src][n_dst] {m, floor(m 2^64 / q_t)} (Shoup)
+    ulonglong2 *mhl = nullptr;   // [n_src][n_dst] {m, m 2^32 mod q_t}       (k_moddown_conv_f64,
+    double2 *fhl = nullptr;      // [n_src][n_dst] {m / q_t, (m 2^32 mod q_t) / q_t}  q_t < 2^41)
     uint64_t *hinv = nullptr;  // [2][n_src]
     int *dst_slot = nullptr;
     int *dst_pid = nullptr;
@@ -138,6 +140,8 @@ struct srk_ctx {
     // caller's stream and nside[lane], so one chunk's pass tail overlaps the
     // next chunk's passes (lane = 1 when called from the key-switch side lane)
     int ntt_streams = 2;
+    int conv_f64 = 1;
+    unsigned conv_cpt = 4;  // coefficients per thread of k_moddown_conv_f64 (amortises its staging)  // ModDown conversion on the FP64 + integer pipes (k_moddown_conv_f64)
     cudaStream_t nside[2] = {nullptr, nullptr};
     cudaEvent_t ev_nfork[2] = {nullptr, nullptr}, ev_njoin[2] = {nullptr, nullptr};
 };
@@ -192,6 +196,19 @@ static int build_plan(srk_ctx *c, BconvPlan &pl, const std::vector<int> &src_pid
             mat2[(size_t)i * nd + t] = make_ulonglong2(m, shoup(m, c->primes[dst_pids[t]]));
         }
     TRY(dupload(c, &pl.mat2, mat2));
+    if (exact) {
+        std::vector<ulonglong2> mhl((size_t)ns * nd);
+        std::vector<double2> fhl((size_t)ns * nd);
+        for (int i = 0; i < ns; i++)
+            for (int t = 0; t < nd; t++) {
+                const uint64_t p = c->primes[dst_pids[t]], m = mat[(size_t)i * nd + t];
+                const uint64_t mh = (uint64_t)(((u128)m << 32) % p);
+                mhl[(size_t)i * nd + t] = make_ulonglong2(m, mh);
+                fhl[(size_t)i * nd + t] = make_double2((double)m / (double)p, (double)mh / (double)p);
+            }
+        TRY(dupload(c, &pl.mhl, mhl));
+        TRY(dupload(c, &pl.fhl, fhl));
+    }
     TRY(dupload(c, &pl.hinv, hv));
     TRY(dupload(c, &pl.dst_slot, dst_slots));
     TRY(dupload(c, &pl.dst_pid, dst_pids));
@@ -259,6 +276,8 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     if (const char *e = getenv("SRK_KS_FUSED")) c->ks_fused = atoi(e);
     if (const char *e = getenv("SRK_KS_STREAMS")) c->ks_streams = atoi(e);
     if (const char *e = getenv("SRK_NTT_STREAMS")) c->ntt_streams = atoi(e);
+    if (const char *e = getenv("SRK_CONV_F64")) c->conv_f64 = atoi(e);
+    if (const char *e = getenv("SRK_CONV_CPT")) c->conv_cpt = std::max(1, atoi(e));
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -598,9 +617,18 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
     struct Chunk {
         int l0, nlc;
         bool f64;
+        int cls;
     };
     std::vector<Chunk> chunks;
-    for (int l0 = 0, nlc = 0; l0 < b.n_limbs; l0 += nlc) {
+    const bool class_split = b.mode == 1 && c->ntt_split;
+    if (class_split) {
+        // ModUp targets mix 40-bit and 60-bit primes per digit: one FP64 launch that
+        // skips the >= 2^41 limbs and one integer launch that skips the rest
+        // (independent, so they run on the two streams side by side)
+        chunks.push_back({0, b.n_limbs, true, 1});
+        chunks.push_back({0, b.n_limbs, false, 2});
+    }
+    for (int l0 = 0, nlc = 0; !class_split && l0 < b.n_limbs; l0 += nlc) {
         nlc = std::min(per, b.n_limbs - l0);
         bool f64 = false;
         if (b.mode == 0 && c->ntt_split) {
@@ -609,7 +637,7 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
             while (k < nlc && f64_limb(l0 + k) == f64) k++;
             nlc = k;
         }
-        chunks.push_back({l0, nlc, f64});
+        chunks.push_back({l0, nlc, f64, 0});
     }
     // independent chunks alternate between s and this lane's NTT side stream
     const int lane = s == c->side ? 1 : 0;
@@ -621,6 +649,7 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
     for (size_t ci = 0; ci < chunks.size(); ci++) {
         const int l0 = chunks[ci].l0, nlc = chunks[ci].nlc;
         const bool f64 = chunks[ci].f64;
+        b.cls = chunks[ci].cls;
         cudaStream_t cs = (two && (ci & 1)) ? c->nside[lane] : s;
         if (!inverse) {
             switch (ld) {
@@ -995,18 +1024,25 @@ static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int n
     dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + 7) / 8);
     const uint64_t *z = g.src;
 #define SRK_CONV_LAUNCH(MK, EX)                                                                         \
-    k_moddown_conv<MK, EX><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2, g.mat_ld, \
-                                                g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n)
+    if (c->conv_f64 && g.mhl)                                                                            \
+        k_moddown_conv_f64<MK, EX><<<dim3(std::max(1u, grid.x / c->conv_cpt), grid.y, grid.z), 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2,  \
+                                                        g.mhl, g.fhl, g.mat_ld, g.corr, bq.ptr,           \
+                                                        bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n); \
+    else                                                                                                 \
+        k_moddown_conv<MK, EX><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2,      \
+                                                    g.mat_ld, g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, \
+                                                    c->d_pc, c->log_n)
     switch (g.n_src) {
         case 1: SRK_CONV_LAUNCH(1, true); break;
         case 2: SRK_CONV_LAUNCH(2, true); break;
         case 3: SRK_CONV_LAUNCH(3, true); break;
         case 4: SRK_CONV_LAUNCH(4, true); break;
         default:
-            if (g.n_src <= 8)
+            if (g.n_src <= 8) {
                 SRK_CONV_LAUNCH(8, false);
-            else
+            } else {
                 SRK_CONV_LAUNCH(16, false);
+            }
     }
 #undef SRK_CONV_LAUNCH
     LAUNCHED();
@@ -1241,6 +1277,8 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             g.n_src = ns;
             g.mat = pr.mat;
             g.mat2 = pr.mat2;
+            g.mhl = pr.mhl;
+            g.fhl = pr.fhl;
             g.mat_ld = pr.n_dst;
             g.corr = pr.dst_corr;
             g.corr_ld = pr.n_dst;
@@ -1287,6 +1325,8 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             f.src_pid0 = c->n_q;
             f.mat = pd.mat;
             f.mat2 = pd.mat2;
+            f.mhl = pd.mhl;
+            f.fhl = pd.fhl;
             f.mat_ld = pd.n_dst;
             f.corr = pd.dst_corr;
             f.corr_ld = pd.n_dst;

@@ -380,6 +380,100 @@ __global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict
     }
 }
 
+// ModDown conversion P -> Q with the FP64 and integer pipes splitting the work
+// (targets q_t < 2^41; the rest take the Shoup path of k_moddown_conv):
+//   z_k = zh_k 2^32 + zl_k,   S' = sum_k zh_k m'_kt + zl_k m_kt  == sum_k z_k m_kt (mod q_t)
+// with m' = m 2^32 mod q_t.  The quotient t = round(S'/q_t) comes from the FP64
+// pipe, T = sum_k zh_k (m'/q) + zl_k (m/q) (every term < 2^32, total rounding
+// error < 2^-16, so S' - t q_t lies in (-q_t, q_t)), and the remainder from the
+// integer pipe in wrapping 64-bit arithmetic: r = S' - t q_t (mod 2^64), exact
+// because |r| < q_t.  Per target: 2K FP64 FMAs + 2K 32x64-bit IMAD products
+// instead of K 64-bit Shoup products (~13 IMAD each).
+#define SRK_CONV_TG 8  // targets per CTA (blockIdx.z groups)
+template <int MAXK, bool EXACT>
+__global__ void __launch_bounds__(256) k_moddown_conv_f64(
+    const uint64_t *__restrict__ z, long long z_ct, long long z_ps, int n_src,
+    const uint8_t *__restrict__ vround, const ulonglong2 *__restrict__ mat2,
+    const ulonglong2 *__restrict__ mhl, const double2 *__restrict__ fhl, int n_dst,
+    const uint64_t *__restrict__ corr, uint64_t *__restrict__ conv, long long c_ct, long long c_ps,
+    const PrimeConst *__restrict__ pc, int log_n) {
+    // the CTA's targets' constants, staged once: {m/q, m'/q} and {m, m'} per (target, source)
+    __shared__ double2 s_f[SRK_CONV_TG][MAXK];
+    __shared__ ulonglong2 s_m[SRK_CONV_TG][MAXK];
+    __shared__ uint64_t s_q[SRK_CONV_TG], s_corr[MAXK + 1][SRK_CONV_TG];
+    const long long n = 1ll << log_n;
+    const int p = blockIdx.y;  // (b, r)
+    const int b = p >> 1, r = p & 1;
+    const int t0 = blockIdx.z * SRK_CONV_TG, nt = min(n_dst - t0, SRK_CONV_TG);
+    const int ns = EXACT ? MAXK : n_src;
+    for (int i = threadIdx.x; i < nt * MAXK; i += blockDim.x) {
+        const int tt = i / MAXK, k = i - tt * MAXK;
+        if (k < ns) {
+            s_f[tt][k] = __ldg(fhl + k * n_dst + t0 + tt);
+            s_m[tt][k] = __ldg(mhl + k * n_dst + t0 + tt);
+        }
+    }
+    for (int i = threadIdx.x; i < nt * (MAXK + 1); i += blockDim.x) {
+        const int v = i / nt, tt = i - v * nt;
+        if (v <= ns) s_corr[v][tt] = __ldg(corr + v * n_dst + t0 + tt);
+    }
+    if (threadIdx.x < nt) s_q[threadIdx.x] = pc[t0 + threadIdx.x].q;
+    __syncthreads();
+    const uint64_t *zp = z + b * z_ct + r * z_ps;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
+         x += (long long)gridDim.x * blockDim.x) {
+        uint64_t zz[MAXK];
+        uint32_t zl[MAXK], zh[MAXK];
+        double dl[MAXK], dh[MAXK];
+#pragma unroll
+        for (int k = 0; k < MAXK; k++) {
+            zz[k] = (EXACT || k < n_src) ? zp[k * n + x] : 0;
+            zl[k] = (uint32_t)zz[k];
+            zh[k] = (uint32_t)(zz[k] >> 32);
+            dl[k] = __hiloint2double(0x43300000, (int)zl[k]) - SRK_F64_TWO52;
+            dh[k] = __hiloint2double(0x43300000, (int)zh[k]) - SRK_F64_TWO52;
+        }
+        const int v = vround[(long long)p * n + x];
+        uint64_t *out = conv + b * c_ct + r * c_ps + (long long)t0 * n + x;
+#pragma unroll
+        for (int tt = 0; tt < SRK_CONV_TG; tt++) {
+            if (tt >= nt) break;
+            const uint64_t q = s_q[tt];
+            uint64_t acc;
+            if (q < SRK_F64_Q) {
+                double T = 0.0;
+                uint64_t S = 0;
+#pragma unroll
+                for (int k = 0; k < MAXK; k++)
+                    if (EXACT || k < n_src) {
+                        const double2 f = s_f[tt][k];     // {m/q, m'/q}
+                        const ulonglong2 m = s_m[tt][k];  // {m, m'}
+                        T = fma(dl[k], f.x, T);
+                        T = fma(dh[k], f.y, T);
+                        S += (uint64_t)zl[k] * m.x;
+                        S += (uint64_t)zh[k] * m.y;
+                    }
+                const long long tq = __double_as_longlong(T + SRK_F64_MAGIC) - 0x4338000000000000ll;
+                const long long rr = (long long)(S - (uint64_t)tq * q);
+                acc = (uint64_t)(rr < 0 ? rr + (long long)q : rr);
+            } else {  // 60-bit target (q_0): Shoup products
+                const uint64_t two_q = 2 * q;
+                acc = 0;
+#pragma unroll
+                for (int k = 0; k < MAXK; k++)
+                    if (EXACT || k < n_src) {
+                        const ulonglong2 mw = __ldg(mat2 + k * n_dst + t0 + tt);
+                        acc += mul_shoup_lazy(zz[k], mw.x, mw.y, q);
+                        acc = acc >= two_q ? acc - two_q : acc;
+                    }
+                acc = acc >= q ? acc - q : acc;
+            }
+            *out = sub_mod(acc, s_corr[v][tt], q);
+            out += n;
+        }
+    }
+}
+
 struct CombineArgs {
     const uint64_t *conv;
     long long conv_ct, conv_ps;

@@ -45,6 +45,7 @@ struct LimbBatch {
     int ppc, n_polys, n_limbs;
     int mode, split, off_a, off_b;
     int alpha, nl, level, L, ne;
+    int cls;  // prime-class filter: 0 all limbs, 1 only q < 2^41 (FP64), 2 only q >= 2^41
 };
 
 __device__ __forceinline__ int batch_pid(const LimbBatch &b, int i) {
@@ -94,6 +95,8 @@ struct FuseArgs {
     int n_src, src_pid0;     // LD_BCONV: z limbs under primes src_pid0 ..
     const uint64_t *mat;     // LD_BCONV: [n_src][mat_ld] conversion constants
     const ulonglong2 *mat2;  // the same with Shoup companions (streaming conversion)
+    const ulonglong2 *mhl;   // {m, m 2^32 mod q_t} and {m/q_t, (m 2^32 mod q_t)/q_t}:
+    const double2 *fhl;      //   FP64-pipe conversion (k_moddown_conv_f64)
     int mat_ld;
     const uint64_t *corr;    // LD_BCONV: [v * prod src primes]_{q_t}, table [v][corr_ld]
     int corr_ld;
@@ -522,6 +525,9 @@ __global__ void __launch_bounds__(256, F64 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB)
         b.ptr + (long long)bi * b.ct_stride + (long long)r * b.poly_stride + (long long)t * n;
     const PrimeConst pc = tb.pc[pid];
     const uint64_t q = pc.q, two_q = pc.two_q;
+    // prime-class split of mixed batches (uniform per CTA): the FP64 kernel never
+    // touches a limb >= 2^41; the integer kernel skips FP64 limbs when filtered
+    if ((F64 || b.cls == 1) ? q >= SRK_F64_Q : (b.cls == 2 && q < SRK_F64_Q)) return;
     const bool small = q < SRK_SMALL_Q;  // uniform per CTA (one limb per CTA)
     const TwPtr tw = {(INV ? tb.itw : tb.tw) + (long long)pid * n, (INV ? tb.itwd : tb.twd) + (long long)pid * n};
     const uint64_t *lsrc = data;  // LD_PLAIN / LD_AUTO source limb
