@@ -140,8 +140,8 @@ struct srk_ctx {
     // caller's stream and nside[lane], so one chunk's pass tail overlaps the
     // next chunk's passes (lane = 1 when called from the key-switch side lane)
     int ntt_streams = 2;
-    int conv_f64 = 1;
-    unsigned conv_cpt = 4;  // coefficients per thread of k_moddown_conv_f64 (amortises its staging)  // ModDown conversion on the FP64 + integer pipes (k_moddown_conv_f64)
+    int conv_f64 = 1;  // ModDown conversion on the FP64 + integer pipes (k_moddown_conv_f64)
+    unsigned conv_cpt = 4;  // coefficients per thread of k_moddown_conv_f64 (amortises its staging)
     cudaStream_t nside[2] = {nullptr, nullptr};
     cudaEvent_t ev_nfork[2] = {nullptr, nullptr}, ev_njoin[2] = {nullptr, nullptr};
 };
@@ -508,28 +508,28 @@ static FuseArgs no_fuse() {
     return f;
 }
 
-template <int LOG_T, bool INV, bool COL, int IO, bool F64, int LOGN>
+template <int LOG_T, bool INV, bool COL, int IO, int KM, int LOGN>
 static void launch_kernel_n(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
                             const NttTables &tb, int log_n, const FuseArgs &ff) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(ntt_pass_kernel<LOG_T, INV, COL, IO, F64, LOGN>,
+        cudaFuncSetAttribute(ntt_pass_kernel<LOG_T, INV, COL, IO, KM, LOGN>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         attr_set = true;
     }
-    ntt_pass_kernel<LOG_T, INV, COL, IO, F64, LOGN><<<grid, threads, smem, s>>>(bb, tb, log_n, ff);
+    ntt_pass_kernel<LOG_T, INV, COL, IO, KM, LOGN><<<grid, threads, smem, s>>>(bb, tb, log_n, ff);
 }
 // ring 2^16 (every BASELINE config past config 1): compile-time shape
-template <int LOG_T, bool INV, bool COL, int IO, bool F64>
+template <int LOG_T, bool INV, bool COL, int IO, int KM>
 static void launch_kernel(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
                           const NttTables &tb, int log_n, const FuseArgs &ff) {
     if constexpr (LOG_T == 8) {
         if (log_n == 16) {
-            launch_kernel_n<LOG_T, INV, COL, IO, F64, 16>(grid, threads, smem, s, bb, tb, log_n, ff);
+            launch_kernel_n<LOG_T, INV, COL, IO, KM, 16>(grid, threads, smem, s, bb, tb, log_n, ff);
             return;
         }
     }
-    launch_kernel_n<LOG_T, INV, COL, IO, F64, 0>(grid, threads, smem, s, bb, tb, log_n, ff);
+    launch_kernel_n<LOG_T, INV, COL, IO, KM, 0>(grid, threads, smem, s, bb, tb, log_n, ff);
 }
 
 template <int LOG_T, bool INV, bool COL, int IO>
@@ -573,13 +573,15 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
     bb.n_limbs = nlc;
     dim3 grid(subs / cb, b.n_polys, nlc);
     bool done = false;
-    if constexpr (IO == 0 || IO == 3) {  // plain / automorphism loads, plain / scaled stores
-        if (f64) {
-            launch_kernel<LOG_T, INV, COL, IO, true>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
-            done = true;
-        }
+    if constexpr (IO == 0 || IO == 3) {  // plain / automorphism loads, plain / scaled stores:
+        // FP64-only kernel for q < 2^41 chunks, Harvey-only integer kernel otherwise
+        if (f64)
+            launch_kernel<LOG_T, INV, COL, IO, 1>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
+        else
+            launch_kernel<LOG_T, INV, COL, IO, 2>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
+    } else {
+        launch_kernel<LOG_T, INV, COL, IO, 0>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
     }
-    if (!done) launch_kernel<LOG_T, INV, COL, IO, false>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
     LAUNCHED();
     return SRK_OK;
 }

@@ -495,7 +495,7 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
 // inverse: row pass) or the fused store of the LAST pass (forward: row pass,
 // inverse: column pass); the intermediate always lives at the batch's own
 // limb storage (b.ptr).
-// F64: every limb of the launch is under a prime < 2^41, so only the FP64
+// KM 1: every limb of the launch is under a prime < 2^41, so only the FP64
 // arithmetic mode is compiled in (no integer-mode code, no register spills).
 // LOGN: compile-time log2 ring degree (0 = runtime log_n_arg), so the strided
 // element addresses of the 2^16 passes fold into immediate offsets.
@@ -503,8 +503,14 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
 #ifndef SRK_NTT_MINB_F64
 #define SRK_NTT_MINB_F64 4
 #endif
-template <int LOG_T, bool INV, bool COL, int IO, bool F64 = false, int LOGN = 0>
-__global__ void __launch_bounds__(256, F64 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB)
+#ifndef SRK_NTT_MINB_INT
+#define SRK_NTT_MINB_INT 3
+#endif
+// KM: 0 = arithmetic mode chosen per limb at run time (fused-IO variants),
+//     1 = FP64 only (limbs under q < 2^41; others skipped),
+//     2 = Harvey lazy integer only (any q < 2^62; with cls 2 the FP64 limbs are skipped)
+template <int LOG_T, bool INV, bool COL, int IO, int KM = 0, int LOGN = 0>
+__global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? SRK_NTT_MINB_INT : SRK_NTT_MINB))
     ntt_pass_kernel(LimbBatch b, NttTables tb, int log_n_arg, const __grid_constant__ FuseArgs f) {
     const int log_n = LOGN ? LOGN : log_n_arg;
     using S = NttShape<LOG_T>;
@@ -527,7 +533,7 @@ __global__ void __launch_bounds__(256, F64 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB)
     const uint64_t q = pc.q, two_q = pc.two_q;
     // prime-class split of mixed batches (uniform per CTA): the FP64 kernel never
     // touches a limb >= 2^41; the integer kernel skips FP64 limbs when filtered
-    if ((F64 || b.cls == 1) ? q >= SRK_F64_Q : (b.cls == 2 && q < SRK_F64_Q)) return;
+    if ((KM == 1 || b.cls == 1) ? q >= SRK_F64_Q : (b.cls == 2 && q < SRK_F64_Q)) return;
     const bool small = q < SRK_SMALL_Q;  // uniform per CTA (one limb per CTA)
     const TwPtr tw = {(INV ? tb.itw : tb.tw) + (long long)pid * n, (INV ? tb.itwd : tb.twd) + (long long)pid * n};
     const uint64_t *lsrc = data;  // LD_PLAIN / LD_AUTO source limb
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(256, F64 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB)
 
     // arithmetic mode, uniform per CTA: 2 = FP64 (q < 2^41), 1 = reduction-free
     // integer (q < 2^46), 0 = Harvey lazy integer
-    const int mode = F64 ? 2 : (q < SRK_F64_Q ? 2 : (small ? 1 : 0));
+    const int mode = KM == 1 ? 2 : (KM == 2 ? 0 : (q < SRK_F64_Q ? 2 : (small ? 1 : 0)));
     // (double) q and 1 / (double) q precomputed per prime (no per-CTA division)
     const F64Q fq = {__longlong_as_double((long long)pc.qd_bits), __longlong_as_double((long long)pc.qinv_bits)};
     // first-pass loads are canonical u64; FP64 limbs convert on load
