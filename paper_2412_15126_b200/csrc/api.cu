@@ -196,7 +196,7 @@ static int build_plan(srk_ctx *c, BconvPlan &pl, const std::vector<int> &src_pid
             mat2[(size_t)i * nd + t] = make_ulonglong2(m, shoup(m, c->primes[dst_pids[t]]));
         }
     TRY(dupload(c, &pl.mat2, mat2));
-    if (exact) {
+    {
         std::vector<ulonglong2> mhl((size_t)ns * nd);
         std::vector<double2> fhl((size_t)ns * nd);
         for (int i = 0; i < ns; i++)
@@ -1165,26 +1165,57 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             m.slot[j] = pl.dst_slot;
             m.pid[j] = pl.dst_pid;
             m.n_dst[j] = pl.n_dst;
+            m.mhl[j] = pl.mhl;
+            m.fhl[j] = pl.fhl;
             maxd = std::max(maxd, pl.n_dst);
         }
+        // FP64-pipe conversion when every source but a digit's first is < 2^41
+        bool f64ok = c->conv_f64 != 0, wide0 = false;
+        for (int j = 0; j < beta; j++)
+            for (int i = 0; i < alpha && j * alpha + i < nl; i++)
+                if (c->primes[j * alpha + i] >= SRK_F64_Q) {
+                    if (i == 0 && j == 0)
+                        wide0 = true;
+                    else
+                        f64ok = false;
+                }
         dim3 grid((unsigned)((n + 255) / 256), B * beta, (maxd + SRK_MODUP_TCH - 1) / SRK_MODUP_TCH);
-        switch (alpha) {
-            case 1: k_modup<1><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 2: k_modup<2><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 3: k_modup<3><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 4: k_modup<4><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 5: k_modup<5><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 6: k_modup<6><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 7: k_modup<7><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 8: k_modup<8><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 9: k_modup<9><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 10: k_modup<10><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 11: k_modup<11><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 12: k_modup<12><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 13: k_modup<13><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 14: k_modup<14><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            case 15: k_modup<15><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-            default: k_modup<16><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+        if (f64ok) {
+            dim3 g2(std::max(1u, grid.x / c->conv_cpt), grid.y, grid.z);
+#define SRK_MODUP_F64(GS)                                                          \
+    case GS:                                                                      \
+        if (wide0)                                                                \
+            k_modup_f64<GS, true><<<g2, 256, 0, s>>>(m, c->d_pc, c->log_n);      \
+        else                                                                      \
+            k_modup_f64<GS, false><<<g2, 256, 0, s>>>(m, c->d_pc, c->log_n);     \
+        break;
+            switch (alpha) {
+                SRK_MODUP_F64(1) SRK_MODUP_F64(2) SRK_MODUP_F64(3) SRK_MODUP_F64(4)
+                SRK_MODUP_F64(5) SRK_MODUP_F64(6) SRK_MODUP_F64(7) SRK_MODUP_F64(8)
+                SRK_MODUP_F64(9) SRK_MODUP_F64(10) SRK_MODUP_F64(11) SRK_MODUP_F64(12)
+                SRK_MODUP_F64(13) SRK_MODUP_F64(14) SRK_MODUP_F64(15) SRK_MODUP_F64(16)
+                default: return fail(SRK_EINVAL, "digit size > 16");
+            }
+#undef SRK_MODUP_F64
+        } else {
+            switch (alpha) {
+                case 1: k_modup<1><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 2: k_modup<2><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 3: k_modup<3><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 4: k_modup<4><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 5: k_modup<5><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 6: k_modup<6><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 7: k_modup<7><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 8: k_modup<8><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 9: k_modup<9><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 10: k_modup<10><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 11: k_modup<11><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 12: k_modup<12><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 13: k_modup<13><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 14: k_modup<14><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 15: k_modup<15><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                default: k_modup<16><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+            }
         }
         LAUNCHED();
     }

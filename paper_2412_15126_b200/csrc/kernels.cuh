@@ -210,6 +210,9 @@ struct ModUpArgs {
     const int *slot[SRK_MAX_DIGITS];
     const int *pid[SRK_MAX_DIGITS];
     int n_dst[SRK_MAX_DIGITS];
+    // FP64 + integer pipe conversion (k_modup_f64): {m, m 2^32 mod q_t}, {m/q_t, (m 2^32 mod q_t)/q_t}
+    const ulonglong2 *mhl[SRK_MAX_DIGITS];
+    const double2 *fhl[SRK_MAX_DIGITS];
 };
 
 #define SRK_MODUP_TCH 8
@@ -247,6 +250,88 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
                 for (int i = 0; i < gs; i++) mac(acc, src[(long long)i * n + x], __ldg(mat + i * nd + t));
                 dst[(long long)__ldg(a.slot[j] + t) * n + x] = reduce_u128(acc, pc[__ldg(a.pid[j] + t)]);
             }
+        }
+    }
+}
+
+// ModUp conversion with the quotient on the FP64 pipe and the remainder in
+// wrapping 64-bit integers (see k_moddown_conv_f64), for every target q_t < 2^62:
+//   S = sum_i y_i m_it (mod 2^64),  T = sum_i y_i (m_it / q_t),  r = S - round(T) q_t.
+// Sources under primes < 2^41 enter whole (|term| < 2^41, T error < 2^-4 over 16
+// terms); a wider source (q_0 in digit 0: WIDE0) enters as y = yh 2^32 + yl with
+// m' = m 2^32 mod q_t.  |S - round(T) q_t| < q_t < 2^63, so the wrapped difference
+// is the exact signed remainder whatever the target's size.
+template <int GS, bool WIDE0>
+__global__ void __launch_bounds__(256, 3) k_modup_f64(const __grid_constant__ ModUpArgs a,
+                                                   const PrimeConst *__restrict__ pc, int log_n) {
+    __shared__ double2 s_f[SRK_MODUP_TCH][GS];
+    __shared__ ulonglong2 s_m[SRK_MODUP_TCH][GS];
+    __shared__ uint64_t s_q[SRK_MODUP_TCH];
+    __shared__ int s_slot[SRK_MODUP_TCH];
+    const long long n = 1ll << log_n;
+    const int b = blockIdx.y / a.beta, j = blockIdx.y - b * a.beta;
+    const int g0 = j * a.alpha, gs = min(a.alpha, a.nl - g0);
+    const int t0 = blockIdx.z * SRK_MODUP_TCH;
+    const int nd = a.n_dst[j];
+    if (t0 >= nd) return;
+    const int nt = min(nd - t0, SRK_MODUP_TCH);
+    for (int i = threadIdx.x; i < nt * GS; i += blockDim.x) {
+        const int tt = i / GS, k = i - tt * GS;
+        if (k < gs) {
+            s_f[tt][k] = __ldg(a.fhl[j] + k * nd + t0 + tt);
+            s_m[tt][k] = __ldg(a.mhl[j] + k * nd + t0 + tt);
+        }
+    }
+    if (threadIdx.x < nt) {
+        s_q[threadIdx.x] = pc[__ldg(a.pid[j] + t0 + threadIdx.x)].q;
+        s_slot[threadIdx.x] = __ldg(a.slot[j] + t0 + threadIdx.x);
+    }
+    __syncthreads();
+    const uint64_t *src = a.dc + b * a.dc_ct + (long long)g0 * n;
+    uint64_t *dst = a.ext + b * a.ext_ct + j * a.ext_dig;
+    const bool wide = WIDE0 && j == 0;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
+         x += (long long)gridDim.x * blockDim.x) {
+        uint64_t y[GS];
+        double dy[GS];
+#pragma unroll
+        for (int i = 0; i < GS; i++) {
+            y[i] = i < gs ? src[(long long)i * n + x] : 0;
+            dy[i] = __longlong_as_double((long long)(y[i] | 0x4330000000000000ull)) - SRK_F64_TWO52;
+        }
+        // wide source 0: halves (dy[0] above is only used when !wide)
+        const uint32_t yl0 = (uint32_t)y[0], yh0 = (uint32_t)(y[0] >> 32);
+        const double dl0 = __hiloint2double(0x43300000, (int)yl0) - SRK_F64_TWO52;
+        const double dh0 = __hiloint2double(0x43300000, (int)yh0) - SRK_F64_TWO52;
+#pragma unroll
+        for (int tt = 0; tt < SRK_MODUP_TCH; tt++) {
+            if (tt >= nt) break;
+            const uint64_t q = s_q[tt];
+            // two FMA chains (latency), one wrapping integer sum
+            double T0 = 0.0, T1 = 0.0;
+            uint64_t S = 0;
+#pragma unroll
+            for (int i = 0; i < GS; i++) {
+                if (i < gs) {
+                    const double2 f = s_f[tt][i];
+                    const ulonglong2 m = s_m[tt][i];
+                    if (i == 0 && wide) {
+                        T0 = fma(dl0, f.x, T0);
+                        T1 = fma(dh0, f.y, T1);
+                        S += (uint64_t)yl0 * m.x;
+                        S += (uint64_t)yh0 * m.y;
+                    } else if (i & 1) {
+                        T1 = fma(dy[i], f.x, T1);
+                        S += y[i] * m.x;
+                    } else {
+                        T0 = fma(dy[i], f.x, T0);
+                        S += y[i] * m.x;
+                    }
+                }
+            }
+            const long long tq = __double_as_longlong((T0 + T1) + SRK_F64_MAGIC) - 0x4338000000000000ll;
+            const long long rr = (long long)(S - (uint64_t)tq * q);
+            dst[(long long)s_slot[tt] * n + x] = (uint64_t)(rr < 0 ? rr + (long long)q : rr);
         }
     }
 }
@@ -381,7 +466,7 @@ __global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict
 }
 
 // ModDown conversion P -> Q with the FP64 and integer pipes splitting the work
-// (targets q_t < 2^41; the rest take the Shoup path of k_moddown_conv):
+// (any target q_t < 2^62: only |S' - t q_t| < q_t < 2^63 is needed):
 //   z_k = zh_k 2^32 + zl_k,   S' = sum_k zh_k m'_kt + zl_k m_kt  == sum_k z_k m_kt (mod q_t)
 // with m' = m 2^32 mod q_t.  The quotient t = round(S'/q_t) comes from the FP64
 // pipe, T = sum_k zh_k (m'/q) + zl_k (m/q) (every term < 2^32, total rounding
@@ -390,8 +475,12 @@ __global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict
 // because |r| < q_t.  Per target: 2K FP64 FMAs + 2K 32x64-bit IMAD products
 // instead of K 64-bit Shoup products (~13 IMAD each).
 #define SRK_CONV_TG 8  // targets per CTA (blockIdx.z groups)
+#ifndef SRK_CONV_UNROLL
+#define SRK_CONV_UNROLL 4
+#endif
+constexpr int kConvUnroll = SRK_CONV_UNROLL;
 template <int MAXK, bool EXACT>
-__global__ void __launch_bounds__(256) k_moddown_conv_f64(
+__global__ void __launch_bounds__(256, 4) k_moddown_conv_f64(
     const uint64_t *__restrict__ z, long long z_ct, long long z_ps, int n_src,
     const uint8_t *__restrict__ vround, const ulonglong2 *__restrict__ mat2,
     const ulonglong2 *__restrict__ mhl, const double2 *__restrict__ fhl, int n_dst,
@@ -435,39 +524,25 @@ __global__ void __launch_bounds__(256) k_moddown_conv_f64(
         }
         const int v = vround[(long long)p * n + x];
         uint64_t *out = conv + b * c_ct + r * c_ps + (long long)t0 * n + x;
-#pragma unroll
+#pragma unroll(kConvUnroll)  // (fully unrolled, the compiler hoists every target's constants: 250 registers)
         for (int tt = 0; tt < SRK_CONV_TG; tt++) {
             if (tt >= nt) break;
             const uint64_t q = s_q[tt];
-            uint64_t acc;
-            if (q < SRK_F64_Q) {
-                double T = 0.0;
-                uint64_t S = 0;
+            double T0 = 0.0, T1 = 0.0;
+            uint64_t S = 0;
 #pragma unroll
-                for (int k = 0; k < MAXK; k++)
-                    if (EXACT || k < n_src) {
-                        const double2 f = s_f[tt][k];     // {m/q, m'/q}
-                        const ulonglong2 m = s_m[tt][k];  // {m, m'}
-                        T = fma(dl[k], f.x, T);
-                        T = fma(dh[k], f.y, T);
-                        S += (uint64_t)zl[k] * m.x;
-                        S += (uint64_t)zh[k] * m.y;
-                    }
-                const long long tq = __double_as_longlong(T + SRK_F64_MAGIC) - 0x4338000000000000ll;
-                const long long rr = (long long)(S - (uint64_t)tq * q);
-                acc = (uint64_t)(rr < 0 ? rr + (long long)q : rr);
-            } else {  // 60-bit target (q_0): Shoup products
-                const uint64_t two_q = 2 * q;
-                acc = 0;
-#pragma unroll
-                for (int k = 0; k < MAXK; k++)
-                    if (EXACT || k < n_src) {
-                        const ulonglong2 mw = __ldg(mat2 + k * n_dst + t0 + tt);
-                        acc += mul_shoup_lazy(zz[k], mw.x, mw.y, q);
-                        acc = acc >= two_q ? acc - two_q : acc;
-                    }
-                acc = acc >= q ? acc - q : acc;
-            }
+            for (int k = 0; k < MAXK; k++)
+                if (EXACT || k < n_src) {
+                    const double2 f = s_f[tt][k];     // {m/q, m'/q}
+                    const ulonglong2 m = s_m[tt][k];  // {m, m'}
+                    T0 = fma(dl[k], f.x, T0);
+                    T1 = fma(dh[k], f.y, T1);
+                    S += (uint64_t)zl[k] * m.x;
+                    S += (uint64_t)zh[k] * m.y;
+                }
+            const long long tq = __double_as_longlong((T0 + T1) + SRK_F64_MAGIC) - 0x4338000000000000ll;
+            const long long rr = (long long)(S - (uint64_t)tq * q);
+            const uint64_t acc = (uint64_t)(rr < 0 ? rr + (long long)q : rr);
             *out = sub_mod(acc, s_corr[v][tt], q);
             out += n;
         }
