@@ -1040,7 +1040,11 @@ static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int n
         case 3: SRK_CONV_LAUNCH(3, true); break;
         case 4: SRK_CONV_LAUNCH(4, true); break;
         default:
-            if (g.n_src <= 8) {
+            if (c->conv_f64 && g.mhl && g.n_src <= 16) {
+                k_moddown_conv_f64_wide<<<dim3(std::max(1u, grid.x / c->conv_cpt), grid.y, grid.z), 256, 0, s>>>(
+                    z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mhl, g.fhl, g.mat_ld, g.corr, bq.ptr,
+                    bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
+            } else if (g.n_src <= 8) {
                 SRK_CONV_LAUNCH(8, false);
             } else {
                 SRK_CONV_LAUNCH(16, false);

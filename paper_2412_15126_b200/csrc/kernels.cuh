@@ -549,6 +549,70 @@ __global__ void __launch_bounds__(256, 4) k_moddown_conv_f64(
     }
 }
 
+// The same conversion for many special primes (the long chain's K = 11..16):
+// sources outer, the CTA's 8 targets inner, so the per-source values live in
+// registers one at a time and only the 8 (T, S) accumulators persist.
+__global__ void __launch_bounds__(256, 3) k_moddown_conv_f64_wide(
+    const uint64_t *__restrict__ z, long long z_ct, long long z_ps, int n_src,
+    const uint8_t *__restrict__ vround, const ulonglong2 *__restrict__ mhl,
+    const double2 *__restrict__ fhl, int n_dst, const uint64_t *__restrict__ corr,
+    uint64_t *__restrict__ conv, long long c_ct, long long c_ps, const PrimeConst *__restrict__ pc,
+    int log_n) {
+    __shared__ double2 s_f[16][SRK_CONV_TG];
+    __shared__ ulonglong2 s_m[16][SRK_CONV_TG];
+    __shared__ uint64_t s_q[SRK_CONV_TG], s_corr[17][SRK_CONV_TG];
+    const long long n = 1ll << log_n;
+    const int p = blockIdx.y;  // (b, r)
+    const int b = p >> 1, r = p & 1;
+    const int t0 = blockIdx.z * SRK_CONV_TG, nt = min(n_dst - t0, SRK_CONV_TG);
+    for (int i = threadIdx.x; i < n_src * SRK_CONV_TG; i += blockDim.x) {
+        const int k = i / SRK_CONV_TG, tt = i - k * SRK_CONV_TG;
+        s_f[k][tt] = tt < nt ? __ldg(fhl + k * n_dst + t0 + tt) : make_double2(0.0, 0.0);
+        s_m[k][tt] = tt < nt ? __ldg(mhl + k * n_dst + t0 + tt) : make_ulonglong2(0, 0);
+    }
+    for (int i = threadIdx.x; i < (n_src + 1) * SRK_CONV_TG; i += blockDim.x) {
+        const int v = i / SRK_CONV_TG, tt = i - v * SRK_CONV_TG;
+        s_corr[v][tt] = tt < nt ? __ldg(corr + v * n_dst + t0 + tt) : 0;
+    }
+    if (threadIdx.x < SRK_CONV_TG) s_q[threadIdx.x] = threadIdx.x < nt ? pc[t0 + threadIdx.x].q : 1;
+    __syncthreads();
+    const uint64_t *zp = z + b * z_ct + r * z_ps;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
+         x += (long long)gridDim.x * blockDim.x) {
+        double T[SRK_CONV_TG];
+        uint64_t S[SRK_CONV_TG];
+#pragma unroll
+        for (int tt = 0; tt < SRK_CONV_TG; tt++) {
+            T[tt] = 0.0;
+            S[tt] = 0;
+        }
+        for (int k = 0; k < n_src; k++) {
+            const uint64_t zz = zp[k * n + x];
+            const uint32_t zl = (uint32_t)zz, zh = (uint32_t)(zz >> 32);
+            const double dl = __hiloint2double(0x43300000, (int)zl) - SRK_F64_TWO52;
+            const double dh = __hiloint2double(0x43300000, (int)zh) - SRK_F64_TWO52;
+#pragma unroll
+            for (int tt = 0; tt < SRK_CONV_TG; tt++) {
+                const double2 f = s_f[k][tt];
+                const ulonglong2 m = s_m[k][tt];
+                T[tt] = fma(dh, f.y, fma(dl, f.x, T[tt]));
+                S[tt] += (uint64_t)zl * m.x + (uint64_t)zh * m.y;
+            }
+        }
+        const int v = vround[(long long)p * n + x];
+        uint64_t *out = conv + b * c_ct + r * c_ps + (long long)t0 * n + x;
+#pragma unroll
+        for (int tt = 0; tt < SRK_CONV_TG; tt++) {
+            if (tt >= nt) break;
+            const uint64_t q = s_q[tt];
+            const long long tq = __double_as_longlong(T[tt] + SRK_F64_MAGIC) - 0x4338000000000000ll;
+            const long long rr = (long long)(S[tt] - (uint64_t)tq * q);
+            const uint64_t acc = (uint64_t)(rr < 0 ? rr + (long long)q : rr);
+            out[(long long)tt * n] = sub_mod(acc, s_corr[v][tt], q);
+        }
+    }
+}
+
 struct CombineArgs {
     const uint64_t *conv;
     long long conv_ct, conv_ps;
