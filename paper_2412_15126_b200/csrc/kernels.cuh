@@ -18,9 +18,11 @@
 __global__ void k_addsub(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
                          uint64_t *__restrict__ out, const PrimeConst *__restrict__ pc, int log_n,
                          int nl, int op, long long total) {
+    const Div32 dv = mk_div32(nl);
     for (long long x = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; x < total;
          x += (long long)gridDim.x * blockDim.x * 2) {
-        const int limb = (int)((x >> log_n) % nl);
+        const uint32_t row = (uint32_t)(x >> log_n);
+        const int limb = (int)(row - div32(row, dv) * nl);
         const uint64_t q = pc[limb].q;
         ulonglong2 va = *reinterpret_cast<const ulonglong2 *>(a + x);
         ulonglong2 r;
@@ -49,9 +51,10 @@ __global__ void k_add_plain(const uint64_t *__restrict__ a, const uint64_t *__re
     const long long n = 1ll << log_n;
     const long long per = 2ll * nl * n;
     const long long total = per * batch;
+    const Div32 dv = mk_div32(2 * nl);
     for (long long x = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; x < total;
          x += (long long)gridDim.x * blockDim.x * 2) {
-        const long long b = x / per, xi = x - b * per;
+        const long long b = div32((uint32_t)(x >> log_n), dv), xi = x - b * per;
         const long long limb_all = xi >> log_n;
         ulonglong2 va = *reinterpret_cast<const ulonglong2 *>(a + x);
         if (limb_all < nl) {
@@ -76,10 +79,11 @@ __global__ void k_mul_pt(const uint64_t *__restrict__ a, int src_nl,
                          const PrimeConst *__restrict__ pc, int log_n, int nl) {
     const long long n = 1ll << log_n;
     const long long total = 2ll * nl * n;
+    const Div32 dv = mk_div32(nl);
     for (long long x = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; x < total;
          x += (long long)gridDim.x * blockDim.x * 2) {
         const long long la = x >> log_n;
-        const int p = (int)(la / nl), limb = (int)(la - (long long)p * nl);
+        const int p = (int)div32((uint32_t)la, dv), limb = (int)(la - (long long)p * nl);
         const long long off = x & (n - 1);
         const long long src = ((long long)p * src_nl + limb) * n + off;
         ulonglong2 va = *reinterpret_cast<const ulonglong2 *>(a + src);
@@ -142,9 +146,10 @@ __global__ void k_rescale_spread(const uint64_t *__restrict__ top, uint64_t *__r
     const long long per = (long long)level * n;
     const long long total = 2ll * batch * per;
     const uint64_t ql = pc[level].q;
+    const Div32 dv = mk_div32(level);
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
-        const long long p = x / per, xi = x - p * per;
+        const long long p = div32((uint32_t)(x >> log_n), dv), xi = x - p * per;
         const int i = (int)(xi >> log_n);
         const PrimeConst P = pc[i];
         const uint64_t v = top[p * n + (xi & (n - 1))];
@@ -161,9 +166,10 @@ __global__ void k_rescale_combine(const uint64_t *__restrict__ a, long long a_ct
     const long long n = 1ll << log_n;
     const long long per = (long long)level * n;
     const long long total = 2ll * batch * per;
+    const Div32 dv = mk_div32(level);
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
-        const long long p = x / per, xi = x - p * per;
+        const long long p = div32((uint32_t)(x >> log_n), dv), xi = x - p * per;
         const long long b = p >> 1, r = p & 1;
         const int i = (int)(xi >> log_n);
         const long long off = xi & (n - 1);
@@ -368,12 +374,13 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
     const long long n = 1ll << log_n;
     const long long total = (long long)a.ne * n;  // acc poly stride
     const long long work = (long long)(a.ne - a.t0) * n;
+    const Div32 dalpha = mk_div32(a.alpha);
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < work;
          x += (long long)gridDim.x * blockDim.x) {
         const int t = a.t0 + (int)(x >> log_n);
         const long long off = x & (n - 1);
         const int pid = t <= a.level ? t : t + (a.L - a.level);
-        const int jt = t < a.nl ? t / a.alpha : -1;
+        const int jt = t < a.nl ? (int)div32((uint32_t)t, dalpha) : -1;
         uint64_t k0[MAXD], k1[MAXD];
 #pragma unroll
         for (int j = 0; j < MAXD; j++) {
@@ -632,9 +639,10 @@ __global__ void k_moddown_combine(const __grid_constant__ CombineArgs a, const P
     const long long n = 1ll << log_n;
     const long long per = (long long)a.nl * n;
     const long long total = 2ll * a.batch * per;
+    const Div32 dv = mk_div32(a.nl);
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
-        const long long p = x / per, xi = x - p * per;
+        const long long p = div32((uint32_t)(x >> log_n), dv), xi = x - p * per;
         const long long b = p >> 1, r = p & 1;
         const int i = (int)(xi >> log_n);
         const long long m = xi & (n - 1);
@@ -694,12 +702,13 @@ __global__ void __launch_bounds__(256, F64 ? SRK_KSC_F64_MINB : SRK_KSC_MINB)
     k_ks_combine(const __grid_constant__ KsCombineArgs a, const PrimeConst *__restrict__ pc, int log_n) {
     const long long n = 1ll << log_n;
     const long long work = (long long)(a.t1 - a.t0) * n;
+    const Div32 dalpha = mk_div32(a.alpha);
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < work;
          x += (long long)gridDim.x * blockDim.x) {
         const int t = a.t0 + (int)(x >> log_n);
         const long long m = x & (n - 1);
         const long long src = a.galois == 1 ? m : (long long)auto_index((uint32_t)m, a.galois, log_n);
-        const int jt = t / a.alpha;
+        const int jt = (int)div32((uint32_t)t, dalpha);
         uint64_t k0[MAXD], k1[MAXD];
 #pragma unroll
         for (int j = 0; j < MAXD; j++) {
@@ -942,9 +951,12 @@ __global__ void k_center_limb0(const uint64_t *__restrict__ t, int64_t *__restri
 // cross-rank modular sum fix-up: limbs hold plain int64 sums (< 2^63)
 __global__ void k_reduce_mod(uint64_t *__restrict__ a, const PrimeConst *__restrict__ pc,
                              int log_n, int nl, long long total) {
+    const Div32 dv = mk_div32(nl);
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
-         x += (long long)gridDim.x * blockDim.x)
-        a[x] = reduce64(a[x], pc[(x >> log_n) % nl]);
+         x += (long long)gridDim.x * blockDim.x) {
+        const uint32_t row = (uint32_t)(x >> log_n);
+        a[x] = reduce64(a[x], pc[row - div32(row, dv) * nl]);
+    }
 }
 
 // special limbs of X = acc + P d for the fused HMult rescale:
@@ -959,9 +971,10 @@ __global__ void k_prep_special(const uint64_t *__restrict__ acc, long long acc_c
     const long long per = (long long)(K + 1) * n;
     const long long total = 2ll * batch * per;
     const uint64_t ql = pc[level].q;
+    const Div32 dv = mk_div32(K + 1);
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
-        const long long p = x / per, xi = x - p * per;
+        const long long p = div32((uint32_t)(x >> log_n), dv), xi = x - p * per;
         const int k = (int)(xi >> log_n);
         const long long off = xi & (n - 1);
         const long long b = p >> 1, r = p & 1;
@@ -996,11 +1009,12 @@ __global__ void k_lincomb(const __grid_constant__ LinCombArgs a, const PrimeCons
     const long long n = 1ll << log_n;
     const long long per = 2ll * a.nl * n;
     const long long total = per * a.batch;
+    const Div32 d2 = mk_div32(2 * a.nl), d1 = mk_div32(a.nl);
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
-        const long long b = x / per, xi = x - b * per;
+        const long long b = div32((uint32_t)(x >> log_n), d2), xi = x - b * per;
         const long long lr = xi >> log_n;
-        const int r = (int)(lr / a.nl), j = (int)(lr - (long long)r * a.nl);
+        const int r = (int)div32((uint32_t)lr, d1), j = (int)(lr - (long long)r * a.nl);
         const long long off = xi & (n - 1);
         U128 acc = {0, 0};
         for (int i = 0; i < a.n_terms; i++) {

@@ -104,3 +104,14 @@ SRK_HD uint64_t reduce64(uint64_t x, const PrimeConst &p) {
     v.lo = x;
     return reduce128(v, p.ratio_hi, p.ratio_lo, p.q);
 }
+
+// Division of small row indices by a runtime divisor without the 64-bit
+// division subroutine: q = (r * m) >> 32 with m = floor(2^32 / d) + 1 is exact
+// for r * d < 2^32 (row counts here are < 2^16, divisors < 2^8).
+struct Div32 {
+    uint64_t m;
+};
+// (floor((2^32 - 1) / d) + 1 == floor(2^32 / d) + 1, or 2^32 / d for d a power of
+// two, which is exact too; a 32-bit division, once per thread)
+SRK_HD Div32 mk_div32(uint32_t d) { return Div32{(uint64_t)(0xFFFFFFFFu / d) + 1}; }
+SRK_HD uint32_t div32(uint32_t r, Div32 d) { return (uint32_t)(((uint64_t)r * d.m) >> 32); }
