@@ -131,7 +131,7 @@ struct srk_ctx {
     // extra loads in them cost more than the streams; profiles/r01), 1 = both
     // fused into the NTT, 2 = conversion separate, combine fused into the store
     int moddown_mode = 0;
-    int rescale_fused = 0;            // same trade-off for the rescale (SRK_RESCALE_FUSED=1)
+    int rescale_fused = 1;            // spread + combine fused into the rescale NTT (SRK_RESCALE_FUSED=0: streaming kernels)
     int ks_fused = 1;                 // Q-limb inner product fused into the combine (SRK_KS_FUSED=0: off)
     int ks_streams = 2;               // hoisted outputs alternate over two streams (SRK_KS_STREAMS)
     cudaStream_t side = nullptr;      // the second lane
@@ -573,9 +573,11 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
     bb.n_limbs = nlc;
     dim3 grid(subs / cb, b.n_polys, nlc);
     bool done = false;
-    if constexpr (IO == 0 || IO == 3) {  // plain / automorphism loads, plain / scaled stores:
-        // FP64-only kernel for q < 2^41 chunks, Harvey-only integer kernel otherwise
-        if (f64)
+    // plain / automorphism / rescale-spread loads, plain / scaled / rescale stores:
+    // FP64-only kernel for q < 2^41 chunks, Harvey-only integer kernel otherwise
+    // (the FP64 spread needs the dropped prime < 2^41 too)
+    if constexpr (IO == 0 || IO == 3 || IO == 2) {
+        if (f64 && (IO != 2 || f.top_q < SRK_F64_Q))
             launch_kernel<LOG_T, INV, COL, IO, 1>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
         else
             launch_kernel<LOG_T, INV, COL, IO, 2>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);

@@ -503,6 +503,9 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
 #ifndef SRK_NTT_MINB_F64
 #define SRK_NTT_MINB_F64 4
 #endif
+#ifndef SRK_ROW_DIRECT
+#define SRK_ROW_DIRECT 0
+#endif
 #ifndef SRK_NTT_MINB_INT
 #define SRK_NTT_MINB_INT 3
 #endif
@@ -583,6 +586,14 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
     const F64Q fq = {__longlong_as_double((long long)pc.qd_bits), __longlong_as_double((long long)pc.qinv_bits)};
     // first-pass loads are canonical u64; FP64 limbs convert on load
     auto load_m = [&](int c) -> uint64_t {
+        if constexpr (FIRST && LD == LD_SPREAD && KM == 1) {
+            // rescale spread on the FP64 path: the centred top-limb value is already a
+            // valid FP64-mode operand for every target prime (|v| < 2^61 would not be:
+            // the top prime is a scaling prime < 2^41 whenever this kernel runs)
+            const long long v = (long long)f.src[bi * f.src_ct + r * f.src_ps + gaddr(c)];
+            const long long vc = v > (long long)(f.top_q >> 1) ? v - (long long)f.top_q : v;
+            return (uint64_t)__double_as_longlong((double)vc);
+        }
         const uint64_t v = load(c);
         return mode == 2 ? (uint64_t)__double_as_longlong(f64_of_u64(v)) : v;
     };
@@ -613,7 +624,29 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
 #pragma unroll
             for (int e = 0; e < E; e++) data[gaddr(u * E + e)] = x[e];  // lazy / FP64 bits
         } else {
-            // final pass: canonical values, staged through smem for coalescing
+            // final pass, plain store: each thread owns 16 contiguous outputs;
+            // 16-byte vector stores straight from registers (SRK_ROW_DIRECT) or
+            // a shared-memory transpose for fully coalesced 8-byte stores
+#if SRK_ROW_DIRECT
+            if constexpr (ST == ST_PLAIN && KM != 0) {
+                uint64_t *o = data + (long long)sub * T + u * E;
+#pragma unroll
+                for (int e = 0; e < E; e += 2) {
+                    uint64_t v0 = x[e], v1 = x[e + 1];
+                    if (mode == 2) {
+                        v0 = canon_u64_of_f64(__longlong_as_double((long long)v0), fq.q, fq.qinv);
+                        v1 = canon_u64_of_f64(__longlong_as_double((long long)v1), fq.q, fq.qinv);
+                    } else {
+                        v0 = v0 >= two_q ? v0 - two_q : v0;
+                        v0 = v0 >= q ? v0 - q : v0;
+                        v1 = v1 >= two_q ? v1 - two_q : v1;
+                        v1 = v1 >= q ? v1 - q : v1;
+                    }
+                    *reinterpret_cast<ulonglong2 *>(o + e) = make_ulonglong2(v0, v1);
+                }
+                return;
+            }
+#endif
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < E; e++) {
