@@ -219,10 +219,21 @@ class PipelinedE2E:
         self.host_out = torch.empty(step.res.shape, dtype=torch.int64, pin_memory=True)
         self.dev_x = torch.empty_like(step.x)
         self.h2d, self.d2h = torch.cuda.Stream(), torch.cuda.Stream()
-        self.ev_in = [torch.cuda.Event() for _ in range(chunks)]
-        self.ev_done = [torch.cuda.Event() for _ in range(chunks)]
+        # half-size first and last chunks: the first H2D and the last D2H are the
+        # only copies with no compute to hide under
         per = -(-step.n_ct // chunks)
-        self.bounds = [(lo, min(per, step.n_ct - lo)) for lo in range(0, step.n_ct, per)]
+        sizes = [max(1, per // 2)]
+        while sum(sizes) < step.n_ct:
+            sizes.append(min(per, step.n_ct - sum(sizes)))
+        if len(sizes) > 2 and sizes[-1] == per:
+            sizes[-1] = per - sizes[0]
+            sizes.append(sizes[0])
+        self.bounds, lo = [], 0
+        for sz in (z for z in sizes if z > 0):
+            self.bounds.append((lo, sz))
+            lo += sz
+        self.ev_in = [torch.cuda.Event() for _ in self.bounds]
+        self.ev_done = [torch.cuda.Event() for _ in self.bounds]
 
     def __call__(self):
         torch = self.torch
