@@ -15,6 +15,7 @@
 
 #include "../../include/slotrank_b200.h"
 #include "kernels.cuh"
+#include "ntt_cluster.cuh"
 #include "modarith.cuh"
 #include "ntt.cuh"
 
@@ -140,6 +141,7 @@ struct srk_ctx {
     // caller's stream and nside[lane], so one chunk's pass tail overlaps the
     // next chunk's passes (lane = 1 when called from the key-switch side lane)
     int ntt_streams = 2;
+    int ntt_cluster = 0;  // 1: forward FP64 plain NTTs as one 8-CTA cluster per limb (slower: DESIGN.md)
     int conv_f64 = 1;  // ModDown conversion on the FP64 + integer pipes (k_moddown_conv_f64)
     unsigned conv_cpt = 4;  // coefficients per thread of k_moddown_conv_f64 (amortises its staging)
     cudaStream_t nside[2] = {nullptr, nullptr};
@@ -276,6 +278,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     if (const char *e = getenv("SRK_KS_FUSED")) c->ks_fused = atoi(e);
     if (const char *e = getenv("SRK_KS_STREAMS")) c->ks_streams = atoi(e);
     if (const char *e = getenv("SRK_NTT_STREAMS")) c->ntt_streams = atoi(e);
+    if (const char *e = getenv("SRK_NTT_CLUSTER")) c->ntt_cluster = atoi(e);
     if (const char *e = getenv("SRK_CONV_F64")) c->conv_f64 = atoi(e);
     if (const char *e = getenv("SRK_CONV_CPT")) c->conv_cpt = std::max(1, atoi(e));
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
@@ -588,6 +591,31 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
     return SRK_OK;
 }
 
+// forward plain NTT of a chunk of FP64 limbs (ring 2^16): one 8-CTA cluster per
+// limb, column -> row exchange in distributed shared memory (ntt_cluster.cuh)
+static int launch_cluster_fwd(const srk_ctx *c, LimbBatch b, int l0, int nlc, const FuseArgs &f,
+                              cudaStream_t s) {
+    static bool attr_set = false;
+    const size_t smem = (size_t)SRK_CL_SMEM_WORDS * 8;
+    if (!attr_set) {
+        CU(cudaFuncSetAttribute(ntt_fwd_cluster_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    LimbBatch bb = b;
+    FuseArgs ff = f;
+    if (l0) {
+        bb.ptr = b.ptr + (long long)l0 * c->n;
+        bb.split = b.split - l0;
+        bb.off_a = b.off_a + l0;
+        bb.off_b = b.off_b + l0;
+        if (ff.src) ff.src += (long long)l0 * c->n;
+    }
+    bb.n_limbs = nlc;
+    ntt_fwd_cluster_f64<<<dim3(SRK_CL_CTAS, b.n_polys, nlc), SRK_CL_THREADS, smem, s>>>(bb, tables(c), ff);
+    LAUNCHED();
+    return SRK_OK;
+}
+
 template <bool INV, bool COL, int IO>
 static int pass_t(const srk_ctx *c, int log_t, LimbBatch b, int l0, int nlc, const FuseArgs &f,
                   cudaStream_t s, bool f64) {
@@ -655,6 +683,10 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
         const bool f64 = chunks[ci].f64;
         b.cls = chunks[ci].cls;
         cudaStream_t cs = (two && (ci & 1)) ? c->nside[lane] : s;
+        if (!inverse && ld == LD_PLAIN && st == ST_PLAIN && f64 && c->log_n == 16 && c->ntt_cluster) {
+            TRY(launch_cluster_fwd(c, b, l0, nlc, f, cs));
+            continue;
+        }
         if (!inverse) {
             switch (ld) {
                 case LD_PLAIN: TRY((pass_t<false, true, LD_PLAIN>(c, log_r, b, l0, nlc, f, cs, f64))); break;
