@@ -457,7 +457,9 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     return SRK_OK;
 }
 
-#define SRK_WS_BATCH 8  // ciphertexts per internal chunk of a batched call
+#ifndef SRK_WS_BATCH
+#define SRK_WS_BATCH 32  // ciphertexts per internal chunk of a batched call (keys read once per chunk)
+#endif
 
 // words of scratch (x N) each op needs for a chunk of B ciphertexts at level l
 static size_t ks_limbs(const srk_ctx *c, int level, int B) {
