@@ -472,7 +472,7 @@ def gpu_arm(args):
     ks_ms = time_region(torch, step.relin_batch, 3)
 
     # e2e: host pinned inputs -> device, step, results -> host (chunk-pipelined)
-    e2e_step = PipelinedE2E(torch, step, chunks=int(os.environ.get("SRK_E2E_CHUNKS", "8")))
+    e2e_step = PipelinedE2E(torch, step, chunks=int(os.environ.get("SRK_E2E_CHUNKS", "6")))
     step.step()
     ref_res = step.res.cpu()  # the unchunked step's results
     e2e_step()
