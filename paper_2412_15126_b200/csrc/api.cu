@@ -141,6 +141,7 @@ struct srk_ctx {
     // caller's stream and nside[lane], so one chunk's pass tail overlaps the
     // next chunk's passes (lane = 1 when called from the key-switch side lane)
     int ntt_streams = 2;
+    int ntt_cta_threads = 128;  // threads per NTT pass CTA (SRK_NTT_CTA; 128: 8 CTAs/SM, cheaper barriers)
     int ntt_cluster = 0;  // 1: forward FP64 plain NTTs as one 8-CTA cluster per limb (slower: DESIGN.md)
     int conv_f64 = 1;  // ModDown conversion on the FP64 + integer pipes (k_moddown_conv_f64)
     unsigned conv_cpt = 4;  // coefficients per thread of k_moddown_conv_f64 (amortises its staging)
@@ -278,6 +279,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     if (const char *e = getenv("SRK_KS_FUSED")) c->ks_fused = atoi(e);
     if (const char *e = getenv("SRK_KS_STREAMS")) c->ks_streams = atoi(e);
     if (const char *e = getenv("SRK_NTT_STREAMS")) c->ntt_streams = atoi(e);
+    if (const char *e = getenv("SRK_NTT_CTA")) c->ntt_cta_threads = std::min(256, std::max(64, atoi(e)));
     if (const char *e = getenv("SRK_NTT_CLUSTER")) c->ntt_cluster = atoi(e);
     if (const char *e = getenv("SRK_CONV_F64")) c->conv_f64 = atoi(e);
     if (const char *e = getenv("SRK_CONV_CPT")) c->conv_cpt = std::max(1, atoi(e));
@@ -542,7 +544,7 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
                        cudaStream_t s, bool f64) {
     using SH = NttShape<LOG_T>;
     const int subs = c->n >> LOG_T;  // sub-transforms per limb
-    int cb = 256 / SH::TPS;
+    int cb = c->ntt_cta_threads / SH::TPS;
     if (cb > subs) cb = subs;
     // small batches (single-ciphertext ops): narrower tiles so the grid covers
     // several waves of the 148 SMs instead of ~1 wave plus a long tail

@@ -144,6 +144,17 @@ class CKKSEngineCore:
         self._pt_bytes = 0
         backend.set_secret(sample_secret(params))
 
+    def use_secret(self, secret: np.ndarray) -> None:
+        """Switch to another ternary secret (e.g. one read by ``wire.load_secret``):
+        evaluation keys are regenerated from it on first use."""
+        s = np.asarray(secret, dtype=np.int64)
+        if s.shape != (self.params.ring_degree,) or np.any(np.abs(s) > 1):
+            raise ValueError("secret must be a ternary vector of ring-degree length")
+        self.backend.set_secret(s)
+        keys = getattr(self.backend, "_keys", None)
+        if keys is not None:
+            keys.clear()
+
     # ------------------------------------------------------------------
     # counters
     # ------------------------------------------------------------------
