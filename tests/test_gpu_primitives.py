@@ -335,3 +335,42 @@ def test_keyswitch_fused_combine_paths(name, fused, require_cuda, monkeypatch):
     got = host(gb, out).reshape(B, 2, lvl + 1, n)
     for i in range(B):
         assert np.array_equal(got[i], orc.mul_relin(a[i], b[i], key, lvl)), i
+
+
+@pytest.mark.parametrize("env", [
+    {"SRK_NTT_CLUSTER": "1"},                        # 8-CTA cluster forward NTT (DSMEM exchange)
+    {"SRK_CONV_F64": "0"},                           # Shoup / 128-bit MAC conversions
+    {"SRK_NTT_STREAMS": "1", "SRK_NTT_CTA": "256"},  # one stream, 256-thread pass CTAs
+    {"SRK_RESCALE_FUSED": "0", "SRK_NTT_SPLIT": "0"},  # streaming rescale, mixed-mode passes
+])
+def test_kernel_switches_ring16(env, require_cuda, monkeypatch):
+    """Every alternative kernel path at ring 2^16 (config 2) gives the oracle's limbs."""
+    from oracle.oracle import OracleCKKS
+    from paper_2412_15126_b200.backend_cuda import CudaBackend
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    p = preset("cfg2")
+    gb, orc = CudaBackend(p), OracleCKKS(p)
+    B, lvl, n = 2, p.max_level, p.ring_degree
+    ps = (lvl + 1) * n
+    a = rand_limbs(p, (B, 2), lvl, 70)
+    t = dev(gb, a)
+    call(gb, "srk_ntt", ptr(t), 2 * B, ps, lvl + 1, 0, 0, gb.stream())
+    fwd = host(gb, t).reshape(B, 2, lvl + 1, n)
+    assert np.array_equal(fwd[1, 1], orc.ntt(a[1, 1], range(lvl + 1))), "forward NTT"
+    call(gb, "srk_ntt", ptr(t), 2 * B, ps, lvl + 1, 0, 1, gb.stream())
+    assert np.array_equal(host(gb, t), a), "inverse NTT"
+    key = _key(p, 71)
+    g = pow(5, 9, 2 * n)
+    ta, tr = dev(gb, a), rot_layout(gb, key, g)
+    out = gb.empty_ct(lvl, polys=2 * B)
+    call(gb, "srk_rotate_batch", ptr(ta), 2 * ps, ptr(tr), ptr(out), 2 * ps, B, lvl, g,
+         gb.workspace(), gb.stream())
+    got = host(gb, out).reshape(B, 2, lvl + 1, n)
+    assert np.array_equal(got[B - 1], orc.rotate_raw(a[B - 1], key, g, lvl)), "rotation"
+    out = gb.empty_ct(lvl - 1, polys=2 * B)
+    call(gb, "srk_rescale_batch", ptr(ta), 2 * ps, ptr(out), 2 * lvl * n, B, lvl, gb.workspace(),
+         gb.stream())
+    got = host(gb, out).reshape(B, 2, lvl, n)
+    assert np.array_equal(got[0], orc.rescale(a[0], lvl)), "rescale"
