@@ -110,6 +110,16 @@ __global__ void k_tensor(const uint64_t *__restrict__ a, const uint64_t *__restr
          x += (long long)gridDim.x * blockDim.x) {
         const PrimeConst P = pc[x >> log_n];
         uint64_t a0 = a[x], a1 = a[ps + x], b0 = b[x], b1 = b[ps + x];
+        if (P.q < SRK_F64_Q) {  // FP64 pipe: exact FMA-split products (ntt.cuh modmul_f64)
+            const double q = __longlong_as_double((long long)P.qd_bits);
+            const double qi = __longlong_as_double((long long)P.qinv_bits);
+            const double fa0 = f64_of_u64(a0), fa1 = f64_of_u64(a1);
+            const double fb0 = f64_of_u64(b0), fb1 = f64_of_u64(b1);
+            d[x] = canon_u64_of_small_f64(modmul_f64(fa0, fb0, q, qi), P.q);
+            d[ps + x] = canon_u64_of_f64(modmul_f64(fa0, fb1, q, qi) + modmul_f64(fa1, fb0, q, qi), q, qi);
+            d[2 * ps + x] = canon_u64_of_small_f64(modmul_f64(fa1, fb1, q, qi), P.q);
+            continue;
+        }
         d[x] = mul_mod(a0, b0, P);
         U128 m = mul_wide(a0, b1);
         mac(m, a1, b0);
