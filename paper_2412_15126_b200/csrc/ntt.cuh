@@ -624,6 +624,29 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
 #pragma unroll
             for (int e = 0; e < E; e++) data[gaddr(u * E + e)] = x[e];  // lazy / FP64 bits
         } else {
+            if constexpr (ST == ST_RESCALE && KM == 1) {
+                // FP64 rescale combine: out = ((acc * pre) - x) * q_l^-1 with the raw
+                // FP64 transform output x (|x| < 17 q, no canonicalisation first)
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; e++) smem[sidx(u * E + e)] = x[e];
+                __syncthreads();
+                const long long nn = 1ll << log_n;
+                const double fm = f64_of_u64(f.mulc.w[limb]);
+                const double fp = f64_of_u64(f.pre.w[limb]);
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const int c = u + TPS * e;
+                    const long long off = (long long)t * nn + (long long)sub * T + c;
+                    double a = f64_of_u64(f.acc[bi * f.acc_ct + r * f.acc_ps + off]);
+                    if (f.pre_mode == 1) a = modmul_f64(a, fp, fq.q, fq.qinv);
+                    if (f.pre_mode == 2) a = modmul_f64(a, f64_of_u64(__ldg(f.pt + bi * f.pt_ct + off)), fq.q, fq.qinv);
+                    const double d = a - __longlong_as_double((long long)smem[sidx(c)]);
+                    f.out[bi * f.out_ct + r * f.out_ps + off] =
+                        canon_u64_of_small_f64(modmul_f64(d, fm, fq.q, fq.qinv), q);
+                }
+                return;
+            }
             // final pass, plain store: each thread owns 16 contiguous outputs;
             // 16-byte vector stores straight from registers (SRK_ROW_DIRECT) or
             // a shared-memory transpose for fully coalesced 8-byte stores
