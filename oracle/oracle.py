@@ -323,6 +323,9 @@ class OracleBackend:
     def index(self, data, i):
         return np.ascontiguousarray(data[i])
 
+    def slice(self, data, a, b):
+        return np.ascontiguousarray(data[a:b])
+
     def stack_plain(self, pts):
         return np.stack(pts)
 

@@ -192,6 +192,9 @@ class CudaBackend:
     def index(self, data, i: int) -> torch.Tensor:
         return data[i]
 
+    def slice(self, data, a: int, b: int) -> torch.Tensor:
+        return data[a:b]  # contiguous view: the C-ABI sees data_ptr() of row a
+
     def stack_plain(self, pts) -> torch.Tensor:
         return torch.stack(pts)
 

@@ -49,12 +49,10 @@ def _three_products(engine, y, u3, u7, site):
     if concat is None:
         return (engine.mul(y, y, site=f"{site}-quad"), engine.mul(u3, y, site=f"{site}-x3"),
                 engine.mul(u7, y, site=f"{site}-x3"))
-    b = y.batch or 1
     prod = engine.mul(concat([y, u3, u7]), concat([y, y, y]), site=f"{site}-quad")
     if y.batch is None:
         return tuple(engine.unstack(prod))
-    singles = engine.unstack(prod)
-    return tuple(engine.stack(singles[i * b:(i + 1) * b]) for i in range(3))
+    return tuple(engine.split(prod, 3))  # views: no copies
 
 
 def odd_poly_eval(engine, x, coeffs, site: str = "composite"):

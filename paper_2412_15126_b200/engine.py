@@ -243,6 +243,17 @@ class CKKSEngineCore:
         return [Ciphertext(self.backend.index(ct.data, i), ct.level, ct.rot_chain, self.params)
                 for i in range(ct.batch)]
 
+    def split(self, ct: Ciphertext, parts: int) -> list:
+        """``parts`` equal consecutive sub-batches of a batched ciphertext, as views
+        of its limbs (no copy); parts of size 1 come back as single ciphertexts."""
+        if ct.batch is None or ct.batch % parts:
+            raise ValueError(f"cannot split a batch of {ct.batch} into {parts} parts")
+        b = ct.batch // parts
+        if b == 1:
+            return self.unstack(ct)
+        return [Ciphertext(self.backend.slice(ct.data, i * b, (i + 1) * b), ct.level, ct.rot_chain,
+                           self.params, b) for i in range(parts)]
+
     def concat(self, cts) -> Ciphertext:
         """One batch from single and/or batched ciphertexts (in order)."""
         singles = []
