@@ -280,8 +280,10 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
 template <int GS, bool WIDE0>
 __global__ void __launch_bounds__(256, 3) k_modup_f64(const __grid_constant__ ModUpArgs a,
                                                    const PrimeConst *__restrict__ pc, int log_n) {
-    __shared__ double2 s_f[SRK_MODUP_TCH][GS];
-    __shared__ ulonglong2 s_m[SRK_MODUP_TCH][GS];
+    // {m, bits(m / q)} per (target, source): one 16-byte broadcast load per term;
+    // the wide source's {m', bits(m' / q)} separately
+    __shared__ ulonglong2 s_mf[SRK_MODUP_TCH][GS];
+    __shared__ ulonglong2 s_w0[SRK_MODUP_TCH];
     __shared__ uint64_t s_q[SRK_MODUP_TCH];
     __shared__ int s_slot[SRK_MODUP_TCH];
     const long long n = 1ll << log_n;
@@ -294,8 +296,10 @@ __global__ void __launch_bounds__(256, 3) k_modup_f64(const __grid_constant__ Mo
     for (int i = threadIdx.x; i < nt * GS; i += blockDim.x) {
         const int tt = i / GS, k = i - tt * GS;
         if (k < gs) {
-            s_f[tt][k] = __ldg(a.fhl[j] + k * nd + t0 + tt);
-            s_m[tt][k] = __ldg(a.mhl[j] + k * nd + t0 + tt);
+            const double2 f = __ldg(a.fhl[j] + k * nd + t0 + tt);
+            const ulonglong2 m = __ldg(a.mhl[j] + k * nd + t0 + tt);
+            s_mf[tt][k] = make_ulonglong2(m.x, (uint64_t)__double_as_longlong(f.x));
+            if (k == 0) s_w0[tt] = make_ulonglong2(m.y, (uint64_t)__double_as_longlong(f.y));
         }
     }
     if (threadIdx.x < nt) {
@@ -329,19 +333,20 @@ __global__ void __launch_bounds__(256, 3) k_modup_f64(const __grid_constant__ Mo
 #pragma unroll
             for (int i = 0; i < GS; i++) {
                 if (i < gs) {
-                    const double2 f = s_f[tt][i];
-                    const ulonglong2 m = s_m[tt][i];
+                    const ulonglong2 mf = s_mf[tt][i];
+                    const double fx = __longlong_as_double((long long)mf.y);
                     if (i == 0 && wide) {
-                        T0 = fma(dl0, f.x, T0);
-                        T1 = fma(dh0, f.y, T1);
-                        S += (uint64_t)yl0 * m.x;
-                        S += (uint64_t)yh0 * m.y;
+                        const ulonglong2 w0 = s_w0[tt];
+                        T0 = fma(dl0, fx, T0);
+                        T1 = fma(dh0, __longlong_as_double((long long)w0.y), T1);
+                        S += (uint64_t)yl0 * mf.x;
+                        S += (uint64_t)yh0 * w0.x;
                     } else if (i & 1) {
-                        T1 = fma(dy[i], f.x, T1);
-                        S += y[i] * m.x;
+                        T1 = fma(dy[i], fx, T1);
+                        S += y[i] * mf.x;
                     } else {
-                        T0 = fma(dy[i], f.x, T0);
-                        S += y[i] * m.x;
+                        T0 = fma(dy[i], fx, T0);
+                        S += y[i] * mf.x;
                     }
                 }
             }
