@@ -67,6 +67,7 @@ class CudaBackend:
         self._ws_bytes = int(self.lib.srk_workspace_bytes(self.ctx))
         self._ws: dict[int, torch.Tensor] = {}
         self._keys: dict[int, torch.Tensor] = {}
+        self._capture_keepalive: list = []  # pinned sources of copies captured in CUDA graphs
         self._key_lock = threading.Lock()
         self.launches = 0
         self._sk_ntt = None
@@ -94,15 +95,28 @@ class CudaBackend:
             self._ws[s] = ws
         return _ptr(ws)
 
+    def release_workspace(self, stream_handle: int) -> None:
+        """Drop the key-switch workspace cached for a stream that is going away."""
+        self._ws.pop(stream_handle, None)
+
     def empty_ct(self, level: int, polys: int = 2) -> torch.Tensor:
         return torch.empty((polys, level + 1, self.n), dtype=torch.int64, device=self.device)
+
+    def _h2d(self, arr: np.ndarray) -> torch.Tensor:
+        """Host array -> device.  Under CUDA-graph capture the source is pinned and
+        kept alive with the backend (the captured copy node re-reads it on replay)."""
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+        if torch.cuda.is_current_stream_capturing():
+            t = t.pin_memory()
+            self._capture_keepalive.append(t)
+            return t.to(self.device, non_blocking=True)
+        return t.to(self.device)
 
     def to_host(self, data: torch.Tensor) -> np.ndarray:
         return data.cpu().numpy().view(np.uint64)
 
     def from_host(self, arr: np.ndarray) -> torch.Tensor:
-        t = torch.from_numpy(np.ascontiguousarray(arr).view(np.int64))
-        return t.to(self.device)
+        return self._h2d(np.ascontiguousarray(arr).view(np.int64))
 
     def _call(self, name: str, *args):
         self.launches += 1
@@ -176,7 +190,7 @@ class CudaBackend:
         return m.cpu().numpy()
 
     def encode_plain(self, coeffs: np.ndarray, level: int) -> torch.Tensor:
-        c = torch.from_numpy(np.ascontiguousarray(coeffs, dtype=np.int64)).to(self.device)
+        c = self._h2d(np.ascontiguousarray(coeffs, dtype=np.int64))
         pt = torch.empty((level + 1, self.n), dtype=torch.int64, device=self.device)
         self._call("srk_encode_plain", _ptr(c), _ptr(pt), level, self.stream())
         return pt
@@ -249,7 +263,7 @@ class CudaBackend:
         n_t = len(terms)
         out = self._out(level, batch)
         k = np.array([[int(r) for r in row] for row in residues], dtype=np.uint64).view(np.int64)
-        k_dev = torch.from_numpy(k).to(self.device, non_blocking=True)
+        k_dev = self._h2d(k)
         ptrs = (ctypes.c_void_p * n_t)(*[_ptr(t) for t in terms])
         limbs = (ctypes.c_int * n_t)(*[lv + 1 for lv in term_levels])
         self._call("srk_lincomb", ptrs, limbs, n_t, _ptr(k_dev), _ptr(out), batch or 1, level,

@@ -143,3 +143,27 @@ def test_chebyshev_sort_matches_reference_simulator(eng12):
     ref = M.read_row(sim, M.sort(sim, sim.encrypt(v), 8, cfg), 8)
     assert np.abs(out - ref).max() < 1e-4
     assert np.abs(out - np.sort(v)).max() < 1e-3
+
+
+@pytest.mark.gpu
+def test_captured_pipeline_replay_new_inputs(require_cuda):
+    """graphs.CapturedPipeline: a rank captured once replays bit-identically to the
+    eager pipeline, including on new input ciphertexts copied into its buffers."""
+    import torch
+
+    from paper_2412_15126_b200.graphs import CapturedPipeline
+
+    eng = M.B200Engine(preset("toy_deep"))
+    cfg = M.KernelConfig(mode="composite", composite=(3, 2))
+    v1 = np.array([0.30, 0.10, 0.80, 0.55, 0.20, 0.95, 0.65, 0.40])
+    v2 = np.array([0.70, 0.15, 0.05, 0.90, 0.35, 0.60, 0.25, 0.45])
+    x1, x2 = eng.encrypt(v1), eng.encrypt(v2)
+    fn = lambda c: M.rank(eng, c, 8, cfg).ranks  # noqa: E731
+    cap = CapturedPipeline(eng, fn, x1)
+    e1 = fn(x1).data.clone()
+    assert torch.equal(cap.replay().data, e1)
+    e2 = fn(x2).data.clone()
+    out = cap.replay(x2)
+    torch.cuda.synchronize()
+    assert torch.equal(out.data, e2)
+    assert np.array_equal(np.rint(M.read_row(eng, out, 8)), fractional_ranks(v2))
