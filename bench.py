@@ -28,6 +28,8 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# long-chain pipelines allocate multi-GiB batched ciphertexts of many sizes
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402

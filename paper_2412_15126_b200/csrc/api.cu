@@ -19,6 +19,10 @@
 #include "modarith.cuh"
 #include "ntt.cuh"
 
+#ifndef SRK_WS_BATCH
+#define SRK_WS_BATCH 32  // ciphertexts per internal chunk of a batched call (keys read once per chunk)
+#endif
+
 typedef unsigned __int128 u128;
 
 // ---------------------------------------------------------------------
@@ -141,6 +145,7 @@ struct srk_ctx {
     // caller's stream and nside[lane], so one chunk's pass tail overlaps the
     // next chunk's passes (lane = 1 when called from the key-switch side lane)
     int ntt_streams = 2;
+    int ws_batch = SRK_WS_BATCH;  // ciphertexts per internal chunk (SRK_WS_BATCH env: smaller workspace)
     int ntt_cta_threads = 128;  // threads per NTT pass CTA (SRK_NTT_CTA; 128: 8 CTAs/SM, cheaper barriers)
     int ntt_cluster = 0;  // 1: forward FP64 plain NTTs as one 8-CTA cluster per limb (slower: DESIGN.md)
     int conv_f64 = 1;  // ModDown conversion on the FP64 + integer pipes (k_moddown_conv_f64)
@@ -279,6 +284,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     if (const char *e = getenv("SRK_KS_FUSED")) c->ks_fused = atoi(e);
     if (const char *e = getenv("SRK_KS_STREAMS")) c->ks_streams = atoi(e);
     if (const char *e = getenv("SRK_NTT_STREAMS")) c->ntt_streams = atoi(e);
+    if (const char *e = getenv("SRK_WS_BATCH")) c->ws_batch = std::max(1, atoi(e));
     if (const char *e = getenv("SRK_NTT_CTA")) c->ntt_cta_threads = std::min(256, std::max(64, atoi(e)));
     if (const char *e = getenv("SRK_NTT_CLUSTER")) c->ntt_cluster = atoi(e);
     if (const char *e = getenv("SRK_CONV_F64")) c->conv_f64 = atoi(e);
@@ -459,9 +465,6 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     return SRK_OK;
 }
 
-#ifndef SRK_WS_BATCH
-#define SRK_WS_BATCH 32  // ciphertexts per internal chunk of a batched call (keys read once per chunk)
-#endif
 
 // words of scratch (x N) each op needs for a chunk of B ciphertexts at level l
 static size_t ks_limbs(const srk_ctx *c, int level, int B) {
@@ -477,8 +480,9 @@ static size_t relin_limbs(const srk_ctx *c, int level, int B) {
 
 extern "C" size_t srk_workspace_bytes(const srk_ctx *c) {
     const int L = c->L;
-    size_t limbs = std::max({relin_limbs(c, L, SRK_WS_BATCH), ks_limbs(c, L, SRK_WS_BATCH) + 4 * (L + 1),
-                             rescale_limbs(L, SRK_WS_BATCH) + 2 * (size_t)(L + 1) * SRK_WS_BATCH,
+    const int WB = c->ws_batch;
+    size_t limbs = std::max({relin_limbs(c, L, WB), ks_limbs(c, L, WB) + 4 * (L + 1),
+                             rescale_limbs(L, WB) + 2 * (size_t)(L + 1) * WB,
                              (size_t)4 * c->n_primes, (size_t)2 * (L + 1)});
     return limbs * c->n * sizeof(uint64_t) + 256;
 }
@@ -959,9 +963,9 @@ static int rescale_impl(srk_ctx *c, const uint64_t *a, long long a_ct, long long
     return SRK_OK;
 }
 
-// chunk a batch of B into SRK_WS_BATCH pieces
+// chunk a batch of B into c->ws_batch pieces
 #define FOR_CHUNKS(B, b0, nb) \
-    for (int b0 = 0, nb = std::min(SRK_WS_BATCH, (B)); b0 < (B); b0 += nb, nb = std::min(SRK_WS_BATCH, (B) - b0))
+    for (int b0 = 0, nb = std::min(c->ws_batch, (B)); b0 < (B); b0 += nb, nb = std::min(c->ws_batch, (B) - b0))
 
 extern "C" int srk_rescale(srk_ctx *c, const uint64_t *a, uint64_t *out, int level, void *ws,
                            void *stream) {
