@@ -167,3 +167,18 @@ def test_captured_pipeline_replay_new_inputs(require_cuda):
     torch.cuda.synchronize()
     assert torch.equal(out.data, e2)
     assert np.array_equal(np.rint(M.read_row(eng, out, 8)), fractional_ranks(v2))
+
+
+def test_cfg4_median_and_percentile_values(eng_long):
+    """Value retrieval (select.py median / percentile: window mask, SumC, Goldschmidt
+    inverse) on the GPU against the plaintext oracle (reference.py:27-87)."""
+    from oracle.plain import kth_smallest, median_value, nearest_rank
+
+    v = np.random.default_rng(4).choice(1024, 16, replace=False) / 1024
+    cfg = M.KernelConfig(mode="composite", composite=(3, 2), indicator_composite=(3, 2),
+                         tie_margin=2.0 ** -9, goldschmidt_iters=4)
+    ct = eng_long.encrypt(v)
+    med = eng_long.decrypt(M.median(eng_long, ct, 16, cfg))[0]
+    assert abs(med - median_value(v)) < 2e-3
+    p90 = eng_long.decrypt(M.percentile(eng_long, ct, 16, 90.0, cfg))[0]
+    assert abs(p90 - kth_smallest(v, nearest_rank(16, 90.0))) < 2e-3
