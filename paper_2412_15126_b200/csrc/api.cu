@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -145,6 +146,7 @@ struct srk_ctx {
     // caller's stream and nside[lane], so one chunk's pass tail overlaps the
     // next chunk's passes (lane = 1 when called from the key-switch side lane)
     int ntt_streams = 2;
+    int md_chunk = 0;  // L2-chunked ModDown: limbs per NTT + combine group (SRK_MD_CHUNK; 0 = off)
     int ws_batch = SRK_WS_BATCH;  // ciphertexts per internal chunk (SRK_WS_BATCH env: smaller workspace)
     int ntt_cta_threads = 128;  // threads per NTT pass CTA (SRK_NTT_CTA; 128: 8 CTAs/SM, cheaper barriers)
     int ntt_cluster = 0;  // 1: forward FP64 plain NTTs as one 8-CTA cluster per limb (slower: DESIGN.md)
@@ -284,6 +286,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     if (const char *e = getenv("SRK_KS_FUSED")) c->ks_fused = atoi(e);
     if (const char *e = getenv("SRK_KS_STREAMS")) c->ks_streams = atoi(e);
     if (const char *e = getenv("SRK_NTT_STREAMS")) c->ntt_streams = atoi(e);
+    if (const char *e = getenv("SRK_MD_CHUNK")) c->md_chunk = std::max(0, atoi(e));
     if (const char *e = getenv("SRK_WS_BATCH")) c->ws_batch = std::max(1, atoi(e));
     if (const char *e = getenv("SRK_NTT_CTA")) c->ntt_cta_threads = std::min(256, std::max(64, atoi(e)));
     if (const char *e = getenv("SRK_NTT_CLUSTER")) c->ntt_cluster = atoi(e);
@@ -1061,8 +1064,11 @@ static uint64_t galois_inverse(const srk_ctx *c, uint64_t g) {
 // forward NTT of the ModDown conversion with the combine fused into its store:
 // either the conversion fused into the first pass's loads (LD_BCONV) or a
 // streaming conversion kernel into the NTT buffer first (then a plain load)
+// after(t0, t1, stream): work that consumes limbs [t0, t1) of the NTT output
+using LimbRangeFn = std::function<int(int, int, cudaStream_t)>;
+
 static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int nout, cudaStream_t s,
-                       bool combine = true) {
+                       bool combine = true, const LimbRangeFn *after = nullptr) {
     if (c->moddown_mode == 1) return ntt_run(c, bq, false, g, LD_BCONV, ST_MODDOWN, s);
     const long long n = c->n;
     dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + 7) / 8);
@@ -1097,7 +1103,44 @@ static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int n
     FuseArgs h = g;
     h.src = nullptr;  // first pass reads the conversion in place
     if (c->moddown_mode == 2) return ntt_run(c, bq, false, h, LD_PLAIN, ST_MODDOWN, s);
+    if (after && c->md_chunk > 0 && bq.mode == 0) {
+        // L2-chunked: each group of limbs (one prime class, <= md_chunk limbs) is
+        // transformed and then consumed by `after` right away, so the consumer
+        // reads the transform's output from L2; groups alternate over two streams
+        std::vector<std::pair<int, int>> groups;
+        for (int t0 = 0, t1 = 0; t0 < bq.n_limbs; t0 = t1) {
+            const bool f64 = c->primes[t0 + bq.off_a] < SRK_F64_Q;
+            t1 = t0 + 1;
+            while (t1 < bq.n_limbs && t1 - t0 < c->md_chunk &&
+                   (c->primes[t1 + bq.off_a] < SRK_F64_Q) == f64)
+                t1++;
+            groups.push_back({t0, t1});
+        }
+        const int lane = s == c->side ? 1 : 0;
+        const bool two = c->ntt_streams >= 2 && groups.size() >= 2 && c->nside[lane];
+        if (two) {
+            CU(cudaEventRecord(c->ev_nfork[lane], s));
+            CU(cudaStreamWaitEvent(c->nside[lane], c->ev_nfork[lane], 0));
+        }
+        for (size_t gi = 0; gi < groups.size(); gi++) {
+            const int t0 = groups[gi].first, t1 = groups[gi].second;
+            cudaStream_t cs = (two && (gi & 1)) ? c->nside[lane] : s;
+            LimbBatch sub = bq;
+            sub.ptr = bq.ptr + (long long)t0 * n;
+            sub.n_limbs = t1 - t0;
+            sub.off_a = sub.off_b = bq.off_a + t0;
+            sub.split = 1 << 30;
+            TRY(ntt_run(c, sub, false, no_fuse(), LD_PLAIN, ST_PLAIN, cs));
+            TRY((*after)(t0, t1, cs));
+        }
+        if (two) {
+            CU(cudaEventRecord(c->ev_njoin[lane], c->nside[lane]));
+            CU(cudaStreamWaitEvent(s, c->ev_njoin[lane], 0));
+        }
+        return SRK_OK;
+    }
     TRY(ntt_run(c, bq, false, no_fuse(), LD_PLAIN, ST_PLAIN, s));
+    if (after) return (*after)(0, bq.n_limbs, s);
     if (!combine) return SRK_OK;
     CombineArgs ca;
     memset(&ca, 0, sizeof ca);
@@ -1426,9 +1469,9 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             f.out_galois = ko.galois;
             f.out_galois_inv = galois_inverse(c, ko.galois);
             f.mulc = c->lc_pinv;
-            TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), f, B, nl, so,
-                            !ks_fused));
-            if (ks_fused) {
+            if (!ks_fused) {
+                TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), f, B, nl, so, true));
+            } else {
                 // 7. out = sigma_g(add + (sum_j e_j key_j - conv) P^-1) over q_0..q_l
                 KsCombineArgs kc;
                 memset(&kc, 0, sizeof kc);
@@ -1455,19 +1498,25 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
                 kc.batch = B;
                 kc.mulc = c->lc_pinv;
                 // runs of limbs of one prime class: FP64 instantiation for q < 2^41
-                for (int t0 = 0, t1 = 0; t0 < nl; t0 = t1) {
-                    const bool f64 = c->primes[t0] < SRK_F64_Q;
-                    t1 = t0 + 1;
-                    while (t1 < nl && (c->primes[t1] < SRK_F64_Q) == f64) t1++;
-                    kc.t0 = t0;
-                    kc.t1 = t1;
-                    const int blocks = grid_for((long long)(t1 - t0) * n);
-                    if (f64)
-                        launch_ks_combine<true>(kc, beta, blocks, so, c);
-                    else
-                        launch_ks_combine<false>(kc, beta, blocks, so, c);
-                    LAUNCHED();
-                }
+                const LimbRangeFn combine = [&](int a0, int a1, cudaStream_t cs) -> int {
+                    for (int t0 = a0, t1 = a0; t0 < a1; t0 = t1) {
+                        const bool f64 = c->primes[t0] < SRK_F64_Q;
+                        t1 = t0 + 1;
+                        while (t1 < a1 && (c->primes[t1] < SRK_F64_Q) == f64) t1++;
+                        KsCombineArgs k2 = kc;
+                        k2.t0 = t0;
+                        k2.t1 = t1;
+                        const int blocks = grid_for((long long)(t1 - t0) * n);
+                        if (f64)
+                            launch_ks_combine<true>(k2, beta, blocks, cs, c);
+                        else
+                            launch_ks_combine<false>(k2, beta, blocks, cs, c);
+                        LAUNCHED();
+                    }
+                    return SRK_OK;
+                };
+                TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), f, B, nl, so,
+                                false, &combine));
             }
         }
     }

@@ -342,6 +342,7 @@ def test_keyswitch_fused_combine_paths(name, fused, require_cuda, monkeypatch):
     {"SRK_CONV_F64": "0"},                           # Shoup / 128-bit MAC conversions
     {"SRK_NTT_STREAMS": "1", "SRK_NTT_CTA": "256"},  # one stream, 256-thread pass CTAs
     {"SRK_RESCALE_FUSED": "0", "SRK_NTT_SPLIT": "0"},  # streaming rescale, mixed-mode passes
+    {"SRK_MD_CHUNK": "2"},                           # L2-chunked ModDown NTT + combine
 ])
 def test_kernel_switches_ring16(env, require_cuda, monkeypatch):
     """Every alternative kernel path at ring 2^16 (config 2) gives the oracle's limbs."""
