@@ -28,8 +28,10 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-# long-chain pipelines allocate multi-GiB batched ciphertexts of many sizes
-os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+# several ranks sharing one GPU (the gloo functional mode): expandable segments
+# keep the long-chain pipelines' multi-GiB blocks from fragmenting the shared HBM
+if os.environ.get("SRK_DIST_BACKEND") == "gloo":
+    os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
@@ -461,7 +463,6 @@ def _graph_latency(eng, fn, x, warmup=1, reps=3):
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
     cap.close()
-    torch.cuda.empty_cache()
     return best
 
 

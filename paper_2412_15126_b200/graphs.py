@@ -42,9 +42,11 @@ class CapturedPipeline:
     """``fn(*inputs)`` captured as one CUDA graph on ``engine``'s device.
 
     ``inputs`` are the engine objects (ciphertexts / block vectors) the graph
-    reads; their limb buffers become the graph's input buffers."""
+    reads; their limb buffers become the graph's input buffers.  ``release_cache``
+    returns the allocator's cached blocks to the device before capture (for
+    pipelines whose graph pool would not fit otherwise, e.g. multi_sort N=1024)."""
 
-    def __init__(self, engine, fn, *inputs, warmup: int = 1):
+    def __init__(self, engine, fn, *inputs, warmup: int = 1, release_cache: bool = False):
         dev = engine.backend.device
         self.engine, self.fn, self.inputs = engine, fn, inputs
         self._in = _datas(list(inputs))
@@ -57,7 +59,8 @@ class CapturedPipeline:
                 fn(*inputs)  # keys, constant plaintexts, kernel attributes, workspace
         torch.cuda.current_stream(dev).wait_stream(self._stream)
         torch.cuda.synchronize(dev)
-        torch.cuda.empty_cache()  # the graph's private pool cannot reuse cached eager blocks
+        if release_cache:  # very large pipelines: the graph's private pool cannot reuse cached blocks
+            torch.cuda.empty_cache()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, stream=self._stream):
             self.output = fn(*inputs)

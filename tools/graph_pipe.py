@@ -42,7 +42,7 @@ for _ in range(3):
     fn(x)
 torch.cuda.synchronize()
 eager = (time.perf_counter() - t0) / 3
-cap = CapturedPipeline(eng, fn, x)
+cap = CapturedPipeline(eng, fn, x, release_cache=what.startswith("sort"))
 cap.replay()
 torch.cuda.synchronize()
 from paper_2412_15126_b200.graphs import _datas  # noqa: E402
