@@ -586,7 +586,6 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
     }
     bb.n_limbs = nlc;
     dim3 grid(subs / cb, b.n_polys, nlc);
-    bool done = false;
     // plain / automorphism / rescale-spread loads, plain / scaled / rescale stores:
     // FP64-only kernel for q < 2^41 chunks, Harvey-only integer kernel otherwise
     // (the FP64 spread needs the dropped prime < 2^41 too)

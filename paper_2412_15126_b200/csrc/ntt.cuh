@@ -503,9 +503,6 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
 #ifndef SRK_NTT_MINB_F64
 #define SRK_NTT_MINB_F64 4
 #endif
-#ifndef SRK_ROW_DIRECT
-#define SRK_ROW_DIRECT 0
-#endif
 #ifndef SRK_NTT_MINB_INT
 #define SRK_NTT_MINB_INT 3
 #endif
@@ -647,29 +644,9 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
                 }
                 return;
             }
-            // final pass, plain store: each thread owns 16 contiguous outputs;
-            // 16-byte vector stores straight from registers (SRK_ROW_DIRECT) or
-            // a shared-memory transpose for fully coalesced 8-byte stores
-#if SRK_ROW_DIRECT
-            if constexpr (ST == ST_PLAIN && KM != 0) {
-                uint64_t *o = data + (long long)sub * T + u * E;
-#pragma unroll
-                for (int e = 0; e < E; e += 2) {
-                    uint64_t v0 = x[e], v1 = x[e + 1];
-                    if (mode == 2) {
-                        v0 = canon_u64_of_f64(__longlong_as_double((long long)v0), fq.q, fq.qinv);
-                        v1 = canon_u64_of_f64(__longlong_as_double((long long)v1), fq.q, fq.qinv);
-                    } else {
-                        v0 = v0 >= two_q ? v0 - two_q : v0;
-                        v0 = v0 >= q ? v0 - q : v0;
-                        v1 = v1 >= two_q ? v1 - two_q : v1;
-                        v1 = v1 >= q ? v1 - q : v1;
-                    }
-                    *reinterpret_cast<ulonglong2 *>(o + e) = make_ulonglong2(v0, v1);
-                }
-                return;
-            }
-#endif
+            // final pass: each thread owns 16 contiguous outputs; a shared-memory
+            // transpose gives fully coalesced 8-byte stores (16-byte vector stores
+            // straight from registers were slower: DESIGN.md)
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < E; e++) {

@@ -182,3 +182,22 @@ def test_cfg4_median_and_percentile_values(eng_long):
     assert abs(med - median_value(v)) < 2e-3
     p90 = eng_long.decrypt(M.percentile(eng_long, ct, 16, 90.0, cfg))[0]
     assert abs(p90 - kth_smallest(v, nearest_rank(16, 90.0))) < 2e-3
+
+
+def test_ragged_inputs_and_capacity(require_cuda, eng_long):
+    """Edge cases of the reference's tests: a length that is not a power of two
+    (pad mask), a ragged last sort block, and the capacity error."""
+    eng = M.B200Engine(preset("cfg3"))
+    v = np.random.default_rng(5).choice(1024, 100, replace=False) / 1024
+    cfg = M.KernelConfig(mode="composite", composite=(4, 2))
+    r = M.read_row(eng, M.rank(eng, eng.encrypt(v), 100, cfg).ranks, 100)
+    assert np.array_equal(np.rint(r), fractional_ranks(v))
+    with pytest.raises(M.CapacityError):
+        M.rank(eng, eng.encrypt(np.zeros(256)), 256, cfg)
+    w = np.random.default_rng(6).choice(2048, 200, replace=False) / 2048
+    scfg = M.SortConfig(kernel=M.KernelConfig(mode="composite", composite=(5, 2),
+                                              indicator_composite=(5, 2)), tie_correction=False)
+    out = M.block_merge(eng_long, M.multi_sort(eng_long, M.block_split(eng_long, w), scfg))
+    assert out.shape == (200,)
+    assert np.array_equal(np.argsort(out), np.arange(200))
+    assert np.abs(out - np.sort(w)).max() < 1e-3
