@@ -965,9 +965,15 @@ static int rescale_impl(srk_ctx *c, const uint64_t *a, long long a_ct, long long
     return SRK_OK;
 }
 
-// chunk a batch of B into c->ws_batch pieces
-#define FOR_CHUNKS(B, b0, nb) \
-    for (int b0 = 0, nb = std::min(c->ws_batch, (B)); b0 < (B); b0 += nb, nb = std::min(c->ws_batch, (B) - b0))
+// chunk a batch of B into balanced pieces of at most c->ws_batch (36 -> 18 + 18,
+// not 32 + 4: a small remainder chunk runs its kernels at a fraction of the GPU)
+static inline int chunk_size(int B, int ws) {
+    const int pieces = (B + ws - 1) / ws;
+    return pieces > 0 ? (B + pieces - 1) / pieces : 1;
+}
+#define FOR_CHUNKS(B, b0, nb)                                                                        \
+    for (int b0 = 0, cs_ = chunk_size((B), c->ws_batch), nb = std::min(cs_, (B)); b0 < (B);         \
+         b0 += nb, nb = std::min(cs_, (B) - b0))
 
 extern "C" int srk_rescale(srk_ctx *c, const uint64_t *a, uint64_t *out, int level, void *ws,
                            void *stream) {
