@@ -61,7 +61,9 @@ int srk_ctx_destroy(srk_ctx *ctx);
 size_t srk_workspace_bytes(const srk_ctx *ctx);
 
 /* batched NTT over n_polys polys of n_limbs limbs each (limb i under prime
- * first_prime + i; poly p at data + p * poly_stride words) */
+ * first_prime + i; poly p at data + p * poly_stride words).  Inputs and
+ * outputs are canonical residues in [0, q) (every entry point takes and returns
+ * canonical limbs; the kernels' lazy / FP64 internal ranges depend on it). */
 int srk_ntt(srk_ctx *ctx, uint64_t *data, int n_polys, long long poly_stride, int n_limbs,
             int first_prime, int inverse, void *stream);
 /* NTT over extended polys at level l: limbs 0..l under Q primes, limbs
