@@ -1069,6 +1069,16 @@ static uint64_t galois_inverse(const srk_ctx *c, uint64_t g) {
 // forward NTT of the ModDown conversion with the combine fused into its store:
 // either the conversion fused into the first pass's loads (LD_BCONV) or a
 // streaming conversion kernel into the NTT buffer first (then a plain load)
+// conversion grids: x shrunk by up to conv_cpt coefficients per thread (to amortise
+// the CTA's constant staging) only while >= ~3 waves of CTAs remain, so the
+// one-ciphertext ops of the pipelines keep enough CTAs in flight
+static inline dim3 conv_grid(const srk_ctx *c, dim3 g) {
+    const unsigned long long ctas = (unsigned long long)g.x * g.y * g.z;
+    unsigned cpt = c->conv_cpt;
+    while (cpt > 1 && ctas / cpt < 148ull * 8 * 3) cpt >>= 1;
+    return dim3(std::max(1u, g.x / cpt), g.y, g.z);
+}
+
 // after(t0, t1, stream): work that consumes limbs [t0, t1) of the NTT output
 using LimbRangeFn = std::function<int(int, int, cudaStream_t)>;
 
@@ -1080,7 +1090,7 @@ static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int n
     const uint64_t *z = g.src;
 #define SRK_CONV_LAUNCH(MK, EX)                                                                         \
     if (c->conv_f64 && g.mhl)                                                                            \
-        k_moddown_conv_f64<MK, EX><<<dim3(std::max(1u, grid.x / c->conv_cpt), grid.y, grid.z), 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2,  \
+        k_moddown_conv_f64<MK, EX><<<conv_grid(c, grid), 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2,  \
                                                         g.mhl, g.fhl, g.mat_ld, g.corr, bq.ptr,           \
                                                         bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n); \
     else                                                                                                 \
@@ -1094,7 +1104,7 @@ static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int n
         case 4: SRK_CONV_LAUNCH(4, true); break;
         default:
             if (c->conv_f64 && g.mhl && g.n_src <= 16) {
-                k_moddown_conv_f64_wide<<<dim3(std::max(1u, grid.x / c->conv_cpt), grid.y, grid.z), 256, 0, s>>>(
+                k_moddown_conv_f64_wide<<<conv_grid(c, grid), 256, 0, s>>>(
                     z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mhl, g.fhl, g.mat_ld, g.corr, bq.ptr,
                     bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
             } else if (g.n_src <= 8) {
@@ -1275,7 +1285,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
                 }
         dim3 grid((unsigned)((n + 255) / 256), B * beta, (maxd + SRK_MODUP_TCH - 1) / SRK_MODUP_TCH);
         if (f64ok) {
-            dim3 g2(std::max(1u, grid.x / c->conv_cpt), grid.y, grid.z);
+            const dim3 g2 = conv_grid(c, grid);
 #define SRK_MODUP_F64(GS)                                                          \
     case GS:                                                                      \
         if (wide0)                                                                \

@@ -327,9 +327,9 @@ __global__ void __launch_bounds__(256, 3) k_modup_f64(const __grid_constant__ Mo
         for (int tt = 0; tt < SRK_MODUP_TCH; tt++) {
             if (tt >= nt) break;
             const uint64_t q = s_q[tt];
-            // two FMA chains (latency), one wrapping integer sum
-            double T0 = 0.0, T1 = 0.0;
-            uint64_t S = 0;
+            // four FMA chains and two wrapping integer sums (latency-bound otherwise)
+            double T[4] = {0.0, 0.0, 0.0, 0.0};
+            uint64_t S[2] = {0, 0};
 #pragma unroll
             for (int i = 0; i < GS; i++) {
                 if (i < gs) {
@@ -337,21 +337,19 @@ __global__ void __launch_bounds__(256, 3) k_modup_f64(const __grid_constant__ Mo
                     const double fx = __longlong_as_double((long long)mf.y);
                     if (i == 0 && wide) {
                         const ulonglong2 w0 = s_w0[tt];
-                        T0 = fma(dl0, fx, T0);
-                        T1 = fma(dh0, __longlong_as_double((long long)w0.y), T1);
-                        S += (uint64_t)yl0 * mf.x;
-                        S += (uint64_t)yh0 * w0.x;
-                    } else if (i & 1) {
-                        T1 = fma(dy[i], fx, T1);
-                        S += y[i] * mf.x;
+                        T[0] = fma(dl0, fx, T[0]);
+                        T[1] = fma(dh0, __longlong_as_double((long long)w0.y), T[1]);
+                        S[0] += (uint64_t)yl0 * mf.x;
+                        S[1] += (uint64_t)yh0 * w0.x;
                     } else {
-                        T0 = fma(dy[i], fx, T0);
-                        S += y[i] * mf.x;
+                        T[i & 3] = fma(dy[i], fx, T[i & 3]);
+                        S[i & 1] += y[i] * mf.x;
                     }
                 }
             }
-            const long long tq = __double_as_longlong((T0 + T1) + SRK_F64_MAGIC) - 0x4338000000000000ll;
-            const long long rr = (long long)(S - (uint64_t)tq * q);
+            const double Tt = (T[0] + T[1]) + (T[2] + T[3]);
+            const long long tq = __double_as_longlong(Tt + SRK_F64_MAGIC) - 0x4338000000000000ll;
+            const long long rr = (long long)((S[0] + S[1]) - (uint64_t)tq * q);
             dst[(long long)s_slot[tt] * n + x] = (uint64_t)(rr < 0 ? rr + (long long)q : rr);
         }
     }
