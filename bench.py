@@ -226,7 +226,8 @@ class PipelinedE2E:
         # half-size first and last chunks: the first H2D and the last D2H are the
         # only copies with no compute to hide under
         per = -(-step.n_ct // chunks)
-        sizes = [max(1, per // 2)]
+        ramp = int(os.environ.get("SRK_E2E_RAMP", "2"))  # first chunk = per / ramp
+        sizes = [max(1, per // ramp)]
         while sum(sizes) < step.n_ct:
             sizes.append(min(per, step.n_ct - sum(sizes)))
         if len(sizes) > 2 and sizes[-1] == per:
