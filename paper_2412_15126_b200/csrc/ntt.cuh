@@ -501,7 +501,7 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
 // element addresses of the 2^16 passes fold into immediate offsets.
 // Grid: x = sub-transform groups, y = poly, z = limb.
 #ifndef SRK_NTT_MINB_F64
-#define SRK_NTT_MINB_F64 4
+#define SRK_NTT_MINB_F64 3
 #endif
 #ifndef SRK_NTT_MINB_INT
 #define SRK_NTT_MINB_INT 3
