@@ -9,6 +9,14 @@
 #include "modarith.cuh"
 #include "ntt.cuh"
 
+// CTAs per SM the conversion kernels' register budgets are sized for
+#ifndef SRK_CONV_MINB
+#define SRK_CONV_MINB 4
+#endif
+#ifndef SRK_MODUP_MINB
+#define SRK_MODUP_MINB 3
+#endif
+
 
 // ---------------------------------------------------------------------
 // elementwise on ciphertexts [2][nl][N] (poly stride may differ per operand)
@@ -278,7 +286,7 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
 // m' = m 2^32 mod q_t.  |S - round(T) q_t| < q_t < 2^63, so the wrapped difference
 // is the exact signed remainder whatever the target's size.
 template <int GS, bool WIDE0>
-__global__ void __launch_bounds__(256, 3) k_modup_f64(const __grid_constant__ ModUpArgs a,
+__global__ void __launch_bounds__(256, SRK_MODUP_MINB) k_modup_f64(const __grid_constant__ ModUpArgs a,
                                                    const PrimeConst *__restrict__ pc, int log_n) {
     // {m, bits(m / q)} per (target, source): one 16-byte broadcast load per term;
     // the wide source's {m', bits(m' / q)} separately
@@ -500,7 +508,7 @@ __global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict
 #endif
 constexpr int kConvUnroll = SRK_CONV_UNROLL;
 template <int MAXK, bool EXACT>
-__global__ void __launch_bounds__(256, 4) k_moddown_conv_f64(
+__global__ void __launch_bounds__(256, SRK_CONV_MINB) k_moddown_conv_f64(
     const uint64_t *__restrict__ z, long long z_ct, long long z_ps, int n_src,
     const uint8_t *__restrict__ vround, const ulonglong2 *__restrict__ mat2,
     const ulonglong2 *__restrict__ mhl, const double2 *__restrict__ fhl, int n_dst,
