@@ -479,6 +479,27 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
             return;
         }
     }
+    if constexpr (ST == ST_RESCALE) {
+        // integer rescale combine with every load issued before the first store
+        // (the out pointer may alias acc / pt as far as the compiler knows)
+        const long long nn = 1ll << log_n;
+        const long long off0 = (long long)t * nn + (long long)sub * T + u;
+        uint64_t av[E], pv[E];
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            av[e] = __ldg(f.acc + bi * f.acc_ct + r * f.acc_ps + off0 + TPS * e);
+            pv[e] = f.pre_mode == 2 ? __ldg(f.pt + bi * f.pt_ct + off0 + TPS * e) : 0;
+        }
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            uint64_t a = av[e];
+            if (f.pre_mode == 1) a = mul_shoup(a, f.pre.w[limb], f.pre.ws[limb], pc.q);
+            if (f.pre_mode == 2) a = mul_mod(a, pv[e], pc);
+            f.out[bi * f.out_ct + r * f.out_ps + off0 + TPS * e] =
+                mul_shoup(sub_mod(a, sm[sidx(u + TPS * e)], pc.q), f.mulc.w[limb], f.mulc.ws[limb], pc.q);
+        }
+        return;
+    }
 #pragma unroll
     for (int e = 0; e < E; e++) {
         const int c = u + TPS * e;
@@ -631,15 +652,23 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
                 const long long nn = 1ll << log_n;
                 const double fm = f64_of_u64(f.mulc.w[limb]);
                 const double fp = f64_of_u64(f.pre.w[limb]);
+                const long long off0 = (long long)t * nn + (long long)sub * T + u;
+                // all loads first: the stores below may alias them as far as the
+                // compiler knows, which otherwise serialises load -> store per element
+                uint64_t av[E], pv[E];
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    av[e] = __ldg(f.acc + bi * f.acc_ct + r * f.acc_ps + off0 + TPS * e);
+                    pv[e] = f.pre_mode == 2 ? __ldg(f.pt + bi * f.pt_ct + off0 + TPS * e) : 0;
+                }
 #pragma unroll
                 for (int e = 0; e < E; e++) {
                     const int c = u + TPS * e;
-                    const long long off = (long long)t * nn + (long long)sub * T + c;
-                    double a = f64_of_u64(f.acc[bi * f.acc_ct + r * f.acc_ps + off]);
+                    double a = f64_of_u64(av[e]);
                     if (f.pre_mode == 1) a = modmul_f64(a, fp, fq.q, fq.qinv);
-                    if (f.pre_mode == 2) a = modmul_f64(a, f64_of_u64(__ldg(f.pt + bi * f.pt_ct + off)), fq.q, fq.qinv);
+                    if (f.pre_mode == 2) a = modmul_f64(a, f64_of_u64(pv[e]), fq.q, fq.qinv);
                     const double d = a - __longlong_as_double((long long)smem[sidx(c)]);
-                    f.out[bi * f.out_ct + r * f.out_ps + off] =
+                    f.out[bi * f.out_ct + r * f.out_ps + off0 + TPS * e] =
                         canon_u64_of_small_f64(modmul_f64(d, fm, fq.q, fq.qinv), q);
                 }
                 return;
