@@ -537,20 +537,37 @@ __global__ void __launch_bounds__(256, SRK_CONV_MINB) k_moddown_conv_f64(
     if (threadIdx.x < nt) s_q[threadIdx.x] = pc[t0 + threadIdx.x].q;
     __syncthreads();
     const uint64_t *zp = z + b * z_ct + r * z_ps;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
-         x += (long long)gridDim.x * blockDim.x) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    // software prefetch: the next coefficient's sources are loaded before this
+    // one's stores (which the compiler cannot move loads across)
+    long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    uint64_t zn[MAXK];
+    int vn = 0;
+    if (x < n) {
+#pragma unroll
+        for (int k = 0; k < MAXK; k++) zn[k] = (EXACT || k < n_src) ? __ldg(zp + k * n + x) : 0;
+        vn = __ldg(vround + (long long)p * n + x);
+    }
+    for (; x < n; x += stride) {
         uint64_t zz[MAXK];
         uint32_t zl[MAXK], zh[MAXK];
         double dl[MAXK], dh[MAXK];
 #pragma unroll
+        for (int k = 0; k < MAXK; k++) zz[k] = zn[k];
+        const int v = vn;
+        if (x + stride < n) {
+#pragma unroll
+            for (int k = 0; k < MAXK; k++)
+                zn[k] = (EXACT || k < n_src) ? __ldg(zp + k * n + x + stride) : 0;
+            vn = __ldg(vround + (long long)p * n + x + stride);
+        }
+#pragma unroll
         for (int k = 0; k < MAXK; k++) {
-            zz[k] = (EXACT || k < n_src) ? zp[k * n + x] : 0;
             zl[k] = (uint32_t)zz[k];
             zh[k] = (uint32_t)(zz[k] >> 32);
             dl[k] = __hiloint2double(0x43300000, (int)zl[k]) - SRK_F64_TWO52;
             dh[k] = __hiloint2double(0x43300000, (int)zh[k]) - SRK_F64_TWO52;
         }
-        const int v = vround[(long long)p * n + x];
         uint64_t *out = conv + b * c_ct + r * c_ps + (long long)t0 * n + x;
 #pragma unroll(kConvUnroll)  // (fully unrolled, the compiler hoists every target's constants: 250 registers)
         for (int tt = 0; tt < SRK_CONV_TG; tt++) {
@@ -614,8 +631,10 @@ __global__ void __launch_bounds__(256, 3) k_moddown_conv_f64_wide(
             T[tt] = 0.0;
             S[tt] = 0;
         }
+        uint64_t znext = __ldg(zp + x);
         for (int k = 0; k < n_src; k++) {
-            const uint64_t zz = zp[k * n + x];
+            const uint64_t zz = znext;  // loaded one source ahead (latency off the chain)
+            if (k + 1 < n_src) znext = __ldg(zp + (k + 1) * n + x);
             const uint32_t zl = (uint32_t)zz, zh = (uint32_t)(zz >> 32);
             const double dl = __hiloint2double(0x43300000, (int)zl) - SRK_F64_TWO52;
             const double dh = __hiloint2double(0x43300000, (int)zh) - SRK_F64_TWO52;
