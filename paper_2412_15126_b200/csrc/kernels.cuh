@@ -9,6 +9,10 @@
 #include "modarith.cuh"
 #include "ntt.cuh"
 
+#ifndef SRK_KSC_UNROLL
+#define SRK_KSC_UNROLL 1
+#endif
+constexpr int kKscUnroll = SRK_KSC_UNROLL;  // batch-pair loop unroll of k_ks_combine (FP64)
 // CTAs per SM the conversion kernels' register budgets are sized for
 #ifndef SRK_CONV_MINB
 #define SRK_CONV_MINB 4
@@ -774,30 +778,32 @@ __global__ void __launch_bounds__(256, F64 ? SRK_KSC_F64_MINB : SRK_KSC_MINB)
                 kf0[j] = (EXACT || j < a.beta) ? f64_of_u64(k0[j]) : 0.0;
                 kf1[j] = (EXACT || j < a.beta) ? f64_of_u64(k1[j]) : 0.0;
             }
+#pragma unroll(kKscUnroll)
             for (int b = 0; b < a.batch; b += 2) {
                 const bool two = b + 1 < a.batch;
                 double e0[MAXD], e1[MAXD];
+                // read-only (__ldg) loads: free to move ahead of the previous pair's stores
 #pragma unroll
                 for (int j = 0; j < MAXD; j++) {
                     if (EXACT || j < a.beta) {
                         const uint64_t *p = j == jt ? a.d + b * a.d_ct + o : a.ext + b * a.ext_ct + j * a.ext_dig + o;
                         const long long st = j == jt ? a.d_ct : a.ext_ct;
-                        e0[j] = f64_of_u64(p[0]);
-                        e1[j] = two ? f64_of_u64(p[st]) : 0.0;
+                        e0[j] = f64_of_u64(__ldg(p));
+                        e1[j] = two ? f64_of_u64(__ldg(p + st)) : 0.0;
                     }
                 }
                 const uint64_t *cv = a.conv + b * a.conv_ct + o;
-                const double cv00 = f64_of_u64(cv[0]), cv01 = f64_of_u64(cv[a.conv_ps]);
-                const double cv10 = two ? f64_of_u64(cv[a.conv_ct]) : 0.0;
-                const double cv11 = two ? f64_of_u64(cv[a.conv_ct + a.conv_ps]) : 0.0;
+                const double cv00 = f64_of_u64(__ldg(cv)), cv01 = f64_of_u64(__ldg(cv + a.conv_ps));
+                const double cv10 = two ? f64_of_u64(__ldg(cv + a.conv_ct)) : 0.0;
+                const double cv11 = two ? f64_of_u64(__ldg(cv + a.conv_ct + a.conv_ps)) : 0.0;
                 double ad00 = 0, ad01 = 0, ad10 = 0, ad11 = 0;
                 if (a.add0) {
-                    ad00 = f64_of_u64(a.add0[b * a.add_ct + o]);
-                    ad10 = two ? f64_of_u64(a.add0[(b + 1) * a.add_ct + o]) : 0.0;
+                    ad00 = f64_of_u64(__ldg(a.add0 + b * a.add_ct + o));
+                    ad10 = two ? f64_of_u64(__ldg(a.add0 + (b + 1) * a.add_ct + o)) : 0.0;
                 }
                 if (a.add1) {
-                    ad01 = f64_of_u64(a.add1[b * a.add_ct + o]);
-                    ad11 = two ? f64_of_u64(a.add1[(b + 1) * a.add_ct + o]) : 0.0;
+                    ad01 = f64_of_u64(__ldg(a.add1 + b * a.add_ct + o));
+                    ad11 = two ? f64_of_u64(__ldg(a.add1 + (b + 1) * a.add_ct + o)) : 0.0;
                 }
                 // |each product| < q, |sum| < beta q, minus conv: < (beta + 1) q < 2^47
                 double s0 = -cv00, s1 = -cv01, u0 = -cv10, u1 = -cv11;
