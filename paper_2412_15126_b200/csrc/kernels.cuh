@@ -426,8 +426,8 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
                 if (j < a.beta) {
                     const uint64_t *p = j == jt ? dd + b * a.d_ct : ext + b * a.ext_ct + j * a.ext_dig;
                     const long long st = j == jt ? a.d_ct : a.ext_ct;
-                    e0[j] = p[0];
-                    e1[j] = two ? p[st] : 0;
+                    e0[j] = __ldg(p);  // read-only: may overlap the previous pair's stores
+                    e1[j] = two ? __ldg(p + st) : 0;
                 }
             }
             U128 a0 = {0, 0}, a1 = {0, 0}, c0 = {0, 0}, c1 = {0, 0};
@@ -833,13 +833,13 @@ __global__ void __launch_bounds__(256, F64 ? SRK_KSC_F64_MINB : SRK_KSC_MINB)
                 if (EXACT || j < a.beta) {
                     const uint64_t *p = j == jt ? a.d + b * a.d_ct + o : a.ext + b * a.ext_ct + j * a.ext_dig + o;
                     const long long st = j == jt ? a.d_ct : a.ext_ct;
-                    e0[j] = p[0];
-                    e1[j] = two ? p[st] : 0;
+                    e0[j] = __ldg(p);
+                    e1[j] = two ? __ldg(p + st) : 0;
                 }
             }
             const uint64_t *cv = a.conv + b * a.conv_ct + o;
-            const uint64_t cv00 = cv[0], cv01 = cv[a.conv_ps];
-            const uint64_t cv10 = two ? cv[a.conv_ct] : 0, cv11 = two ? cv[a.conv_ct + a.conv_ps] : 0;
+            const uint64_t cv00 = __ldg(cv), cv01 = __ldg(cv + a.conv_ps);
+            const uint64_t cv10 = two ? __ldg(cv + a.conv_ct) : 0, cv11 = two ? __ldg(cv + a.conv_ct + a.conv_ps) : 0;
             uint64_t ad00 = 0, ad01 = 0, ad10 = 0, ad11 = 0;
             if (a.add0) {
                 ad00 = a.add0[b * a.add_ct + o];
