@@ -121,7 +121,7 @@ __global__ void k_tensor(const uint64_t *__restrict__ a, const uint64_t *__restr
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < ps;
          x += (long long)gridDim.x * blockDim.x) {
         const PrimeConst P = pc[x >> log_n];
-        uint64_t a0 = a[x], a1 = a[ps + x], b0 = b[x], b1 = b[ps + x];
+        uint64_t a0 = __ldg(a + x), a1 = __ldg(a + ps + x), b0 = __ldg(b + x), b1 = __ldg(b + ps + x);
         if (P.q < SRK_F64_Q) {  // FP64 pipe: exact FMA-split products (ntt.cuh modmul_f64)
             const double q = __longlong_as_double((long long)P.qd_bits);
             const double qi = __longlong_as_double((long long)P.qinv_bits);
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
                     const uint64_t *p = j == jt ? dd + b * a.d_ct : ext + b * a.ext_ct + j * a.ext_dig;
                     const long long st = j == jt ? a.d_ct : a.ext_ct;
                     e0[j] = __ldg(p);  // read-only: may overlap the previous pair's stores
-                    e1[j] = two ? __ldg(p + st) : 0;
+                    e1[j] = (two ? __ldg(p + (two ? st : 0)) : 0);
                 }
             }
             U128 a0 = {0, 0}, a1 = {0, 0}, c0 = {0, 0}, c1 = {0, 0};
@@ -782,28 +782,30 @@ __global__ void __launch_bounds__(256, F64 ? SRK_KSC_F64_MINB : SRK_KSC_MINB)
             for (int b = 0; b < a.batch; b += 2) {
                 const bool two = b + 1 < a.batch;
                 double e0[MAXD], e1[MAXD];
-                // read-only (__ldg) loads: free to move ahead of the previous pair's stores
+                // read-only (__ldg) loads: free to move ahead of the previous pair's stores;
+                // the second ciphertext's addresses fall back to the first's when there is
+                // none, so a speculated load never leaves the batch
 #pragma unroll
                 for (int j = 0; j < MAXD; j++) {
                     if (EXACT || j < a.beta) {
                         const uint64_t *p = j == jt ? a.d + b * a.d_ct + o : a.ext + b * a.ext_ct + j * a.ext_dig + o;
                         const long long st = j == jt ? a.d_ct : a.ext_ct;
                         e0[j] = f64_of_u64(__ldg(p));
-                        e1[j] = two ? f64_of_u64(__ldg(p + st)) : 0.0;
+                        e1[j] = (two ? f64_of_u64(__ldg(p + (two ? st : 0))) : 0.0);
                     }
                 }
                 const uint64_t *cv = a.conv + b * a.conv_ct + o;
                 const double cv00 = f64_of_u64(__ldg(cv)), cv01 = f64_of_u64(__ldg(cv + a.conv_ps));
-                const double cv10 = two ? f64_of_u64(__ldg(cv + a.conv_ct)) : 0.0;
-                const double cv11 = two ? f64_of_u64(__ldg(cv + a.conv_ct + a.conv_ps)) : 0.0;
+                const double cv10 = (two ? f64_of_u64(__ldg(cv + (two ? a.conv_ct : 0))) : 0.0);
+                const double cv11 = (two ? f64_of_u64(__ldg(cv + (two ? a.conv_ct + a.conv_ps : 0))) : 0.0);
                 double ad00 = 0, ad01 = 0, ad10 = 0, ad11 = 0;
                 if (a.add0) {
                     ad00 = f64_of_u64(__ldg(a.add0 + b * a.add_ct + o));
-                    ad10 = two ? f64_of_u64(__ldg(a.add0 + (b + 1) * a.add_ct + o)) : 0.0;
+                    ad10 = (two ? f64_of_u64(__ldg(a.add0 + (two ? b + 1 : b) * a.add_ct + o)) : 0.0);
                 }
                 if (a.add1) {
                     ad01 = f64_of_u64(__ldg(a.add1 + b * a.add_ct + o));
-                    ad11 = two ? f64_of_u64(__ldg(a.add1 + (b + 1) * a.add_ct + o)) : 0.0;
+                    ad11 = (two ? f64_of_u64(__ldg(a.add1 + (two ? b + 1 : b) * a.add_ct + o)) : 0.0);
                 }
                 // |each product| < q, |sum| < beta q, minus conv: < (beta + 1) q < 2^47
                 double s0 = -cv00, s1 = -cv01, u0 = -cv10, u1 = -cv11;
@@ -834,12 +836,12 @@ __global__ void __launch_bounds__(256, F64 ? SRK_KSC_F64_MINB : SRK_KSC_MINB)
                     const uint64_t *p = j == jt ? a.d + b * a.d_ct + o : a.ext + b * a.ext_ct + j * a.ext_dig + o;
                     const long long st = j == jt ? a.d_ct : a.ext_ct;
                     e0[j] = __ldg(p);
-                    e1[j] = two ? __ldg(p + st) : 0;
+                    e1[j] = (two ? __ldg(p + (two ? st : 0)) : 0);
                 }
             }
             const uint64_t *cv = a.conv + b * a.conv_ct + o;
             const uint64_t cv00 = __ldg(cv), cv01 = __ldg(cv + a.conv_ps);
-            const uint64_t cv10 = two ? __ldg(cv + a.conv_ct) : 0, cv11 = two ? __ldg(cv + a.conv_ct + a.conv_ps) : 0;
+            const uint64_t cv10 = (two ? __ldg(cv + (two ? a.conv_ct : 0)) : 0), cv11 = (two ? __ldg(cv + (two ? a.conv_ct + a.conv_ps : 0)) : 0);
             uint64_t ad00 = 0, ad01 = 0, ad10 = 0, ad11 = 0;
             if (a.add0) {
                 ad00 = a.add0[b * a.add_ct + o];
