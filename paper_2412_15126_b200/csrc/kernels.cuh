@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(256, SRK_MODUP_MINB) k_modup_f64(const __grid_
         double dy[GS];
 #pragma unroll
         for (int i = 0; i < GS; i++) {
-            y[i] = i < gs ? src[(long long)i * n + x] : 0;
+            y[i] = i < gs ? __ldg(src + (long long)i * n + x) : 0;  // read-only: may pass the stores
             dy[i] = __longlong_as_double((long long)(y[i] | 0x4330000000000000ull)) - SRK_F64_TWO52;
         }
         // wide source 0: halves (dy[0] above is only used when !wide)
