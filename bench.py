@@ -399,7 +399,8 @@ def run_pipelines(torch, quick=False):
     eng.cost_reset()
     dt, res = timed(lambda: read_row(eng, rank(eng, ct, 128, ccfg).ranks, 128), reps=2)
     out["rank_n128_chebyshev_d1024_s"] = {
-        "latency_s": dt, "exact_ranks": bool(np.array_equal(np.rint(res), fractional_ranks(v128))),
+        "latency_s": dt, "graph_replay_s": _graph_latency(eng, lambda c: rank(eng, c, 128, ccfg).ranks, ct),
+        "exact_ranks": bool(np.array_equal(np.rint(res), fractional_ranks(v128))),
         "max_rank_err": float(np.abs(res - fractional_ranks(v128)).max()),
         "cost": eng.cost_snapshot().__dict__, "params": "cfg3", "kernel": "chebyshev d=1024 (reference)"}
     del eng

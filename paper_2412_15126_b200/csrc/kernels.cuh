@@ -1066,7 +1066,7 @@ __global__ void k_lincomb(const __grid_constant__ LinCombArgs a, const PrimeCons
         const long long off = xi & (n - 1);
         U128 acc = {0, 0};
         for (int i = 0; i < a.n_terms; i++) {
-            const uint64_t v = a.term[i][b * a.term_ct[i] + r * a.term_ps[i] + (long long)j * n + off];
+            const uint64_t v = __ldg(a.term[i] + b * a.term_ct[i] + r * a.term_ps[i] + (long long)j * n + off);
             mac(acc, v, __ldg(a.k + (long long)i * a.nl + j));
             if ((i & 7) == 7) {  // keep the 128-bit sum bounded: reduce every 8 products
                 U128 red = {0, reduce_u128(acc, pc[j])};
