@@ -269,18 +269,26 @@ def bench_config(p):
             "l2": "inputs 1.9 GiB per operand set >> 126 MB L2 (no flush needed)"}
 
 
-# integer-pipe roof of the NTT: a radix-2 64-bit Shoup butterfly is
-# 11.3 IMAD (fma pipe, 64 lanes/clk/SM) per the SASS of ntt_pass_kernel
-IMAD_PER_BUTTERFLY = 11.3
+def _profile(name):
+    """A committed ncu summary (profiles/r02 first, then r01), or None."""
+    for rnd in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", rnd, name)
+        try:
+            with open(path) as fh:
+                return f"profiles/{rnd}/{name}", json.load(fh)
+        except (OSError, ValueError):
+            continue
+    return None, None
 
 
-def int_roofline(p, n_limbs, ms, sm_mhz):
-    bfly = n_limbs * (p.ring_degree // 2) * p.log_n
-    achieved = bfly / (ms * 1e-3) / 1e12
-    peak = 148 * 64 * (sm_mhz or 1965.0) * 1e6 / IMAD_PER_BUTTERFLY / 1e12
-    return {"bound": "int (IMAD pipe)", "achieved": round(achieved, 3), "peak": round(peak, 3),
-            "unit": "T butterflies/s", "frac": round(achieved / peak, 4),
-            "model": f"{IMAD_PER_BUTTERFLY} IMAD per butterfly (SASS), 148 SMs x 64 IMAD/clk x sm clock"}
+def pipe_roofline():
+    """FP64 / integer pipe utilisation of the NTT passes from the committed
+    ``ncu --set full`` capture (the NTT's real bound: DESIGN.md, kernels)."""
+    src, d = _profile("ntt_pipe_util.json")
+    if d is None:
+        return None
+    return {"bound": "fp64 / fma pipes (ncu)", "source": src + " (" + d.get("command", "") + ")",
+            "kernels": d["kernels"]}
 
 
 def time_region(torch, fn, reps, barrier=None):
@@ -298,25 +306,23 @@ def time_region(torch, fn, reps, barrier=None):
 
 
 def ntt_traffic():
-    """DRAM bytes of one forward NTT of the bench batch from the committed ncu capture."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ntt_fwd_traffic.json")
-    try:
-        with open(path) as fh:
-            return int(json.load(fh)["dram_bytes"])
-    except (OSError, ValueError, KeyError):
-        return None
+    """(source, DRAM bytes) of one forward NTT of the bench batch from the committed ncu capture."""
+    src, d = _profile("ntt_fwd_traffic.json")
+    return (src, int(d["dram_bytes"])) if d else (None, None)
+
+
+def keyswitch_traffic():
+    """(source, DRAM bytes) of 64 HMult+relinearise from the committed ncu launch list."""
+    src, d = _profile("relin64_traffic.json")
+    return (src, int(d["dram_bytes"])) if d else (None, None)
 
 
 def kernel_roofline():
     """Per-kernel DRAM GB/s of one primitive step from the committed ncu capture."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
-                        "kernel_roofline_step64.json")
-    try:
-        with open(path) as fh:
-            d = json.load(fh)
-    except (OSError, ValueError):
+    src, d = _profile("kernel_roofline_step64.json")
+    if d is None:
         return None
-    return {"source": "profiles/r01/kernel_roofline_step64.json (" + d.get("note", "") + ")",
+    return {"source": src + " (" + d.get("note", "") + ")", "peak_gbs": d.get("peak_gbs"),
             "kernels": [{k: e[k] for k in ("kernel", "time_share", "dram_gb_per_s", "frac_of_hbm")}
                         for e in d["kernels"] if e["time_share"] >= 0.01]}
 
@@ -357,26 +363,48 @@ def run_sharded_sort(torch, dist):
             "gpus": comm.world, "sharding": f"block pairs + placements round-robin, {dist.get_backend()} all-reduce"}
 
 
+def _timed(torch, fn, reps=1):
+    """Best-of-reps wall seconds of fn() bracketed by device syncs."""
+    best, r = None, None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fn()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best, r
+
+
+def _census(eng, fn):
+    """One run's CostReport (reset before, snapshot after: one pipeline, not several)."""
+    eng.cost_reset()
+    r = fn()
+    return eng.cost_snapshot().__dict__, r
+
+
 def run_pipelines(torch, quick=False):
-    """BASELINE pipeline latencies (seconds) on cuda:current, decrypted results checked."""
+    """BASELINE pipeline latencies (seconds) on cuda:current, decrypted results checked.
+    Every ``cost`` is the CostReport of exactly one run of the pipeline."""
     from oracle.plain import fractional_ranks  # result-level checker only
     from paper_2412_15126_b200 import (B200Engine, KernelConfig, SortConfig, StatisticQuery,
                                        block_merge, block_split, multi_sort, order_statistic_mask,
-                                       rank, read_row)
+                                       order_statistic_value, rank, read_row)
     from paper_2412_15126_b200.params import preset
 
     out = {}
-
-    def timed(fn, reps=1):
-        best = None
-        for _ in range(reps):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            r = fn()
-            torch.cuda.synchronize()
-            dt = time.perf_counter() - t0
-            best = dt if best is None else min(best, dt)
-        return best, r
+    # config 1: rank N=16 on ring 2^12 (composite g3^4 o f3^2)
+    v16 = np.random.default_rng(0).choice(64, 16, replace=False) / 64
+    eng = B200Engine(preset("cfg1"))
+    cfg1 = KernelConfig(mode="composite", composite=(4, 2))
+    ct = eng.encrypt(v16)
+    rank(eng, ct, 16, cfg1)  # warm-up: keys, plaintext cache
+    cost, _ = _census(eng, lambda: rank(eng, ct, 16, cfg1))
+    dt, res = _timed(torch, lambda: read_row(eng, rank(eng, ct, 16, cfg1).ranks, 16), reps=3)
+    out["rank_n16_s"] = {"latency_s": dt, "graph_replay_s": _graph_latency(eng, lambda c: rank(eng, c, 16, cfg1).ranks, ct),
+                         "exact_ranks": bool(np.array_equal(np.rint(res), fractional_ranks(v16))),
+                         "cost": cost, "params": "cfg1", "kernel": "composite g3^4 o f3^2"}
+    del eng
 
     # config 3: rank N=128, composite g3^4 o f3^2, ring 2^16, 29 levels
     rng = np.random.default_rng(0)
@@ -385,62 +413,139 @@ def run_pipelines(torch, quick=False):
     cfg = KernelConfig(mode="composite", composite=(4, 2))
     ct = eng.encrypt(v128)
     rank(eng, ct, 128, cfg)  # warm-up: Galois / relin key generation, plaintext cache
-    eng.cost_reset()
-    dt, res = timed(lambda: read_row(eng, rank(eng, ct, 128, cfg).ranks, 128), reps=3)
+    cost, _ = _census(eng, lambda: rank(eng, ct, 128, cfg))
+    dt, res = _timed(torch, lambda: read_row(eng, rank(eng, ct, 128, cfg).ranks, 128), reps=3)
     exact = bool(np.array_equal(np.rint(res), fractional_ranks(v128)))
     out["rank_n128_s"] = {"latency_s": dt, "graph_replay_s": _graph_latency(eng, lambda c: rank(eng, c, 128, cfg).ranks, ct),
                           "exact_ranks": exact,
                           "max_rank_err": float(np.abs(res - fractional_ranks(v128)).max()),
-                          "cost": eng.cost_snapshot().__dict__, "params": "cfg3",
-                          "kernel": "composite g3^4 o f3^2"}
+                          "cost": cost, "params": "cfg3", "kernel": "composite g3^4 o f3^2"}
     # the reference's own comparison: Chebyshev interpolant, degree 1024
     ccfg = KernelConfig(mode="chebyshev", degree=1024)
     rank(eng, ct, 128, ccfg)
-    eng.cost_reset()
-    dt, res = timed(lambda: read_row(eng, rank(eng, ct, 128, ccfg).ranks, 128), reps=2)
+    cost, _ = _census(eng, lambda: rank(eng, ct, 128, ccfg))
+    dt, res = _timed(torch, lambda: read_row(eng, rank(eng, ct, 128, ccfg).ranks, 128), reps=2)
     out["rank_n128_chebyshev_d1024_s"] = {
         "latency_s": dt, "graph_replay_s": _graph_latency(eng, lambda c: rank(eng, c, 128, ccfg).ranks, ct),
         "exact_ranks": bool(np.array_equal(np.rint(res), fractional_ranks(v128))),
         "max_rank_err": float(np.abs(res - fractional_ranks(v128)).max()),
-        "cost": eng.cost_snapshot().__dict__, "params": "cfg3", "kernel": "chebyshev d=1024 (reference)"}
+        "cost": cost, "params": "cfg3", "kernel": "chebyshev d=1024 (reference)"}
     del eng
     torch.cuda.empty_cache()
     if quick:
         return out
 
-    # config 4: argmin / argmax / k=64 masks N=128 on the long chain
+    # config 4: argmin / argmax / k=64 masks AND selected values, N=128, long chain
     eng = B200Engine(preset("long"))
     cfg4 = KernelConfig(mode="composite", composite=(4, 2), indicator_composite=(4, 2),
-                        tie_margin=2.0 ** -11)
+                        tie_margin=2.0 ** -11, goldschmidt_iters=8)
     ct = eng.encrypt(v128)
     order = np.argsort(v128)
-    for name, q, want in (("argmin", StatisticQuery("min"), order[0]),
-                          ("argmax", StatisticQuery("max"), order[-1]),
-                          ("median_k64", StatisticQuery("kth", k=64), order[63])):
-        order_statistic_mask(eng, ct, 128, q, cfg4)  # warm-up keys
-        dt, m = timed(lambda: read_row(eng, order_statistic_mask(eng, ct, 128, q, cfg4), 128))
+    for name, q, pos in (("argmin", StatisticQuery("min"), 0),
+                         ("argmax", StatisticQuery("max"), 127),
+                         ("median_k64", StatisticQuery("kth", k=64), 63)):
+        want = order[pos]
+        order_statistic_value(eng, ct, 128, q, cfg4)  # warm-up keys
+        cost, _ = _census(eng, lambda q=q: order_statistic_mask(eng, ct, 128, q, cfg4))
+        dt, m = _timed(torch, lambda q=q: read_row(eng, order_statistic_mask(eng, ct, 128, q, cfg4), 128))
         gdt = _graph_latency(eng, lambda c, q=q: order_statistic_mask(eng, c, 128, q, cfg4), ct)
+        vcost, _ = _census(eng, lambda q=q: order_statistic_value(eng, ct, 128, q, cfg4))
+        vdt, val = _timed(torch, lambda q=q: eng.decrypt(order_statistic_value(eng, ct, 128, q, cfg4))[0])
+        vgdt = _graph_latency(eng, lambda c, q=q: order_statistic_value(eng, c, 128, q, cfg4), ct)
         out[f"{name}_n128_s"] = {"latency_s": dt, "graph_replay_s": gdt,
                                  "index_ok": bool(int(np.argmax(m)) == int(want)),
                                  "max_onehot_err": float(np.abs(m - np.eye(128)[want]).max()),
-                                 "params": "long"}
+                                 "cost": cost,
+                                 "value_latency_s": vdt, "value_graph_replay_s": vgdt,
+                                 "value": float(val), "value_err": float(abs(val - v128[want])),
+                                 "value_cost": vcost, "params": "long",
+                                 "note": "value = mask + SumC(mask*v) * Goldschmidt(SumC(mask)), 8 iterations"}
 
     # config 5: sort N=1024 (8 blocks of 128), composite comparisons
     v1024 = np.random.default_rng(0).choice(8192, 1024, replace=False) / 8192
     scfg = SortConfig(kernel=KernelConfig(mode="composite", composite=(6, 2),
                                           indicator_composite=(6, 2)), tie_correction=False)
     bv = block_split(eng, v1024)
-    eng.cost_reset()
-    dt, srt = timed(lambda: block_merge(eng, multi_sort(eng, bv, scfg)))
-    cost = eng.cost_snapshot().__dict__
-    warm, _ = timed(lambda: block_merge(eng, multi_sort(eng, bv, scfg)))
-    out["sort_n1024_s"] = {"latency_s": dt, "warm_latency_s": warm, "order_ok": bool(np.array_equal(np.argsort(srt), np.arange(1024))),
+    first, _ = _timed(torch, lambda: block_merge(eng, multi_sort(eng, bv, scfg)))
+    cost, _ = _census(eng, lambda: multi_sort(eng, bv, scfg))
+    warm, srt = _timed(torch, lambda: block_merge(eng, multi_sort(eng, bv, scfg)))
+    out["sort_n1024_s"] = {"latency_s": first, "warm_latency_s": warm,
+                           "order_ok": bool(np.array_equal(np.argsort(srt), np.arange(1024))),
                            "max_abs_err": float(np.abs(srt - np.sort(v1024)).max()),
                            "cost": cost, "params": "long", "gpus": 1,
                            "note": "latency_s: first run (includes generating this pipeline's Galois keys and "
-                                   "encoding its constants); warm_latency_s: second run (a CUDA-graph replay, "
-                                   "tools/graph_pipe.py sort1024, is 2% faster still: the batched sort is "
-                                   "GPU-bound)"}
+                                   "encoding its constants); warm_latency_s: second run"}
+    del eng, bv
+    torch.cuda.empty_cache()
+    # the tie-corrected sort (block tie offsets) needs two more levels: long58
+    eng = B200Engine(preset("long58"))
+    scfg = SortConfig(kernel=KernelConfig(mode="composite", composite=(6, 2),
+                                          indicator_composite=(6, 2)), tie_correction=True)
+    bv = block_split(eng, v1024)
+    first, _ = _timed(torch, lambda: block_merge(eng, multi_sort(eng, bv, scfg)))
+    cost, _ = _census(eng, lambda: multi_sort(eng, bv, scfg))
+    warm, srt = _timed(torch, lambda: block_merge(eng, multi_sort(eng, bv, scfg)))
+    out["sort_n1024_tie_corrected_s"] = {
+        "latency_s": first, "warm_latency_s": warm,
+        "order_ok": bool(np.array_equal(np.argsort(srt), np.arange(1024))),
+        "max_abs_err": float(np.abs(srt - np.sort(v1024)).max()),
+        "cost": cost, "params": "long58", "gpus": 1}
+    del eng, bv
+    torch.cuda.empty_cache()
+    return out
+
+
+def cpu_pipelines(quick=False):
+    """CPU time of the same pipelines beside the GPU latencies (rank 0, N=1):
+    * ``oracle_engine``: the product's engine over the CPU RNS-CKKS oracle
+      (oracle/ckks_oracle.c, OpenMP over all host threads) -- the like-for-like
+      CKKS baseline, same circuit, parameters and keys as the GPU run;
+    * ``slot_simulator``: oracle/slotsim.py, the reference simulator
+      (HESimulator, reference engine.py:133-328) restated in numpy, single thread:
+      the reference's own CPU path (float64 slots, no cryptography)."""
+    import paper_2412_15126_b200 as M
+    from oracle.oracle import oracle_engine
+    from oracle.slotsim import SimParams, SlotSim
+    from paper_2412_15126_b200.params import preset
+
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    out = {"cores": threads, "nproc": os.cpu_count()}
+    v16 = np.random.default_rng(0).choice(64, 16, replace=False) / 64
+    v128 = np.random.default_rng(0).choice(1024, 128, replace=False) / 1024
+    v1024 = np.random.default_rng(0).choice(8192, 1024, replace=False) / 8192
+    cfg = M.KernelConfig(mode="composite", composite=(4, 2))
+
+    def wall(fn):
+        t0 = time.perf_counter()
+        fn()
+        return time.perf_counter() - t0
+
+    # oracle engine (CKKS on the CPU): cfg1 rank N=16 whole; cfg3 rank N=128 whole
+    for name, preset_name, v, n in (("rank_n16_cfg1", "cfg1", v16, 16), ("rank_n128_cfg3", "cfg3", v128, 128)):
+        if quick and n > 16:
+            continue
+        e = oracle_engine(preset(preset_name))
+        ct = e.encrypt(v)
+        first = wall(lambda: M.rank(e, ct, n, cfg))  # includes this pipeline's key generation
+        warm = wall(lambda: M.rank(e, ct, n, cfg))
+        out[f"oracle_engine_{name}_s"] = {"latency_s": warm, "first_run_s": first, "threads": threads}
+        del e
+    # the reference simulator restated (slot arithmetic only, single thread)
+    sims = {}
+    s1 = SlotSim(SimParams(2048, 22))
+    sims["rank_n16_cfg1"] = lambda: M.rank(s1, s1.encrypt(v16), 16, cfg)
+    s3 = SlotSim(SimParams(32768, 29))
+    sims["rank_n128_cfg3"] = lambda: M.rank(s3, s3.encrypt(v128), 128, cfg)
+    sl = SlotSim(SimParams(32768, 56))
+    cfg4 = M.KernelConfig(mode="composite", composite=(4, 2), indicator_composite=(4, 2),
+                          tie_margin=2.0 ** -11, goldschmidt_iters=8)
+    sims["argmax_value_n128"] = lambda: M.order_statistic_value(sl, sl.encrypt(v128), 128, M.StatisticQuery("max"), cfg4)
+    scfg = M.SortConfig(kernel=M.KernelConfig(mode="composite", composite=(6, 2), indicator_composite=(6, 2)),
+                        tie_correction=False)
+    sims["sort_n1024"] = lambda: M.multi_sort(sl, M.block_split(sl, v1024), scfg)
+    for name, fn in sims.items():
+        fn()  # warm-up (coefficient caches)
+        out[f"slot_simulator_{name}_s"] = min(wall(fn) for _ in range(3))
     return out
 
 
@@ -542,6 +647,8 @@ def gpu_arm(args):
         peak = float(peaks.get("hbm_gbs", 6650.0))
         ntt_gbs = parts["ntt_fwd"] / (ntt_ms * 1e-3) / GB
         ks_gbs = ks_bytes / (ks_ms * 1e-3) / GB
+        ntt_src, ntt_tr = ntt_traffic()
+        ks_src, ks_tr = keyswitch_traffic()
         value = world * step_bytes / (ms * 1e-3) / GB
         line = {
             "metric": "NTT+KeySwitch GB/s vs HBM roof (cfg2 primitive step, 64 ct, ring 2^16, 30+3 limbs)",
@@ -561,27 +668,36 @@ def gpu_arm(args):
             "api_calls_per_step": launches,
             "roofline": {"bound": "hbm", "kernel": "forward NTT (ntt_pass_kernel x2 per chunk)",
                          "achieved": round(ntt_gbs, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(ntt_gbs / peak, 4), "traffic": ntt_traffic(),
-                         "traffic_source": "profiles/r01/ntt_fwd_traffic.json (ncu --set full, same workload)",
+                         "frac": round(ntt_gbs / peak, 4), "traffic": ntt_tr,
+                         "traffic_source": ntt_src,
                          "algorithmic_bytes": parts["ntt_fwd"], "ms": round(ntt_ms, 4),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
             "kernel_roofline": kernel_roofline(),
-            "roofline_int": int_roofline(p, N_CT * 2 * len(p.q_primes), ntt_ms,
-                                         clk.summary().get("sm_mhz")),
+            "roofline_pipes": pipe_roofline(),
             "roofline_keyswitch": {"bound": "hbm", "unit_of_work": "64 x HMult+relinearise (no rescale)", "achieved": round(ks_gbs, 1), "peak": peak,
                                    "unit": "GB/s", "frac": round(ks_gbs / peak, 4),
-                                   "algorithmic_bytes": ks_bytes, "ms": round(ks_ms, 4)},
+                                   "algorithmic_bytes": ks_bytes, "ms": round(ks_ms, 4),
+                                   "traffic": ks_tr, "traffic_source": ks_src,
+                                   "traffic_over_algorithmic": round(ks_tr / ks_bytes, 2) if ks_tr else None},
             "roofline_inverse_ntt": {"achieved": round(parts["ntt_inv"] / (intt_ms * 1e-3) / GB, 1),
                                      "ms": round(intt_ms, 4)},
             "e2e": {"value": round(world * step_bytes / (e2e_ms * 1e-3) / GB, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": int(host_x.numel() * 8),
                     "d2h_bytes_per_step": int(host_out.numel() * 8), "ms_per_step": round(e2e_ms, 3),
-                    "pipeline": f"{len(e2e_step.bounds)} chunks: H2D / compute / D2H on three streams"},
+                    "pipeline": f"{len(e2e_step.bounds)} chunks: H2D / compute / D2H on three streams",
+                    "outputs_copied": "the 64 rescaled ciphertexts (d2h); the other 16 output sets of the step "
+                                      "(forward/inverse NTT in place, 64 products, 15 x 64 rotations) stay resident "
+                                      "in HBM as the inputs of the next op, as in a pipeline"},
             "clocks": clk.summary(),
             "pipelines": pipelines,
         }
         if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(args, threads=1 if args.quick else None)
+            line["cpu_baseline"] = cpu_baseline(args)
+            if pipelines is not None and world == 1:
+                try:
+                    line["cpu_pipelines"] = cpu_pipelines(quick=args.quick)
+                except Exception as e:  # never blocks the GPU line
+                    line["cpu_pipelines"] = {"failed": str(e)}
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
@@ -591,8 +707,11 @@ def gpu_arm(args):
 # ----------------------------------------------------------------------
 # CPU arms (oracle)
 # ----------------------------------------------------------------------
-def cpu_sample(threads=None, n_ct=1, rotations=2):
-    """Time the oracle on a bounded sample of the step; return GB/s of the same metric."""
+def cpu_sample(threads=None, n_ct=4, rotations=len(ROT_STEPS)):
+    """Time the oracle on a bounded sample of the step (n_ct ciphertexts through the
+    whole primitive set, all 15 rotations); GB/s of the same metric, with the
+    algorithmic bytes charged per ciphertext exactly as on the GPU arm
+    (step bytes x n_ct / 64: the evaluation keys amortised over the 64)."""
     if threads:
         os.environ["OMP_NUM_THREADS"] = str(threads)
     from oracle.oracle import OracleCKKS
@@ -610,13 +729,13 @@ def cpu_sample(threads=None, n_ct=1, rotations=2):
             a[..., i, :] = rng.integers(0, q, shape_prefix + (p.ring_degree,), dtype=np.uint64)
         return a
 
-    x, y = rnd((2,)), rnd((2,))
+    xs, ys = [rnd((2,)) for _ in range(n_ct)], [rnd((2,)) for _ in range(n_ct)]
     key = np.empty((p.dnum, 2, n_all, p.ring_degree), dtype=np.uint64)
     for i, q in enumerate(p.all_primes):
         key[:, :, i, :] = rng.integers(0, q, (p.dnum, 2, p.ring_degree), dtype=np.uint64)
     L = nl - 1
     t0 = time.perf_counter()
-    for _ in range(n_ct):
+    for x, y in zip(xs, ys):
         f = np.stack([o.ntt(x[k], range(nl)) for k in range(2)])
         np.stack([o.ntt(f[k], range(nl), inverse=True) for k in range(2)])
         prod = o.mul_relin(x, y, key, L)
@@ -624,22 +743,21 @@ def cpu_sample(threads=None, n_ct=1, rotations=2):
             o.rotate_raw(x, key, pow(5, ROT_STEPS[k], 2 * p.ring_degree), L)
         o.rescale(prod, L)
     dt = time.perf_counter() - t0
-    parts, _ = algorithmic_bytes(p, n_ct=n_ct)
-    n = p.ring_degree
-    ct_b = 2 * nl * n * 8
-    evk = 2 * p.dnum * (nl + len(p.p_primes)) * n * 8
-    sample_bytes = (parts["ntt_fwd"] + parts["ntt_inv"] + parts["hmult_relin"] + parts["rescale"]
-                    + rotations * (n_ct * 2 * ct_b + evk))
+    parts, _ = algorithmic_bytes(p)
+    share = n_ct / N_CT
+    sample_bytes = share * (parts["ntt_fwd"] + parts["ntt_inv"] + parts["hmult_relin"] + parts["rescale"]
+                            + parts["rotate_15"] * rotations / len(ROT_STEPS))
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return {"value": round(sample_bytes / dt / GB, 4), "unit": "GB/s", "cores": cores,
             "kind": "port", "seconds": round(dt, 3),
-            "sample": f"{n_ct} ct of cfg2: fwd+inv NTT, 1 HMult/relin, {rotations} of 15 rotations, "
-                      f"1 rescale (oracle/ckks_oracle.c, scalar __int128 arithmetic)"}
+            "sample": f"{n_ct} of the 64 cfg2 ciphertexts through the whole step (fwd+inv NTT, HMult/relin, "
+                      f"{rotations} rotations, rescale), bytes charged as {n_ct}/64 of the step "
+                      f"(oracle/ckks_oracle.c, OpenMP over limbs, scalar __int128 arithmetic)"}
 
 
 def cpu_baseline(args, threads=None):
     try:
-        return cpu_sample(threads=threads)
+        return cpu_sample(threads=threads, n_ct=1 if args.quick else 4)
     except Exception as e:  # the baseline never blocks the GPU line
         return {"value": None, "unit": "GB/s", "cores": None, "kind": "port", "sample": f"failed: {e}"}
 
@@ -653,9 +771,9 @@ def reference_arm(args):
     vals = []
     res = None
     for _ in range(args.warmup if args.warmup < 2 else 1):
-        cpu_sample()
+        cpu_sample(n_ct=1)
     for _ in range(args.steps):
-        res = cpu_sample()
+        res = cpu_sample(n_ct=1)  # one ciphertext of the step per timed step (bounded run time)
         vals.append(res["value"])
     v = float(np.median(vals))
     line = {

@@ -568,7 +568,7 @@ void orc_rotate(const orc_ctx *c, const uint64_t *a, const uint64_t *gkey, uint6
 /* ------------------------------------------------------------------ */
 
 /* counter-based generator: word(seed, stream, ctr) -- restated bit for bit
- * by csrc/sampling.cuh so uniform polynomials agree between CPU and GPU */
+ * by k_uniform in csrc/kernels.cuh so uniform polynomials agree between CPU and GPU */
 static inline uint64_t mix64(uint64_t z) {
     z += 0x9e3779b97f4a7c15ull;
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;

@@ -16,7 +16,6 @@
 
 #include "../../include/slotrank_b200.h"
 #include "kernels.cuh"
-#include "ntt_cluster.cuh"
 #include "modarith.cuh"
 #include "ntt.cuh"
 
@@ -130,28 +129,17 @@ struct srk_ctx {
     LimbConsts lc_pinv;               // P^-1 mod q_i
     LimbConsts lc_pmod;               // P mod prime_i (all primes)
     std::vector<LimbConsts> lc_qlinv; // [level]: q_level^-1 mod q_i
-    int ntt_chunk = 128;              // limbs per L2-resident NTT chunk
-    int ntt_split = 1;                // FP64-only pass kernels for runs of < 2^41 primes (SRK_NTT_SPLIT)
-    // ModDown forward NTT: 0 = conversion and combine in separate streaming
-    // kernels (default: fastest on B200 -- the NTT passes are latency-bound and
-    // extra loads in them cost more than the streams; profiles/r01), 1 = both
-    // fused into the NTT, 2 = conversion separate, combine fused into the store
-    int moddown_mode = 0;
-    int rescale_fused = 1;            // spread + combine fused into the rescale NTT (SRK_RESCALE_FUSED=0: streaming kernels)
-    int ks_fused = 1;                 // Q-limb inner product fused into the combine (SRK_KS_FUSED=0: off)
-    int ks_streams = 2;               // hoisted outputs alternate over two streams (SRK_KS_STREAMS)
+    int ntt_chunk = 128;              // limb-polys per L2-resident NTT chunk (SRK_NTT_CHUNK: tests force chunking)
+    int ks_streams = 2;               // hoisted outputs alternate over two streams
     cudaStream_t side = nullptr;      // the second lane
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // NTT chunk lanes: independent limb chunks of one NTT alternate between the
     // caller's stream and nside[lane], so one chunk's pass tail overlaps the
     // next chunk's passes (lane = 1 when called from the key-switch side lane)
     int ntt_streams = 2;
-    int md_chunk = 0;  // L2-chunked ModDown: limbs per NTT + combine group (SRK_MD_CHUNK; 0 = off)
     int ws_batch = SRK_WS_BATCH;  // ciphertexts per internal chunk (SRK_WS_BATCH env: smaller workspace)
-    int ntt_cta_threads = 128;  // threads per NTT pass CTA (SRK_NTT_CTA; 128: 8 CTAs/SM, cheaper barriers)
-    int ntt_cluster = 0;  // 1: forward FP64 plain NTTs as one 8-CTA cluster per limb (slower: DESIGN.md)
-    int conv_f64 = 1;  // ModDown conversion on the FP64 + integer pipes (k_moddown_conv_f64)
-    unsigned conv_cpt = 4;  // coefficients per thread of k_moddown_conv_f64 (amortises its staging)
+    int ntt_cta_threads = 128;  // threads per NTT pass CTA (128: 8 CTAs/SM, cheaper barriers)
+    unsigned conv_cpt = 4;  // coefficients per thread of the conversions (amortises their staging)
     cudaStream_t nside[2] = {nullptr, nullptr};
     cudaEvent_t ev_nfork[2] = {nullptr, nullptr}, ev_njoin[2] = {nullptr, nullptr};
 };
@@ -279,19 +267,10 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     c->alpha = (n_q + dnum - 1) / dnum;
     c->n_primes = n_q + n_p;
     c->primes.assign(primes, primes + c->n_primes);
+    // two run-time settings: the NTT chunk (tests force multi-chunk launches) and the
+    // key-switch workspace batch (several ranks sharing one GPU need a smaller one)
     if (const char *e = getenv("SRK_NTT_CHUNK")) c->ntt_chunk = std::max(1, atoi(e));
-    if (const char *e = getenv("SRK_NTT_SPLIT")) c->ntt_split = atoi(e);
-    if (const char *e = getenv("SRK_MODDOWN_MODE")) c->moddown_mode = atoi(e);
-    if (const char *e = getenv("SRK_RESCALE_FUSED")) c->rescale_fused = atoi(e);
-    if (const char *e = getenv("SRK_KS_FUSED")) c->ks_fused = atoi(e);
-    if (const char *e = getenv("SRK_KS_STREAMS")) c->ks_streams = atoi(e);
-    if (const char *e = getenv("SRK_NTT_STREAMS")) c->ntt_streams = atoi(e);
-    if (const char *e = getenv("SRK_MD_CHUNK")) c->md_chunk = std::max(0, atoi(e));
     if (const char *e = getenv("SRK_WS_BATCH")) c->ws_batch = std::max(1, atoi(e));
-    if (const char *e = getenv("SRK_NTT_CTA")) c->ntt_cta_threads = std::min(256, std::max(64, atoi(e)));
-    if (const char *e = getenv("SRK_NTT_CLUSTER")) c->ntt_cluster = atoi(e);
-    if (const char *e = getenv("SRK_CONV_F64")) c->conv_f64 = atoi(e);
-    if (const char *e = getenv("SRK_CONV_CPT")) c->conv_cpt = std::max(1, atoi(e));
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -515,8 +494,6 @@ static FuseArgs no_fuse() {
     FuseArgs f;
     memset(&f, 0, sizeof f);
     f.galois = 1;
-    f.add_galois = 1;
-    f.acc_galois = 1;
     f.out_galois = 1;
     f.out_galois_inv = 1;
     return f;
@@ -525,11 +502,15 @@ static FuseArgs no_fuse() {
 template <int LOG_T, bool INV, bool COL, int IO, int KM, int LOGN>
 static void launch_kernel_n(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
                             const NttTables &tb, int log_n, const FuseArgs &ff) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    // the attribute is per device: one bit per device ordinal
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_relaxed) & bit)) {
         cudaFuncSetAttribute(ntt_pass_kernel<LOG_T, INV, COL, IO, KM, LOGN>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        attr_set = true;
+        attr_done.fetch_or(bit, std::memory_order_relaxed);
     }
     ntt_pass_kernel<LOG_T, INV, COL, IO, KM, LOGN><<<grid, threads, smem, s>>>(bb, tb, log_n, ff);
 }
@@ -573,8 +554,9 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
         if (ff.add0) ff.add0 += (long long)l0 * c->n;
         if (ff.add1) ff.add1 += (long long)l0 * c->n;
         if (ff.pt) ff.pt += (long long)l0 * c->n;
-        if (ff.mat) ff.mat += l0;
-        if (ff.corr) ff.corr += l0;
+        if (ff.ks_d) ff.ks_d += (long long)l0 * c->n;
+        if (ff.ks_ext) ff.ks_ext += (long long)l0 * c->n;
+        if (ff.ks_key) ff.ks_key += (long long)l0 * c->n;
         for (int k = 0; k + l0 < SRK_MAXP; k++) {
             ff.mulc.w[k] = f.mulc.w[k + l0];
             ff.mulc.ws[k] = f.mulc.ws[k + l0];
@@ -586,42 +568,14 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
     }
     bb.n_limbs = nlc;
     dim3 grid(subs / cb, b.n_polys, nlc);
-    // plain / automorphism / rescale-spread loads, plain / scaled / rescale stores:
-    // FP64-only kernel for q < 2^41 chunks, Harvey-only integer kernel otherwise
-    // (the FP64 spread needs the dropped prime < 2^41 too)
-    if constexpr (IO == 0 || IO == 3 || IO == 2) {
-        if (f64 && (IO != 2 || f.top_q < SRK_F64_Q))
-            launch_kernel<LOG_T, INV, COL, IO, 1>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
-        else
-            launch_kernel<LOG_T, INV, COL, IO, 2>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
-    } else {
-        launch_kernel<LOG_T, INV, COL, IO, 0>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
-    }
-    LAUNCHED();
-    return SRK_OK;
-}
-
-// forward plain NTT of a chunk of FP64 limbs (ring 2^16): one 8-CTA cluster per
-// limb, column -> row exchange in distributed shared memory (ntt_cluster.cuh)
-static int launch_cluster_fwd(const srk_ctx *c, LimbBatch b, int l0, int nlc, const FuseArgs &f,
-                              cudaStream_t s) {
-    static bool attr_set = false;
-    const size_t smem = (size_t)SRK_CL_SMEM_WORDS * 8;
-    if (!attr_set) {
-        CU(cudaFuncSetAttribute(ntt_fwd_cluster_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
-    }
-    LimbBatch bb = b;
-    FuseArgs ff = f;
-    if (l0) {
-        bb.ptr = b.ptr + (long long)l0 * c->n;
-        bb.split = b.split - l0;
-        bb.off_a = b.off_a + l0;
-        bb.off_b = b.off_b + l0;
-        if (ff.src) ff.src += (long long)l0 * c->n;
-    }
-    bb.n_limbs = nlc;
-    ntt_fwd_cluster_f64<<<dim3(SRK_CL_CTAS, b.n_polys, nlc), SRK_CL_THREADS, smem, s>>>(bb, tables(c), ff);
+    // FP64-only kernel for q < 2^41 chunks, Harvey-only integer kernel otherwise; both
+    // passes of a transform use the same one (the intermediate format differs).  The
+    // rescale's FP64 spread needs the dropped prime < 2^41 too (IO 2 on either pass:
+    // LD_SPREAD first, ST_RESCALE last)
+    if (f64 && (IO != 2 || f.top_q < SRK_F64_Q))
+        launch_kernel<LOG_T, INV, COL, IO, 1>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
+    else
+        launch_kernel<LOG_T, INV, COL, IO, 2>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
     LAUNCHED();
     return SRK_OK;
 }
@@ -638,8 +592,8 @@ static int pass_t(const srk_ctx *c, int log_t, LimbBatch b, int l0, int nlc, con
     }
 }
 
-// forward: first pass fused load `ld` (LD_PLAIN/LD_BCONV/LD_SPREAD), last pass store `st`
-// (ST_PLAIN/ST_MODDOWN/ST_RESCALE); inverse: ld in {LD_PLAIN, LD_AUTO}, st in {ST_PLAIN, ST_SCALE}
+// forward: first pass fused load `ld` (LD_PLAIN/LD_SPREAD), last pass store `st`
+// (ST_PLAIN/ST_KSC/ST_RESCALE); inverse: ld in {LD_PLAIN, LD_AUTO}, st in {ST_PLAIN, ST_SCALE}
 static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &f, int ld, int st,
                    cudaStream_t s) {
     if (b.n_limbs <= 0 || b.n_polys <= 0) return SRK_OK;
@@ -662,23 +616,19 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
         int cls;
     };
     std::vector<Chunk> chunks;
-    const bool class_split = b.mode == 1 && c->ntt_split;
-    if (class_split) {
+    if (b.mode == 1) {
         // ModUp targets mix 40-bit and 60-bit primes per digit: one FP64 launch that
         // skips the >= 2^41 limbs and one integer launch that skips the rest
         // (independent, so they run on the two streams side by side)
         chunks.push_back({0, b.n_limbs, true, 1});
         chunks.push_back({0, b.n_limbs, false, 2});
     }
-    for (int l0 = 0, nlc = 0; !class_split && l0 < b.n_limbs; l0 += nlc) {
+    for (int l0 = 0, nlc = 0; b.mode == 0 && l0 < b.n_limbs; l0 += nlc) {
         nlc = std::min(per, b.n_limbs - l0);
-        bool f64 = false;
-        if (b.mode == 0 && c->ntt_split) {
-            f64 = f64_limb(l0);
-            int k = 1;
-            while (k < nlc && f64_limb(l0 + k) == f64) k++;
-            nlc = k;
-        }
+        const bool f64 = f64_limb(l0);
+        int k = 1;
+        while (k < nlc && f64_limb(l0 + k) == f64) k++;
+        nlc = k;
         chunks.push_back({l0, nlc, f64, 0});
     }
     // independent chunks alternate between s and this lane's NTT side stream
@@ -693,27 +643,15 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
         const bool f64 = chunks[ci].f64;
         b.cls = chunks[ci].cls;
         cudaStream_t cs = (two && (ci & 1)) ? c->nside[lane] : s;
-        if (!inverse && ld == LD_PLAIN && st == ST_PLAIN && f64 && c->log_n == 16 && c->ntt_cluster) {
-            TRY(launch_cluster_fwd(c, b, l0, nlc, f, cs));
-            continue;
-        }
         if (!inverse) {
             switch (ld) {
                 case LD_PLAIN: TRY((pass_t<false, true, LD_PLAIN>(c, log_r, b, l0, nlc, f, cs, f64))); break;
-                case LD_BCONV:
-                    if (f.n_src <= 4)
-                        TRY((pass_t<false, true, LD_BCONV>(c, log_r, b, l0, nlc, f, cs, f64)));
-                    else if (f.n_src <= 8)
-                        TRY((pass_t<false, true, LD_BCONV8>(c, log_r, b, l0, nlc, f, cs, f64)));
-                    else
-                        TRY((pass_t<false, true, LD_BCONV16>(c, log_r, b, l0, nlc, f, cs, f64)));
-                    break;
                 case LD_SPREAD: TRY((pass_t<false, true, LD_SPREAD>(c, log_r, b, l0, nlc, f, cs, f64))); break;
                 default: return fail(SRK_EINVAL, "bad forward load mode");
             }
             switch (st) {
                 case ST_PLAIN: TRY((pass_t<false, false, ST_PLAIN>(c, log_c, b, l0, nlc, f, cs, f64))); break;
-                case ST_MODDOWN: TRY((pass_t<false, false, ST_MODDOWN>(c, log_c, b, l0, nlc, f, cs, f64))); break;
+                case ST_KSC: TRY((pass_t<false, false, ST_KSC>(c, log_c, b, l0, nlc, f, cs, f64))); break;
                 case ST_RESCALE: TRY((pass_t<false, false, ST_RESCALE>(c, log_c, b, l0, nlc, f, cs, f64))); break;
                 default: return fail(SRK_EINVAL, "bad forward store mode");
             }
@@ -896,7 +834,7 @@ extern "C" int srk_tensor(srk_ctx *c, const uint64_t *a, const uint64_t *b, uint
                           int level, void *stream) {
     TRY(check_level(c, level));
     const long long total = (long long)(level + 1) * c->n;
-    k_tensor<<<grid_for(total), 256, 0, S(stream)>>>(a, b, d, c->d_pc, c->log_n, level + 1);
+    k_tensor<<<grid_for(total), 256, 0, S(stream)>>>(a, b, 0, d, 0, c->d_pc, c->log_n, level + 1, 1);
     LAUNCHED();
     return SRK_OK;
 }
@@ -948,21 +886,12 @@ static int rescale_impl(srk_ctx *c, const uint64_t *a, long long a_ct, long long
     g.acc_ct = a_ct;
     g.acc_ps = a_ps;
     g.pre_mode = mode;
-    g.pt = pt;
-    g.pt_ct = pt_ct;
+    g.pt = pt ? pt : a;  // never null: the store's loads may be speculated
+    g.pt_ct = pt ? pt_ct : 0;
     if (k) g.pre = *k;
     g.mulc = c->lc_qlinv[level];
     LimbBatch bq = cbatch(tb, B, 2, 2ll * level * n, (long long)level * n, level, 0);
-    if (c->rescale_fused) return ntt_run(c, bq, false, g, LD_SPREAD, ST_RESCALE, s);
-    // streaming spread -> plain NTT -> streaming combine
-    k_rescale_spread<<<grid_for(2ll * B * level * n), 256, 0, s>>>(top, tb, c->d_pc, c->log_n, level, B);
-    LAUNCHED();
-    TRY(ntt_run(c, bq, false, no_fuse(), LD_PLAIN, ST_PLAIN, s));
-    k_rescale_combine<<<grid_for(2ll * B * level * n), 256, 0, s>>>(
-        a, a_ct, a_ps, pt, pt_ct, k ? *k : LimbConsts{}, mode, tb, c->lc_qlinv[level], out, out_ct,
-        c->d_pc, c->log_n, level, B);
-    LAUNCHED();
-    return SRK_OK;
+    return ntt_run(c, bq, false, g, LD_SPREAD, ST_RESCALE, s);
 }
 
 // chunk a batch of B into balanced pieces of at most c->ws_batch (36 -> 18 + 18,
@@ -1042,18 +971,73 @@ extern "C" int srk_mul_plain_rescale(srk_ctx *c, const uint64_t *a, const uint64
 }
 
 // ---------------------------------------------------------------------
-// hybrid key switching of B polys d (ct stride d_ct, NTT form, level `level`):
+// hybrid key switching (keyswitch_impl below)
+// ---------------------------------------------------------------------
+// conversion grids: x shrunk by up to conv_cpt coefficients per thread (to amortise
+// the CTA's constant staging) only while >= ~3 waves of CTAs remain, so the
+// one-ciphertext ops of the pipelines keep enough CTAs in flight
+static inline dim3 conv_grid(const srk_ctx *c, dim3 g) {
+    const unsigned long long ctas = (unsigned long long)g.x * g.y * g.z;
+    unsigned cpt = c->conv_cpt;
+    while (cpt > 1 && ctas / cpt < 148ull * 8 * 3) cpt >>= 1;
+    return dim3(std::max(1u, g.x / cpt), g.y, g.z);
+}
+
+// ModDown base conversion P (or P u {q_l}) -> q_0..q_{nout-1} with exact rounding,
+// coefficient domain, into conv [B][2][nout] (ct stride cv_ct, poly stride cv_ps):
+//   conv[t] = sum_k z_k m_kt - v [prod src]_{q_t},  v = round(sum_k z_k / p_k)
+static int moddown_conv(srk_ctx *c, const BconvPlan &pl, const uint64_t *z, long long z_ct, long long z_ps,
+                        const uint8_t *vround, uint64_t *conv, long long cv_ct, long long cv_ps, int B,
+                        int nout, cudaStream_t s) {
+    const long long n = c->n;
+    const int ns = pl.n_src;
+    dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + SRK_CONV_TG - 1) / SRK_CONV_TG);
+    const dim3 g2 = conv_grid(c, grid);
+#define SRK_CONV_LAUNCH(MK)                                                                               \
+    k_moddown_conv_f64<MK, true><<<g2, 256, 0, s>>>(z, z_ct, z_ps, ns, vround, pl.mhl, pl.fhl, pl.n_dst,  \
+                                                    pl.dst_corr, conv, cv_ct, cv_ps, c->d_pc, c->log_n)
+    switch (ns) {
+        case 1: SRK_CONV_LAUNCH(1); break;
+        case 2: SRK_CONV_LAUNCH(2); break;
+        case 3: SRK_CONV_LAUNCH(3); break;
+        case 4: SRK_CONV_LAUNCH(4); break;
+        default:
+            if (ns > 17) return fail(SRK_EINVAL, "ModDown with more than 17 source primes");
+            k_moddown_conv_f64_wide<<<g2, 256, 0, s>>>(z, z_ct, z_ps, ns, vround, pl.mhl, pl.fhl, pl.n_dst,
+                                                       pl.dst_corr, conv, cv_ct, cv_ps, c->d_pc, c->log_n);
+    }
+#undef SRK_CONV_LAUNCH
+    LAUNCHED();
+    return SRK_OK;
+}
+
+struct KsOut {
+    uint64_t *out;
+    long long out_ct, out_ps;
+    const uint64_t *key;
+    uint64_t galois;
+    const uint64_t *add0, *add1;  // optional addends (nullptr: none)
+    long long add_ct;
+};
+
+// Hybrid key switching of B polys d (ct stride d_ct, NTT form, level `level`):
 //   1. INTT(d) with (Q_j/q_i)^-1 folded into the N^-1 scale  -> dc
 //   2. ModUp base conversion of every digit                   -> ext (coef)
 //   3. NTT of every ModUp target limb (one batched call)
-// then, for each Galois element g of `galois[0..n_out)` (1 = plain switch):
-//   4. inner product with key g, composed with X -> X^g        -> acc
-//   5. INTT of acc's special limbs with (P/p_k)^-1 folded in
-//   6. NTT(ModDown conversion, exact rounding) with the combine
-//      out = add + (acc - conv) P^-1 fused into its store
-// out[o]: ct stride out_ct, c0 at +0, c1 at +out_ps.  add0 (gathered through
-// g when add_galois_is_g) and add1 are optional per-ciphertext addends.
-// ---------------------------------------------------------------------
+// then, for each output o (Galois element g; 1 = relinearisation):
+//   4. inner product with key g over the special limbs only    -> acc_P
+//   5. INTT of acc_P with (P/p_k)^-1 folded in, rounding term v
+//   6. ModDown conversion P -> Q (coefficient domain)          -> conv
+//   7. NTT(conv) whose row pass computes, per output limb t,
+//        out = sigma_g(add + (sum_j e_j key_j - NTT(conv)) P^-1)
+//      -- the ciphertext-modulus limbs' inner product is never written to HBM
+//      (ST_KSC, ntt.cuh ksc_epilogue).
+// Rotations run in sigma_g^-1 space (rotation-layout keys): exact ModDown commutes
+// with sigma_g, so only the last store permutes.
+// rescale_d: fused HMult rescale -- outs[0].add0/add1 are d0/d1 (ct stride add_ct,
+// poly stride = level+1 limbs) and the output is round((acc + P d) / (P q_level)) at
+// level-1: special basis S = P u {q_level}, bit-identical to ModDown then rescale
+// (consecutive roundings by odd moduli compose exactly).
 static uint64_t galois_inverse(const srk_ctx *c, uint64_t g) {
     // (Z/2N)^* has order N, so g^-1 = g^(N-1) mod 2N
     const uint64_t two_n = 2ull * c->n;
@@ -1066,153 +1050,6 @@ static uint64_t galois_inverse(const srk_ctx *c, uint64_t g) {
     return r;
 }
 
-// forward NTT of the ModDown conversion with the combine fused into its store:
-// either the conversion fused into the first pass's loads (LD_BCONV) or a
-// streaming conversion kernel into the NTT buffer first (then a plain load)
-// conversion grids: x shrunk by up to conv_cpt coefficients per thread (to amortise
-// the CTA's constant staging) only while >= ~3 waves of CTAs remain, so the
-// one-ciphertext ops of the pipelines keep enough CTAs in flight
-static inline dim3 conv_grid(const srk_ctx *c, dim3 g) {
-    const unsigned long long ctas = (unsigned long long)g.x * g.y * g.z;
-    unsigned cpt = c->conv_cpt;
-    while (cpt > 1 && ctas / cpt < 148ull * 8 * 3) cpt >>= 1;
-    return dim3(std::max(1u, g.x / cpt), g.y, g.z);
-}
-
-// after(t0, t1, stream): work that consumes limbs [t0, t1) of the NTT output
-using LimbRangeFn = std::function<int(int, int, cudaStream_t)>;
-
-static int moddown_ntt(srk_ctx *c, LimbBatch bq, const FuseArgs &g, int B, int nout, cudaStream_t s,
-                       bool combine = true, const LimbRangeFn *after = nullptr) {
-    if (c->moddown_mode == 1) return ntt_run(c, bq, false, g, LD_BCONV, ST_MODDOWN, s);
-    const long long n = c->n;
-    dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + 7) / 8);
-    const uint64_t *z = g.src;
-#define SRK_CONV_LAUNCH(MK, EX)                                                                         \
-    if (c->conv_f64 && g.mhl)                                                                            \
-        k_moddown_conv_f64<MK, EX><<<conv_grid(c, grid), 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2,  \
-                                                        g.mhl, g.fhl, g.mat_ld, g.corr, bq.ptr,           \
-                                                        bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n); \
-    else                                                                                                 \
-        k_moddown_conv<MK, EX><<<grid, 256, 0, s>>>(z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mat2,      \
-                                                    g.mat_ld, g.corr, bq.ptr, bq.ct_stride, bq.poly_stride, \
-                                                    c->d_pc, c->log_n)
-    switch (g.n_src) {
-        case 1: SRK_CONV_LAUNCH(1, true); break;
-        case 2: SRK_CONV_LAUNCH(2, true); break;
-        case 3: SRK_CONV_LAUNCH(3, true); break;
-        case 4: SRK_CONV_LAUNCH(4, true); break;
-        default:
-            if (c->conv_f64 && g.mhl && g.n_src <= 16) {
-                k_moddown_conv_f64_wide<<<conv_grid(c, grid), 256, 0, s>>>(
-                    z, g.src_ct, g.src_ps, g.n_src, g.vround, g.mhl, g.fhl, g.mat_ld, g.corr, bq.ptr,
-                    bq.ct_stride, bq.poly_stride, c->d_pc, c->log_n);
-            } else if (g.n_src <= 8) {
-                SRK_CONV_LAUNCH(8, false);
-            } else {
-                SRK_CONV_LAUNCH(16, false);
-            }
-    }
-#undef SRK_CONV_LAUNCH
-    LAUNCHED();
-    FuseArgs h = g;
-    h.src = nullptr;  // first pass reads the conversion in place
-    if (c->moddown_mode == 2) return ntt_run(c, bq, false, h, LD_PLAIN, ST_MODDOWN, s);
-    if (after && c->md_chunk > 0 && bq.mode == 0) {
-        // L2-chunked: each group of limbs (one prime class, <= md_chunk limbs) is
-        // transformed and then consumed by `after` right away, so the consumer
-        // reads the transform's output from L2; groups alternate over two streams
-        std::vector<std::pair<int, int>> groups;
-        for (int t0 = 0, t1 = 0; t0 < bq.n_limbs; t0 = t1) {
-            const bool f64 = c->primes[t0 + bq.off_a] < SRK_F64_Q;
-            t1 = t0 + 1;
-            while (t1 < bq.n_limbs && t1 - t0 < c->md_chunk &&
-                   (c->primes[t1 + bq.off_a] < SRK_F64_Q) == f64)
-                t1++;
-            groups.push_back({t0, t1});
-        }
-        const int lane = s == c->side ? 1 : 0;
-        const bool two = c->ntt_streams >= 2 && groups.size() >= 2 && c->nside[lane];
-        if (two) {
-            CU(cudaEventRecord(c->ev_nfork[lane], s));
-            CU(cudaStreamWaitEvent(c->nside[lane], c->ev_nfork[lane], 0));
-        }
-        for (size_t gi = 0; gi < groups.size(); gi++) {
-            const int t0 = groups[gi].first, t1 = groups[gi].second;
-            cudaStream_t cs = (two && (gi & 1)) ? c->nside[lane] : s;
-            LimbBatch sub = bq;
-            sub.ptr = bq.ptr + (long long)t0 * n;
-            sub.n_limbs = t1 - t0;
-            sub.off_a = sub.off_b = bq.off_a + t0;
-            sub.split = 1 << 30;
-            TRY(ntt_run(c, sub, false, no_fuse(), LD_PLAIN, ST_PLAIN, cs));
-            TRY((*after)(t0, t1, cs));
-        }
-        if (two) {
-            CU(cudaEventRecord(c->ev_njoin[lane], c->nside[lane]));
-            CU(cudaStreamWaitEvent(s, c->ev_njoin[lane], 0));
-        }
-        return SRK_OK;
-    }
-    TRY(ntt_run(c, bq, false, no_fuse(), LD_PLAIN, ST_PLAIN, s));
-    if (after) return (*after)(0, bq.n_limbs, s);
-    if (!combine) return SRK_OK;
-    CombineArgs ca;
-    memset(&ca, 0, sizeof ca);
-    ca.conv = bq.ptr;
-    ca.conv_ct = bq.ct_stride;
-    ca.conv_ps = bq.poly_stride;
-    ca.acc = g.acc;
-    ca.acc_ct = g.acc_ct;
-    ca.acc_ps = g.acc_ps;
-    ca.add0 = g.add0;
-    ca.add1 = g.add1;
-    ca.add_ct = g.add_ct;
-    ca.out = g.out;
-    ca.out_ct = g.out_ct;
-    ca.out_ps = g.out_ps;
-    ca.galois = g.out_galois;
-    ca.nl = nout;
-    ca.batch = B;
-    ca.add_scaled = g.add_scaled;
-    ca.mulc = g.mulc;
-    ca.addc = g.addc;
-    k_moddown_combine<<<grid_for(2ll * B * nout * n), 256, 0, s>>>(ca, c->d_pc, c->log_n);
-    LAUNCHED();
-    return SRK_OK;
-}
-
-template <bool F64>
-static void launch_ks_combine(const KsCombineArgs &kc, int beta, int blocks, cudaStream_t s, const srk_ctx *c) {
-    switch (beta) {
-        case 1: k_ks_combine<1, true, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-        case 2: k_ks_combine<2, true, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-        case 3: k_ks_combine<3, true, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-        case 4: k_ks_combine<4, true, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n); break;
-        default:
-            if (beta <= 8)
-                k_ks_combine<8, false, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
-            else if (beta <= 16)
-                k_ks_combine<16, false, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
-            else
-                k_ks_combine<64, false, F64><<<blocks, 256, 0, s>>>(kc, c->d_pc, c->log_n);
-    }
-}
-
-struct KsOut {
-    uint64_t *out;
-    long long out_ct, out_ps;
-    const uint64_t *key;
-    uint64_t galois;
-    const uint64_t *add0, *add1;
-    long long add_ct;
-    bool gather_add0;
-};
-
-// rescale_d: fused HMult rescale -- outs[0].add0/add1 are d0/d1 (ct stride
-// add_ct, poly stride = level+1 limbs) and the output is
-// round((acc + P d) / (P q_level)) at level-1 (bit-identical to ModDown then
-// rescale: consecutive roundings by odd moduli compose exactly)
 static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const KsOut *outs,
                           int n_out, int level, int B, uint64_t *ws, cudaStream_t s,
                           bool rescale_d = false) {
@@ -1220,6 +1057,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
     const int nl = level + 1, K = c->n_p, ne = nl + K;
     const int alpha = c->alpha, beta = (nl + alpha - 1) / alpha;
     if (beta > SRK_MAX_DIGITS) return fail(SRK_EINVAL, "too many digits");
+    if (rescale_d && level < 1) return fail(SRK_EINVAL, "cannot rescale a level-0 ciphertext");
     uint64_t *dc = ws;                                 // [B][nl]
     uint64_t *ext = dc + (long long)B * nl * n;        // [B][beta][ne]
     // per-output scratch, one set per stream lane (outputs alternate between the
@@ -1240,7 +1078,6 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
     const bool dual = n_out >= 2 && !rescale_d && c->ks_streams >= 2 && c->side;
     cudaStream_t lane_s[2] = {s, dual ? c->side : s};
 
-    if (rescale_d && level < 1) return fail(SRK_EINVAL, "cannot rescale a level-0 ciphertext");
     // 1. INTT with the ModUp scale folded in
     {
         FuseArgs f = no_fuse();
@@ -1274,7 +1111,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             maxd = std::max(maxd, pl.n_dst);
         }
         // FP64-pipe conversion when every source but a digit's first is < 2^41
-        bool f64ok = c->conv_f64 != 0, wide0 = false;
+        bool f64ok = true, wide0 = false;
         for (int j = 0; j < beta; j++)
             for (int i = 0; i < alpha && j * alpha + i < nl; i++)
                 if (c->primes[j * alpha + i] >= SRK_F64_Q) {
@@ -1302,6 +1139,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             }
 #undef SRK_MODUP_F64
         } else {
+            // general parameter sets (wide scaling primes): 128-bit MAC + Barrett
             switch (alpha) {
                 case 1: k_modup<1><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
                 case 2: k_modup<2><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
@@ -1336,9 +1174,6 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         b.ne = ne;
         TRY(ntt_run(c, b, false, no_fuse(), LD_PLAIN, ST_PLAIN, s));
     }
-    const BconvPlan &pd = c->moddown[level];
-    // the ciphertext-modulus limbs' inner product is fused into the combine
-    const bool ks_fused = !rescale_d && c->moddown_mode == 0 && c->ks_fused;
     if (dual) {
         CU(cudaEventRecord(c->ev_fork, s));
         CU(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
@@ -1349,7 +1184,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         cudaStream_t so = lane_s[lane];
         uint64_t *acc = lane_acc[lane], *conv = lane_conv[lane], *zb = lane_zb[lane];
         uint8_t *vround = lane_vround[lane];
-        // 4. inner product (+ automorphism)
+        // 4. inner product over the special limbs (+ limb `level` for the fused rescale)
         KsInnerArgs ka;
         ka.d = d;
         ka.d_ct = d_ct;
@@ -1368,7 +1203,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         ka.alpha = alpha;
         ka.beta = beta;
         ka.batch = B;
-        ka.t0 = ks_fused ? nl : 0;
+        ka.t0 = rescale_d ? level : nl;
         {
             const int blocks = grid_for((long long)(ne - ka.t0) * n);
             switch (beta) {
@@ -1386,6 +1221,30 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             }
             LAUNCHED();
         }
+        // the store's arguments: out = sigma_g(add + (sum_j e_j key_j - NTT(conv)) mulc)
+        FuseArgs g = no_fuse();
+        g.out = ko.out;
+        g.out_ct = ko.out_ct;
+        g.out_ps = ko.out_ps;
+        g.has_add0 = ko.add0 != nullptr;
+        g.has_add1 = ko.add1 != nullptr;
+        g.add0 = ko.add0 ? ko.add0 : d;  // valid dummies: loads are never speculated from null
+        g.add1 = ko.add1 ? ko.add1 : d;
+        g.add_ct = ko.add_ct;
+        g.ks_d = d;
+        g.ks_d_ct = d_ct;
+        g.ks_ext = ext;
+        g.ks_ext_ct = (long long)beta * ne * n;
+        g.ks_ext_dig = (long long)ne * n;
+        g.ks_key = ko.key;
+        g.ks_key_j = 2ll * c->n_primes * n;
+        g.ks_key_r = (long long)c->n_primes * n;
+        g.ks_alpha = alpha;
+        g.ks_beta = beta;
+        int nout;
+        const BconvPlan *plan;
+        const uint64_t *zsrc;
+        long long z_ct, z_ps;
         if (rescale_d) {
             // 5'. special basis S = P u {q_l}: X_S = (acc_P, acc_l + P d_l), INTT with
             //     N^-1 (S/s_k)^-1 folded in; rounding term over K+1 limbs
@@ -1405,39 +1264,17 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             k_moddown_v<<<grid_for(2ll * B * n), 256, 0, so>>>(zb, 2ll * ns * n, (long long)ns * n, K,
                                                               c->n_q, ns, level, vround, c->d_pc, c->log_n, B);
             LAUNCHED();
-            // 6'. NTT(conversion S -> q_0..q_{l-1}) with out = (acc - conv) (P q_l)^-1 + d q_l^-1
-            const BconvPlan &pr = c->moddown_rs[level];
-            FuseArgs g = no_fuse();
-            g.src = zb;
-            g.src_ct = 2ll * ns * n;
-            g.src_ps = (long long)ns * n;
-            g.n_src = ns;
-            g.mat = pr.mat;
-            g.mat2 = pr.mat2;
-            g.mhl = pr.mhl;
-            g.fhl = pr.fhl;
-            g.mat_ld = pr.n_dst;
-            g.corr = pr.dst_corr;
-            g.corr_ld = pr.n_dst;
-            g.vround = vround;
-            g.out = ko.out;
-            g.out_ct = ko.out_ct;
-            g.out_ps = ko.out_ps;
-            g.acc = acc;
-            g.acc_ct = 2ll * ne * n;
-            g.acc_ps = (long long)ne * n;
-            g.add0 = ko.add0;
-            g.add1 = ko.add1;
-            g.add_ct = ko.add_ct;
+            // out = (acc - conv) (P q_l)^-1 + d q_l^-1 over q_0..q_{l-1}
+            nout = level;
+            plan = &c->moddown_rs[level];
+            zsrc = zb;
+            z_ct = 2ll * ns * n;
+            z_ps = (long long)ns * n;
+            g.mulc = c->lc_rs_mulc[level];
             g.add_scaled = 1;
             g.addc = c->lc_qlinv[level];
-            g.mulc = c->lc_rs_mulc[level];
-            TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * level * n, (long long)level * n, level, 0), g, B,
-                            level, so));
-            continue;
-        }
-        // 5. INTT of the special limbs, (P/p_k)^-1 folded in -> zb
-        {
+        } else {
+            // 5. INTT of the special limbs, (P/p_k)^-1 folded in -> zb; rounding term
             FuseArgs f = no_fuse();
             f.mulc = c->lc_moddown_scale;
             f.src = acc + (long long)nl * n;
@@ -1447,93 +1284,23 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             b.split = 0;
             b.off_b = c->n_q;
             TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, so));
+            k_moddown_v<<<grid_for(2ll * B * n), 256, 0, so>>>(zb, 2ll * K * n, (long long)K * n, K,
+                                                              c->n_q, K, 0, vround, c->d_pc, c->log_n, B);
+            LAUNCHED();
+            nout = nl;
+            plan = &c->moddown[level];
+            zsrc = zb;
+            z_ct = 2ll * K * n;
+            z_ps = (long long)K * n;
+            g.mulc = c->lc_pinv;
+            g.out_galois = ko.galois;
+            g.out_galois_inv = galois_inverse(c, ko.galois);
         }
-        // 6. ModDown: rounding term once per coefficient, then NTT(conversion)
-        //    with the combine in its store
-        k_moddown_v<<<grid_for(2ll * B * n), 256, 0, so>>>(zb, 2ll * K * n, (long long)K * n, K,
-                                                          c->n_q, K, 0, vround, c->d_pc, c->log_n, B);
-        LAUNCHED();
-        {
-            FuseArgs f = no_fuse();
-            f.src = zb;
-            f.src_ct = 2ll * K * n;
-            f.src_ps = (long long)K * n;
-            f.n_src = K;
-            f.src_pid0 = c->n_q;
-            f.mat = pd.mat;
-            f.mat2 = pd.mat2;
-            f.mhl = pd.mhl;
-            f.fhl = pd.fhl;
-            f.mat_ld = pd.n_dst;
-            f.corr = pd.dst_corr;
-            f.corr_ld = pd.n_dst;
-            f.vround = vround;
-            f.out = ko.out;
-            f.out_ct = ko.out_ct;
-            f.out_ps = ko.out_ps;
-            f.acc = acc;
-            f.acc_ct = 2ll * ne * n;
-            f.acc_ps = (long long)ne * n;
-            // rotation: everything above ran in sigma_g^-1 space (rotation-layout key);
-            // exact ModDown commutes with sigma_g, so out = sigma_g(add + ModDown(acc'))
-            f.acc_galois = 1;
-            f.add0 = ko.add0;
-            f.add1 = ko.add1;
-            f.add_ct = ko.add_ct;
-            f.add_galois = 1;
-            f.out_galois = ko.galois;
-            f.out_galois_inv = galois_inverse(c, ko.galois);
-            f.mulc = c->lc_pinv;
-            if (!ks_fused) {
-                TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), f, B, nl, so, true));
-            } else {
-                // 7. out = sigma_g(add + (sum_j e_j key_j - conv) P^-1) over q_0..q_l
-                KsCombineArgs kc;
-                memset(&kc, 0, sizeof kc);
-                kc.d = d;
-                kc.d_ct = d_ct;
-                kc.ext = ext;
-                kc.ext_ct = (long long)beta * ne * n;
-                kc.ext_dig = (long long)ne * n;
-                kc.key = ko.key;
-                kc.conv = conv;
-                kc.conv_ct = 2ll * nl * n;
-                kc.conv_ps = (long long)nl * n;
-                kc.add0 = ko.add0;
-                kc.add1 = ko.add1;
-                kc.add_ct = ko.add_ct;
-                kc.out = ko.out;
-                kc.out_ct = ko.out_ct;
-                kc.out_ps = ko.out_ps;
-                kc.galois = ko.galois;
-                kc.n_primes = c->n_primes;
-                kc.nl = nl;
-                kc.alpha = alpha;
-                kc.beta = beta;
-                kc.batch = B;
-                kc.mulc = c->lc_pinv;
-                // runs of limbs of one prime class: FP64 instantiation for q < 2^41
-                const LimbRangeFn combine = [&](int a0, int a1, cudaStream_t cs) -> int {
-                    for (int t0 = a0, t1 = a0; t0 < a1; t0 = t1) {
-                        const bool f64 = c->primes[t0] < SRK_F64_Q;
-                        t1 = t0 + 1;
-                        while (t1 < a1 && (c->primes[t1] < SRK_F64_Q) == f64) t1++;
-                        KsCombineArgs k2 = kc;
-                        k2.t0 = t0;
-                        k2.t1 = t1;
-                        const int blocks = grid_for((long long)(t1 - t0) * n);
-                        if (f64)
-                            launch_ks_combine<true>(k2, beta, blocks, cs, c);
-                        else
-                            launch_ks_combine<false>(k2, beta, blocks, cs, c);
-                        LAUNCHED();
-                    }
-                    return SRK_OK;
-                };
-                TRY(moddown_ntt(c, cbatch(conv, B, 2, 2ll * nl * n, (long long)nl * n, nl, 0), f, B, nl, so,
-                                false, &combine));
-            }
-        }
+        // 6. conversion, 7. NTT with the key-switch combine in its store
+        TRY(moddown_conv(c, *plan, zsrc, z_ct, z_ps, vround, conv, 2ll * nout * n, (long long)nout * n, B,
+                         nout, so));
+        TRY(ntt_run(c, cbatch(conv, B, 2, 2ll * nout * n, (long long)nout * n, nout, 0), false, g, LD_PLAIN,
+                    ST_KSC, so));
     }
     if (dual) {
         CU(cudaEventRecord(c->ev_join, c->side));
@@ -1546,7 +1313,7 @@ extern "C" int srk_keyswitch(srk_ctx *c, const uint64_t *d, const uint64_t *key,
                              uint64_t *out1, int level, void *ws, void *stream) {
     TRY(check_level(c, level));
     if (out1 - out0 <= 0) return fail(SRK_EINVAL, "out1 must follow out0");
-    KsOut o = {out0, 0, (long long)(out1 - out0), key, 1, nullptr, nullptr, 0, false};
+    KsOut o = {out0, 0, (long long)(out1 - out0), key, 1, nullptr, nullptr, 0};
     return keyswitch_impl(c, d, 0, &o, 1, level, 1, (uint64_t *)ws, S(stream));
 }
 
@@ -1558,17 +1325,14 @@ static int mul_relin_chunk(srk_ctx *c, const uint64_t *a, const uint64_t *b, lon
     uint64_t *d = ws;                       // [B][3][nl]
     uint64_t *prod = d + (long long)B * 3 * ps;  // [B][2][nl]
     uint64_t *rest = prod + (long long)B * 2 * ps;
-    for (int i = 0; i < B; i++) {
-        k_tensor<<<grid_for(ps), 256, 0, s>>>(a + i * ab_ct, b + i * ab_ct, d + i * 3 * ps, c->d_pc,
-                                              c->log_n, level + 1);
-        LAUNCHED();
-    }
+    k_tensor<<<grid_for(B * ps), 256, 0, s>>>(a, b, ab_ct, d, 3 * ps, c->d_pc, c->log_n, level + 1, B);
+    LAUNCHED();
     (void)prod;
     if (rescale) {  // HMult rescale fused into the key switch's ModDown
-        KsOut o = {out, out_ct, (long long)level * n, rlk, 1, d, d + ps, 3 * ps, false};
+        KsOut o = {out, out_ct, (long long)level * n, rlk, 1, d, d + ps, 3 * ps};
         return keyswitch_impl(c, d + 2 * ps, 3 * ps, &o, 1, level, B, rest, s, true);
     }
-    KsOut o = {out, out_ct, ps, rlk, 1, d, d + ps, 3 * ps, false};
+    KsOut o = {out, out_ct, ps, rlk, 1, d, d + ps, 3 * ps};
     return keyswitch_impl(c, d + 2 * ps, 3 * ps, &o, 1, level, B, rest, s);
 }
 
@@ -1620,7 +1384,7 @@ extern "C" int srk_rotate_batch(srk_ctx *c, const uint64_t *a, long long a_ct, c
     const long long ps = (long long)(level + 1) * c->n;
     FOR_CHUNKS(batch, b0, nb) {
         const uint64_t *ab = a + b0 * a_ct;
-        KsOut o = {out + b0 * out_ct, out_ct, ps, gkey, galois, ab, nullptr, a_ct, true};
+        KsOut o = {out + b0 * out_ct, out_ct, ps, gkey, galois, ab, nullptr, a_ct};
         TRY(keyswitch_impl(c, ab + ps, a_ct, &o, 1, level, nb, (uint64_t *)ws, S(stream)));
     }
     return SRK_OK;
@@ -1645,7 +1409,7 @@ extern "C" int srk_rotate_hoisted(srk_ctx *c, const uint64_t *a, long long a_ct,
         const uint64_t *ab = a + b0 * a_ct;
         for (int r = 0; r < n_rot; r++) {
             if (!(galois[r] & 1)) return fail(SRK_EINVAL, "Galois element must be odd");
-            o[r] = {outs[r] + b0 * out_ct, out_ct, ps, gkeys[r], galois[r], ab, nullptr, a_ct, true};
+            o[r] = {outs[r] + b0 * out_ct, out_ct, ps, gkeys[r], galois[r], ab, nullptr, a_ct};
         }
         TRY(keyswitch_impl(c, ab + ps, a_ct, o.data(), n_rot, level, nb, (uint64_t *)ws, S(stream)));
     }

@@ -9,10 +9,6 @@
 #include "modarith.cuh"
 #include "ntt.cuh"
 
-#ifndef SRK_KSC_UNROLL
-#define SRK_KSC_UNROLL 1
-#endif
-constexpr int kKscUnroll = SRK_KSC_UNROLL;  // batch-pair loop unroll of k_ks_combine (FP64)
 // CTAs per SM the conversion kernels' register budgets are sized for
 #ifndef SRK_CONV_MINB
 #define SRK_CONV_MINB 4
@@ -112,14 +108,21 @@ __global__ void k_mul_pt(const uint64_t *__restrict__ a, int src_nl,
     }
 }
 
-// d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1   (d: [3][nl][N])
-__global__ void k_tensor(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
-                         uint64_t *__restrict__ d, const PrimeConst *__restrict__ pc, int log_n,
-                         int nl) {
+// d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 for `batch` pairs (a, b at ct stride
+// ab_ct, poly stride nl N; d: [3][nl][N] at stride d_ct) -- one launch per batch
+__global__ void k_tensor(const uint64_t *__restrict__ a0p, const uint64_t *__restrict__ b0p, long long ab_ct,
+                         uint64_t *__restrict__ d0p, long long d_ct, const PrimeConst *__restrict__ pc,
+                         int log_n, int nl, int batch) {
     const long long n = 1ll << log_n;
     const long long ps = (long long)nl * n;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < ps;
-         x += (long long)gridDim.x * blockDim.x) {
+    const Div32 dv = mk_div32(nl);
+    for (long long xx = blockIdx.x * (long long)blockDim.x + threadIdx.x; xx < ps * batch;
+         xx += (long long)gridDim.x * blockDim.x) {
+        const uint32_t row = (uint32_t)(xx >> log_n);
+        const long long bi = div32(row, dv);
+        const long long x = xx - bi * ps;
+        const uint64_t *a = a0p + bi * ab_ct, *b = b0p + bi * ab_ct;
+        uint64_t *d = d0p + bi * d_ct;
         const PrimeConst P = pc[x >> log_n];
         uint64_t a0 = __ldg(a + x), a1 = __ldg(a + ps + x), b0 = __ldg(b + x), b1 = __ldg(b + ps + x);
         if (P.q < SRK_F64_Q) {  // FP64 pipe: exact FMA-split products (ntt.cuh modmul_f64)
@@ -158,49 +161,6 @@ __global__ void k_rescale_top(const uint64_t *__restrict__ a, long long a_ct, lo
         const long long off = x & (n - 1);
         top[x] = mul_mod(a[b * a_ct + p * a_ps + (long long)level * n + off],
                          pt[b * pt_ct + (long long)level * n + off], P);
-    }
-}
-
-// t[b][p][i] = centred(top[b][p]) mod q_i for i < level  (streaming rescale spread)
-__global__ void k_rescale_spread(const uint64_t *__restrict__ top, uint64_t *__restrict__ t,
-                                 const PrimeConst *__restrict__ pc, int log_n, int level, int batch) {
-    const long long n = 1ll << log_n;
-    const long long per = (long long)level * n;
-    const long long total = 2ll * batch * per;
-    const uint64_t ql = pc[level].q;
-    const Div32 dv = mk_div32(level);
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
-         x += (long long)gridDim.x * blockDim.x) {
-        const long long p = div32((uint32_t)(x >> log_n), dv), xi = x - p * per;
-        const int i = (int)(xi >> log_n);
-        const PrimeConst P = pc[i];
-        const uint64_t v = top[p * n + (xi & (n - 1))];
-        t[x] = v > (ql >> 1) ? sub_mod(reduce64(v, P), reduce64(ql, P), P.q) : reduce64(v, P);
-    }
-}
-
-// out[b][p][i] = (a[b][p][i] * pre_i - t[b][p][i]) * q_l^-1   (streaming rescale combine)
-__global__ void k_rescale_combine(const uint64_t *__restrict__ a, long long a_ct, long long a_ps,
-                                  const uint64_t *__restrict__ pt, long long pt_ct, LimbConsts k,
-                                  int mode, const uint64_t *__restrict__ t, LimbConsts qlinv,
-                                  uint64_t *__restrict__ out, long long out_ct,
-                                  const PrimeConst *__restrict__ pc, int log_n, int level, int batch) {
-    const long long n = 1ll << log_n;
-    const long long per = (long long)level * n;
-    const long long total = 2ll * batch * per;
-    const Div32 dv = mk_div32(level);
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
-         x += (long long)gridDim.x * blockDim.x) {
-        const long long p = div32((uint32_t)(x >> log_n), dv), xi = x - p * per;
-        const long long b = p >> 1, r = p & 1;
-        const int i = (int)(xi >> log_n);
-        const long long off = xi & (n - 1);
-        const PrimeConst P = pc[i];
-        uint64_t v = a[b * a_ct + r * a_ps + (long long)i * n + off];
-        if (mode == 1) v = mul_shoup(v, k.w[i], k.ws[i], P.q);
-        if (mode == 2) v = mul_mod(v, pt[b * pt_ct + (long long)i * n + off], P);
-        v = sub_mod(v, t[x], P.q);
-        out[b * out_ct + r * per + (long long)i * n + off] = mul_shoup(v, qlinv.w[i], qlinv.ws[i], P.q);
     }
 }
 
@@ -451,52 +411,6 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
     }
 }
 
-// ModDown conversion as a streaming kernel (alternative to the fused NTT load):
-//   conv[b][r][t][n] = sum_k z_k[n] mat[k][t] - corr[v(n)][t]  mod q_t
-// one thread per coefficient and chunk of 8 targets: the K z-words and v are
-// loaded once and reused for every target of the chunk.  Each term is a
-// Shoup product (mat2 = {m, floor(m 2^64 / q_t)}) in [0, 2q), folded into a
-// [0, 2q) running sum -- about half the instructions of a 128-bit MAC chain
-// plus one two-word Barrett reduction.
-// EXACT: n_src == MAXK (no per-source guards: the constant loads and Shoup
-// products of a target are straight-line code)
-template <int MAXK, bool EXACT>
-__global__ void __launch_bounds__(256) k_moddown_conv(const uint64_t *__restrict__ z, long long z_ct,
-                                                      long long z_ps, int n_src,
-                                                      const uint8_t *__restrict__ vround,
-                                                      const ulonglong2 *__restrict__ mat2, int n_dst,
-                                                      const uint64_t *__restrict__ corr,
-                                                      uint64_t *__restrict__ conv, long long c_ct,
-                                                      long long c_ps, const PrimeConst *__restrict__ pc,
-                                                      int log_n) {
-    const long long n = 1ll << log_n;
-    const int p = blockIdx.y;  // (b, r)
-    const int b = p >> 1, r = p & 1;
-    const int t0 = blockIdx.z * 8, t1 = min(n_dst, t0 + 8);
-    const uint64_t *zp = z + b * z_ct + r * z_ps;
-    uint64_t *cp = conv + b * c_ct + r * c_ps;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
-         x += (long long)gridDim.x * blockDim.x) {
-        uint64_t zz[MAXK];
-#pragma unroll
-        for (int k = 0; k < MAXK; k++) zz[k] = (EXACT || k < n_src) ? zp[k * n + x] : 0;
-        const int v = vround[(long long)p * n + x];
-        for (int t = t0; t < t1; t++) {
-            const uint64_t q = pc[t].q, two_q = 2 * q;
-            uint64_t acc = 0;
-#pragma unroll
-            for (int k = 0; k < MAXK; k++)
-                if (EXACT || k < n_src) {
-                    const ulonglong2 mw = __ldg(mat2 + k * n_dst + t);
-                    acc += mul_shoup_lazy(zz[k], mw.x, mw.y, q);
-                    acc = acc >= two_q ? acc - two_q : acc;
-                }
-            acc = acc >= q ? acc - q : acc;
-            cp[(long long)t * n + x] = sub_mod(acc, __ldg(corr + v * n_dst + t), q);
-        }
-    }
-}
-
 // ModDown conversion P -> Q with the FP64 and integer pipes splitting the work
 // (any target q_t < 2^62: only |S' - t q_t| < q_t < 2^63 is needed):
 //   z_k = zh_k 2^32 + zl_k,   S' = sum_k zh_k m'_kt + zl_k m_kt  == sum_k z_k m_kt (mod q_t)
@@ -514,7 +428,7 @@ constexpr int kConvUnroll = SRK_CONV_UNROLL;
 template <int MAXK, bool EXACT>
 __global__ void __launch_bounds__(256, SRK_CONV_MINB) k_moddown_conv_f64(
     const uint64_t *__restrict__ z, long long z_ct, long long z_ps, int n_src,
-    const uint8_t *__restrict__ vround, const ulonglong2 *__restrict__ mat2,
+    const uint8_t *__restrict__ vround,
     const ulonglong2 *__restrict__ mhl, const double2 *__restrict__ fhl, int n_dst,
     const uint64_t *__restrict__ corr, uint64_t *__restrict__ conv, long long c_ct, long long c_ps,
     const PrimeConst *__restrict__ pc, int log_n) {
@@ -660,216 +574,6 @@ __global__ void __launch_bounds__(256, 3) k_moddown_conv_f64_wide(
             const long long rr = (long long)(S[tt] - (uint64_t)tq * q);
             const uint64_t acc = (uint64_t)(rr < 0 ? rr + (long long)q : rr);
             out[(long long)tt * n] = sub_mod(acc, s_corr[v][tt], q);
-        }
-    }
-}
-
-struct CombineArgs {
-    const uint64_t *conv;
-    long long conv_ct, conv_ps;
-    const uint64_t *acc;
-    long long acc_ct, acc_ps;
-    const uint64_t *add0, *add1;
-    long long add_ct;
-    uint64_t *out;
-    long long out_ct, out_ps;
-    uint64_t galois;
-    int nl, batch, add_scaled;
-    LimbConsts mulc, addc;
-};
-
-__global__ void k_moddown_combine(const __grid_constant__ CombineArgs a, const PrimeConst *__restrict__ pc,
-                                  int log_n) {
-    const long long n = 1ll << log_n;
-    const long long per = (long long)a.nl * n;
-    const long long total = 2ll * a.batch * per;
-    const Div32 dv = mk_div32(a.nl);
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
-         x += (long long)gridDim.x * blockDim.x) {
-        const long long p = div32((uint32_t)(x >> log_n), dv), xi = x - p * per;
-        const long long b = p >> 1, r = p & 1;
-        const int i = (int)(xi >> log_n);
-        const long long m = xi & (n - 1);
-        const long long src = a.galois == 1 ? m : (long long)auto_index((uint32_t)m, a.galois, log_n);
-        const long long o = (long long)i * n + src;
-        const PrimeConst P = pc[i];
-        uint64_t v = sub_mod(a.acc[b * a.acc_ct + r * a.acc_ps + o], a.conv[b * a.conv_ct + r * a.conv_ps + o], P.q);
-        v = mul_shoup(v, a.mulc.w[i], a.mulc.ws[i], P.q);
-        const uint64_t *ad = r == 0 ? a.add0 : a.add1;
-        if (ad) {
-            uint64_t av = ad[b * a.add_ct + o];
-            if (a.add_scaled) av = mul_shoup(av, a.addc.w[i], a.addc.ws[i], P.q);
-            v = add_mod(v, av, P.q);
-        }
-        a.out[b * a.out_ct + r * a.out_ps + (long long)i * n + m] = v;
-    }
-}
-
-// Key-switch inner product of the ciphertext-modulus limbs fused into the
-// ModDown combine (the special limbs' inner product ran first through
-// k_ks_inner with t0 = nl, was INTT'd and converted):
-//   out[b][r][i][m] = (sum_j e_j key_r_j - conv[b][r]) P^-1 (+ add_r)  at src = sigma(m)
-// so the 2 x nl accumulator limbs are never written or re-read.  Thread = one
-// coefficient of one limb for every ciphertext of the batch (keys in
-// registers); all reads are at the sigma-gathered index, which keeps each
-// aligned 2^k block of m inside an aligned 2^k block of src (coalesced).
-struct KsCombineArgs {
-    const uint64_t *d;
-    long long d_ct;
-    const uint64_t *ext;
-    long long ext_ct, ext_dig;
-    const uint64_t *key;
-    const uint64_t *conv;
-    long long conv_ct, conv_ps;
-    const uint64_t *add0, *add1;
-    long long add_ct;
-    uint64_t *out;
-    long long out_ct, out_ps;
-    uint64_t galois;
-    int n_primes, nl, alpha, beta, batch;
-    int t0, t1;  // limb range of this launch
-    LimbConsts mulc;
-};
-
-#ifndef SRK_KSC_MINB
-#define SRK_KSC_MINB 3
-#endif
-// EXACT: beta == MAXD (no per-digit predicates)
-#ifndef SRK_KSC_F64_MINB
-#define SRK_KSC_F64_MINB 4
-#endif
-// F64: every limb in [t0, t1) is under a prime < 2^41 (launched separately
-// from the integer limbs so the FP64 instantiation carries no integer code
-// and runs at higher occupancy -- the kernel is HBM-latency bound)
-template <int MAXD, bool EXACT, bool F64>
-__global__ void __launch_bounds__(256, F64 ? SRK_KSC_F64_MINB : SRK_KSC_MINB)
-    k_ks_combine(const __grid_constant__ KsCombineArgs a, const PrimeConst *__restrict__ pc, int log_n) {
-    const long long n = 1ll << log_n;
-    const long long work = (long long)(a.t1 - a.t0) * n;
-    const Div32 dalpha = mk_div32(a.alpha);
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < work;
-         x += (long long)gridDim.x * blockDim.x) {
-        const int t = a.t0 + (int)(x >> log_n);
-        const long long m = x & (n - 1);
-        const long long src = a.galois == 1 ? m : (long long)auto_index((uint32_t)m, a.galois, log_n);
-        const int jt = (int)div32((uint32_t)t, dalpha);
-        uint64_t k0[MAXD], k1[MAXD];
-#pragma unroll
-        for (int j = 0; j < MAXD; j++) {
-            if (EXACT || j < a.beta) {
-                const uint64_t *kj = a.key + ((long long)j * 2 * a.n_primes + t) * n + src;
-                k0[j] = __ldg(kj);
-                k1[j] = __ldg(kj + (long long)a.n_primes * n);
-            }
-        }
-        const PrimeConst P = pc[t];
-        const uint64_t w = a.mulc.w[t], ws = a.mulc.ws[t];
-        const long long o = (long long)t * n + src;
-        if constexpr (F64) {
-            // limbs under primes < 2^41: the whole inner product and combine on the
-            // FP64 pipe (exact FMA-split products, as in the NTT's FP64 mode); the
-            // integer path below stays for the 60-bit limbs
-            const double qd = __longlong_as_double((long long)P.qd_bits);
-            const double qi = __longlong_as_double((long long)P.qinv_bits);
-            const double wf = f64_of_u64(w);
-            double kf0[MAXD], kf1[MAXD];
-#pragma unroll
-            for (int j = 0; j < MAXD; j++) {
-                kf0[j] = (EXACT || j < a.beta) ? f64_of_u64(k0[j]) : 0.0;
-                kf1[j] = (EXACT || j < a.beta) ? f64_of_u64(k1[j]) : 0.0;
-            }
-#pragma unroll(kKscUnroll)
-            for (int b = 0; b < a.batch; b += 2) {
-                const bool two = b + 1 < a.batch;
-                double e0[MAXD], e1[MAXD];
-                // read-only (__ldg) loads: free to move ahead of the previous pair's stores;
-                // the second ciphertext's addresses fall back to the first's when there is
-                // none, so a speculated load never leaves the batch
-#pragma unroll
-                for (int j = 0; j < MAXD; j++) {
-                    if (EXACT || j < a.beta) {
-                        const uint64_t *p = j == jt ? a.d + b * a.d_ct + o : a.ext + b * a.ext_ct + j * a.ext_dig + o;
-                        const long long st = j == jt ? a.d_ct : a.ext_ct;
-                        e0[j] = f64_of_u64(__ldg(p));
-                        e1[j] = (two ? f64_of_u64(__ldg(p + (two ? st : 0))) : 0.0);
-                    }
-                }
-                const uint64_t *cv = a.conv + b * a.conv_ct + o;
-                const double cv00 = f64_of_u64(__ldg(cv)), cv01 = f64_of_u64(__ldg(cv + a.conv_ps));
-                const double cv10 = (two ? f64_of_u64(__ldg(cv + (two ? a.conv_ct : 0))) : 0.0);
-                const double cv11 = (two ? f64_of_u64(__ldg(cv + (two ? a.conv_ct + a.conv_ps : 0))) : 0.0);
-                double ad00 = 0, ad01 = 0, ad10 = 0, ad11 = 0;
-                if (a.add0) {
-                    ad00 = f64_of_u64(__ldg(a.add0 + b * a.add_ct + o));
-                    ad10 = (two ? f64_of_u64(__ldg(a.add0 + (two ? b + 1 : b) * a.add_ct + o)) : 0.0);
-                }
-                if (a.add1) {
-                    ad01 = f64_of_u64(__ldg(a.add1 + b * a.add_ct + o));
-                    ad11 = (two ? f64_of_u64(__ldg(a.add1 + (two ? b + 1 : b) * a.add_ct + o)) : 0.0);
-                }
-                // |each product| < q, |sum| < beta q, minus conv: < (beta + 1) q < 2^47
-                double s0 = -cv00, s1 = -cv01, u0 = -cv10, u1 = -cv11;
-#pragma unroll
-                for (int j = 0; j < MAXD; j++) {
-                    if (EXACT || j < a.beta) {
-                        s0 += modmul_f64(e0[j], kf0[j], qd, qi);
-                        s1 += modmul_f64(e0[j], kf1[j], qd, qi);
-                        u0 += modmul_f64(e1[j], kf0[j], qd, qi);
-                        u1 += modmul_f64(e1[j], kf1[j], qd, qi);
-                    }
-                }
-                uint64_t *op = a.out + b * a.out_ct + (long long)t * n + m;
-                op[0] = canon_u64_of_f64(modmul_f64(s0, wf, qd, qi) + ad00, qd, qi);
-                op[a.out_ps] = canon_u64_of_f64(modmul_f64(s1, wf, qd, qi) + ad01, qd, qi);
-                if (two) {
-                    op[a.out_ct] = canon_u64_of_f64(modmul_f64(u0, wf, qd, qi) + ad10, qd, qi);
-                    op[a.out_ct + a.out_ps] = canon_u64_of_f64(modmul_f64(u1, wf, qd, qi) + ad11, qd, qi);
-                }
-            }
-        } else {
-        for (int b = 0; b < a.batch; b += 2) {
-            const bool two = b + 1 < a.batch;
-            uint64_t e0[MAXD], e1[MAXD];
-#pragma unroll
-            for (int j = 0; j < MAXD; j++) {
-                if (EXACT || j < a.beta) {
-                    const uint64_t *p = j == jt ? a.d + b * a.d_ct + o : a.ext + b * a.ext_ct + j * a.ext_dig + o;
-                    const long long st = j == jt ? a.d_ct : a.ext_ct;
-                    e0[j] = __ldg(p);
-                    e1[j] = (two ? __ldg(p + (two ? st : 0)) : 0);
-                }
-            }
-            const uint64_t *cv = a.conv + b * a.conv_ct + o;
-            const uint64_t cv00 = __ldg(cv), cv01 = __ldg(cv + a.conv_ps);
-            const uint64_t cv10 = (two ? __ldg(cv + (two ? a.conv_ct : 0)) : 0), cv11 = (two ? __ldg(cv + (two ? a.conv_ct + a.conv_ps : 0)) : 0);
-            uint64_t ad00 = 0, ad01 = 0, ad10 = 0, ad11 = 0;
-            if (a.add0) {
-                ad00 = a.add0[b * a.add_ct + o];
-                ad10 = two ? a.add0[(b + 1) * a.add_ct + o] : 0;
-            }
-            if (a.add1) {
-                ad01 = a.add1[b * a.add_ct + o];
-                ad11 = two ? a.add1[(b + 1) * a.add_ct + o] : 0;
-            }
-            U128 s0 = {0, 0}, s1 = {0, 0}, u0 = {0, 0}, u1 = {0, 0};
-#pragma unroll
-            for (int j = 0; j < MAXD; j++) {
-                if (EXACT || j < a.beta) {
-                    mac(s0, e0[j], k0[j]);
-                    mac(s1, e0[j], k1[j]);
-                    mac(u0, e1[j], k0[j]);
-                    mac(u1, e1[j], k1[j]);
-                }
-            }
-            uint64_t *op = a.out + b * a.out_ct + (long long)t * n + m;
-            op[0] = add_mod(mul_shoup(sub_mod(reduce_u128(s0, P), cv00, P.q), w, ws, P.q), ad00, P.q);
-            op[a.out_ps] = add_mod(mul_shoup(sub_mod(reduce_u128(s1, P), cv01, P.q), w, ws, P.q), ad01, P.q);
-            if (two) {
-                op[a.out_ct] = add_mod(mul_shoup(sub_mod(reduce_u128(u0, P), cv10, P.q), w, ws, P.q), ad10, P.q);
-                op[a.out_ct + a.out_ps] =
-                    add_mod(mul_shoup(sub_mod(reduce_u128(u1, P), cv11, P.q), w, ws, P.q), ad11, P.q);
-            }
-        }
         }
     }
 }

@@ -76,52 +76,47 @@ __device__ __forceinline__ uint32_t auto_index(uint32_t k, uint64_t g, int log_n
 }
 
 // Fused first-pass loads / last-pass stores (see ntt_pass_kernel).
-enum { LD_PLAIN = 0, LD_BCONV = 1, LD_SPREAD = 2, LD_AUTO = 3, LD_BCONV8 = 4, LD_BCONV16 = 5 };
-// ModDown conversion load, bucketed by the number of special primes it reads
-__host__ __device__ constexpr bool is_bconv(int ld) {
-    return ld == LD_BCONV || ld == LD_BCONV8 || ld == LD_BCONV16;
-}
-__host__ __device__ constexpr int bconv_maxk(int ld) {
-    return ld == LD_BCONV ? 4 : (ld == LD_BCONV8 ? 8 : 16);
-}
-enum { ST_PLAIN = 0, ST_MODDOWN = 1, ST_RESCALE = 2, ST_SCALE = 3 };
+enum { LD_PLAIN = 0, LD_SPREAD = 2, LD_AUTO = 3 };
+enum { ST_PLAIN = 0, ST_KSC = 1, ST_RESCALE = 2, ST_SCALE = 3 };
 
 struct FuseArgs {
     // loads: source poly (b, r) at src + b*src_ct + r*src_ps (+ slot t * N for
-    // LD_PLAIN / LD_AUTO; LD_BCONV reads n_src limbs, LD_SPREAD one limb)
+    // LD_PLAIN / LD_AUTO; LD_SPREAD reads one limb)
     const uint64_t *src;
     long long src_ct, src_ps;
     uint64_t galois;         // LD_AUTO: X -> X^galois gather
-    int n_src, src_pid0;     // LD_BCONV: z limbs under primes src_pid0 ..
-    const uint64_t *mat;     // LD_BCONV: [n_src][mat_ld] conversion constants
-    const ulonglong2 *mat2;  // the same with Shoup companions (streaming conversion)
-    const ulonglong2 *mhl;   // {m, m 2^32 mod q_t} and {m/q_t, (m 2^32 mod q_t)/q_t}:
-    const double2 *fhl;      //   FP64-pipe conversion (k_moddown_conv_f64)
-    int mat_ld;
-    const uint64_t *corr;    // LD_BCONV: [v * prod src primes]_{q_t}, table [v][corr_ld]
-    int corr_ld;
-    const uint8_t *vround;   // LD_BCONV: v = round(sum z_k / p_k) per (b, r, n), k_moddown_v
     uint64_t top_q;          // LD_SPREAD: modulus of the limb being spread
     // stores: out(b, r, t) from the transform result x and
-    //   ST_MODDOWN: add_r + (acc - x) * mulc          (add0 gathered if add_galois != 1)
+    //   ST_KSC    : sigma_{out_galois}(add_r + (sum_j e_j key_j - x) * mulc)   (key switch)
     //   ST_RESCALE: (acc * pre - x) * mulc            (pre: const pre_k or plaintext pt)
     //   ST_SCALE  : x * mulc   (replaces N^-1 in the inverse transform)
     uint64_t *out;
     long long out_ct, out_ps;
     const uint64_t *acc;
     long long acc_ct, acc_ps;
-    uint64_t acc_galois;     // ST_MODDOWN: read acc through X -> X^acc_galois (1 = none)
+    // ST_KSC addends (c0 of a rotation, d0 / d1 of a product): valid pointers always
+    // (a dummy when has_add* is 0, so no load can ever be speculated from null)
     const uint64_t *add0, *add1;
     long long add_ct;
-    uint64_t add_galois;
-    uint64_t out_galois;     // ST_MODDOWN: write sigma_{out_galois}(result) (1 = identity);
+    int has_add0, has_add1;
+    uint64_t out_galois;     // ST_KSC: write sigma_{out_galois}(result) (1 = identity);
     uint64_t out_galois_inv; //   rows of T elements map to rows, staged through smem
+    // ST_KSC inner product sum_j e_j key_j over the ciphertext-modulus limbs:
+    // e_j = the key-switched poly d itself for the digit holding the limb, else
+    // the ModUp digit ext[j]; key[j][r] in device layout (rotation-permuted)
+    const uint64_t *ks_d;
+    long long ks_d_ct;
+    const uint64_t *ks_ext;
+    long long ks_ext_ct, ks_ext_dig;
+    const uint64_t *ks_key;
+    long long ks_key_j, ks_key_r;  // key strides: digit, poly (words)
+    int ks_alpha, ks_beta;
     int pre_mode;            // 0 none, 1 per-limb constant, 2 plaintext
-    const uint64_t *pt;      // [limbs][N] per ciphertext at stride pt_ct (0 = shared)
-    long long pt_ct;
+    const uint64_t *pt;      // [limbs][N] per ciphertext at stride pt_ct (0 = shared); never
+    long long pt_ct;         //   null (points at acc when pre_mode != 2)
     LimbConsts mulc;
     LimbConsts pre;
-    LimbConsts addc;         // ST_MODDOWN: add_r scaled by addc (when add_scaled)
+    LimbConsts addc;         // ST_KSC: add_r scaled by addc (when add_scaled)
     int add_scaled;
 };
 
@@ -167,30 +162,6 @@ template <int LOG_T>
 __device__ __forceinline__ int row_sidx(int sb, int c) {
     using S = NttShape<LOG_T>;
     return sb * (S::T + S::T / S::E) + c + (c >> S::LE1);
-}
-
-// Reduction-free butterflies for primes below 2^46 (all scaling primes):
-// forward outputs grow by at most 2q per stage (T in [0, 2q)), so 16 stages
-// stay below 34q; inverse sums at most double per stage, and the difference
-// is offset by M = q << k (a multiple of q above any operand at step k), so
-// 16 steps stay below 2^16 q < 2^62.  Only the final pass reduces.
-#define SRK_SMALL_Q (1ull << 46)
-#ifndef SRK_NTT_MINB
-#define SRK_NTT_MINB 3  // CTAs per SM the register budget is sized for
-#endif
-
-__device__ __forceinline__ void ct_bfly_small(uint64_t &x, uint64_t &y, uint64_t w, uint64_t ws,
-                                              uint64_t q, uint64_t two_q) {
-    uint64_t T = mul_shoup_lazy(y, w, ws, q);
-    y = x - T + two_q;
-    x = x + T;
-}
-
-__device__ __forceinline__ void gs_bfly_small(uint64_t &x, uint64_t &y, uint64_t w, uint64_t ws,
-                                              uint64_t q, uint64_t m) {
-    uint64_t D = x - y + m;
-    x = x + y;
-    y = mul_shoup_lazy(D, w, ws, q);
 }
 
 // ---------------------------------------------------------------------------
@@ -260,8 +231,7 @@ __device__ __forceinline__ void gs_bfly_f64(uint64_t &xb, uint64_t &yb, double w
 // template recursion so x[] never spills to local memory.
 //   tw_group(g) -> twiddle for butterfly group g of the stage;
 //   group g covers x[g*2*HALF .. g*2*HALF + 2*HALF), pairs (e, e + HALF).
-// SM: 0 = Harvey lazy (any prime < 2^62), 1 = reduction-free integer (q < 2^46),
-// 2 = FP64 (q < 2^41); m = inverse difference offset (q << step) for SM 1
+// SM: 0 = Harvey lazy (any prime < 2^62), 2 = FP64 (q < 2^41)
 struct F64Q {
     double q, qinv;
 };
@@ -285,17 +255,13 @@ __device__ __forceinline__ void reg_stage(uint64_t (&x)[E], TwPtr tp, TwFn tw_id
             uint64_t &a = x[g * 2 * HALF + k];
             uint64_t &b = x[g * 2 * HALF + k + HALF];
             if (GS) {
-                if (SM == 2)
+                if constexpr (SM == 2)
                     gs_bfly_f64(a, b, wf, fq.q, fq.qinv);
-                else if (SM == 1)
-                    gs_bfly_small(a, b, w.x, w.y, q, m);
                 else
                     gs_bfly(a, b, w.x, w.y, q, two_q);
             } else {
-                if (SM == 2)
+                if constexpr (SM == 2)
                     ct_bfly_f64(a, b, wf, fq.q, fq.qinv);
-                else if (SM == 1)
-                    ct_bfly_small(a, b, w.x, w.y, q, two_q);
                 else
                     ct_bfly(a, b, w.x, w.y, q, two_q);
             }
@@ -377,96 +343,128 @@ __device__ __forceinline__ uint64_t fused_load(const FuseArgs &f, const PrimeCon
         // centred representative of v mod top_q, reduced mod this prime
         return v > (f.top_q >> 1) ? sub_mod(reduce64(v, P), reduce64(f.top_q, P), P.q)
                                   : reduce64(v, P);
-    } else {  // ModDown conversion: handled by bconv_load (per-thread hoisted constants)
-        return 0;
     }
 }
 
-// ModDown conversion with exact rounding (v precomputed once per coefficient):
-//   sum_k z_k[n] * mat[k][t] - corr[v(n)][t]   mod q_t
-// mat column / corr table for this limb are hoisted into registers by the caller.
-template <int MAXK>
-__device__ __forceinline__ uint64_t bconv_load(const FuseArgs &f, const uint64_t *z,
-                                               const uint8_t *vr, const uint64_t (&m)[MAXK],
-                                               const PrimeConst &P, long long n, int log_n, int t) {
-    const long long nn = 1ll << log_n;
-    U128 acc = {0, 0};
-#pragma unroll
-    for (int k = 0; k < MAXK; k++)
-        if (k < f.n_src) mac(acc, z[k * nn + n], m[k]);
-    const int v = vr[n];
-    return sub_mod(reduce_u128(acc, P), __ldg(f.corr + v * f.corr_ld + t), P.q);
-}
-
-// last-pass element store; x canonical in [0, q)
+// last-pass element store (ST_PLAIN / ST_SCALE); x canonical in [0, q)
 template <int ST>
 __device__ __forceinline__ void fused_store(const FuseArgs &f, int bi, int r, int t, int limb,
                                             const PrimeConst &P, long long n, int log_n,
                                             uint64_t x, uint64_t *plain_dst) {
-    if constexpr (ST == ST_PLAIN || ST == ST_SCALE) {
-        plain_dst[n] = x;
-    } else {
-        const long long nn = 1ll << log_n;
-        const long long off = (long long)t * nn + n;
-        const long long aoff = (ST == ST_MODDOWN && f.acc_galois != 1)
-                                   ? (long long)t * nn + auto_index((uint32_t)n, f.acc_galois, log_n)
-                                   : off;
-        uint64_t a = f.acc[bi * f.acc_ct + r * f.acc_ps + aoff];
-        uint64_t v;
-        if constexpr (ST == ST_RESCALE) {
-            if (f.pre_mode == 1) a = mul_shoup(a, f.pre.w[limb], f.pre.ws[limb], P.q);
-            if (f.pre_mode == 2) a = mul_mod(a, __ldg(f.pt + bi * f.pt_ct + off), P);
-            v = mul_shoup(sub_mod(a, x, P.q), f.mulc.w[limb], f.mulc.ws[limb], P.q);
+    static_assert(ST == ST_PLAIN || ST == ST_SCALE, "other stores run in row_final_store");
+    plain_dst[n] = x;
+}
+
+// ST_KSC epilogue of the forward row pass (the ModDown NTT of a key switch):
+// the ciphertext-modulus limbs' key-switch inner product and the ModDown combine
+//     v = (sum_j e_j[n] key_j[r][t][n] - x[n]) * mulc[t]  +  add_r[n] (* addc[t])
+// at every element n = sub*T + c of this thread's strided slots c = u + TPS e, in
+// place in smem (sidx layout).  x[n] is the transform output: raw FP64 bits
+// (|x| < 17 q) in FP64 mode, canonical in integer mode.  Elements are processed
+// in groups of G so that 2G independent digit / key loads are in flight per
+// digit step (the loads are L2/HBM-latency bound otherwise).
+template <int LOG_T, int KM, typename SIdx>
+__device__ __forceinline__ void ksc_epilogue(const FuseArgs &f, uint64_t *sm, SIdx sidx, int bi, int r,
+                                             int t, int pid, int limb, const PrimeConst &pc, F64Q fq,
+                                             int sub, int u, int log_n) {
+    using S = NttShape<LOG_T>;
+    constexpr int T = S::T, E = S::E, TPS = S::TPS;
+    constexpr int G = E < 8 ? E : 8;
+    const long long nn = 1ll << log_n;
+    const long long off0 = (long long)t * nn + (long long)sub * T + u;  // element e at + TPS e
+    const int jt = pid / f.ks_alpha;  // the digit that holds this limb
+    const uint64_t *dsrc = f.ks_d + bi * f.ks_d_ct + off0;
+    const uint64_t *esrc = f.ks_ext + bi * f.ks_ext_ct + off0;
+    const uint64_t *ksrc = f.ks_key + r * f.ks_key_r + off0;
+    const int has_add = r == 0 ? f.has_add0 : f.has_add1;
+    const uint64_t *asrc = (r == 0 ? f.add0 : f.add1) + bi * f.add_ct + off0;
+#pragma unroll
+    for (int g0 = 0; g0 < E; g0 += G) {
+        if constexpr (KM == 1) {
+            double s[G];
+#pragma unroll
+            for (int e = 0; e < G; e++) s[e] = -__longlong_as_double((long long)sm[sidx(u + TPS * (g0 + e))]);
+            for (int j = 0; j < f.ks_beta; j++) {
+                const uint64_t *ej = (j == jt ? dsrc : esrc + j * f.ks_ext_dig) + TPS * g0;
+                const uint64_t *kj = ksrc + j * f.ks_key_j + TPS * g0;
+                uint64_t ev[G], kv[G];
+#pragma unroll
+                for (int e = 0; e < G; e++) {
+                    ev[e] = __ldg(ej + TPS * e);
+                    kv[e] = __ldg(kj + TPS * e);
+                }
+                // |each product| < q, |sum| < (beta + 17) q < 2^51
+#pragma unroll
+                for (int e = 0; e < G; e++)
+                    s[e] += modmul_f64(f64_of_u64(ev[e]), f64_of_u64(kv[e]), fq.q, fq.qinv);
+            }
+            const double wf = f64_of_u64(f.mulc.w[limb]);
+            uint64_t av[G];
+#pragma unroll
+            for (int e = 0; e < G; e++) av[e] = has_add ? __ldg(asrc + TPS * (g0 + e)) : 0;
+            const double af = f.add_scaled ? f64_of_u64(f.addc.w[limb]) : 1.0;
+#pragma unroll
+            for (int e = 0; e < G; e++) {
+                double v = modmul_f64(s[e], wf, fq.q, fq.qinv);
+                double a = f64_of_u64(av[e]);
+                if (f.add_scaled) a = modmul_f64(a, af, fq.q, fq.qinv);
+                sm[sidx(u + TPS * (g0 + e))] = canon_u64_of_f64(v + a, fq.q, fq.qinv);
+            }
         } else {
-            v = mul_shoup(sub_mod(a, x, P.q), f.mulc.w[limb], f.mulc.ws[limb], P.q);
-            const uint64_t *ad = r == 0 ? f.add0 : f.add1;
-            if (ad) {
-                const uint64_t *base = ad + bi * f.add_ct + (long long)t * nn;
-                const long long src = (r == 0 && f.add_galois != 1)
-                                          ? (long long)auto_index((uint32_t)n, f.add_galois, log_n)
-                                          : n;
-                uint64_t av = base[src];
-                if (f.add_scaled) av = mul_shoup(av, f.addc.w[limb], f.addc.ws[limb], P.q);
-                v = add_mod(v, av, P.q);
+            // integer limbs (q >= 2^41): 128-bit accumulation, one Barrett reduction
+            // per 16 products (products < 2^124)
+            U128 s[G];
+#pragma unroll
+            for (int e = 0; e < G; e++) s[e] = {0, 0};
+            for (int j = 0; j < f.ks_beta; j++) {
+                const uint64_t *ej = (j == jt ? dsrc : esrc + j * f.ks_ext_dig) + TPS * g0;
+                const uint64_t *kj = ksrc + j * f.ks_key_j + TPS * g0;
+                uint64_t ev[G], kv[G];
+#pragma unroll
+                for (int e = 0; e < G; e++) {
+                    ev[e] = __ldg(ej + TPS * e);
+                    kv[e] = __ldg(kj + TPS * e);
+                }
+#pragma unroll
+                for (int e = 0; e < G; e++) mac(s[e], ev[e], kv[e]);
+                if ((j & 15) == 15) {
+#pragma unroll
+                    for (int e = 0; e < G; e++) s[e] = {0, reduce_u128(s[e], pc)};
+                }
+            }
+            uint64_t av[G];
+#pragma unroll
+            for (int e = 0; e < G; e++) av[e] = has_add ? __ldg(asrc + TPS * (g0 + e)) : 0;
+#pragma unroll
+            for (int e = 0; e < G; e++) {
+                const int c = u + TPS * (g0 + e);
+                uint64_t v = mul_shoup(sub_mod(reduce_u128(s[e], pc), sm[sidx(c)], pc.q), f.mulc.w[limb],
+                                       f.mulc.ws[limb], pc.q);
+                uint64_t a = av[e];
+                if (f.add_scaled) a = mul_shoup(a, f.addc.w[limb], f.addc.ws[limb], pc.q);
+                sm[sidx(c)] = add_mod(v, a, pc.q);
             }
         }
-        f.out[bi * f.out_ct + r * f.out_ps + off] = v;
     }
 }
 
-// Final phase of a forward row pass whose canonical results sit in smem
-// (sidx layout).  Plain/fused stores write each element in place; with
-// ST_MODDOWN and out_galois != 1 the combined values are first written back
-// to smem, then every row (chunk) is emitted permuted:
-//   out[m] = w[pi(m)],  pi = X -> X^out_galois on NTT slots,
-// which maps chunk sub to chunk d = pi^-1(sub*T) / T as a whole, so both the
-// reads (acc, add) and the writes stay coalesced.
-template <int LOG_T, int ST, typename SIdx>
+// Final phase of a forward row pass whose results sit in smem (sidx layout).
+// Plain stores write each element in place.  ST_KSC combines in place
+// (ksc_epilogue) and, with out_galois != 1, then emits every row (chunk)
+// permuted:  out[m] = w[pi(m)],  pi = X -> X^out_galois on NTT slots, which maps
+// chunk sub to chunk d = pi^-1(sub*T) / T as a whole, so both the reads (digits,
+// keys, addends) and the writes stay coalesced.
+template <int LOG_T, int ST, int KM, typename SIdx>
 __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm, SIdx sidx, int bi,
-                                                int r, int t, int limb, const PrimeConst &pc,
-                                                int sub, int u, int log_n, uint64_t *data) {
+                                                int r, int t, int pid, int limb, const PrimeConst &pc,
+                                                F64Q fq, int sub, int u, int log_n, uint64_t *data) {
     using S = NttShape<LOG_T>;
     constexpr int T = S::T, E = S::E, TPS = S::TPS;
-    if constexpr (ST == ST_MODDOWN) {
+    if constexpr (ST == ST_KSC) {
+        ksc_epilogue<LOG_T, KM>(f, sm, sidx, bi, r, t, pid, limb, pc, fq, sub, u, log_n);
+        const long long nn = 1ll << log_n;
         if (f.out_galois != 1) {
-#pragma unroll
-            for (int e = 0; e < E; e++) {
-                const int c = u + TPS * e;
-                const long long n = (long long)sub * T + c;
-                const long long nn = 1ll << log_n;
-                const long long off = (long long)t * nn + n;
-                uint64_t v = mul_shoup(sub_mod(f.acc[bi * f.acc_ct + r * f.acc_ps + off], sm[sidx(c)], pc.q),
-                                       f.mulc.w[limb], f.mulc.ws[limb], pc.q);
-                const uint64_t *ad = r == 0 ? f.add0 : f.add1;
-                if (ad) {
-                    uint64_t av = ad[bi * f.add_ct + off];
-                    if (f.add_scaled) av = mul_shoup(av, f.addc.w[limb], f.addc.ws[limb], pc.q);
-                    v = add_mod(v, av, pc.q);
-                }
-                sm[sidx(c)] = v;
-            }
             __syncthreads();
-            const long long nn = 1ll << log_n;
             const int d = (int)(auto_index((uint32_t)((long long)sub * T), f.out_galois_inv, log_n) >> LOG_T);
             uint64_t *o = f.out + bi * f.out_ct + r * f.out_ps + (long long)t * nn + (long long)d * T;
 #pragma unroll
@@ -476,12 +474,17 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
                                     (uint32_t)sub * T);
                 o[c] = sm[sidx(p)];
             }
-            return;
+        } else {
+            uint64_t *o = f.out + bi * f.out_ct + r * f.out_ps + (long long)t * nn + (long long)sub * T;
+#pragma unroll
+            for (int e = 0; e < E; e++) o[u + TPS * e] = sm[sidx(u + TPS * e)];
         }
+        return;
     }
     if constexpr (ST == ST_RESCALE) {
         // integer rescale combine with every load issued before the first store
-        // (the out pointer may alias acc / pt as far as the compiler knows)
+        // (the out pointer may alias acc / pt as far as the compiler knows);
+        // f.pt is never null (host points it at acc when there is no plaintext)
         const long long nn = 1ll << log_n;
         const long long off0 = (long long)t * nn + (long long)sub * T + u;
         uint64_t av[E], pv[E];
@@ -500,10 +503,12 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
         }
         return;
     }
+    if constexpr (ST == ST_PLAIN || ST == ST_SCALE) {
 #pragma unroll
-    for (int e = 0; e < E; e++) {
-        const int c = u + TPS * e;
-        fused_store<ST>(f, bi, r, t, limb, pc, (long long)sub * T + c, log_n, sm[sidx(c)], data);
+        for (int e = 0; e < E; e++) {
+            const int c = u + TPS * e;
+            fused_store<ST>(f, bi, r, t, limb, pc, (long long)sub * T + c, log_n, sm[sidx(c)], data);
+        }
     }
 }
 
@@ -527,12 +532,12 @@ __device__ __forceinline__ void row_final_store(const FuseArgs &f, uint64_t *sm,
 #ifndef SRK_NTT_MINB_INT
 #define SRK_NTT_MINB_INT 3
 #endif
-// KM: 0 = arithmetic mode chosen per limb at run time (fused-IO variants),
-//     1 = FP64 only (limbs under q < 2^41; others skipped),
+// KM: 1 = FP64 only (limbs under q < 2^41; others skipped),
 //     2 = Harvey lazy integer only (any q < 2^62; with cls 2 the FP64 limbs are skipped)
-template <int LOG_T, bool INV, bool COL, int IO, int KM = 0, int LOGN = 0>
-__global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? SRK_NTT_MINB_INT : SRK_NTT_MINB))
+template <int LOG_T, bool INV, bool COL, int IO, int KM, int LOGN = 0>
+__global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB_INT)
     ntt_pass_kernel(LimbBatch b, NttTables tb, int log_n_arg, const __grid_constant__ FuseArgs f) {
+    static_assert(KM == 1 || KM == 2, "FP64 or Harvey pass kernels only");
     const int log_n = LOGN ? LOGN : log_n_arg;
     using S = NttShape<LOG_T>;
     constexpr int T = S::T, E = S::E, TPS = S::TPS, LE1 = S::LE1, LE2 = S::LE2;
@@ -555,7 +560,6 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
     // prime-class split of mixed batches (uniform per CTA): the FP64 kernel never
     // touches a limb >= 2^41; the integer kernel skips FP64 limbs when filtered
     if ((KM == 1 || b.cls == 1) ? q >= SRK_F64_Q : (b.cls == 2 && q < SRK_F64_Q)) return;
-    const bool small = q < SRK_SMALL_Q;  // uniform per CTA (one limb per CTA)
     const TwPtr tw = {(INV ? tb.itw : tb.tw) + (long long)pid * n, (INV ? tb.itwd : tb.twd) + (long long)pid * n};
     const uint64_t *lsrc = data;  // LD_PLAIN / LD_AUTO source limb
     if constexpr (FIRST && (LD == LD_PLAIN || LD == LD_AUTO)) {
@@ -580,26 +584,13 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
     auto sidx = [&](int c) -> int {
         return COL ? c * CB + sb : row_sidx<LOG_T>(sb, c);
     };
-    constexpr int MAXK = bconv_maxk(LD);
-    uint64_t bm[MAXK];
-    const uint64_t *bz = nullptr;
-    const uint8_t *bvr = nullptr;
-    if constexpr (FIRST && is_bconv(LD)) {
-#pragma unroll
-        for (int k = 0; k < MAXK; k++)
-            bm[k] = k < f.n_src ? __ldg(f.mat + (long long)k * f.mat_ld + t) : 0;
-        bz = f.src + (long long)bi * f.src_ct + (long long)r * f.src_ps;
-        bvr = f.vround + ((long long)bi * 2 + r) * n;
-    }
     auto load = [&](int c) -> uint64_t {
-        if constexpr (FIRST && is_bconv(LD)) return bconv_load<MAXK>(f, bz, bvr, bm, pc, gaddr(c), log_n, t);
-        else if constexpr (FIRST) return fused_load<LD>(f, tb.pc, bi, r, t, pc, gaddr(c), log_n, lsrc);
+        if constexpr (FIRST) return fused_load<LD>(f, tb.pc, bi, r, t, pc, gaddr(c), log_n, lsrc);
         else return data[gaddr(c)];
     };
 
-    // arithmetic mode, uniform per CTA: 2 = FP64 (q < 2^41), 1 = reduction-free
-    // integer (q < 2^46), 0 = Harvey lazy integer
-    const int mode = KM == 1 ? 2 : (KM == 2 ? 0 : (q < SRK_F64_Q ? 2 : (small ? 1 : 0)));
+    // arithmetic mode, uniform per launch: 2 = FP64 (q < 2^41), 0 = Harvey lazy integer
+    constexpr int mode = KM == 1 ? 2 : 0;
     // (double) q and 1 / (double) q precomputed per prime (no per-CTA division)
     const F64Q fq = {__longlong_as_double((long long)pc.qd_bits), __longlong_as_double((long long)pc.qinv_bits)};
     // first-pass loads are canonical u64; FP64 limbs convert on load
@@ -613,17 +604,16 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
             return (uint64_t)__double_as_longlong((double)vc);
         }
         const uint64_t v = load(c);
-        return mode == 2 ? (uint64_t)__double_as_longlong(f64_of_u64(v)) : v;
+        if constexpr (mode == 2) return (uint64_t)__double_as_longlong(f64_of_u64(v));
+        else return v;
     };
     uint64_t x[E];
     if (!INV) {
         // ---- round 1: strided ownership c = u + TPS e, strides T/2 .. TPS
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = FIRST ? load_m(u + TPS * e) : data[gaddr(u + TPS * e)];
-        if (mode == 2)
+        if constexpr (mode == 2)
             FwdR1<E, LE1, 2>::run(x, tw, base, q, two_q, fq);
-        else if (mode == 1)
-            FwdR1<E, LE1, 1>::run(x, tw, base, q, two_q);
         else
             FwdR1<E, LE1, 0>::run(x, tw, base, q, two_q);
 #pragma unroll
@@ -632,10 +622,8 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
         // ---- round 2: contiguous ownership c = u E + e, strides TPS/2 .. 1
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = smem[sidx(u * E + e)];
-        if (mode == 2)
+        if constexpr (mode == 2)
             FwdR2<E, TPS, LE1, LE2, 2>::run(x, tw, base, u, q, two_q, fq);
-        else if (mode == 1)
-            FwdR2<E, TPS, LE1, LE2, 1>::run(x, tw, base, u, q, two_q);
         else
             FwdR2<E, TPS, LE1, LE2, 0>::run(x, tw, base, u, q, two_q);
         if (COL) {
@@ -680,20 +668,18 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 uint64_t v = x[e];
-                if (mode == 2) {
-                    v = canon_u64_of_f64(__longlong_as_double((long long)v), fq.q, fq.qinv);
+                if constexpr (mode == 2) {
+                    // ST_KSC consumes the raw FP64 value (|x| < 17 q) in its own reduction
+                    if constexpr (ST != ST_KSC)
+                        v = canon_u64_of_f64(__longlong_as_double((long long)v), fq.q, fq.qinv);
                 } else {
-                    if (mode == 1) {  // v < 34 q: one Barrett step (floor(2^64/q)) then one subtraction
-                        v -= mulhi64(v, pc.ratio_hi) * q;
-                    } else {
-                        v = v >= two_q ? v - two_q : v;
-                    }
+                    v = v >= two_q ? v - two_q : v;
                     v = v >= q ? v - q : v;
                 }
                 smem[sidx(u * E + e)] = v;
             }
             __syncthreads();
-            row_final_store<LOG_T, ST>(f, smem, sidx, bi, r, t, limb, pc, sub, u, log_n, data);
+            row_final_store<LOG_T, ST, KM>(f, smem, sidx, bi, r, t, pid, limb, pc, fq, sub, u, log_n, data);
         }
     } else {
         // ---- round 1: contiguous ownership, strides 1 .. E/2
@@ -702,7 +688,7 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 uint64_t v = data[gaddr(u * E + e)];
-                if (mode == 2)
+                if constexpr (mode == 2)
                     v = (uint64_t)__double_as_longlong(
                         centre_f64(__longlong_as_double((long long)v), fq.q, fq.qinv));
                 x[e] = v;
@@ -716,10 +702,8 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
         }
         // step numbers of the inverse: row pass 0.., column pass log_n - LOG_T ..
         const int k0 = COL ? log_n - LOG_T : 0;
-        if (mode == 2)
+        if constexpr (mode == 2)
             InvR1<E, LOG_T, LE1, 2>::run(x, tw, base, u, q, two_q, k0, fq);
-        else if (mode == 1)
-            InvR1<E, LOG_T, LE1, 1>::run(x, tw, base, u, q, two_q, k0);
         else
             InvR1<E, LOG_T, LE1, 0>::run(x, tw, base, u, q, two_q, k0);
         if (!COL) __syncthreads();
@@ -729,10 +713,8 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
         // ---- round 2: strided ownership c = u + TPS e, strides E .. T/2
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = smem[sidx(u + TPS * e)];
-        if (mode == 2)
+        if constexpr (mode == 2)
             InvR2<E, TPS, LE2, 2>::run(x, tw, base, q, two_q, k0 + LE1, fq);
-        else if (mode == 1)
-            InvR2<E, TPS, LE2, 1>::run(x, tw, base, q, two_q, k0 + LE1);
         else
             InvR2<E, TPS, LE2, 0>::run(x, tw, base, q, two_q, k0 + LE1);
         if (COL) {
@@ -742,7 +724,7 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : (KM == 2 ? S
                 m = f.mulc.w[limb];
                 ms = f.mulc.ws[limb];
             }
-            if (mode == 2) {
+            if constexpr (mode == 2) {
                 const double mf = f64_of_u64(m);
 #pragma unroll
                 for (int e = 0; e < E; e++)  // modmul_f64 output is already in (-q, q)

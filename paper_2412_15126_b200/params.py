@@ -251,8 +251,15 @@ PRESETS = {
     "cfg2": dict(log_n=16, levels=29, special=3, special_bits=60, dnum=3, hamming_weight=192),
     # config 3: same chain, special primes sized to the 420-bit digit
     "cfg3": dict(log_n=16, levels=29, special=8, special_bits=60, dnum=3, hamming_weight=192),
+    # config 3 at the reference's 1e-6 slot tolerance for ranks: Delta = 2^47 (the
+    # diagonal comparisons amplify CKKS noise ~1900x; tools/delta_study.py), integer
+    # kernels (scaling primes >= 2^41), 10 special primes for the 480-bit digits
+    "cfg3_hp": dict(log_n=16, levels=29, special=10, special_bits=60, dnum=3, hamming_weight=192,
+                    scale_bits=47),
     # configs 4/5: long non-secure chain for masks + values and the N=1024 sort
     "long": dict(log_n=16, levels=56, special=11, special_bits=60, dnum=4, hamming_weight=192),
+    # the tie-corrected N=1024 sort (block tie offsets) needs two more levels
+    "long58": dict(log_n=16, levels=58, special=11, special_bits=60, dnum=4, hamming_weight=192),
     # small rings for CPU tests
     "toy": dict(log_n=10, levels=12, special=4, special_bits=60, dnum=4, hamming_weight=32),
     "toy_deep": dict(log_n=11, levels=40, special=6, special_bits=60, dnum=6, hamming_weight=32),

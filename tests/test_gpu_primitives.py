@@ -297,18 +297,16 @@ def test_ntt_chunking_and_kernel_variants(name, chunk, require_cuda, monkeypatch
     assert np.array_equal(got[B - 1], orc.rescale(a[B - 1], lvl))
 
 
-@pytest.mark.parametrize("fused", ["0", "1"])
 @pytest.mark.parametrize("name", ["toy", "cfg1"])
-def test_keyswitch_fused_combine_paths(name, fused, require_cuda, monkeypatch):
-    """SRK_KS_FUSED=1 (inner product fused into the ModDown combine) and =0
-    (separate k_ks_inner + combine) give the oracle's limbs for rotate,
-    hoisted rotate and relinearise (odd batch: the two-at-a-time tail)."""
+def test_keyswitch_fused_combine_paths(name, require_cuda):
+    """The ciphertext-modulus inner product fused into the ModDown NTT's store
+    (ST_KSC) gives the oracle's limbs for rotate, hoisted rotate and relinearise
+    (odd batch; ring 2^12 with 23 digits: the runtime digit loop)."""
     import ctypes
 
     from oracle.oracle import OracleCKKS
     from paper_2412_15126_b200.backend_cuda import CudaBackend
 
-    monkeypatch.setenv("SRK_KS_FUSED", fused)
     p = preset(name)
     gb, orc = CudaBackend(p), OracleCKKS(p)
     B, lvl, n = 3, p.max_level - 1, p.ring_degree
@@ -338,14 +336,11 @@ def test_keyswitch_fused_combine_paths(name, fused, require_cuda, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [
-    {"SRK_NTT_CLUSTER": "1"},                        # 8-CTA cluster forward NTT (DSMEM exchange)
-    {"SRK_CONV_F64": "0"},                           # Shoup / 128-bit MAC conversions
-    {"SRK_NTT_STREAMS": "1", "SRK_NTT_CTA": "256"},  # one stream, 256-thread pass CTAs
-    {"SRK_RESCALE_FUSED": "0", "SRK_NTT_SPLIT": "0"},  # streaming rescale, mixed-mode passes
-    {"SRK_MD_CHUNK": "2"},                           # L2-chunked ModDown NTT + combine
+    {"SRK_NTT_CHUNK": "8"},   # many small NTT chunks on both stream lanes
+    {"SRK_WS_BATCH": "1"},    # one ciphertext per internal key-switch chunk
 ])
 def test_kernel_switches_ring16(env, require_cuda, monkeypatch):
-    """Every alternative kernel path at ring 2^16 (config 2) gives the oracle's limbs."""
+    """The run-time settings at ring 2^16 (config 2) give the oracle's limbs."""
     from oracle.oracle import OracleCKKS
     from paper_2412_15126_b200.backend_cuda import CudaBackend
 

@@ -1,4 +1,5 @@
 // Pipe-throughput microbenchmark (B200): DFMA, IMAD.WIDE (64x64 mulhi), I2F/F2I 64-bit.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/pipes tools/micro/pipes.cu
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>

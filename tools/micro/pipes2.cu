@@ -1,4 +1,5 @@
 // Do DFMA and IMAD pipes overlap? Is rint (FRND.F64) full rate? (B200)
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/pipes2 tools/micro/pipes2.cu
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
