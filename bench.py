@@ -475,6 +475,17 @@ def run_pipelines(torch, quick=False):
                            "cost": cost, "params": "long", "gpus": 1,
                            "note": "latency_s: first run (includes generating this pipeline's Galois keys and "
                                    "encoding its constants); warm_latency_s: second run"}
+    # the same sort in the packed layout (two blocks per ciphertext: 18 comparison and
+    # 32 indicator evaluations instead of 36 / 64; packing.py)
+    pcfg = SortConfig(kernel=scfg.kernel, tie_correction=False, packed=True)
+    first, _ = _timed(torch, lambda: block_merge(eng, multi_sort(eng, bv, pcfg)))
+    cost, _ = _census(eng, lambda: multi_sort(eng, bv, pcfg))
+    warm, srt = _timed(torch, lambda: block_merge(eng, multi_sort(eng, bv, pcfg)))
+    out["sort_n1024_packed_s"] = {"latency_s": first, "warm_latency_s": warm,
+                                  "order_ok": bool(np.array_equal(np.argsort(srt), np.arange(1024))),
+                                  "max_abs_err": float(np.abs(srt - np.sort(v1024)).max()),
+                                  "cost": cost, "params": "long", "gpus": 1,
+                                  "layout": "two 128x128 blocks per ciphertext (opt-in, packing.py)"}
     del eng, bv
     torch.cuda.empty_cache()
     # the tie-corrected sort (block tie offsets) needs two more levels: long58

@@ -2,24 +2,32 @@
 
 Restates reference ``multi_rank_pipeline`` / ``multi_sort``
 (``pkg/src/slotrank/ranking.py:307-392``, ``sorting.py:106-142``) with the
-independent units spread over ranks:
+independent units spread over ranks, in five phases,
+each ONE level exchange (a tiny int64 all-reduce, the phase's only host sync)
+plus ONE collective on the stacked ciphertexts of the phase:
 
-* the L(L+1)/2 block-pair comparisons C(i, j), i <= j, are dealt
-  round-robin over ranks; each rank folds its own pairs into per-block
-  partial sums  U_i = sum_{j>=i} C(i, j)  and  D_i = sum_{j<i} (1 - C(j, i));
-* the L^2 indicator placements (i, j) of the sort are dealt the same way and
-  folded into per-output-block partial sums;
-* every partial sum is combined with ONE all-reduce of its RNS limbs
-  (int64 sum -- limbs are < 2^60 and world <= 8, so no overflow) followed
-  by a mod-q fix-up (``srk_reduce_mod`` on the GPU); block i is then finished
-  (SumR / SumC / TransC / +1/2) by rank i % world and broadcast.
+0. ReplR(block) and ReplC(TransR(block)) for blocks i with i % world == rank,
+   batched; all-gather of the stacked results (every rank needs every block);
+1. the L(L+1)/2 block-pair comparisons C(i, j), i <= j, dealt round-robin;
+   each rank folds its own pairs into per-block partial sums
+   U_i = sum_{j>=i} C(i, j), D_i = sum_{j<i} (1 - C(j, i)) (and the tie-offset
+   pieces); all partials of all blocks go through one all-reduce of their RNS
+   limbs (int64 sum -- limbs are < 2^60 and world <= 8, so no overflow)
+   followed by one mod-q fix-up launch;
+2. block i is finished (SumR / SumC / TransC / +1/2) by rank i % world; the
+   finished blocks are all-gathered;
+3. the L^2 indicator placements (i, j) of the sort are dealt round-robin and
+   folded into per-output-block partial sums: one all-reduce + fix-up;
+4. output block i is finished (SumC + TransC) by its owner; one all-gather.
 
-Modular addition is exact and associative, so the ciphertexts every rank
-ends with are bit-identical to the single-GPU pipeline's for any world size
-(tests/test_shard_gloo.py checks it with 2 gloo ranks on the CPU oracle).
-Evaluation keys are replicated (every rank generates them from the shared
-seed); only ciphertexts cross NVLink.  With world == 1 this is exactly the
-single-GPU pipeline.
+Modular addition is exact and associative, so the ciphertexts every rank ends
+with are bit-identical to the single-GPU pipeline's for any world size whenever
+the partial sums sit at one level (every BASELINE configuration; with a padded
+last block the min-level alignment is applied per rank, as in the single-GPU
+``engine.add``).  tests/test_shard_gloo.py checks it with 2 gloo ranks on the
+CPU oracle.  Evaluation keys are replicated (every rank generates them from the
+shared seed); only ciphertexts cross NVLink.  With world == 1 every collective
+is skipped and this is exactly the single-GPU pipeline.
 """
 
 from __future__ import annotations
@@ -28,13 +36,14 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .chebyshev import KernelConfig, equality_from_compare, with_input_range
+from .chebyshev import KernelConfig, equality_from_compare, indicator_kernel, with_input_range
 from .matrix import MatrixLayout, replicate, sum_axis, transpose_vector
 from .ranking import (
     BlockVector,
     MultiRankPipeline,
-    _triangle_mask,
     _prefix_vector,
+    _triangle_mask,
+    batched,
     block_pairs,
     compare_block_pairs,
     finish_block_rank,
@@ -42,13 +51,12 @@ from .ranking import (
     replicated_blocks,
     upper_partial,
 )
-from .chebyshev import indicator_kernel
-from .ranking import batched
 from .sorting import SortConfig, _neg_rank_targets, common_level, place_block
 
 __all__ = ["Comm", "multi_rank_sharded", "multi_sort_sharded"]
 
 _NO_LEVEL = 1 << 20
+MAX_WORLD = 8  # int64 sums of world residues < 2^60 must not overflow
 
 
 @dataclass
@@ -63,80 +71,203 @@ class Comm:
         self.dist = dist
         self.rank = dist.get_rank(self.group)
         self.world = dist.get_world_size(self.group)
+        if self.world > MAX_WORLD:
+            raise ValueError(f"shard.py sums int64 limbs (< 2^60) over ranks: world <= {MAX_WORLD}")
+        self.collectives = 0  # data collectives issued (tests assert O(1) per phase)
+        self.level_syncs = 0  # host syncs (one small level exchange per phase)
 
     def owner(self, unit_index: int) -> int:
         return unit_index % self.world
 
-    def min_int(self, v: int) -> int:
+    def device(self):
         import torch
 
-        t = torch.tensor([v], dtype=torch.int64, device=self._device())
+        if self.dist.get_backend(self.group) == "nccl":
+            return torch.device("cuda", torch.cuda.current_device())
+        return "cpu"
+
+    def min_levels(self, levels: list[int]) -> list[int]:
+        """Element-wise MIN over ranks of a level vector (_NO_LEVEL = absent): the
+        phase's single host sync."""
+        import torch
+
+        t = torch.tensor(levels, dtype=torch.int64, device=self.device())
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
-        return int(t.item())
+        self.level_syncs += 1
+        return [int(x) for x in t.cpu().tolist()]
 
-    def _device(self):
+    def all_reduce(self, t):
+        self.dist.all_reduce(t, group=self.group)
+        self.collectives += 1
+
+    def all_gather(self, t):
+        """[world * k, ...] from every rank's [k, ...] (rank-major)."""
         import torch
 
-        return torch.device("cuda", torch.cuda.current_device()) if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(parts, t.contiguous(), group=self.group)
+        self.collectives += 1
+        return torch.cat(parts)
 
 
-def _sum_across(engine, ct, comm: Comm):
-    """Modular sum over ranks of one ciphertext per rank (None = zero)."""
-    if comm.world == 1:
-        return ct
-    level = comm.min_int(ct.level if ct is not None else _NO_LEVEL)
-    if level == _NO_LEVEL:
-        return None
-    if ct is not None and ct.level != level:
-        ct = engine.at_level(ct, level)
-    t = engine.backend.as_tensor(ct.data) if ct is not None else engine.backend.zeros_tensor(level)
-    comm.dist.all_reduce(t, group=comm.group)
-    data = engine.backend.reduce_mod_tensor(t, level)
-    return engine.wrap(data, level, ct.rot_chain if ct is not None else 0)
+def _lv(ct) -> int:
+    return _NO_LEVEL if ct is None else ct.level
 
 
-def _broadcast(engine, ct, src: int, comm: Comm):
-    """Ciphertext held by rank ``src`` on every rank (level broadcast first)."""
-    if comm.world == 1:
-        return ct
+def _stacked(engine, cts, levels):
+    """int64 tensor [k][2][max level + 1][N] of ciphertexts brought to ``levels``
+    (zeros for None; shorter limb counts zero-padded)."""
     import torch
 
-    lvl = torch.tensor([ct.level if comm.rank == src else 0], dtype=torch.int64, device=comm._device())
-    comm.dist.broadcast(lvl, src, group=comm.group)
-    level = int(lvl.item())
-    t = engine.backend.as_tensor(ct.data) if comm.rank == src else engine.backend.zeros_tensor(level)
-    comm.dist.broadcast(t, src, group=comm.group)
-    return ct if comm.rank == src else engine.wrap(engine.backend.from_tensor(t, level), level, 0)
+    be = engine.backend
+    top = max(lv for lv in levels if lv != _NO_LEVEL)
+    rows = []
+    for ct, lv in zip(cts, levels):
+        if ct is None or lv == _NO_LEVEL:
+            rows.append(be.zeros_tensor(top))
+            continue
+        if ct.level != lv:
+            ct = engine.at_level(ct, lv)
+        t = be.as_tensor(ct.data)
+        if lv < top:
+            pad = be.zeros_tensor(top)
+            pad[:, : lv + 1] = t
+            t = pad
+        rows.append(t)
+    return torch.stack(rows)
+
+
+def _unstacked(engine, t, levels, reduce_mod: bool):
+    """Ciphertexts (None where absent) from a stacked tensor at ``levels``."""
+    be = engine.backend
+    out = []
+    for k, lv in enumerate(levels):
+        if lv == _NO_LEVEL:
+            out.append(None)
+            continue
+        x = t[k, :, : lv + 1].contiguous()
+        data = be.reduce_mod_tensor(x, lv) if reduce_mod else be.from_tensor(x, lv)
+        out.append(engine.wrap(data, lv, 0))
+    return out
+
+
+def _sum_all(engine, cts, comm: Comm):
+    """Modular sums over ranks of a list of ciphertexts (one all-reduce): each
+    rank's item is brought to the minimum level over ranks first."""
+    if comm.world == 1:
+        return list(cts)
+    levels = comm.min_levels([_lv(c) for c in cts])
+    if all(lv == _NO_LEVEL for lv in levels):
+        return [None] * len(cts)
+    t = _stacked(engine, cts, levels)
+    comm.all_reduce(t)
+    return _unstacked(engine, t, levels, reduce_mod=True)
+
+
+def _gather_owned(engine, owned: dict, count: int, comm: Comm):
+    """Every rank ends with all ``count`` items; item i is computed by rank
+    comm.owner(i) (``owned`` maps its indices to ciphertexts): one all-gather."""
+    if comm.world == 1:
+        return [owned[i] for i in range(count)]
+    levels = comm.min_levels([_lv(owned.get(i)) for i in range(count)])
+    per = -(-count // comm.world)
+    # slot s of rank r holds item r + s * world
+    local = [owned.get(comm.rank + s * comm.world) for s in range(per)]
+    local_lv = [levels[comm.rank + s * comm.world] if comm.rank + s * comm.world < count else _NO_LEVEL
+                for s in range(per)]
+    top = max(lv for lv in levels if lv != _NO_LEVEL)
+    t = _stacked(engine, local + [None], local_lv + [top])[:per]  # pad row fixes the limb count
+    g = comm.all_gather(t)  # [world * per], rank-major
+    out = []
+    for i in range(count):
+        r, s = i % comm.world, i // comm.world
+        lv = levels[i]
+        out.append(None if lv == _NO_LEVEL else
+                   engine.wrap(engine.backend.from_tensor(g[r * per + s, :, : lv + 1].contiguous(), lv), lv, 0))
+    return out
+
+
+def _replicated_sharded(engine, bv: BlockVector, layout: MatrixLayout, comm: Comm):
+    """Phase 0: (rows, cols) of every block, each computed once over the world."""
+    count = len(bv.blocks)
+    if comm.world == 1:
+        return replicated_blocks(engine, bv, layout)
+    mine = [i for i in range(count) if comm.owner(i) == comm.rank]
+    owned = {}
+    if mine:
+        sub = BlockVector(blocks=tuple(bv.blocks[i] for i in mine), block_size=bv.block_size,
+                          total_len=bv.total_len)
+        rows, cols = replicated_blocks(engine, sub, layout)
+        for i, r, c in zip(mine, rows, cols):
+            owned[2 * i], owned[2 * i + 1] = r, c
+    both = _gather_pairs(engine, owned, count, comm)  # items 2i (row), 2i + 1 (col)
+    return [both[2 * i] for i in range(count)], [both[2 * i + 1] for i in range(count)]
+
+
+def _gather_pairs(engine, owned2: dict, count: int, comm: Comm):
+    """All-gather of 2 items per block (row, col) -- block i's pair computed by
+    comm.owner(i), stacked along a second axis -- in one collective."""
+    import torch
+
+    if comm.world == 1:
+        return [owned2[k] for k in range(2 * count)]
+    lv = comm.min_levels([_lv(owned2.get(k)) for k in range(2 * count)])
+    per = -(-count // comm.world)
+    top = max(x for x in lv if x != _NO_LEVEL)
+    rows = []
+    for s in range(per):
+        i = comm.rank + s * comm.world
+        pair = [owned2.get(2 * i), owned2.get(2 * i + 1)] if i < count else [None, None]
+        pl = [lv[2 * i], lv[2 * i + 1]] if i < count else [_NO_LEVEL, _NO_LEVEL]
+        rows.append(_stacked(engine, pair + [None], pl + [top])[:2])
+    t = torch.stack(rows)  # [per][2][2][top+1][N]
+    g = comm.all_gather(t)  # [world * per][2]...
+    out = []
+    for k in range(2 * count):
+        i, c = divmod(k, 2)
+        r, s = i % comm.world, i // comm.world
+        x = lv[k]
+        out.append(None if x == _NO_LEVEL else
+                   engine.wrap(engine.backend.from_tensor(g[r * per + s, c, :, : x + 1].contiguous(), x), x, 0))
+    return out
 
 
 def multi_rank_sharded(engine, bv: BlockVector, cfg: KernelConfig, comm: Comm, *,
                        tie_correction: bool = False) -> MultiRankPipeline:
-    """``multi_rank_pipeline`` with the block pairs dealt over ``comm``'s ranks."""
+    """``multi_rank_pipeline`` with blocks, block pairs and block finishes dealt over
+    ``comm``'s ranks (phases 0-2 of the module docstring)."""
     b, count = bv.block_size, len(bv.blocks)
     layout = MatrixLayout(b, engine.params.slot_count)
     valid_last = bv.valid_in(count - 1)
-    rows, cols = replicated_blocks(engine, bv, layout)
+    rows, cols = _replicated_sharded(engine, bv, layout, comm)
     pairs = block_pairs(count)
     mine = [p for idx, p in enumerate(pairs) if comm.owner(idx) == comm.rank]
-    comparisons = compare_block_pairs(engine, mine, rows, cols, cfg, layout, count, valid_last)
+    comparisons = compare_block_pairs(engine, mine, rows, cols, cfg, layout, count, valid_last) if mine else {}
     equalities = {p: equality_from_compare(engine, c) for p, c in comparisons.items()} if tie_correction else {}
-    blocks = []
+    # phase 1: every partial of every block in one all-reduce
+    parts = []
     for i in range(count):
-        upper = _sum_across(engine, upper_partial(engine, comparisons, i, count), comm)
-        lower = _sum_across(engine, lower_partial(engine, comparisons, i), comm) if i > 0 else None
+        parts.append(upper_partial(engine, comparisons, i, count))
+        parts.append(lower_partial(engine, comparisons, i) if i > 0 else None)
+        if tie_correction:
+            tp = _tie_partials(engine, equalities, i, count, layout)
+            parts.extend([tp["cross"], tp["diag"], tp["total"]])
+    stride = 5 if tie_correction else 2
+    summed = _sum_all(engine, parts, comm)
+    # phase 2: owners finish their blocks; one all-gather
+    owned = {}
+    for i in range(count):
+        if comm.owner(i) != comm.rank:
+            continue
+        upper, lower = summed[stride * i], summed[stride * i + 1]
         tie = None
         if tie_correction:
-            parts = _tie_partials(engine, equalities, i, count, layout)
-            parts = {k: _sum_across(engine, v, comm) for k, v in parts.items()}
-        owner = comm.owner(i)
-        if comm.rank == owner:
-            if tie_correction:
-                def tie(i=i, parts=parts):
-                    return _finish_tie(engine, parts, i, bv.valid_in(i), layout)
-            ranks_i = finish_block_rank(engine, upper, lower, i, bv, layout, tie)
-        else:
-            ranks_i = None
-        blocks.append(_broadcast(engine, ranks_i, owner, comm))
+            tp = {"cross": summed[stride * i + 2], "diag": summed[stride * i + 3], "total": summed[stride * i + 4]}
+
+            def tie(i=i, tp=tp):
+                return _finish_tie(engine, tp, i, bv.valid_in(i), layout)
+        owned[i] = finish_block_rank(engine, upper, lower, i, bv, layout, tie)
+    blocks = _gather_owned(engine, owned, count, comm)
     return MultiRankPipeline(
         ranks=BlockVector(blocks=tuple(blocks), block_size=b, total_len=bv.total_len),
         comparisons=comparisons,
@@ -181,7 +312,8 @@ def _finish_tie(engine, parts, i, valid_i, layout):
 
 
 def multi_sort_sharded(engine, bv: BlockVector, cfg: SortConfig, comm: Comm) -> BlockVector:
-    """``multi_sort`` with pairs and the L^2 placements dealt over ranks."""
+    """``multi_sort`` with the ranking sharded as above and the L^2 placements dealt
+    over ranks (phases 3-4 of the module docstring)."""
     ranking = multi_rank_sharded(engine, bv, cfg.kernel, comm, tie_correction=cfg.tie_correction)
     layout = ranking.layout
     b, count = bv.block_size, len(bv.blocks)
@@ -205,7 +337,8 @@ def multi_sort_sharded(engine, bv: BlockVector, cfg: SortConfig, comm: Comm) -> 
             engine.note_indicator_eval()
         prod = engine.mul(sel, engine.stack([ranking.row_replicated[j] for _, j in mine]), site="sort-place")
         placed_all = dict(zip(mine, engine.unstack(prod)))
-    out = []
+    # phase 3: per-output-block partial sums, one all-reduce
+    partial = []
     for i in range(count):
         acc = None
         for (ii, j) in mine:
@@ -215,10 +348,10 @@ def multi_sort_sharded(engine, bv: BlockVector, cfg: SortConfig, comm: Comm) -> 
             if placed is None:
                 placed = place_block(engine, spreads[j], ranking.row_replicated[j], i, layout, window)
             acc = placed if acc is None else engine.add(acc, placed)
-        acc = _sum_across(engine, acc, comm)
-        owner = comm.owner(i)
-        blk = None
-        if comm.rank == owner:
-            blk = transpose_vector(engine, sum_axis(engine, acc, layout, "col"), layout, "col_to_row")
-        out.append(_broadcast(engine, blk, owner, comm))
+        partial.append(acc)
+    summed = _sum_all(engine, partial, comm)
+    # phase 4: owners finish (SumC + TransC); one all-gather
+    owned = {i: transpose_vector(engine, sum_axis(engine, summed[i], layout, "col"), layout, "col_to_row")
+             for i in range(count) if comm.owner(i) == comm.rank}
+    out = _gather_owned(engine, owned, count, comm)
     return BlockVector(blocks=tuple(out), block_size=b, total_len=bv.total_len)

@@ -237,9 +237,10 @@ def test_cfg4_masks_and_values_n128_vs_slotsim(eng_long, kind):
     assert verr < BOUNDS["cfg4_value"], verr
 
 
-def _multi_sort_check(eng, v, tie_correction, bound):
+def _multi_sort_check(eng, v, tie_correction, bound, packed=False):
     scfg = M.SortConfig(kernel=M.KernelConfig(mode="composite", composite=(6, 2),
-                                              indicator_composite=(6, 2)), tie_correction=tie_correction)
+                                              indicator_composite=(6, 2)), tie_correction=tie_correction,
+                        packed=packed)
     eng.cost_reset()
     out = M.block_merge(eng, M.multi_sort(eng, M.block_split(eng, v), scfg))
     sim = _sim(eng)
@@ -262,3 +263,13 @@ def test_cfg5_multi_sort_n1024_tie_corrected(require_cuda):
     eng = M.B200Engine(preset("long58"))
     v = np.random.default_rng(0).choice(8192, 1024, replace=False) / 8192
     _multi_sort_check(eng, v, True, BOUNDS["cfg5_sort_tc"])
+
+
+def test_cfg5_multi_sort_n1024_packed(eng_long):
+    """Two blocks per ciphertext (packing.py: 18 comparison + 32 indicator
+    evaluations, BASELINE's 32 ciphertexts): same circuit on the slot oracle
+    within 1e-6, order exact."""
+    v = np.random.default_rng(0).choice(8192, 1024, replace=False) / 8192
+    _multi_sort_check(eng_long, v, False, BOUNDS["cfg5_sort"], packed=True)
+    rep = eng_long.cost_snapshot()
+    assert rep.cmp_evals == 18 and rep.ind_evals == 32

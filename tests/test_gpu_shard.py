@@ -25,15 +25,19 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, what, out_dir):
+def _worker(rank, world, port, what, out_dir, backend="gloo"):
     import torch
     import torch.distributed as dist
 
     from paper_2412_15126_b200.shard import Comm, multi_rank_sharded, multi_sort_sharded
 
-    torch.cuda.set_device(0)
+    dev = rank if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     eng = M.B200Engine(preset("toy_sort"))
     bv = M.block_split(eng, VALUES)
     comm = Comm()
@@ -47,9 +51,14 @@ def _worker(rank, world, port, what, out_dir):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
 @pytest.mark.parametrize("what", ["rank", "sort"])
-def test_two_rank_gpu_shards_are_bit_identical(tmp_path, what, require_cuda):
-    mp.spawn(_worker, args=(2, _port(), what, str(tmp_path)), nprocs=2, join=True)
+def test_two_rank_gpu_shards_are_bit_identical(tmp_path, what, backend, require_cuda):
+    import torch
+
+    if backend == "nccl" and torch.cuda.device_count() < 2:
+        pytest.skip("NCCL sharding needs 2 GPUs (one rank per GPU)")
+    mp.spawn(_worker, args=(2, _port(), what, str(tmp_path), backend), nprocs=2, join=True)
     eng = M.B200Engine(preset("toy_sort"))
     bv = M.block_split(eng, VALUES)
     if what == "rank":

@@ -24,7 +24,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, what, out_dir):
+def _worker(rank, world, port, what, out_dir, values=None, tie=False):
     import torch.distributed as dist
 
     from oracle.oracle import oracle_engine
@@ -33,13 +33,14 @@ def _worker(rank, world, port, what, out_dir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     eng = oracle_engine(preset("toy_sort"))
-    bv = M.block_split(eng, VALUES)
+    bv = M.block_split(eng, VALUES if values is None else values)
     comm = Comm()
     if what == "rank":
-        res = multi_rank_sharded(eng, bv, KCFG, comm).ranks
+        res = multi_rank_sharded(eng, bv, KCFG, comm, tie_correction=tie).ranks
     else:
-        res = multi_sort_sharded(eng, bv, M.SortConfig(kernel=KCFG, tie_correction=False), comm)
-    np.savez(os.path.join(out_dir, f"{what}_{rank}.npz"), *[b.data for b in res.blocks])
+        res = multi_sort_sharded(eng, bv, M.SortConfig(kernel=KCFG, tie_correction=tie), comm)
+    np.savez(os.path.join(out_dir, f"{what}_{rank}.npz"), *[b.data for b in res.blocks],
+             counts=np.array([comm.collectives, comm.level_syncs]))
     dist.destroy_process_group()
 
 
@@ -62,7 +63,7 @@ def test_two_rank_shards_are_bit_identical(tmp_path, what):
     eng, res = _single(what)
     for r in range(2):
         got = np.load(tmp_path / f"{what}_{r}.npz")
-        assert len(got.files) == len(res.blocks)
+        assert len([f for f in got.files if f.startswith('arr_')]) == len(res.blocks)
         for i, blk in enumerate(res.blocks):
             assert np.array_equal(got[f"arr_{i}"], blk.data), (r, i)
     vals = M.block_merge(eng, res)
@@ -72,3 +73,24 @@ def test_two_rank_shards_are_bit_identical(tmp_path, what):
         assert np.array_equal(np.rint(vals), fractional_ranks(VALUES))
     else:
         assert np.abs(vals - np.sort(VALUES)).max() < 5e-3
+
+
+TIES = np.repeat(np.random.default_rng(9).choice(64, 48, replace=False) / 64, 2)  # 96 values, all tied
+
+
+@pytest.mark.slow
+def test_three_rank_tie_corrected_sort_bit_identical_and_o1_collectives(tmp_path):
+    """3 ranks, 3 unpadded blocks, tie correction (block tie offsets,
+    reference ranking.py:395-423): bit-identical blocks, and exactly one data
+    collective + one level exchange per phase (5 phases)."""
+    mp.spawn(_worker, args=(3, _port(), "sort", str(tmp_path), TIES, True), nprocs=3, join=True)
+    from oracle.oracle import oracle_engine
+
+    eng = oracle_engine(preset("toy_sort"))
+    res = M.multi_sort(eng, M.block_split(eng, TIES), M.SortConfig(kernel=KCFG, tie_correction=True))
+    for r in range(3):
+        got = np.load(tmp_path / f"sort_{r}.npz")
+        assert list(got["counts"]) == [5, 5]
+        for i, blk in enumerate(res.blocks):
+            assert np.array_equal(got[f"arr_{i}"], blk.data), (r, i)
+    assert np.abs(M.block_merge(eng, res) - np.sort(TIES)).max() < 5e-2
