@@ -359,6 +359,9 @@ __device__ __forceinline__ void fused_store(const FuseArgs &f, int bi, int r, in
     plain_dst[n] = x;
 }
 
+#ifndef SRK_EARLY_LOADS
+#define SRK_EARLY_LOADS 1  // first-pass data loads issued before the prime-constant load
+#endif
 #ifndef SRK_KSC_G
 #define SRK_KSC_G 8  // elements per digit step of the ST_KSC epilogue (2G loads in flight)
 #endif
@@ -608,7 +611,10 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB
     extern __shared__ uint64_t smem[];
 
     const int n = 1 << log_n;
-    const int CB = blockDim.x / TPS;  // sub-transforms per CTA
+    // sub-transforms per CTA (a power of two): shifts and masks, no division subroutine
+    constexpr int LTPS = LOG_T - LE1;
+    const int lcb = (31 - __clz((int)blockDim.x)) - LTPS;
+    const int CB = 1 << lcb;
     const int limb = blockIdx.z, poly = blockIdx.y;
     const int bi = b.ppc == 2 ? poly >> 1 : (b.ppc == 1 ? poly : poly / b.ppc);
     const int r = poly - bi * b.ppc;
@@ -616,45 +622,18 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB
     if (!limb_map(b, r, limb, t, pid)) return;
     uint64_t *data =
         b.ptr + (long long)bi * b.ct_stride + (long long)r * b.poly_stride + (long long)t * n;
-    const PrimeConst pc = tb.pc[pid];
-    const uint64_t q = pc.q, two_q = pc.two_q;
-    // prime-class split of mixed batches (uniform per CTA): the FP64 kernel never
-    // touches a limb >= 2^41; the integer kernel skips FP64 limbs when filtered
-    if ((KM == 1 || b.cls == 1) ? q >= SRK_F64_Q : (b.cls == 2 && q < SRK_F64_Q)) return;
-    const TwPtr tw = {(INV ? tb.itw : tb.tw) + (long long)pid * n, (INV ? tb.itwd : tb.twd) + (long long)pid * n};
-    if constexpr (ST == ST_KSC && SRK_KSC_PREFETCH) {
-        // the epilogue's digit / key / addend rows of this CTA (CB consecutive chunks,
-        // contiguous) are pulled into L2 while the butterflies run: one bulk prefetch
-        // per array, issued by one thread each
-        const int a = threadIdx.x, beta = f.ks_beta;
-        if (a <= 2 * beta) {
-            const int cb = blockDim.x / NttShape<LOG_T>::TPS;
-            const long long base = (long long)t * n + (long long)blockIdx.x * cb * NttShape<LOG_T>::T;
-            const uint32_t bytes = (uint32_t)(cb * NttShape<LOG_T>::T * 8);
-            const uint64_t *p = nullptr;
-            if (a < beta) {
-                p = (a == pid / f.ks_alpha ? f.ks_d + bi * f.ks_d_ct : f.ks_ext + bi * f.ks_ext_ct + a * f.ks_ext_dig);
-            } else if (a < 2 * beta) {
-                p = f.ks_key + (a - beta) * f.ks_key_j + r * f.ks_key_r;
-            } else if (r == 0 ? f.has_add0 : f.has_add1) {
-                p = (r == 0 ? f.add0 : f.add1) + bi * f.add_ct;
-            }
-            if (p) prefetch_l2_bulk(p + base, bytes);
-        }
-    }
     const uint64_t *lsrc = data;  // LD_PLAIN / LD_AUTO source limb
     if constexpr (FIRST && (LD == LD_PLAIN || LD == LD_AUTO)) {
         if (f.src) lsrc = f.src + (long long)bi * f.src_ct + (long long)r * f.src_ps + (long long)t * n;
     }
-
     const int tid = threadIdx.x;
     int sb, u;  // local sub-transform and thread-within-sub-transform
     if (COL) {
-        sb = tid % CB;
-        u = tid / CB;
+        sb = tid & (CB - 1);
+        u = tid >> lcb;
     } else {
-        sb = tid / TPS;
-        u = tid % TPS;
+        sb = tid >> LTPS;
+        u = tid & (TPS - 1);
     }
     const int sub = blockIdx.x * CB + sb;  // column index (COL) or chunk index
     const int C = n >> LOG_T;               // COL: #columns ; ROW: #rows (chunks)
@@ -665,13 +644,52 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB
     auto sidx = [&](int c) -> int {
         return COL ? c * CB + sb : row_sidx<LOG_T>(sb, c);
     };
+    const TwPtr tw = {(INV ? tb.itw : tb.tw) + (long long)pid * n, (INV ? tb.itwd : tb.twd) + (long long)pid * n};
+    // arithmetic mode, uniform per launch: 2 = FP64 (q < 2^41), 0 = Harvey lazy integer
+    constexpr int mode = KM == 1 ? 2 : 0;
+    // the first loads need no prime constant: issue them before its (dependent) load
+    uint64_t x[E];
+    constexpr bool RAW = SRK_EARLY_LOADS && !(FIRST && LD == LD_SPREAD);
+    auto raw = [&](int c) -> uint64_t {
+        if constexpr (FIRST && LD == LD_AUTO) return __ldg(lsrc + auto_index((uint32_t)gaddr(c), f.galois, log_n));
+        else if constexpr (FIRST) return lsrc[gaddr(c)];
+        else return data[gaddr(c)];
+    };
+    if constexpr (RAW) {
+#pragma unroll
+        for (int e = 0; e < E; e++) x[e] = raw((INV && COL) ? u * E + e : u + TPS * e);
+    } else if constexpr (INV && COL) {
+#pragma unroll
+        for (int e = 0; e < E; e++) x[e] = data[gaddr(u * E + e)];
+    }
+    const PrimeConst pc = tb.pc[pid];
+    const uint64_t q = pc.q, two_q = pc.two_q;
+    // prime-class split of mixed batches (uniform per CTA): the FP64 kernel never
+    // touches a limb >= 2^41; the integer kernel skips FP64 limbs when filtered
+    if ((KM == 1 || b.cls == 1) ? q >= SRK_F64_Q : (b.cls == 2 && q < SRK_F64_Q)) return;
+    if constexpr (ST == ST_KSC && SRK_KSC_PREFETCH) {
+        // the epilogue's digit / key / addend rows of this CTA (CB consecutive chunks,
+        // contiguous) are pulled into L2 while the butterflies run: one bulk prefetch
+        // per array, issued by one thread each
+        const int a = threadIdx.x, beta = f.ks_beta;
+        if (a <= 2 * beta) {
+            const long long base0 = (long long)t * n + (long long)blockIdx.x * CB * T;
+            const uint32_t bytes = (uint32_t)(CB * T * 8);
+            const uint64_t *p = nullptr;
+            if (a < beta) {
+                p = (a == pid / f.ks_alpha ? f.ks_d + bi * f.ks_d_ct : f.ks_ext + bi * f.ks_ext_ct + a * f.ks_ext_dig);
+            } else if (a < 2 * beta) {
+                p = f.ks_key + (a - beta) * f.ks_key_j + r * f.ks_key_r;
+            } else if (r == 0 ? f.has_add0 : f.has_add1) {
+                p = (r == 0 ? f.add0 : f.add1) + bi * f.add_ct;
+            }
+            if (p) prefetch_l2_bulk(p + base0, bytes);
+        }
+    }
     auto load = [&](int c) -> uint64_t {
         if constexpr (FIRST) return fused_load<LD>(f, tb.pc, bi, r, t, pc, gaddr(c), log_n, lsrc);
         else return data[gaddr(c)];
     };
-
-    // arithmetic mode, uniform per launch: 2 = FP64 (q < 2^41), 0 = Harvey lazy integer
-    constexpr int mode = KM == 1 ? 2 : 0;
     // (double) q and 1 / (double) q precomputed per prime (no per-CTA division)
     const F64Q fq = {__longlong_as_double((long long)pc.qd_bits), __longlong_as_double((long long)pc.qinv_bits)};
     // first-pass loads are canonical u64; FP64 limbs convert on load
@@ -688,11 +706,15 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB
         if constexpr (mode == 2) return (uint64_t)__double_as_longlong(f64_of_u64(v));
         else return v;
     };
-    uint64_t x[E];
+    // first-pass conversion of the raw loads (canonical u64 -> FP64 operand)
+    auto cvt = [&](uint64_t v) -> uint64_t {
+        if constexpr (mode == 2 && FIRST) return (uint64_t)__double_as_longlong(f64_of_u64(v));
+        else return v;
+    };
     if (!INV) {
         // ---- round 1: strided ownership c = u + TPS e, strides T/2 .. TPS
 #pragma unroll
-        for (int e = 0; e < E; e++) x[e] = FIRST ? load_m(u + TPS * e) : data[gaddr(u + TPS * e)];
+        for (int e = 0; e < E; e++) x[e] = RAW ? cvt(x[e]) : load_m(u + TPS * e);
         if constexpr (mode == 2)
             FwdR1<E, LE1, 2>::run(x, tw, base, q, two_q, fq);
         else
@@ -768,7 +790,7 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB
             // second pass: FP64 sums doubled every stage of the first -> re-centre
 #pragma unroll
             for (int e = 0; e < E; e++) {
-                uint64_t v = data[gaddr(u * E + e)];
+                uint64_t v = x[e];  // data[gaddr(u * E + e)], loaded above
                 if constexpr (mode == 2)
                     v = (uint64_t)__double_as_longlong(
                         centre_f64(__longlong_as_double((long long)v), fq.q, fq.qinv));
@@ -776,7 +798,7 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB
             }
         } else {
 #pragma unroll
-            for (int e = 0; e < E; e++) smem[sidx(u + TPS * e)] = load_m(u + TPS * e);
+            for (int e = 0; e < E; e++) smem[sidx(u + TPS * e)] = RAW ? cvt(x[e]) : load_m(u + TPS * e);
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < E; e++) x[e] = smem[sidx(u * E + e)];
