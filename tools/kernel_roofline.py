@@ -9,7 +9,10 @@ import re
 import sys
 from collections import defaultdict
 
-PEAK = 6553.3  # MEASURED_PEAKS.json hbm copy GB/s
+import os
+
+_PEAKS = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+PEAK = float(json.load(open(_PEAKS))["hbm_gbs"]) if os.path.exists(_PEAKS) else 6450.3  # measured copy GB/s
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
          "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
 
@@ -39,10 +42,13 @@ for name, e in sorted(per.items(), key=lambda kv: -kv[1]["s"]):
     out.append({"kernel": name, "launches": e["launches"], "time_share": round(e["s"] / total, 4),
                 "avg_us": round(e["s"] / e["launches"] * 1e6, 2), "dram_gb_per_s": round(gbs, 1),
                 "frac_of_hbm": round(gbs / PEAK, 3)})
+total_bytes = sum(e["bytes"] for e in per.values())
 json.dump({"command": sys.argv[3] if len(sys.argv) > 3 else "", "peak_gbs": PEAK,
            "note": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                   "--clock-control none (caches flushed between launches, launches serialised)",
+                   "--clock-control none " + (sys.argv[4] if len(sys.argv) > 4 else "") + " (launches serialised)",
+           "dram_bytes": int(total_bytes), "time_s": total,
            "kernels": out}, open(sys.argv[2], "w"), indent=1)
+print(f"total: {total * 1e3:.3f} ms, DRAM {total_bytes / 1e9:.2f} GB")
 for k in out:
     print(f"{k['kernel'][:60]:60s} {k['launches']:5d} {100 * k['time_share']:5.1f}% {k['avg_us']:8.1f}us "
           f"{k['dram_gb_per_s']:7.0f} GB/s {100 * k['frac_of_hbm']:5.1f}%")

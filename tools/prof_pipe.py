@@ -19,11 +19,12 @@ if what == "rank":
     ct = eng.encrypt(v)
     run = lambda: M.rank(eng, ct, 128, cfg).ranks  # noqa: E731
 else:
-    nv = int(what[4:] or 256)  # "sort" = N=256, "sort1024" = N=1024, ...
+    packed = what.startswith("p")  # "psort1024": the packed layout (packing.py)
+    nv = int(what.lstrip("p")[4:] or 256)  # "sort" = N=256, "sort1024" = N=1024, ...
     eng = M.B200Engine(preset("long"))
     v = np.random.default_rng(0).choice(8 * nv, nv, replace=False) / (8 * nv)
     cfg = M.SortConfig(kernel=M.KernelConfig(mode="composite", composite=(6, 2), indicator_composite=(6, 2)),
-                       tie_correction=False)
+                       tie_correction=False, packed=packed)
     bv = M.block_split(eng, v)
     run = lambda: M.multi_sort(eng, bv, cfg)  # noqa: E731
 run()  # warm-up: keys, constants (outside the profiler range)
