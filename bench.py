@@ -344,23 +344,30 @@ def _event_time(torch, fn, dist=None):
 
 
 def run_sharded_sort(torch, dist):
-    """Config 5 on every rank: multi_sort of N=1024 sharded over the world (shard.py)."""
+    """Config 5 on every rank: multi_sort of N=1024 sharded over the world (shard.py),
+    in the reference layout and in the packed layout (packing.py)."""
     from paper_2412_15126_b200 import (B200Engine, KernelConfig, SortConfig, block_merge, block_split)
     from paper_2412_15126_b200.params import preset
     from paper_2412_15126_b200.shard import Comm, multi_sort_sharded
 
     eng = B200Engine(preset("long"))
     v1024 = np.random.default_rng(0).choice(8192, 1024, replace=False) / 8192
-    scfg = SortConfig(kernel=KernelConfig(mode="composite", composite=(6, 2), indicator_composite=(6, 2)),
-                      tie_correction=False)
+    kcfg = KernelConfig(mode="composite", composite=(6, 2), indicator_composite=(6, 2))
     bv = block_split(eng, v1024)
     comm = Comm()
-    multi_sort_sharded(eng, bv, scfg, comm)  # warm-up: keys, plaintext cache
-    dt, res = _event_time(torch, lambda: multi_sort_sharded(eng, bv, scfg, comm), dist)
-    srt = block_merge(eng, res)
-    return {"latency_s": dt, "order_ok": bool(np.array_equal(np.argsort(srt), np.arange(1024))),
-            "max_abs_err": float(np.abs(srt - np.sort(v1024)).max()), "params": "long",
-            "gpus": comm.world, "sharding": f"block pairs + placements round-robin, {dist.get_backend()} all-reduce"}
+    out = {}
+    for name, packed in (("sort_n1024_s", False), ("sort_n1024_packed_s", True)):
+        scfg = SortConfig(kernel=kcfg, tie_correction=False, packed=packed)
+        multi_sort_sharded(eng, bv, scfg, comm)  # warm-up: keys, plaintext cache
+        c0, s0 = comm.collectives, comm.level_syncs
+        dt, res = _event_time(torch, lambda: multi_sort_sharded(eng, bv, scfg, comm), dist)
+        srt = block_merge(eng, res)
+        out[name] = {"latency_s": dt, "order_ok": bool(np.array_equal(np.argsort(srt), np.arange(1024))),
+                     "max_abs_err": float(np.abs(srt - np.sort(v1024)).max()), "params": "long",
+                     "gpus": comm.world, "collectives": comm.collectives - c0, "level_syncs": comm.level_syncs - s0,
+                     "sharding": f"5 phases (shard.py), {dist.get_backend()}",
+                     "layout": "packed (packing.py)" if packed else "reference"}
+    return out
 
 
 def _timed(torch, fn, reps=1):
@@ -475,6 +482,17 @@ def run_pipelines(torch, quick=False):
                            "cost": cost, "params": "long", "gpus": 1,
                            "note": "latency_s: first run (includes generating this pipeline's Galois keys and "
                                    "encoding its constants); warm_latency_s: second run"}
+    # rank N=1024 (multi_rank: the 36 block-pair comparisons + complement folds), both layouts
+    from paper_2412_15126_b200 import multi_rank
+    from oracle.plain import fractional_ranks as _fr
+    for name, pk in (("rank_n1024_s", False), ("rank_n1024_packed_s", True)):
+        first, _ = _timed(torch, lambda pk=pk: block_merge(eng, multi_rank(eng, bv, scfg.kernel, packed=pk)))
+        cost, _ = _census(eng, lambda pk=pk: multi_rank(eng, bv, scfg.kernel, packed=pk))
+        warm, rk = _timed(torch, lambda pk=pk: block_merge(eng, multi_rank(eng, bv, scfg.kernel, packed=pk)))
+        out[name] = {"latency_s": first, "warm_latency_s": warm,
+                     "exact_ranks": bool(np.array_equal(np.rint(rk), _fr(v1024))),
+                     "max_rank_err": float(np.abs(rk - _fr(v1024)).max()), "cost": cost, "params": "long",
+                     "layout": "two blocks per ciphertext (packing.py)" if pk else "reference (one block per ciphertext)"}
     # the same sort in the packed layout (two blocks per ciphertext: 18 comparison and
     # 32 indicator evaluations instead of 36 / 64; packing.py)
     pcfg = SortConfig(kernel=scfg.kernel, tie_correction=False, packed=True)
@@ -650,7 +668,7 @@ def gpu_arm(args):
             dist.barrier()
             sharded = run_sharded_sort(torch, dist) if not args.quick else None
             if rank_id == 0 and sharded is not None:
-                pipelines["sort_n1024_s"] = sharded
+                pipelines.update(sharded)
 
     if rank_id == 0:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(

@@ -55,6 +55,12 @@ from .sorting import SortConfig, _neg_rank_targets, common_level, place_block
 
 __all__ = ["Comm", "multi_rank_sharded", "multi_sort_sharded"]
 
+# The packed layout (packing.py, two blocks per ciphertext) shards the same way:
+# packed comparisons / placements are the units dealt round-robin, the
+# per-half partial sums go through the phase's all-reduce, and the owner folds
+# the halves (one rotation by slots/2) -- after the reduction, so the result is
+# bit-identical to the single-GPU packed run.
+
 _NO_LEVEL = 1 << 20
 MAX_WORLD = 8  # int64 sums of world residues < 2^60 must not overflow
 
@@ -233,9 +239,13 @@ def _gather_pairs(engine, owned2: dict, count: int, comm: Comm):
 
 
 def multi_rank_sharded(engine, bv: BlockVector, cfg: KernelConfig, comm: Comm, *,
-                       tie_correction: bool = False) -> MultiRankPipeline:
+                       tie_correction: bool = False, packed: bool = False) -> MultiRankPipeline:
     """``multi_rank_pipeline`` with blocks, block pairs and block finishes dealt over
     ``comm``'s ranks (phases 0-2 of the module docstring)."""
+    if packed:
+        if tie_correction:
+            raise ValueError("the packed layout has no tie correction")
+        return _multi_rank_sharded_packed(engine, bv, cfg, comm)
     b, count = bv.block_size, len(bv.blocks)
     layout = MatrixLayout(b, engine.params.slot_count)
     valid_last = bv.valid_in(count - 1)
@@ -314,6 +324,10 @@ def _finish_tie(engine, parts, i, valid_i, layout):
 def multi_sort_sharded(engine, bv: BlockVector, cfg: SortConfig, comm: Comm) -> BlockVector:
     """``multi_sort`` with the ranking sharded as above and the L^2 placements dealt
     over ranks (phases 3-4 of the module docstring)."""
+    if getattr(cfg, "packed", False):
+        if cfg.tie_correction:
+            raise ValueError("the packed layout has no tie correction")
+        return _multi_sort_sharded_packed(engine, bv, cfg.kernel, comm)
     ranking = multi_rank_sharded(engine, bv, cfg.kernel, comm, tie_correction=cfg.tie_correction)
     layout = ranking.layout
     b, count = bv.block_size, len(bv.blocks)
@@ -353,5 +367,136 @@ def multi_sort_sharded(engine, bv: BlockVector, cfg: SortConfig, comm: Comm) -> 
     # phase 4: owners finish (SumC + TransC); one all-gather
     owned = {i: transpose_vector(engine, sum_axis(engine, summed[i], layout, "col"), layout, "col_to_row")
              for i in range(count) if comm.owner(i) == comm.rank}
+    out = _gather_owned(engine, owned, count, comm)
+    return BlockVector(blocks=tuple(out), block_size=b, total_len=bv.total_len)
+
+
+# ---------------------------------------------------------------------------
+# packed layout (packing.py) over ranks
+# ---------------------------------------------------------------------------
+def _multi_rank_sharded_packed(engine, bv: BlockVector, cfg: KernelConfig, comm: Comm) -> MultiRankPipeline:
+    from .packing import _add, _rot_many, _two_halves, can_pack
+    from .chebyshev import compare_kernel
+    from .ranking import _row_band_mask
+
+    b, count = bv.block_size, len(bv.blocks)
+    slots = engine.params.slot_count
+    half = slots // 2
+    if not can_pack(engine, b):
+        raise ValueError(f"two {b}x{b} blocks do not fit {slots} slots")
+    layout = MatrixLayout(b, slots)
+    valid_last = bv.valid_in(count - 1)
+    rows, cols = _replicated_sharded(engine, bv, layout, comm)
+    pairs = block_pairs(count)
+    packs = [(pairs[k], pairs[k + 1] if k + 1 < len(pairs) else None) for k in range(0, len(pairs), 2)]
+    mine = [k for k in range(len(packs)) if comm.owner(k) == comm.rank]
+    hi_i = sorted({packs[k][1][0] for k in mine if packs[k][1] is not None})
+    hi_j = sorted({packs[k][1][1] for k in mine if packs[k][1] is not None})
+    rot_rows = dict(zip(hi_i, _rot_many(engine, [rows[i] for i in hi_i], half)))
+    rot_cols = dict(zip(hi_j, _rot_many(engine, [cols[j] for j in hi_j], half)))
+    xs = [_add(engine, rows[packs[k][0][0]], rot_rows[packs[k][1][0]] if packs[k][1] else None) for k in mine]
+    ys = [_add(engine, cols[packs[k][0][1]], rot_cols[packs[k][1][1]] if packs[k][1] else None) for k in mine]
+    cmp_mine = []
+    if len(mine) > 1 and batched(engine):
+        cmp_mine = engine.unstack(compare_kernel(engine, engine.stack(xs), engine.stack(ys), cfg))
+        for _ in range(len(mine) - 1):
+            engine.note_compare_eval()
+    elif mine:
+        cmp_mine = [compare_kernel(engine, x, y, cfg) for x, y in zip(xs, ys)]
+    if valid_last < b:
+        band, ones = _row_band_mask(slots, b, valid_last), np.ones(slots)
+        for idx, k in enumerate(mine):
+            lo, hi = packs[k]
+            lo_pad, hi_pad = lo[1] == count - 1, hi is not None and hi[1] == count - 1
+            if lo_pad or hi_pad:
+                m = _two_halves(band if lo_pad else ones, band if hi_pad else ones, half)
+                cmp_mine[idx] = engine.mul_plain(cmp_mine[idx], m, site="block-pad-mask")
+    up = [[None, None] for _ in range(count)]
+    low = [[None, None] for _ in range(count)]
+    for c, k in zip(cmp_mine, mine):
+        for h, pair in enumerate(packs[k]):
+            if pair is None:
+                continue
+            i, j = pair
+            up[i][h] = _add(engine, up[i][h], c)
+            if j > i:
+                low[j][h] = _add(engine, low[j][h], engine.add_plain(engine.negate(c), 1.0))
+    parts = []
+    for i in range(count):
+        parts.extend([up[i][0], up[i][1], low[i][0], low[i][1]])
+    summed = _sum_all(engine, parts, comm)
+    owned = {}
+    for i in range(count):
+        if comm.owner(i) != comm.rank:
+            continue
+        u0, u1, l0, l1 = summed[4 * i: 4 * i + 4]
+        upper = _add(engine, u0, engine.rotate(u1, half) if u1 is not None else None)
+        lower = None
+        if i > 0:
+            lower = _add(engine, l0, engine.rotate(l1, half) if l1 is not None else None)
+        owned[i] = finish_block_rank(engine, upper, lower, i, bv, layout, None)
+    blocks = _gather_owned(engine, owned, count, comm)
+    return MultiRankPipeline(
+        ranks=BlockVector(blocks=tuple(blocks), block_size=b, total_len=bv.total_len),
+        comparisons={"packed_mine": cmp_mine},
+        row_replicated=rows,
+        col_replicated=cols,
+        layout=layout,
+    )
+
+
+def _multi_sort_sharded_packed(engine, bv: BlockVector, kcfg: KernelConfig, comm: Comm) -> BlockVector:
+    from .packing import _add, _rot_many, _two_halves
+
+    ranking = _multi_rank_sharded_packed(engine, bv, kcfg, comm)
+    layout = ranking.layout
+    b, count = bv.block_size, len(bv.blocks)
+    slots = engine.params.slot_count
+    half = slots // 2
+    window = with_input_range(kcfg, -float(b * count), float(b * count))
+    rank_blocks = common_level(engine, ranking.ranks.blocks)
+    jpairs = [(j, j + 1 if j + 1 < count else None) for j in range(0, count, 2)]
+    units = [(i, m) for i in range(count) for m in range(len(jpairs))]
+    mine = [u for idx, u in enumerate(units) if comm.owner(idx) == comm.rank]
+    ms = sorted({m for _, m in mine})
+    need = sorted({j for m in ms for j in jpairs[m] if j is not None})
+    if batched(engine) and len(need) > 1:
+        spreads = dict(zip(need, engine.unstack(replicate(engine, engine.stack([rank_blocks[j] for j in need]),
+                                                               layout, "row"))))
+    else:
+        spreads = {j: replicate(engine, rank_blocks[j], layout, "row") for j in need}
+    his = [jpairs[m][1] for m in ms if jpairs[m][1] is not None]
+    rot = _rot_many(engine, [spreads[j] for j in his] + [ranking.row_replicated[j] for j in his], half)
+    rot_spread, rot_rowrep = dict(zip(his, rot[: len(his)])), dict(zip(his, rot[len(his):]))
+    spread_p = {m: _add(engine, spreads[jpairs[m][0]], rot_spread.get(jpairs[m][1])) for m in ms}
+    rowrep_p = {m: _add(engine, ranking.row_replicated[jpairs[m][0]], rot_rowrep.get(jpairs[m][1])) for m in ms}
+
+    def targets(i):
+        t = _neg_rank_targets(slots, b, "row", b * i + 1)
+        return _two_halves(t, t, half)
+
+    placed = []
+    if batched(engine) and len(mine) > 1:
+        tg = np.stack([targets(i) for i, _ in mine])
+        shifted = engine.add_plain(engine.stack([spread_p[m] for _, m in mine]), tg)
+        sel = indicator_kernel(engine, shifted, -0.5, 0.5, window, boundary="open")
+        for _ in range(len(mine) - 1):
+            engine.note_indicator_eval()
+        placed = engine.unstack(engine.mul(sel, engine.stack([rowrep_p[m] for _, m in mine]), site="sort-place"))
+    else:
+        for i, m in mine:
+            sel = indicator_kernel(engine, engine.add_plain(spread_p[m], targets(i)), -0.5, 0.5, window,
+                                   boundary="open")
+            placed.append(engine.mul(sel, rowrep_p[m], site="sort-place"))
+    accs = [None] * count
+    for (i, _), p in zip(mine, placed):
+        accs[i] = _add(engine, accs[i], p)
+    summed = _sum_all(engine, accs, comm)
+    owned = {}
+    for i in range(count):
+        if comm.owner(i) != comm.rank:
+            continue
+        f = engine.add(summed[i], engine.rotate(summed[i], half))
+        owned[i] = transpose_vector(engine, sum_axis(engine, f, layout, "col"), layout, "col_to_row")
     out = _gather_owned(engine, owned, count, comm)
     return BlockVector(blocks=tuple(out), block_size=b, total_len=bv.total_len)

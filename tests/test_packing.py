@@ -41,3 +41,15 @@ def test_packed_requires_untied_and_room():
     from paper_2412_15126_b200.packing import can_pack
 
     assert can_pack(sim, 128) and not can_pack(sim, 256)
+
+
+def test_packed_multi_rank_equals_reference_layout():
+    from oracle.plain import fractional_ranks
+
+    v = np.random.default_rng(0).choice(8192, 1024, replace=False) / 8192
+    sim = SlotSim(SimParams(32768, 56))
+    bv = M.block_split(sim, v)
+    ref = M.block_merge(sim, M.multi_rank(sim, bv, KCFG))
+    got = M.block_merge(sim, M.multi_rank(sim, bv, KCFG, packed=True))
+    assert np.abs(got - ref).max() < 1e-9
+    assert np.array_equal(np.rint(got), fractional_ranks(v))

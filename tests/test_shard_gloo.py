@@ -24,7 +24,12 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, what, out_dir, values=None, tie=False):
+def _params(pname):
+    # ring 2^12 (2048 slots, blocks of 32): two blocks fit one ciphertext (packing.py)
+    return preset("toy_sort", log_n=12) if pname == "toy_sort12" else preset(pname)
+
+
+def _worker(rank, world, port, what, out_dir, values=None, tie=False, packed=False, pname="toy_sort"):
     import torch.distributed as dist
 
     from oracle.oracle import oracle_engine
@@ -32,13 +37,13 @@ def _worker(rank, world, port, what, out_dir, values=None, tie=False):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    eng = oracle_engine(preset("toy_sort"))
+    eng = oracle_engine(_params(pname))
     bv = M.block_split(eng, VALUES if values is None else values)
     comm = Comm()
     if what == "rank":
-        res = multi_rank_sharded(eng, bv, KCFG, comm, tie_correction=tie).ranks
+        res = multi_rank_sharded(eng, bv, KCFG, comm, tie_correction=tie, packed=packed).ranks
     else:
-        res = multi_sort_sharded(eng, bv, M.SortConfig(kernel=KCFG, tie_correction=tie), comm)
+        res = multi_sort_sharded(eng, bv, M.SortConfig(kernel=KCFG, tie_correction=tie, packed=packed), comm)
     np.savez(os.path.join(out_dir, f"{what}_{rank}.npz"), *[b.data for b in res.blocks],
              counts=np.array([comm.collectives, comm.level_syncs]))
     dist.destroy_process_group()
@@ -94,3 +99,26 @@ def test_three_rank_tie_corrected_sort_bit_identical_and_o1_collectives(tmp_path
         for i, blk in enumerate(res.blocks):
             assert np.array_equal(got[f"arr_{i}"], blk.data), (r, i)
     assert np.abs(M.block_merge(eng, res) - np.sort(TIES)).max() < 5e-2
+
+
+PACKVALS = np.random.default_rng(11).choice(128, 96, replace=False) / 128  # 3 blocks of 32
+
+
+@pytest.mark.slow
+def test_three_rank_packed_sort_bit_identical(tmp_path):
+    """The packed layout (packing.py) sharded over 3 ranks: packed comparisons and
+    placements dealt round-robin, halves folded after the all-reduce -- the same
+    limbs as the single-process packed sort."""
+    mp.spawn(_worker, args=(3, _port(), "sort", str(tmp_path), PACKVALS, False, True, "toy_sort12"),
+             nprocs=3, join=True)
+    from oracle.oracle import oracle_engine
+
+    eng = oracle_engine(_params("toy_sort12"))
+    res = M.multi_sort(eng, M.block_split(eng, PACKVALS),
+                       M.SortConfig(kernel=KCFG, tie_correction=False, packed=True))
+    for r in range(3):
+        got = np.load(tmp_path / f"sort_{r}.npz")
+        assert list(got["counts"]) == [5, 5]
+        for i, blk in enumerate(res.blocks):
+            assert np.array_equal(got[f"arr_{i}"], blk.data), (r, i)
+    assert np.abs(M.block_merge(eng, res) - np.sort(PACKVALS)).max() < 5e-3

@@ -8,7 +8,7 @@ raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], captu
 rows = list(csv.reader(raw))
 hdr, units = rows[0], dict(zip(rows[0], rows[1]))
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-         "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+         "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
 for r in rows[2:]:
     d = dict(zip(hdr, r))
 

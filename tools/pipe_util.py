@@ -35,7 +35,7 @@ for r in rows[2:]:
         except ValueError:
             e[k] = None
     try:
-        dur = float(d["gpu__time_duration.sum"]) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(
+        dur = float(d["gpu__time_duration.sum"]) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}.get(
             units.get("gpu__time_duration.sum"), 1.0)
     except (KeyError, ValueError):
         dur = None
