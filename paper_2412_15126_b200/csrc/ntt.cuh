@@ -198,10 +198,6 @@ __device__ __forceinline__ double centre_f64(double v, double q, double qinv) {
     const double t = fma(v, qinv, SRK_F64_MAGIC) - SRK_F64_MAGIC;
     return fma(-t, q, v);
 }
-// double of a signed |v| < 2^51 (bit trick: IADD + DADD, no I2F)
-__device__ __forceinline__ double f64_of_i64(long long v) {
-    return __longlong_as_double(v + 0x4338000000000000ll) - SRK_F64_MAGIC;
-}
 // signed integer of an integer-valued double |r| < 2^51: r + 1.5*2^52 keeps
 // exponent 52, so its bit pattern is 0x4338000000000000 + r (one DADD + IADD)
 __device__ __forceinline__ long long i64_of_f64(double r) {
@@ -359,22 +355,7 @@ __device__ __forceinline__ void fused_store(const FuseArgs &f, int bi, int r, in
     plain_dst[n] = x;
 }
 
-#ifndef SRK_EARLY_LOADS
-#define SRK_EARLY_LOADS 1  // first-pass data loads issued before the prime-constant load
-#endif
-#ifndef SRK_KSC_G
 #define SRK_KSC_G 8  // elements per digit step of the ST_KSC epilogue (2G loads in flight)
-#endif
-#ifndef SRK_KSC_SPLIT
-#define SRK_KSC_SPLIT 0  // inner product: FP64 quotient + integer remainder (0: one FP64 modmul per term)
-#endif
-#ifndef SRK_KSC_PREFETCH
-#define SRK_KSC_PREFETCH 0  // bulk L2 prefetch of the epilogue's rows at kernel start
-#endif
-// one bulk L2 prefetch (TMA unit, no registers): bytes multiple of 16, 16-B aligned
-__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 // ST_KSC epilogue of the forward row pass (the ModDown NTT of a key switch):
 // the ciphertext-modulus limbs' key-switch inner product and the ModDown combine
@@ -401,7 +382,7 @@ __device__ __forceinline__ void ksc_epilogue(const FuseArgs &f, uint64_t *sm, SI
     const uint64_t *asrc = (r == 0 ? f.add0 : f.add1) + bi * f.add_ct + off0;
 #pragma unroll
     for (int g0 = 0; g0 < E; g0 += G) {
-        if constexpr (KM == 1 && !SRK_KSC_SPLIT) {
+        if constexpr (KM == 1) {
             double s[G];
 #pragma unroll
             for (int e = 0; e < G; e++) s[e] = -__longlong_as_double((long long)sm[sidx(u + TPS * (g0 + e))]);
@@ -429,50 +410,6 @@ __device__ __forceinline__ void ksc_epilogue(const FuseArgs &f, uint64_t *sm, SI
                 double a = f64_of_u64(av[e]);
                 if (f.add_scaled) a = modmul_f64(a, af, fq.q, fq.qinv);
                 sm[sidx(u + TPS * (g0 + e))] = canon_u64_of_f64(v + a, fq.q, fq.qinv);
-            }
-        } else if constexpr (KM == 1) {
-            // sum_j e_j k_j mod q from two halves on two pipes: the quotient
-            // t = round(sum_j e_j (k_j / q)) on the FP64 pipe (each term's error
-            // < 2^-11, so t is within 1 of the nearest quotient) and the
-            // remainder sum_j e_j k_j - t q in wrapping 64-bit integers (exact:
-            // it lies in (-2q, 2q)); then one FP64 modmul by mulc
-            double T[G];
-            uint64_t S[G];
-#pragma unroll
-            for (int e = 0; e < G; e++) {
-                T[e] = 0.0;
-                S[e] = 0;
-            }
-            for (int j = 0; j < f.ks_beta; j++) {
-                const uint64_t *ej = (j == jt ? dsrc : esrc + j * f.ks_ext_dig) + TPS * g0;
-                const uint64_t *kj = ksrc + j * f.ks_key_j + TPS * g0;
-                uint64_t ev[G], kv[G];
-#pragma unroll
-                for (int e = 0; e < G; e++) {
-                    ev[e] = __ldg(ej + TPS * e);
-                    kv[e] = __ldg(kj + TPS * e);
-                }
-#pragma unroll
-                for (int e = 0; e < G; e++) {
-                    T[e] = fma(f64_of_u64(ev[e]), f64_of_u64(kv[e]) * fq.qinv, T[e]);
-                    S[e] += ev[e] * kv[e];
-                }
-            }
-            const double wf = f64_of_u64(f.mulc.w[limb]);
-            uint64_t av[G];
-#pragma unroll
-            for (int e = 0; e < G; e++) av[e] = has_add ? __ldg(asrc + TPS * (g0 + e)) : 0;
-            const double af = f.add_scaled ? f64_of_u64(f.addc.w[limb]) : 1.0;
-#pragma unroll
-            for (int e = 0; e < G; e++) {
-                const int c = u + TPS * (g0 + e);
-                const long long tq = __double_as_longlong(T[e] + SRK_F64_MAGIC) - 0x4338000000000000ll;
-                const long long rr = (long long)(S[e] - (uint64_t)tq * pc.q);  // (-2q, 2q)
-                const double d = f64_of_i64(rr) - __longlong_as_double((long long)sm[sidx(c)]);
-                double v = modmul_f64(d, wf, fq.q, fq.qinv);
-                double a = f64_of_u64(av[e]);
-                if (f.add_scaled) a = modmul_f64(a, af, fq.q, fq.qinv);
-                sm[sidx(c)] = canon_u64_of_f64(v + a, fq.q, fq.qinv);
             }
         } else {
             // integer limbs (q >= 2^41): 128-bit accumulation, one Barrett reduction
@@ -649,7 +586,7 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB
     constexpr int mode = KM == 1 ? 2 : 0;
     // the first loads need no prime constant: issue them before its (dependent) load
     uint64_t x[E];
-    constexpr bool RAW = SRK_EARLY_LOADS && !(FIRST && LD == LD_SPREAD);
+    constexpr bool RAW = !(FIRST && LD == LD_SPREAD);
     auto raw = [&](int c) -> uint64_t {
         if constexpr (FIRST && LD == LD_AUTO) return __ldg(lsrc + auto_index((uint32_t)gaddr(c), f.galois, log_n));
         else if constexpr (FIRST) return lsrc[gaddr(c)];
@@ -658,34 +595,12 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB
     if constexpr (RAW) {
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = raw((INV && COL) ? u * E + e : u + TPS * e);
-    } else if constexpr (INV && COL) {
-#pragma unroll
-        for (int e = 0; e < E; e++) x[e] = data[gaddr(u * E + e)];
     }
     const PrimeConst pc = tb.pc[pid];
     const uint64_t q = pc.q, two_q = pc.two_q;
     // prime-class split of mixed batches (uniform per CTA): the FP64 kernel never
     // touches a limb >= 2^41; the integer kernel skips FP64 limbs when filtered
     if ((KM == 1 || b.cls == 1) ? q >= SRK_F64_Q : (b.cls == 2 && q < SRK_F64_Q)) return;
-    if constexpr (ST == ST_KSC && SRK_KSC_PREFETCH) {
-        // the epilogue's digit / key / addend rows of this CTA (CB consecutive chunks,
-        // contiguous) are pulled into L2 while the butterflies run: one bulk prefetch
-        // per array, issued by one thread each
-        const int a = threadIdx.x, beta = f.ks_beta;
-        if (a <= 2 * beta) {
-            const long long base0 = (long long)t * n + (long long)blockIdx.x * CB * T;
-            const uint32_t bytes = (uint32_t)(CB * T * 8);
-            const uint64_t *p = nullptr;
-            if (a < beta) {
-                p = (a == pid / f.ks_alpha ? f.ks_d + bi * f.ks_d_ct : f.ks_ext + bi * f.ks_ext_ct + a * f.ks_ext_dig);
-            } else if (a < 2 * beta) {
-                p = f.ks_key + (a - beta) * f.ks_key_j + r * f.ks_key_r;
-            } else if (r == 0 ? f.has_add0 : f.has_add1) {
-                p = (r == 0 ? f.add0 : f.add1) + bi * f.add_ct;
-            }
-            if (p) prefetch_l2_bulk(p + base0, bytes);
-        }
-    }
     auto load = [&](int c) -> uint64_t {
         if constexpr (FIRST) return fused_load<LD>(f, tb.pc, bi, r, t, pc, gaddr(c), log_n, lsrc);
         else return data[gaddr(c)];
