@@ -117,6 +117,13 @@ int srk_rescale_batch(srk_ctx *ctx, const uint64_t *a, long long a_ct, uint64_t 
 int srk_mul_relin_batch(srk_ctx *ctx, const uint64_t *a, const uint64_t *b, long long ab_ct,
                         const uint64_t *rlk, uint64_t *out, long long out_ct, int batch, int level,
                         int rescale, void *ws, void *stream);
+/* the same over a table of operand pairs: a[i] x b[i] for i < batch (HOST arrays of
+ * DEVICE pointers to [2][level+1][N] ciphertexts; pairs may share operands -- the
+ * composite polynomials' (y y, u3 y, u7 y) -- so no batch is copied together first);
+ * out packed at ct stride out_ct.  HESimulator.mul on several pairs at once. */
+int srk_mul_relin_ptrs(srk_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, int batch,
+                       const uint64_t *rlk, uint64_t *out, long long out_ct, int level, int rescale,
+                       void *ws, void *stream);
 int srk_rotate_batch(srk_ctx *ctx, const uint64_t *a, long long a_ct, const uint64_t *gkey,
                      uint64_t *out, long long out_ct, int batch, int level, uint64_t galois,
                      void *ws, void *stream);

@@ -291,6 +291,9 @@ class OracleBackend:
         return self.o.mul_relin_rescale(np.ascontiguousarray(a), np.ascontiguousarray(b), self.relin_key(),
                                         level)
 
+    def mul_relin_rescale_pairs(self, pairs, level):
+        return np.stack([self.mul_relin_rescale(a, b, level) for a, b in pairs])
+
     @_batched
     def rotate(self, a, galois, level):
         return self.o.rotate_raw(a, self.galois_key(galois), galois, level)

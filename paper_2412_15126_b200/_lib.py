@@ -49,6 +49,8 @@ EXPORTS = {
                           c_void_p],
     "srk_mul_relin_batch": [c_void_p, _u64p, _u64p, c_longlong, _u64p, _u64p, c_longlong, c_int,
                             c_int, c_int, c_void_p, c_void_p],
+    "srk_mul_relin_ptrs": [c_void_p, c_void_p, c_void_p, c_int, _u64p, _u64p, c_longlong, c_int, c_int,
+                           c_void_p, c_void_p],
     "srk_addsub_batch": [c_void_p, _u64p, _u64p, _u64p, c_int, c_int, c_int, c_void_p],
     "srk_add_plain_batch": [c_void_p, _u64p, _u64p, c_longlong, POINTER(c_uint64), _u64p, c_int,
                             c_int, c_void_p],

@@ -252,6 +252,18 @@ class CudaBackend:
                    2 * level * self.n, batch or 1, level, 1, self.workspace(), self.stream())
         return out
 
+    def mul_relin_rescale_pairs(self, pairs, level: int) -> torch.Tensor:
+        """a_i x b_i for every (a_i, b_i) in ``pairs`` (each a [2][level+1][N] ciphertext,
+        operands may repeat), relinearised and rescaled, packed [len][2][level][N]:
+        one pointer table, no copy of the operands into a batch first."""
+        n = len(pairs)
+        out = self._out(level - 1, n)
+        ta = (ctypes.c_void_p * n)(*[_ptr(a) for a, _ in pairs])
+        tb = (ctypes.c_void_p * n)(*[_ptr(b) for _, b in pairs])
+        self._call("srk_mul_relin_ptrs", ta, tb, n, _ptr(self.relin_key()), _ptr(out), 2 * level * self.n,
+                   level, 1, self.workspace(), self.stream())
+        return out
+
     def rescale(self, a, level: int, batch=None) -> torch.Tensor:
         out = self._out(level - 1, batch)
         self._call("srk_rescale_batch", _ptr(a), 2 * (level + 1) * self.n, _ptr(out),

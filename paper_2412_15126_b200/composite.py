@@ -44,7 +44,14 @@ def _mul_plain_at(engine, x, c: float, level: int, site: str):
 
 
 def _three_products(engine, y, u3, u7, site):
-    """(y*y, u3*y, u7*y): one lock-step batch on engines that stack ciphertexts."""
+    """(y*y, u3*y, u7*y): one lock-step batch on engines that stack ciphertexts (the
+    pairs go to the kernels as a pointer table: y is not copied three times)."""
+    mul_pairs = getattr(engine, "mul_pairs", None)
+    if mul_pairs is not None:
+        prod = mul_pairs([(y, y), (u3, y), (u7, y)], site=f"{site}-quad")
+        if y.batch is None:
+            return tuple(engine.unstack(prod))
+        return tuple(engine.split(prod, 3))  # views: no copies
     concat = getattr(engine, "concat", None)
     if concat is None:
         return (engine.mul(y, y, site=f"{site}-quad"), engine.mul(u3, y, site=f"{site}-x3"),

@@ -1366,6 +1366,43 @@ extern "C" int srk_mul_relin_batch(srk_ctx *c, const uint64_t *a, const uint64_t
     return SRK_OK;
 }
 
+// pairs a[i] x b[i] (host table of device pointers), chunked like the batch form
+extern "C" int srk_mul_relin_ptrs(srk_ctx *c, const uint64_t *const *a, const uint64_t *const *b, int batch,
+                                  const uint64_t *rlk, uint64_t *out, long long out_ct, int level, int rescale,
+                                  void *ws, void *stream) {
+    TRY(check_level(c, level));
+    if (!a || !b || batch < 1) return fail(SRK_EINVAL, "need a non-empty pair table");
+    if (rescale && level < 1) return fail(SRK_EINVAL, "depth exhausted");
+    const long long n = c->n, nl = level + 1, ps = nl * n;
+    const int ws_b = std::min(c->ws_batch, SRK_PAIRS_MAX);
+    const int pieces = (batch + ws_b - 1) / ws_b;
+    const int per = (batch + pieces - 1) / pieces;
+    for (int b0 = 0; b0 < batch; b0 += per) {
+        const int nb = std::min(per, batch - b0);
+        uint64_t *d = (uint64_t *)ws;  // [nb][3][nl]
+        uint64_t *rest = d + (long long)nb * 5 * ps;
+        TensorPairs tp;
+        memset(&tp, 0, sizeof tp);
+        for (int i = 0; i < nb; i++) {
+            if (!a[b0 + i] || !b[b0 + i]) return fail(SRK_EINVAL, "null operand in the pair table");
+            tp.a[i] = a[b0 + i];
+            tp.b[i] = b[b0 + i];
+        }
+        k_tensor_pairs<<<grid_for((long long)nb * ps), 256, 0, S(stream)>>>(tp, d, 3 * ps, c->d_pc, c->log_n,
+                                                                          (int)nl, nb);
+        LAUNCHED();
+        uint64_t *o = out + (long long)b0 * out_ct;
+        if (rescale) {
+            KsOut ko = {o, out_ct, (long long)level * n, rlk, 1, d, d + ps, 3 * ps};
+            TRY(keyswitch_impl(c, d + 2 * ps, 3 * ps, &ko, 1, level, nb, rest, S(stream), true));
+        } else {
+            KsOut ko = {o, out_ct, ps, rlk, 1, d, d + ps, 3 * ps};
+            TRY(keyswitch_impl(c, d + 2 * ps, 3 * ps, &ko, 1, level, nb, rest, S(stream)));
+        }
+    }
+    return SRK_OK;
+}
+
 extern "C" int srk_automorph(srk_ctx *c, const uint64_t *a, uint64_t *out,
                              long long n_limbs_total, uint64_t galois, void *stream) {
     if (!(galois & 1)) return fail(SRK_EINVAL, "Galois element must be odd");

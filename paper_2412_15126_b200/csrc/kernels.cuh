@@ -143,6 +143,45 @@ __global__ void k_tensor(const uint64_t *__restrict__ a0p, const uint64_t *__res
     }
 }
 
+// the same over a pointer table: pair i = (a[i], b[i]) (poly stride nl N each),
+// d[i] at d + i d_ct -- operands shared between pairs are read where they lie
+#define SRK_PAIRS_MAX 32
+struct TensorPairs {
+    const uint64_t *a[SRK_PAIRS_MAX];
+    const uint64_t *b[SRK_PAIRS_MAX];
+};
+__global__ void k_tensor_pairs(const __grid_constant__ TensorPairs tp, uint64_t *__restrict__ d0p, long long d_ct,
+                               const PrimeConst *__restrict__ pc, int log_n, int nl, int batch) {
+    const long long n = 1ll << log_n;
+    const long long ps = (long long)nl * n;
+    const Div32 dv = mk_div32(nl);
+    for (long long xx = blockIdx.x * (long long)blockDim.x + threadIdx.x; xx < ps * batch;
+         xx += (long long)gridDim.x * blockDim.x) {
+        const uint32_t row = (uint32_t)(xx >> log_n);
+        const int bi = (int)div32(row, dv);
+        const long long x = xx - (long long)bi * ps;
+        const uint64_t *a = tp.a[bi], *b = tp.b[bi];
+        uint64_t *d = d0p + bi * d_ct;
+        const PrimeConst P = pc[x >> log_n];
+        uint64_t a0 = __ldg(a + x), a1 = __ldg(a + ps + x), b0 = __ldg(b + x), b1 = __ldg(b + ps + x);
+        if (P.q < SRK_F64_Q) {
+            const double q = __longlong_as_double((long long)P.qd_bits);
+            const double qi = __longlong_as_double((long long)P.qinv_bits);
+            const double fa0 = f64_of_u64(a0), fa1 = f64_of_u64(a1);
+            const double fb0 = f64_of_u64(b0), fb1 = f64_of_u64(b1);
+            d[x] = canon_u64_of_small_f64(modmul_f64(fa0, fb0, q, qi), P.q);
+            d[ps + x] = canon_u64_of_f64(modmul_f64(fa0, fb1, q, qi) + modmul_f64(fa1, fb0, q, qi), q, qi);
+            d[2 * ps + x] = canon_u64_of_small_f64(modmul_f64(fa1, fb1, q, qi), P.q);
+            continue;
+        }
+        d[x] = mul_mod(a0, b0, P);
+        U128 m = mul_wide(a0, b1);
+        mac(m, a1, b0);
+        d[ps + x] = reduce_u128(m, P);
+        d[2 * ps + x] = mul_mod(a1, b1, P);
+    }
+}
+
 // ---------------------------------------------------------------------
 // rescale helpers
 // ---------------------------------------------------------------------

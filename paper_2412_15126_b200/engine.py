@@ -428,6 +428,43 @@ class CKKSEngineCore:
             self._ctct += nb or 1
         return self._emit(data, level - 1, max(x.rot_chain, y.rot_chain), nb)
 
+    def mul_pairs(self, pairs, site: str = "mul") -> Ciphertext:
+        """[x_i * y_i for (x_i, y_i) in pairs] as ONE batched ciphertext (batched operands
+        expand to their members; a single operand broadcasts over a batched partner).
+        Counted as one ct x ct multiplication per member; the operands are handed to
+        the kernels through a pointer table (no batch assembled by copying)."""
+        if not hasattr(self.backend, "mul_relin_rescale_pairs"):
+            prods = [self.mul(x, y, site=site) for x, y in pairs]
+            return self.concat(prods)
+        singles = []
+        for x, y in pairs:
+            self._check(x, y)
+            xs, ys = self.unstack(x), self.unstack(y)
+            if len(xs) != len(ys):
+                if len(xs) == 1:
+                    xs = xs * len(ys)
+                elif len(ys) == 1:
+                    ys = ys * len(xs)
+                else:
+                    raise ValueError("batched operands of different sizes")
+            singles.extend(zip(xs, ys))
+        level = min(min(x.level, y.level) for x, y in singles)
+        if level < 1:
+            raise DepthBudgetError(site, level)
+        aligned = {}
+
+        def al(ct):
+            key = id(ct)
+            if key not in aligned:
+                aligned[key] = (ct, self._align(ct, level))
+            return aligned[key][1]
+
+        data = self.backend.mul_relin_rescale_pairs([(al(x), al(y)) for x, y in singles], level)
+        with self._lock:
+            self._ctct += len(singles)
+        chain = max(max(x.rot_chain, y.rot_chain) for x, y in singles)
+        return self._emit(data, level - 1, chain, len(singles))
+
     supports_mul_plain_level = True
 
     def mul_plain(self, x: Ciphertext, p, site: str = "mul_plain", level: int | None = None) -> Ciphertext:
