@@ -370,3 +370,31 @@ def test_kernel_switches_ring16(env, require_cuda, monkeypatch):
          gb.stream())
     got = host(gb, out).reshape(B, 2, lvl, n)
     assert np.array_equal(got[0], orc.rescale(a[0], lvl)), "rescale"
+
+
+@pytest.mark.parametrize("name", ["toy", "cfg1"])
+def test_mul_relin_pointer_table(name, require_cuda):
+    """srk_mul_relin_ptrs: pairs sharing operands (the composite polynomials'
+    (y y, u y, v y)), more pairs than one internal chunk, rescaled -- each output
+    equals the oracle's relinearised, rescaled product of its own pair."""
+    import ctypes
+
+    from oracle.oracle import OracleCKKS
+    from paper_2412_15126_b200.backend_cuda import CudaBackend
+
+    p = preset(name)
+    gb, orc = CudaBackend(p), OracleCKKS(p)
+    lvl, n = p.max_level, p.ring_degree
+    cts = rand_limbs(p, (5, 2), lvl, 80)
+    key = _key(p, 81)
+    tc, tk = [dev(gb, c) for c in cts], dev(gb, key)
+    pairs = [(i % 5, (3 * i + 1) % 5) for i in range(37)]  # 37 > 32: two chunks
+    ta = (ctypes.c_void_p * 37)(*[ptr(tc[i]) for i, _ in pairs])
+    tb = (ctypes.c_void_p * 37)(*[ptr(tc[j]) for _, j in pairs])
+    out = gb.empty_ct(lvl - 1, polys=2 * 37)
+    call(gb, "srk_mul_relin_ptrs", ta, tb, 37, ptr(tk), ptr(out), 2 * lvl * n, lvl, 1, gb.workspace(),
+         gb.stream())
+    got = host(gb, out).reshape(37, 2, lvl, n)
+    for k in (0, 1, 31, 32, 36):
+        i, j = pairs[k]
+        assert np.array_equal(got[k], orc.rescale(orc.mul_relin(cts[i], cts[j], key, lvl), lvl)), k
