@@ -3,8 +3,12 @@
 Restates reference ``multi_rank_pipeline`` / ``multi_sort``
 (``pkg/src/slotrank/ranking.py:307-392``, ``sorting.py:106-142``) with the
 independent units spread over ranks, in five phases,
-each ONE level exchange (a tiny int64 all-reduce, the phase's only host sync)
-plus ONE collective on the stacked ciphertexts of the phase:
+each ONE collective on the stacked ciphertexts of the phase.  The level every
+exchanged ciphertext will have is known in advance on every rank: the first
+call of a configuration traces the single-GPU circuit on the level tracer
+(``levels.py``: the engine's own level rules over data-free tokens) and caches
+the level vectors, so no level is ever exchanged and nothing synchronises the
+host (the pipeline can be captured as one CUDA graph with its collectives):
 
 0. ReplR(block) and ReplC(TransR(block)) for blocks i with i % world == rank,
    batched; all-gather of the stacked results (every rank needs every block);
@@ -80,7 +84,9 @@ class Comm:
         if self.world > MAX_WORLD:
             raise ValueError(f"shard.py sums int64 limbs (< 2^60) over ranks: world <= {MAX_WORLD}")
         self.collectives = 0  # data collectives issued (tests assert O(1) per phase)
-        self.level_syncs = 0  # host syncs (one small level exchange per phase)
+        self.level_syncs = 0  # host syncs (level exchanges: 0 once a level plan is cached)
+        self.planned = None   # level vectors of the coming exchanges, in order (levels.py trace)
+        self.recorder = None  # list collecting each exchange's level vector (tracing)
 
     def owner(self, unit_index: int) -> int:
         return unit_index % self.world
@@ -92,9 +98,19 @@ class Comm:
             return torch.device("cuda", torch.cuda.current_device())
         return "cpu"
 
+    def exchange_levels(self, levels: list[int]) -> list[int]:
+        """The levels the items of this exchange will have on every rank: the next
+        planned vector (no communication), else one MIN all-reduce (a host sync)."""
+        if self.recorder is not None:
+            self.recorder.append(list(levels))
+        if self.world == 1:
+            return list(levels)
+        if self.planned:
+            return self.planned.pop(0)
+        return self.min_levels(levels)
+
     def min_levels(self, levels: list[int]) -> list[int]:
-        """Element-wise MIN over ranks of a level vector (_NO_LEVEL = absent): the
-        phase's single host sync."""
+        """Element-wise MIN over ranks of a level vector (_NO_LEVEL = absent)."""
         import torch
 
         t = torch.tensor(levels, dtype=torch.int64, device=self.device())
@@ -114,6 +130,47 @@ class Comm:
         self.dist.all_gather(parts, t.contiguous(), group=self.group)
         self.collectives += 1
         return torch.cat(parts)
+
+
+class _TraceComm:
+    """world-1 stand-in for ``Comm`` that records every exchange's level vector."""
+
+    rank, world = 0, 1
+
+    def __init__(self):
+        self.recorder, self.planned = [], None
+        self.collectives = self.level_syncs = 0
+
+    def owner(self, unit_index: int) -> int:
+        return 0
+
+    def exchange_levels(self, levels):
+        self.recorder.append(list(levels))
+        return list(levels)
+
+
+def _with_plan(engine, comm, key, bv: BlockVector, run):
+    """Run ``run(eng, bv, comm)`` with the level vector of every exchange known in
+    advance: the first call traces the single-GPU circuit on the level tracer
+    (levels.py, no data, no communication) and caches the vectors on the engine."""
+    if comm.world == 1:
+        return run(engine, bv, comm)
+    from .levels import level_tracer
+
+    plans = engine.__dict__.setdefault("_shard_level_plans", {})
+    full = key + (bv.block_size, bv.total_len, tuple(b.level for b in bv.blocks))
+    if full not in plans:
+        tr = level_tracer(engine)
+        tbv = BlockVector(blocks=tuple(tr.token(b.level) for b in bv.blocks), block_size=bv.block_size,
+                          total_len=bv.total_len)
+        tc = _TraceComm()
+        run(tr, tbv, tc)
+        plans[full] = tc.recorder
+    comm.planned = [list(v) for v in plans[full]]
+    try:
+        return run(engine, bv, comm)
+    finally:
+        comm.planned = None
 
 
 def _lv(ct) -> int:
@@ -160,9 +217,9 @@ def _unstacked(engine, t, levels, reduce_mod: bool):
 def _sum_all(engine, cts, comm: Comm):
     """Modular sums over ranks of a list of ciphertexts (one all-reduce): each
     rank's item is brought to the minimum level over ranks first."""
+    levels = comm.exchange_levels([_lv(c) for c in cts])
     if comm.world == 1:
         return list(cts)
-    levels = comm.min_levels([_lv(c) for c in cts])
     if all(lv == _NO_LEVEL for lv in levels):
         return [None] * len(cts)
     t = _stacked(engine, cts, levels)
@@ -173,9 +230,9 @@ def _sum_all(engine, cts, comm: Comm):
 def _gather_owned(engine, owned: dict, count: int, comm: Comm):
     """Every rank ends with all ``count`` items; item i is computed by rank
     comm.owner(i) (``owned`` maps its indices to ciphertexts): one all-gather."""
+    levels = comm.exchange_levels([_lv(owned.get(i)) for i in range(count)])
     if comm.world == 1:
         return [owned[i] for i in range(count)]
-    levels = comm.min_levels([_lv(owned.get(i)) for i in range(count)])
     per = -(-count // comm.world)
     # slot s of rank r holds item r + s * world
     local = [owned.get(comm.rank + s * comm.world) for s in range(per)]
@@ -197,7 +254,9 @@ def _replicated_sharded(engine, bv: BlockVector, layout: MatrixLayout, comm: Com
     """Phase 0: (rows, cols) of every block, each computed once over the world."""
     count = len(bv.blocks)
     if comm.world == 1:
-        return replicated_blocks(engine, bv, layout)
+        rows, cols = replicated_blocks(engine, bv, layout)
+        comm.exchange_levels([c.level for pair in zip(rows, cols) for c in pair])
+        return rows, cols
     mine = [i for i in range(count) if comm.owner(i) == comm.rank]
     owned = {}
     if mine:
@@ -215,9 +274,9 @@ def _gather_pairs(engine, owned2: dict, count: int, comm: Comm):
     comm.owner(i), stacked along a second axis -- in one collective."""
     import torch
 
+    lv = comm.exchange_levels([_lv(owned2.get(k)) for k in range(2 * count)])
     if comm.world == 1:
         return [owned2[k] for k in range(2 * count)]
-    lv = comm.min_levels([_lv(owned2.get(k)) for k in range(2 * count)])
     per = -(-count // comm.world)
     top = max(x for x in lv if x != _NO_LEVEL)
     rows = []
@@ -241,7 +300,15 @@ def _gather_pairs(engine, owned2: dict, count: int, comm: Comm):
 def multi_rank_sharded(engine, bv: BlockVector, cfg: KernelConfig, comm: Comm, *,
                        tie_correction: bool = False, packed: bool = False) -> MultiRankPipeline:
     """``multi_rank_pipeline`` with blocks, block pairs and block finishes dealt over
-    ``comm``'s ranks (phases 0-2 of the module docstring)."""
+    ``comm``'s ranks (phases 0-2 of the module docstring); every exchange's levels
+    come from a cached trace of the circuit (no host synchronisation)."""
+    return _with_plan(engine, comm, ("rank", cfg, tie_correction, packed), bv,
+                      lambda e, v, c: _multi_rank_sharded(e, v, cfg, c, tie_correction=tie_correction,
+                                                          packed=packed))
+
+
+def _multi_rank_sharded(engine, bv: BlockVector, cfg: KernelConfig, comm: Comm, *,
+                        tie_correction: bool = False, packed: bool = False) -> MultiRankPipeline:
     if packed:
         if tie_correction:
             raise ValueError("the packed layout has no tie correction")
@@ -323,12 +390,17 @@ def _finish_tie(engine, parts, i, valid_i, layout):
 
 def multi_sort_sharded(engine, bv: BlockVector, cfg: SortConfig, comm: Comm) -> BlockVector:
     """``multi_sort`` with the ranking sharded as above and the L^2 placements dealt
-    over ranks (phases 3-4 of the module docstring)."""
+    over ranks (phases 3-4 of the module docstring); no host synchronisation once
+    the level plan of this configuration is cached."""
+    return _with_plan(engine, comm, ("sort", cfg), bv, lambda e, v, c: _multi_sort_sharded(e, v, cfg, c))
+
+
+def _multi_sort_sharded(engine, bv: BlockVector, cfg: SortConfig, comm: Comm) -> BlockVector:
     if getattr(cfg, "packed", False):
         if cfg.tie_correction:
             raise ValueError("the packed layout has no tie correction")
         return _multi_sort_sharded_packed(engine, bv, cfg.kernel, comm)
-    ranking = multi_rank_sharded(engine, bv, cfg.kernel, comm, tie_correction=cfg.tie_correction)
+    ranking = _multi_rank_sharded(engine, bv, cfg.kernel, comm, tie_correction=cfg.tie_correction)
     layout = ranking.layout
     b, count = bv.block_size, len(bv.blocks)
     window = with_input_range(cfg.kernel, -float(b * count), float(b * count))

@@ -86,8 +86,9 @@ TIES = np.repeat(np.random.default_rng(9).choice(64, 48, replace=False) / 64, 2)
 @pytest.mark.slow
 def test_three_rank_tie_corrected_sort_bit_identical_and_o1_collectives(tmp_path):
     """3 ranks, 3 unpadded blocks, tie correction (block tie offsets,
-    reference ranking.py:395-423): bit-identical blocks, and exactly one data
-    collective + one level exchange per phase (5 phases)."""
+    reference ranking.py:395-423): bit-identical blocks, exactly one data
+    collective per phase (5 phases) and no level exchange: every exchange's
+    levels come from the cached level-tracer plan (levels.py)."""
     mp.spawn(_worker, args=(3, _port(), "sort", str(tmp_path), TIES, True), nprocs=3, join=True)
     from oracle.oracle import oracle_engine
 
@@ -95,7 +96,7 @@ def test_three_rank_tie_corrected_sort_bit_identical_and_o1_collectives(tmp_path
     res = M.multi_sort(eng, M.block_split(eng, TIES), M.SortConfig(kernel=KCFG, tie_correction=True))
     for r in range(3):
         got = np.load(tmp_path / f"sort_{r}.npz")
-        assert list(got["counts"]) == [5, 5]
+        assert list(got["counts"]) == [5, 0]  # 5 collectives, no level exchange (levels.py plan)
         for i, blk in enumerate(res.blocks):
             assert np.array_equal(got[f"arr_{i}"], blk.data), (r, i)
     assert np.abs(M.block_merge(eng, res) - np.sort(TIES)).max() < 5e-2
@@ -118,7 +119,7 @@ def test_three_rank_packed_sort_bit_identical(tmp_path):
                        M.SortConfig(kernel=KCFG, tie_correction=False, packed=True))
     for r in range(3):
         got = np.load(tmp_path / f"sort_{r}.npz")
-        assert list(got["counts"]) == [5, 5]
+        assert list(got["counts"]) == [5, 0]  # 5 collectives, no level exchange (levels.py plan)
         for i, blk in enumerate(res.blocks):
             assert np.array_equal(got[f"arr_{i}"], blk.data), (r, i)
     assert np.abs(M.block_merge(eng, res) - np.sort(PACKVALS)).max() < 5e-3
