@@ -648,6 +648,7 @@ void orc_keygen(const orc_ctx *c, const uint64_t *s_ntt, const uint64_t *sfrom_n
 void orc_encrypt(const orc_ctx *c, const uint64_t *m_ntt, const uint64_t *s_ntt, const int64_t *e,
                  uint64_t seed, uint64_t seq, uint64_t *out, int level) {
     const int n = c->n, nl = level + 1;
+    if (nl < 1) return;
     int *ids = (int *)malloc(sizeof(int) * nl);
     for (int i = 0; i < nl; i++) ids[i] = i;
     uint64_t *c1 = out + (size_t)nl * n;
