@@ -69,6 +69,7 @@ class CudaBackend:
         self._keys: dict[int, torch.Tensor] = {}
         self._capture_keepalive: list = []  # pinned sources of copies captured in CUDA graphs
         self._key_lock = threading.Lock()
+        self._call_lock = threading.RLock()
         self.launches = 0
         self._sk_ntt = None
 
@@ -119,8 +120,13 @@ class CudaBackend:
         return self._h2d(np.ascontiguousarray(arr).view(np.int64))
 
     def _call(self, name: str, *args):
-        self.launches += 1
-        _lib.check(getattr(self.lib, name)(self.ctx, *args))
+        # one C-ABI call enqueues a whole op (several kernels, the context's side
+        # streams and events); ctypes releases the GIL, so concurrent host threads
+        # (ops on distinct inputs may run concurrently, reference SPEC.md:121) are
+        # serialised here -- each op's launch sequence stays contiguous
+        with self._call_lock:
+            self.launches += 1
+            _lib.check(getattr(self.lib, name)(self.ctx, *args))
 
     # ------------------------------------------------------------------
     # keys

@@ -201,3 +201,29 @@ def test_ragged_inputs_and_capacity(require_cuda, eng_long):
     assert out.shape == (200,)
     assert np.array_equal(np.argsort(out), np.arange(200))
     assert np.abs(out - np.sort(w)).max() < 1e-3
+
+
+def test_concurrent_ops_from_host_threads(eng12):
+    """Ops on distinct inputs from 8 host threads (reference SPEC.md:121; the
+    reference's thread-pool multi_rank, ranking.py:345-347): every result equals
+    the single-threaded one limb for limb and the counters add up exactly."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
+    xs = [eng12.encrypt(np.linspace(-1, 1, 64) * (i + 1) / 9) for i in range(8)]
+
+    def work(i):
+        x = xs[i]
+        return eng12.mul(eng12.rotate(x, i + 1), eng12.add(x, x))
+
+    seq = [work(i).data.clone() for i in range(8)]
+    torch.cuda.synchronize()
+    eng12.cost_reset()
+    with ThreadPoolExecutor(8) as pool:
+        par = list(pool.map(work, range(8)))
+    torch.cuda.synchronize()
+    for a, b in zip(seq, par):
+        assert torch.equal(a, b.data)
+    rep = eng12.cost_snapshot()
+    assert rep.rotations == 8 and rep.ctct_mults == 8 and rep.additions == 8
