@@ -439,6 +439,20 @@ def run_pipelines(torch, quick=False):
         "cost": cost, "params": "cfg3", "kernel": "chebyshev d=1024 (reference)"}
     del eng
     torch.cuda.empty_cache()
+    # the same rank at Delta = 2^47 (cfg3_hp: the reference's 1e-6 slot tolerance, DESIGN "Parity")
+    eng = B200Engine(preset("cfg3_hp"))
+    ct = eng.encrypt(v128)
+    rank(eng, ct, 128, cfg)
+    cost, _ = _census(eng, lambda: rank(eng, ct, 128, cfg))
+    dt, res = _timed(torch, lambda: read_row(eng, rank(eng, ct, 128, cfg).ranks, 128), reps=3)
+    out["rank_n128_hp_s"] = {"latency_s": dt,
+                             "graph_replay_s": _graph_latency(eng, lambda c: rank(eng, c, 128, cfg).ranks, ct),
+                             "exact_ranks": bool(np.array_equal(np.rint(res), fractional_ranks(v128))),
+                             "max_rank_err": float(np.abs(res - fractional_ranks(v128)).max()),
+                             "cost": cost, "params": "cfg3_hp (Delta 2^47, 10 special primes)",
+                             "kernel": "composite g3^4 o f3^2"}
+    del eng
+    torch.cuda.empty_cache()
     if quick:
         return out
 
