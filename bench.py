@@ -291,6 +291,32 @@ def pipe_roofline():
             "kernels": d["kernels"]}
 
 
+def fp64_roofline(torch, lib, p, ntt_ms, ntt_bytes, hbm_peak):
+    """The forward NTT against the FP64 pipe (its binding unit: DESIGN.md, kernels).
+    Peak = FP64 FMA issue rate measured here with srk_fp64_probe (148 x 8 CTAs of
+    8 independent FMA chains per thread); work = the FP64 instructions the passes
+    issue per transform: 8 per butterfly (6 for the exact FMA-split product, 2 for
+    x +- t) and 5 per coefficient for the u64 <-> f64 edges, limbs under primes
+    < 2^41 only (the 60-bit limb 0 runs on the integer pipe)."""
+    n = p.ring_degree
+    log_n = n.bit_length() - 1
+    f64_limbs = sum(1 for q in p.q_primes if q < (1 << 41))
+    instr = N_CT * 2 * f64_limbs * (log_n * (n // 2) * 8 + n * 5)
+    ctas, iters = 148 * 8, 20000
+    sink = torch.zeros(8, dtype=torch.float64, device="cuda")
+    run = lambda: lib.srk_fp64_probe(ctas, iters, sink.data_ptr(), torch.cuda.current_stream().cuda_stream)  # noqa: E731
+    run()
+    probe_ms = min(time_region(torch, run, 3) for _ in range(3))
+    peak = ctas * 256 * 8 * iters / (probe_ms * 1e-3)
+    roof_ms = instr / peak * 1e3
+    return {"bound": "fp64 pipe", "kernel": "forward NTT (ntt_pass_kernel x2 per chunk)",
+            "fp64_instructions": instr, "peak_fp64_instr_per_s": round(peak, -9),
+            "peak_source": "srk_fp64_probe timed here (independent FMA chains, CUDA events)",
+            "achieved_fp64_instr_per_s": round(instr / (ntt_ms * 1e-3), -9),
+            "frac": round(roof_ms / ntt_ms, 4), "ms_at_fp64_roof": round(roof_ms, 4),
+            "hbm_frac_at_fp64_roof": round(ntt_bytes / (roof_ms * 1e-3) / GB / hbm_peak, 4)}
+
+
 def time_region(torch, fn, reps, barrier=None):
     """CUDA-event time of ``reps`` calls of fn (ms per call), synchronized both sides."""
     torch.cuda.synchronize()
@@ -657,6 +683,9 @@ def gpu_arm(args):
     ntt_ms = time_region(torch, lambda: step.ntt(step.x, False), 5)
     intt_ms = time_region(torch, lambda: step.ntt(step.x, True), 5)
     ks_ms = time_region(torch, step.relin_batch, 3)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    fp64_roof = fp64_roofline(torch, step.lib, p, ntt_ms, parts["ntt_fwd"], float(peaks.get("hbm_gbs", 6650.0)))
 
     # e2e: host pinned inputs -> device, step, results -> host (chunk-pipelined)
     e2e_step = PipelinedE2E(torch, step, chunks=int(os.environ.get("SRK_E2E_CHUNKS", "6")))
@@ -685,8 +714,6 @@ def gpu_arm(args):
                 pipelines.update(sharded)
 
     if rank_id == 0:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
         peak = float(peaks.get("hbm_gbs", 6650.0))
         ntt_gbs = parts["ntt_fwd"] / (ntt_ms * 1e-3) / GB
         ks_gbs = ks_bytes / (ks_ms * 1e-3) / GB
@@ -714,8 +741,10 @@ def gpu_arm(args):
                          "frac": round(ntt_gbs / peak, 4), "traffic": ntt_tr,
                          "traffic_source": ntt_src,
                          "algorithmic_bytes": parts["ntt_fwd"], "ms": round(ntt_ms, 4),
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+                         "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured copy)" if "gpu_name" in peaks
+                                         else "B200_PROFILING.md fallback (no MEASURED_PEAKS.json)")},
             "kernel_roofline": kernel_roofline(),
+            "roofline_fp64": fp64_roof,
             "roofline_pipes": pipe_roofline(),
             "roofline_keyswitch": {"bound": "hbm", "unit_of_work": "64 x HMult+relinearise (no rescale)", "achieved": round(ks_gbs, 1), "peak": peak,
                                    "unit": "GB/s", "frac": round(ks_gbs / peak, 4),

@@ -53,6 +53,11 @@ int srk_version(void);
 /* kernels launched by this library so far in this process (bench evidence) */
 unsigned long long srk_kernel_launches(void);
 
+/* measurement aid (bench.py's FP64 roof): launches one kernel of `ctas` CTAs x 256
+ * threads in which every thread issues iters x 8 independent FP64 FMAs and nothing
+ * else; the caller times it with events on `stream`.  sink: >= 1 device word. */
+int srk_fp64_probe(int ctas, int iters, double *sink, void *stream);
+
 /* context: primes[0..n_q) = Q chain, primes[n_q..n_q+n_p) = special primes;
  * roots[i] = primitive 2N-th root of unity mod primes[i] */
 int srk_ctx_create(int device, int log_n, const uint64_t *primes, const uint64_t *roots, int n_q,

@@ -24,6 +24,7 @@ EXPORTS = {
     "srk_last_error": [],
     "srk_version": [],
     "srk_kernel_launches": [],
+    "srk_fp64_probe": [c_int, c_int, c_void_p, c_void_p],
     "srk_ctx_create": [c_int, c_int, POINTER(c_uint64), POINTER(c_uint64), c_int, c_int, c_int,
                        POINTER(c_void_p)],
     "srk_ctx_destroy": [c_void_p],

@@ -12,6 +12,7 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/slotrank_b200.h"
@@ -69,6 +70,29 @@ extern "C" const char *srk_last_error(void) { return g_err.c_str(); }
 extern "C" int srk_version(void) { return 1; }
 // number of kernels this library has launched in this process
 extern "C" unsigned long long srk_kernel_launches(void) { return g_launches.load(); }
+
+// FP64 pipe probe: 8 independent FMA chains per thread (the NTT passes' binding pipe;
+// bench.py divides the transforms' FP64 instruction count by this rate)
+__global__ void __launch_bounds__(256) k_fp64_probe(int iters, double *sink) {
+    double a[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) a[i] = 1.0 + threadIdx.x * 1e-9 + i;
+    const double m = 1.0000000001, c = 1e-12;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) a[i] = fma(a[i], m, c);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s += a[i];
+    if (s == 12345.678) sink[0] = s;  // never true: keeps the chains alive
+}
+extern "C" int srk_fp64_probe(int ctas, int iters, double *sink, void *stream) {
+    if (ctas < 1 || iters < 1 || !sink) return fail(SRK_EINVAL, "bad FP64 probe arguments");
+    k_fp64_probe<<<ctas, 256, 0, (cudaStream_t)stream>>>(iters, sink);
+    LAUNCHED();
+    return SRK_OK;
+}
 
 // ---------------------------------------------------------------------
 // host modular helpers
@@ -140,6 +164,7 @@ struct srk_ctx {
     int ws_batch = SRK_WS_BATCH;  // ciphertexts per internal chunk (SRK_WS_BATCH env: smaller workspace)
     int ntt_cta_threads = 128;  // threads per NTT pass CTA (128: 8 CTAs/SM, cheaper barriers)
     unsigned conv_cpt = 4;  // coefficients per thread of the conversions (amortises their staging)
+    bool pdl = true;  // programmatic dependent launch of the kernel chains (SRK_PDL=0: plain launches)
     cudaStream_t nside[2] = {nullptr, nullptr};
     cudaEvent_t ev_nfork[2] = {nullptr, nullptr}, ev_njoin[2] = {nullptr, nullptr};
 };
@@ -271,6 +296,7 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     // key-switch workspace batch (several ranks sharing one GPU need a smaller one)
     if (const char *e = getenv("SRK_NTT_CHUNK")) c->ntt_chunk = std::max(1, atoi(e));
     if (const char *e = getenv("SRK_WS_BATCH")) c->ws_batch = std::max(1, atoi(e));
+    if (const char *e = getenv("SRK_PDL")) c->pdl = atoi(e) != 0;
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -499,9 +525,30 @@ static FuseArgs no_fuse() {
     return f;
 }
 
+// Launch with (pdl) or without the programmatic-stream-serialisation attribute: a
+// kernel that calls pdl_wait() before its first dependent access may be scheduled
+// while the previous kernel of the stream drains (its launch latency and prologue
+// overlap that tail).  Only kernels containing pdl_wait() may be launched with pdl.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             bool pdl, Args &&...args) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <int LOG_T, bool INV, bool COL, int IO, int KM, int LOGN>
 static void launch_kernel_n(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
-                            const NttTables &tb, int log_n, const FuseArgs &ff) {
+                            const NttTables &tb, int log_n, const FuseArgs &ff, bool pdl) {
     // the attribute is per device: one bit per device ordinal
     static std::atomic<unsigned long long> attr_done{0};
     int dev = 0;
@@ -512,19 +559,20 @@ static void launch_kernel_n(dim3 grid, int threads, size_t smem, cudaStream_t s,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         attr_done.fetch_or(bit, std::memory_order_relaxed);
     }
-    ntt_pass_kernel<LOG_T, INV, COL, IO, KM, LOGN><<<grid, threads, smem, s>>>(bb, tb, log_n, ff);
+    launch_ex(ntt_pass_kernel<LOG_T, INV, COL, IO, KM, LOGN>, grid, dim3(threads), smem, s, pdl, bb, tb, log_n,
+              ff);
 }
 // ring 2^16 (every BASELINE config past config 1): compile-time shape
 template <int LOG_T, bool INV, bool COL, int IO, int KM>
 static void launch_kernel(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
-                          const NttTables &tb, int log_n, const FuseArgs &ff) {
+                          const NttTables &tb, int log_n, const FuseArgs &ff, bool pdl) {
     if constexpr (LOG_T == 8) {
         if (log_n == 16) {
-            launch_kernel_n<LOG_T, INV, COL, IO, KM, 16>(grid, threads, smem, s, bb, tb, log_n, ff);
+            launch_kernel_n<LOG_T, INV, COL, IO, KM, 16>(grid, threads, smem, s, bb, tb, log_n, ff, pdl);
             return;
         }
     }
-    launch_kernel_n<LOG_T, INV, COL, IO, KM, 0>(grid, threads, smem, s, bb, tb, log_n, ff);
+    launch_kernel_n<LOG_T, INV, COL, IO, KM, 0>(grid, threads, smem, s, bb, tb, log_n, ff, pdl);
 }
 
 template <int LOG_T, bool INV, bool COL, int IO>
@@ -573,9 +621,9 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
     // rescale's FP64 spread needs the dropped prime < 2^41 too (IO 2 on either pass:
     // LD_SPREAD first, ST_RESCALE last)
     if (f64 && (IO != 2 || f.top_q < SRK_F64_Q))
-        launch_kernel<LOG_T, INV, COL, IO, 1>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
+        launch_kernel<LOG_T, INV, COL, IO, 1>(grid, threads, smem, s, bb, tables(c), c->log_n, ff, c->pdl);
     else
-        launch_kernel<LOG_T, INV, COL, IO, 2>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
+        launch_kernel<LOG_T, INV, COL, IO, 2>(grid, threads, smem, s, bb, tables(c), c->log_n, ff, c->pdl);
     LAUNCHED();
     return SRK_OK;
 }
@@ -983,6 +1031,35 @@ static inline dim3 conv_grid(const srk_ctx *c, dim3 g) {
     return dim3(std::max(1u, g.x / cpt), g.y, g.z);
 }
 
+// source-tile buffers of a conversion launch: two (the next tile streams in while
+// this one is converted) when a CTA walks several tiles and two CTAs of that size
+// still fit an SM, else one
+static inline int bconv_nbuf(const srk_ctx *c, int n_src, bool multi_tile) {
+    (void)c;
+    return multi_tile && bconv_smem_bytes(n_src, 2) <= 100 * 1024 ? 2 : 1;
+}
+// opt in to > 48 KiB of dynamic shared memory (once per kernel and device)
+template <typename K>
+static int bconv_attr(K kern, size_t smem) {
+    if (smem <= 32 * 1024) return SRK_OK;  // static tables (< 8 KiB) + this stay under the 48 KiB default
+    static std::mutex mu;
+    static std::vector<std::pair<const void *, unsigned long long>> done;  // kernel -> device bits
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &e : done)
+        if (e.first == (const void *)kern) {
+            if (e.second & bit) return SRK_OK;
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            e.second |= bit;
+            return SRK_OK;
+        }
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    done.emplace_back((const void *)kern, bit);
+    return SRK_OK;
+}
+
 // ModDown base conversion P (or P u {q_l}) -> q_0..q_{nout-1} with exact rounding,
 // coefficient domain, into conv [B][2][nout] (ct stride cv_ct, poly stride cv_ps):
 //   conv[t] = sum_k z_k m_kt - v [prod src]_{q_t},  v = round(sum_k z_k / p_k)
@@ -991,22 +1068,20 @@ static int moddown_conv(srk_ctx *c, const BconvPlan &pl, const uint64_t *z, long
                         int nout, cudaStream_t s) {
     const long long n = c->n;
     const int ns = pl.n_src;
-    dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + SRK_CONV_TG - 1) / SRK_CONV_TG);
+    if (ns > SRK_BCONV_MAXSRC) return fail(SRK_EINVAL, "ModDown with more than 17 source primes");
+    dim3 grid((unsigned)((n + SRK_BCONV_TILE - 1) / SRK_BCONV_TILE), 2 * B, (nout + SRK_BCONV_TG - 1) / SRK_BCONV_TG);
     const dim3 g2 = conv_grid(c, grid);
-#define SRK_CONV_LAUNCH(MK)                                                                               \
-    k_moddown_conv_f64<MK, true><<<g2, 256, 0, s>>>(z, z_ct, z_ps, ns, vround, pl.mhl, pl.fhl, pl.n_dst,  \
-                                                    pl.dst_corr, conv, cv_ct, cv_ps, c->d_pc, c->log_n)
-    switch (ns) {
-        case 1: SRK_CONV_LAUNCH(1); break;
-        case 2: SRK_CONV_LAUNCH(2); break;
-        case 3: SRK_CONV_LAUNCH(3); break;
-        case 4: SRK_CONV_LAUNCH(4); break;
-        default:
-            if (ns > 17) return fail(SRK_EINVAL, "ModDown with more than 17 source primes");
-            k_moddown_conv_f64_wide<<<g2, 256, 0, s>>>(z, z_ct, z_ps, ns, vround, pl.mhl, pl.fhl, pl.n_dst,
-                                                       pl.dst_corr, conv, cv_ct, cv_ps, c->d_pc, c->log_n);
+    const int nbuf = bconv_nbuf(c, ns, g2.x < grid.x);
+    const size_t smem = bconv_smem_bytes(ns, nbuf);
+    if (nbuf == 2) {
+        TRY(bconv_attr(k_moddown_conv<2>, smem));
+        launch_ex(k_moddown_conv<2>, g2, dim3(256), smem, s, c->pdl, z, z_ct, z_ps, ns, vround, pl.mhl, pl.fhl,
+                  pl.n_dst, pl.dst_corr, conv, cv_ct, cv_ps, c->d_pc, c->log_n);
+    } else {
+        TRY(bconv_attr(k_moddown_conv<1>, smem));
+        launch_ex(k_moddown_conv<1>, g2, dim3(256), smem, s, c->pdl, z, z_ct, z_ps, ns, vround, pl.mhl, pl.fhl,
+                  pl.n_dst, pl.dst_corr, conv, cv_ct, cv_ps, c->d_pc, c->log_n);
     }
-#undef SRK_CONV_LAUNCH
     LAUNCHED();
     return SRK_OK;
 }
@@ -1121,42 +1196,41 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
                         f64ok = false;
                 }
         dim3 grid((unsigned)((n + 255) / 256), B * beta, (maxd + SRK_MODUP_TCH - 1) / SRK_MODUP_TCH);
-        if (f64ok) {
-            const dim3 g2 = conv_grid(c, grid);
-#define SRK_MODUP_F64(GS)                                                          \
-    case GS:                                                                      \
-        if (wide0)                                                                \
-            k_modup_f64<GS, true><<<g2, 256, 0, s>>>(m, c->d_pc, c->log_n);      \
-        else                                                                      \
-            k_modup_f64<GS, false><<<g2, 256, 0, s>>>(m, c->d_pc, c->log_n);     \
-        break;
-            switch (alpha) {
-                SRK_MODUP_F64(1) SRK_MODUP_F64(2) SRK_MODUP_F64(3) SRK_MODUP_F64(4)
-                SRK_MODUP_F64(5) SRK_MODUP_F64(6) SRK_MODUP_F64(7) SRK_MODUP_F64(8)
-                SRK_MODUP_F64(9) SRK_MODUP_F64(10) SRK_MODUP_F64(11) SRK_MODUP_F64(12)
-                SRK_MODUP_F64(13) SRK_MODUP_F64(14) SRK_MODUP_F64(15) SRK_MODUP_F64(16)
-                default: return fail(SRK_EINVAL, "digit size > 16");
+        if (f64ok && alpha <= 16) {
+            dim3 gb((unsigned)((n + SRK_BCONV_TILE - 1) / SRK_BCONV_TILE), B * beta, (maxd + SRK_BCONV_TG - 1) / SRK_BCONV_TG);
+            const dim3 g2 = conv_grid(c, gb);
+            const int nbuf = bconv_nbuf(c, alpha, g2.x < gb.x);
+            const size_t smem = bconv_smem_bytes(alpha, nbuf);
+#define SRK_MODUP_CONV(W, NB)                                                     \
+    do {                                                                          \
+        TRY(bconv_attr(k_modup_conv<W, NB>, smem));                               \
+        launch_ex(k_modup_conv<W, NB>, g2, dim3(256), smem, s, c->pdl, m, c->d_pc, c->log_n); \
+    } while (0)
+            if (nbuf == 2) {
+                if (wide0) SRK_MODUP_CONV(true, 2); else SRK_MODUP_CONV(false, 2);
+            } else {
+                if (wide0) SRK_MODUP_CONV(true, 1); else SRK_MODUP_CONV(false, 1);
             }
-#undef SRK_MODUP_F64
+#undef SRK_MODUP_CONV
         } else {
             // general parameter sets (wide scaling primes): 128-bit MAC + Barrett
             switch (alpha) {
-                case 1: k_modup<1><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 2: k_modup<2><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 3: k_modup<3><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 4: k_modup<4><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 5: k_modup<5><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 6: k_modup<6><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 7: k_modup<7><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 8: k_modup<8><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 9: k_modup<9><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 10: k_modup<10><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 11: k_modup<11><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 12: k_modup<12><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 13: k_modup<13><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 14: k_modup<14><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                case 15: k_modup<15><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
-                default: k_modup<16><<<grid, 256, 0, s>>>(m, c->d_pc, c->log_n); break;
+                case 1: launch_ex(k_modup<1>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 2: launch_ex(k_modup<2>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 3: launch_ex(k_modup<3>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 4: launch_ex(k_modup<4>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 5: launch_ex(k_modup<5>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 6: launch_ex(k_modup<6>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 7: launch_ex(k_modup<7>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 8: launch_ex(k_modup<8>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 9: launch_ex(k_modup<9>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 10: launch_ex(k_modup<10>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 11: launch_ex(k_modup<11>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 12: launch_ex(k_modup<12>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 13: launch_ex(k_modup<13>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 14: launch_ex(k_modup<14>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 15: launch_ex(k_modup<15>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                default: launch_ex(k_modup<16>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
             }
         }
         LAUNCHED();
@@ -1207,17 +1281,17 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         {
             const int blocks = grid_for((long long)(ne - ka.t0) * n);
             switch (beta) {
-                case 1: k_ks_inner<1><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n); break;
-                case 2: k_ks_inner<2><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n); break;
-                case 3: k_ks_inner<3><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n); break;
-                case 4: k_ks_inner<4><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n); break;
+                case 1: launch_ex(k_ks_inner<1>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 2: launch_ex(k_ks_inner<2>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 3: launch_ex(k_ks_inner<3>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 4: launch_ex(k_ks_inner<4>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
                 default:
                     if (beta <= 8)
-                        k_ks_inner<8><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n);
+                        launch_ex(k_ks_inner<8>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n);
                     else if (beta <= 16)
-                        k_ks_inner<16><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n);
+                        launch_ex(k_ks_inner<16>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n);
                     else
-                        k_ks_inner<64><<<blocks, 256, 0, so>>>(ka, c->d_pc, c->log_n);
+                        launch_ex(k_ks_inner<64>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n);
             }
             LAUNCHED();
         }
@@ -1250,9 +1324,9 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             //     N^-1 (S/s_k)^-1 folded in; rounding term over K+1 limbs
             const int ns = K + 1;
             const uint64_t pm = c->lc_pmod.w[level], pms = c->lc_pmod.ws[level];
-            k_prep_special<<<grid_for(2ll * B * ns * n), 256, 0, so>>>(
-                acc, 2ll * ne * n, (long long)ne * n, ko.add0, ko.add_ct, (long long)nl * n, zb, pm, pms,
-                c->d_pc, c->log_n, level, K, B);
+            launch_ex(k_prep_special, dim3(grid_for(2ll * B * ns * n)), dim3(256), 0, so, c->pdl,
+                      (const uint64_t *)acc, 2ll * ne * n, (long long)ne * n, ko.add0, ko.add_ct,
+                      (long long)nl * n, zb, pm, pms, (const PrimeConst *)c->d_pc, c->log_n, level, K, B);
             LAUNCHED();
             FuseArgs f = no_fuse();
             f.mulc = c->lc_rs_scale[level];
@@ -1261,8 +1335,9 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             b.off_a = c->n_q;
             b.off_b = level - K;
             TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, so));
-            k_moddown_v<<<grid_for(2ll * B * n), 256, 0, so>>>(zb, 2ll * ns * n, (long long)ns * n, K,
-                                                              c->n_q, ns, level, vround, c->d_pc, c->log_n, B);
+            launch_ex(k_moddown_v, dim3(grid_for(2ll * B * n)), dim3(256), 0, so, c->pdl, (const uint64_t *)zb,
+                      2ll * ns * n, (long long)ns * n, K, c->n_q, ns, level, vround, (const PrimeConst *)c->d_pc,
+                      c->log_n, B);
             LAUNCHED();
             // out = (acc - conv) (P q_l)^-1 + d q_l^-1 over q_0..q_{l-1}
             nout = level;
@@ -1284,8 +1359,9 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             b.split = 0;
             b.off_b = c->n_q;
             TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, so));
-            k_moddown_v<<<grid_for(2ll * B * n), 256, 0, so>>>(zb, 2ll * K * n, (long long)K * n, K,
-                                                              c->n_q, K, 0, vround, c->d_pc, c->log_n, B);
+            launch_ex(k_moddown_v, dim3(grid_for(2ll * B * n)), dim3(256), 0, so, c->pdl, (const uint64_t *)zb,
+                      2ll * K * n, (long long)K * n, K, c->n_q, K, 0, vround, (const PrimeConst *)c->d_pc,
+                      c->log_n, B);
             LAUNCHED();
             nout = nl;
             plan = &c->moddown[level];

@@ -8,14 +8,7 @@
 
 #include "modarith.cuh"
 #include "ntt.cuh"
-
-// CTAs per SM the conversion kernels' register budgets are sized for
-#ifndef SRK_CONV_MINB
-#define SRK_CONV_MINB 4
-#endif
-#ifndef SRK_MODUP_MINB
-#define SRK_MODUP_MINB 3
-#endif
+#include "bconv.cuh"
 
 
 // ---------------------------------------------------------------------
@@ -221,27 +214,10 @@ __global__ void k_automorph(const uint64_t *__restrict__ a, uint64_t *__restrict
 // ---------------------------------------------------------------------
 // hybrid key switching, batched over B ciphertexts
 // ---------------------------------------------------------------------
-#define SRK_MAX_DIGITS 64
-
-// ModUp base conversion for every digit of every ciphertext:
+// ModUp base conversion for every digit of every ciphertext (ModUpArgs, bconv.cuh):
 //   ext[b][j][slot_t] = sum_{i in G_j} y_i * mat_j[i][t]  mod p_t
 // y = dc[b][G_j] already multiplied by (Q_j/q_i)^-1 (folded into the INTT).
 // grid: x = coefficient blocks, y = b * beta + j, z = chunks of 8 targets.
-struct ModUpArgs {
-    const uint64_t *dc;
-    long long dc_ct;
-    uint64_t *ext;
-    long long ext_ct, ext_dig;
-    int nl, beta, alpha;
-    const uint64_t *mat[SRK_MAX_DIGITS];
-    const int *slot[SRK_MAX_DIGITS];
-    const int *pid[SRK_MAX_DIGITS];
-    int n_dst[SRK_MAX_DIGITS];
-    // FP64 + integer pipe conversion (k_modup_f64): {m, m 2^32 mod q_t}, {m/q_t, (m 2^32 mod q_t)/q_t}
-    const ulonglong2 *mhl[SRK_MAX_DIGITS];
-    const double2 *fhl[SRK_MAX_DIGITS];
-};
-
 #define SRK_MODUP_TCH 8
 
 // GS = exact digit size (compile-time: no predicated MACs); digits smaller
@@ -256,6 +232,8 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
     const int nd = a.n_dst[j];
     if (t0 >= nd) return;
     const int t1 = min(nd, t0 + SRK_MODUP_TCH);
+    pdl_trigger();
+    pdl_wait();
     const uint64_t *src = a.dc + b * a.dc_ct + (long long)g0 * n;
     uint64_t *dst = a.ext + b * a.ext_ct + j * a.ext_dig;
     const uint64_t *mat = a.mat[j];
@@ -277,91 +255,6 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
                 for (int i = 0; i < gs; i++) mac(acc, src[(long long)i * n + x], __ldg(mat + i * nd + t));
                 dst[(long long)__ldg(a.slot[j] + t) * n + x] = reduce_u128(acc, pc[__ldg(a.pid[j] + t)]);
             }
-        }
-    }
-}
-
-// ModUp conversion with the quotient on the FP64 pipe and the remainder in
-// wrapping 64-bit integers (see k_moddown_conv_f64), for every target q_t < 2^62:
-//   S = sum_i y_i m_it (mod 2^64),  T = sum_i y_i (m_it / q_t),  r = S - round(T) q_t.
-// Sources under primes < 2^41 enter whole (|term| < 2^41, T error < 2^-4 over 16
-// terms); a wider source (q_0 in digit 0: WIDE0) enters as y = yh 2^32 + yl with
-// m' = m 2^32 mod q_t.  |S - round(T) q_t| < q_t < 2^63, so the wrapped difference
-// is the exact signed remainder whatever the target's size.
-template <int GS, bool WIDE0>
-__global__ void __launch_bounds__(256, SRK_MODUP_MINB) k_modup_f64(const __grid_constant__ ModUpArgs a,
-                                                   const PrimeConst *__restrict__ pc, int log_n) {
-    // {m, bits(m / q)} per (target, source): one 16-byte broadcast load per term;
-    // the wide source's {m', bits(m' / q)} separately
-    __shared__ ulonglong2 s_mf[SRK_MODUP_TCH][GS];
-    __shared__ ulonglong2 s_w0[SRK_MODUP_TCH];
-    __shared__ uint64_t s_q[SRK_MODUP_TCH];
-    __shared__ int s_slot[SRK_MODUP_TCH];
-    const long long n = 1ll << log_n;
-    const int b = blockIdx.y / a.beta, j = blockIdx.y - b * a.beta;
-    const int g0 = j * a.alpha, gs = min(a.alpha, a.nl - g0);
-    const int t0 = blockIdx.z * SRK_MODUP_TCH;
-    const int nd = a.n_dst[j];
-    if (t0 >= nd) return;
-    const int nt = min(nd - t0, SRK_MODUP_TCH);
-    for (int i = threadIdx.x; i < nt * GS; i += blockDim.x) {
-        const int tt = i / GS, k = i - tt * GS;
-        if (k < gs) {
-            const double2 f = __ldg(a.fhl[j] + k * nd + t0 + tt);
-            const ulonglong2 m = __ldg(a.mhl[j] + k * nd + t0 + tt);
-            s_mf[tt][k] = make_ulonglong2(m.x, (uint64_t)__double_as_longlong(f.x));
-            if (k == 0) s_w0[tt] = make_ulonglong2(m.y, (uint64_t)__double_as_longlong(f.y));
-        }
-    }
-    if (threadIdx.x < nt) {
-        s_q[threadIdx.x] = pc[__ldg(a.pid[j] + t0 + threadIdx.x)].q;
-        s_slot[threadIdx.x] = __ldg(a.slot[j] + t0 + threadIdx.x);
-    }
-    __syncthreads();
-    const uint64_t *src = a.dc + b * a.dc_ct + (long long)g0 * n;
-    uint64_t *dst = a.ext + b * a.ext_ct + j * a.ext_dig;
-    const bool wide = WIDE0 && j == 0;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
-         x += (long long)gridDim.x * blockDim.x) {
-        uint64_t y[GS];
-        double dy[GS];
-#pragma unroll
-        for (int i = 0; i < GS; i++) {
-            y[i] = i < gs ? __ldg(src + (long long)i * n + x) : 0;  // read-only: may pass the stores
-            dy[i] = __longlong_as_double((long long)(y[i] | 0x4330000000000000ull)) - SRK_F64_TWO52;
-        }
-        // wide source 0: halves (dy[0] above is only used when !wide)
-        const uint32_t yl0 = (uint32_t)y[0], yh0 = (uint32_t)(y[0] >> 32);
-        const double dl0 = __hiloint2double(0x43300000, (int)yl0) - SRK_F64_TWO52;
-        const double dh0 = __hiloint2double(0x43300000, (int)yh0) - SRK_F64_TWO52;
-#pragma unroll
-        for (int tt = 0; tt < SRK_MODUP_TCH; tt++) {
-            if (tt >= nt) break;
-            const uint64_t q = s_q[tt];
-            // four FMA chains and two wrapping integer sums (latency-bound otherwise)
-            double T[4] = {0.0, 0.0, 0.0, 0.0};
-            uint64_t S[2] = {0, 0};
-#pragma unroll
-            for (int i = 0; i < GS; i++) {
-                if (i < gs) {
-                    const ulonglong2 mf = s_mf[tt][i];
-                    const double fx = __longlong_as_double((long long)mf.y);
-                    if (i == 0 && wide) {
-                        const ulonglong2 w0 = s_w0[tt];
-                        T[0] = fma(dl0, fx, T[0]);
-                        T[1] = fma(dh0, __longlong_as_double((long long)w0.y), T[1]);
-                        S[0] += (uint64_t)yl0 * mf.x;
-                        S[1] += (uint64_t)yh0 * w0.x;
-                    } else {
-                        T[i & 3] = fma(dy[i], fx, T[i & 3]);
-                        S[i & 1] += y[i] * mf.x;
-                    }
-                }
-            }
-            const double Tt = (T[0] + T[1]) + (T[2] + T[3]);
-            const long long tq = __double_as_longlong(Tt + SRK_F64_MAGIC) - 0x4338000000000000ll;
-            const long long rr = (long long)((S[0] + S[1]) - (uint64_t)tq * q);
-            dst[(long long)s_slot[tt] * n + x] = (uint64_t)(rr < 0 ? rr + (long long)q : rr);
         }
     }
 }
@@ -399,6 +292,8 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
     const long long total = (long long)a.ne * n;  // acc poly stride
     const long long work = (long long)(a.ne - a.t0) * n;
     const Div32 dalpha = mk_div32(a.alpha);
+    pdl_trigger();
+    pdl_wait();
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < work;
          x += (long long)gridDim.x * blockDim.x) {
         const int t = a.t0 + (int)(x >> log_n);
@@ -450,173 +345,6 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
     }
 }
 
-// ModDown conversion P -> Q with the FP64 and integer pipes splitting the work
-// (any target q_t < 2^62: only |S' - t q_t| < q_t < 2^63 is needed):
-//   z_k = zh_k 2^32 + zl_k,   S' = sum_k zh_k m'_kt + zl_k m_kt  == sum_k z_k m_kt (mod q_t)
-// with m' = m 2^32 mod q_t.  The quotient t = round(S'/q_t) comes from the FP64
-// pipe, T = sum_k zh_k (m'/q) + zl_k (m/q) (every term < 2^32, total rounding
-// error < 2^-16, so S' - t q_t lies in (-q_t, q_t)), and the remainder from the
-// integer pipe in wrapping 64-bit arithmetic: r = S' - t q_t (mod 2^64), exact
-// because |r| < q_t.  Per target: 2K FP64 FMAs + 2K 32x64-bit IMAD products
-// instead of K 64-bit Shoup products (~13 IMAD each).
-#define SRK_CONV_TG 8  // targets per CTA (blockIdx.z groups)
-#ifndef SRK_CONV_UNROLL
-#define SRK_CONV_UNROLL 4
-#endif
-constexpr int kConvUnroll = SRK_CONV_UNROLL;
-template <int MAXK, bool EXACT>
-__global__ void __launch_bounds__(256, SRK_CONV_MINB) k_moddown_conv_f64(
-    const uint64_t *__restrict__ z, long long z_ct, long long z_ps, int n_src,
-    const uint8_t *__restrict__ vround,
-    const ulonglong2 *__restrict__ mhl, const double2 *__restrict__ fhl, int n_dst,
-    const uint64_t *__restrict__ corr, uint64_t *__restrict__ conv, long long c_ct, long long c_ps,
-    const PrimeConst *__restrict__ pc, int log_n) {
-    // the CTA's targets' constants, staged once: {m/q, m'/q} and {m, m'} per (target, source)
-    __shared__ double2 s_f[SRK_CONV_TG][MAXK];
-    __shared__ ulonglong2 s_m[SRK_CONV_TG][MAXK];
-    __shared__ uint64_t s_q[SRK_CONV_TG], s_corr[MAXK + 1][SRK_CONV_TG];
-    const long long n = 1ll << log_n;
-    const int p = blockIdx.y;  // (b, r)
-    const int b = p >> 1, r = p & 1;
-    const int t0 = blockIdx.z * SRK_CONV_TG, nt = min(n_dst - t0, SRK_CONV_TG);
-    const int ns = EXACT ? MAXK : n_src;
-    for (int i = threadIdx.x; i < nt * MAXK; i += blockDim.x) {
-        const int tt = i / MAXK, k = i - tt * MAXK;
-        if (k < ns) {
-            s_f[tt][k] = __ldg(fhl + k * n_dst + t0 + tt);
-            s_m[tt][k] = __ldg(mhl + k * n_dst + t0 + tt);
-        }
-    }
-    for (int i = threadIdx.x; i < nt * (MAXK + 1); i += blockDim.x) {
-        const int v = i / nt, tt = i - v * nt;
-        if (v <= ns) s_corr[v][tt] = __ldg(corr + v * n_dst + t0 + tt);
-    }
-    if (threadIdx.x < nt) s_q[threadIdx.x] = pc[t0 + threadIdx.x].q;
-    __syncthreads();
-    const uint64_t *zp = z + b * z_ct + r * z_ps;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    // software prefetch: the next coefficient's sources are loaded before this
-    // one's stores (which the compiler cannot move loads across)
-    long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    uint64_t zn[MAXK];
-    int vn = 0;
-    if (x < n) {
-#pragma unroll
-        for (int k = 0; k < MAXK; k++) zn[k] = (EXACT || k < n_src) ? __ldg(zp + k * n + x) : 0;
-        vn = __ldg(vround + (long long)p * n + x);
-    }
-    for (; x < n; x += stride) {
-        uint64_t zz[MAXK];
-        uint32_t zl[MAXK], zh[MAXK];
-        double dl[MAXK], dh[MAXK];
-#pragma unroll
-        for (int k = 0; k < MAXK; k++) zz[k] = zn[k];
-        const int v = vn;
-        if (x + stride < n) {
-#pragma unroll
-            for (int k = 0; k < MAXK; k++)
-                zn[k] = (EXACT || k < n_src) ? __ldg(zp + k * n + x + stride) : 0;
-            vn = __ldg(vround + (long long)p * n + x + stride);
-        }
-#pragma unroll
-        for (int k = 0; k < MAXK; k++) {
-            zl[k] = (uint32_t)zz[k];
-            zh[k] = (uint32_t)(zz[k] >> 32);
-            dl[k] = __hiloint2double(0x43300000, (int)zl[k]) - SRK_F64_TWO52;
-            dh[k] = __hiloint2double(0x43300000, (int)zh[k]) - SRK_F64_TWO52;
-        }
-        uint64_t *out = conv + b * c_ct + r * c_ps + (long long)t0 * n + x;
-#pragma unroll(kConvUnroll)  // (fully unrolled, the compiler hoists every target's constants: 250 registers)
-        for (int tt = 0; tt < SRK_CONV_TG; tt++) {
-            if (tt >= nt) break;
-            const uint64_t q = s_q[tt];
-            double T0 = 0.0, T1 = 0.0;
-            uint64_t S = 0;
-#pragma unroll
-            for (int k = 0; k < MAXK; k++)
-                if (EXACT || k < n_src) {
-                    const double2 f = s_f[tt][k];     // {m/q, m'/q}
-                    const ulonglong2 m = s_m[tt][k];  // {m, m'}
-                    T0 = fma(dl[k], f.x, T0);
-                    T1 = fma(dh[k], f.y, T1);
-                    S += (uint64_t)zl[k] * m.x;
-                    S += (uint64_t)zh[k] * m.y;
-                }
-            const long long tq = __double_as_longlong((T0 + T1) + SRK_F64_MAGIC) - 0x4338000000000000ll;
-            const long long rr = (long long)(S - (uint64_t)tq * q);
-            const uint64_t acc = (uint64_t)(rr < 0 ? rr + (long long)q : rr);
-            *out = sub_mod(acc, s_corr[v][tt], q);
-            out += n;
-        }
-    }
-}
-
-// The same conversion for many special primes (the long chain's K = 11..16):
-// sources outer, the CTA's 8 targets inner, so the per-source values live in
-// registers one at a time and only the 8 (T, S) accumulators persist.
-__global__ void __launch_bounds__(256, 3) k_moddown_conv_f64_wide(
-    const uint64_t *__restrict__ z, long long z_ct, long long z_ps, int n_src,
-    const uint8_t *__restrict__ vround, const ulonglong2 *__restrict__ mhl,
-    const double2 *__restrict__ fhl, int n_dst, const uint64_t *__restrict__ corr,
-    uint64_t *__restrict__ conv, long long c_ct, long long c_ps, const PrimeConst *__restrict__ pc,
-    int log_n) {
-    __shared__ double2 s_f[16][SRK_CONV_TG];
-    __shared__ ulonglong2 s_m[16][SRK_CONV_TG];
-    __shared__ uint64_t s_q[SRK_CONV_TG], s_corr[17][SRK_CONV_TG];
-    const long long n = 1ll << log_n;
-    const int p = blockIdx.y;  // (b, r)
-    const int b = p >> 1, r = p & 1;
-    const int t0 = blockIdx.z * SRK_CONV_TG, nt = min(n_dst - t0, SRK_CONV_TG);
-    for (int i = threadIdx.x; i < n_src * SRK_CONV_TG; i += blockDim.x) {
-        const int k = i / SRK_CONV_TG, tt = i - k * SRK_CONV_TG;
-        s_f[k][tt] = tt < nt ? __ldg(fhl + k * n_dst + t0 + tt) : make_double2(0.0, 0.0);
-        s_m[k][tt] = tt < nt ? __ldg(mhl + k * n_dst + t0 + tt) : make_ulonglong2(0, 0);
-    }
-    for (int i = threadIdx.x; i < (n_src + 1) * SRK_CONV_TG; i += blockDim.x) {
-        const int v = i / SRK_CONV_TG, tt = i - v * SRK_CONV_TG;
-        s_corr[v][tt] = tt < nt ? __ldg(corr + v * n_dst + t0 + tt) : 0;
-    }
-    if (threadIdx.x < SRK_CONV_TG) s_q[threadIdx.x] = threadIdx.x < nt ? pc[t0 + threadIdx.x].q : 1;
-    __syncthreads();
-    const uint64_t *zp = z + b * z_ct + r * z_ps;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n;
-         x += (long long)gridDim.x * blockDim.x) {
-        double T[SRK_CONV_TG];
-        uint64_t S[SRK_CONV_TG];
-#pragma unroll
-        for (int tt = 0; tt < SRK_CONV_TG; tt++) {
-            T[tt] = 0.0;
-            S[tt] = 0;
-        }
-        uint64_t znext = __ldg(zp + x);
-        for (int k = 0; k < n_src; k++) {
-            const uint64_t zz = znext;  // loaded one source ahead (latency off the chain)
-            if (k + 1 < n_src) znext = __ldg(zp + (k + 1) * n + x);
-            const uint32_t zl = (uint32_t)zz, zh = (uint32_t)(zz >> 32);
-            const double dl = __hiloint2double(0x43300000, (int)zl) - SRK_F64_TWO52;
-            const double dh = __hiloint2double(0x43300000, (int)zh) - SRK_F64_TWO52;
-#pragma unroll
-            for (int tt = 0; tt < SRK_CONV_TG; tt++) {
-                const double2 f = s_f[k][tt];
-                const ulonglong2 m = s_m[k][tt];
-                T[tt] = fma(dh, f.y, fma(dl, f.x, T[tt]));
-                S[tt] += (uint64_t)zl * m.x + (uint64_t)zh * m.y;
-            }
-        }
-        const int v = vround[(long long)p * n + x];
-        uint64_t *out = conv + b * c_ct + r * c_ps + (long long)t0 * n + x;
-#pragma unroll
-        for (int tt = 0; tt < SRK_CONV_TG; tt++) {
-            if (tt >= nt) break;
-            const uint64_t q = s_q[tt];
-            const long long tq = __double_as_longlong(T[tt] + SRK_F64_MAGIC) - 0x4338000000000000ll;
-            const long long rr = (long long)(S[tt] - (uint64_t)tq * q);
-            const uint64_t acc = (uint64_t)(rr < 0 ? rr + (long long)q : rr);
-            out[(long long)tt * n] = sub_mod(acc, s_corr[v][tt], q);
-        }
-    }
-}
-
 // exact ModDown rounding term per coefficient: v = round(sum_k z_k / p_k)
 // (64.64 fixed point, f_k = z_k R1 + hi(z_k R0), R = floor(2^128 / p_k));
 // z: B*2 polys (ct stride z_ct, poly stride z_ps) of K limbs; v: [B*2][N]
@@ -626,6 +354,8 @@ __global__ void k_moddown_v(const uint64_t *__restrict__ z, long long z_ct, long
                             const PrimeConst *__restrict__ pc, int log_n, int batch) {
     const long long n = 1ll << log_n;
     const long long total = 2ll * batch * n;
+    pdl_trigger();
+    pdl_wait();
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
         const long long p = x >> log_n;
@@ -763,6 +493,8 @@ __global__ void k_prep_special(const uint64_t *__restrict__ acc, long long acc_c
     const long long total = 2ll * batch * per;
     const uint64_t ql = pc[level].q;
     const Div32 dv = mk_div32(K + 1);
+    pdl_trigger();
+    pdl_wait();
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
         const long long p = div32((uint32_t)(x >> log_n), dv), xi = x - p * per;
