@@ -164,7 +164,6 @@ struct srk_ctx {
     int ws_batch = SRK_WS_BATCH;  // ciphertexts per internal chunk (SRK_WS_BATCH env: smaller workspace)
     int ntt_cta_threads = 128;  // threads per NTT pass CTA (128: 8 CTAs/SM, cheaper barriers)
     unsigned conv_cpt = 4;  // coefficients per thread of the conversions (amortises their staging)
-    bool pdl = true;  // programmatic dependent launch of the kernel chains (SRK_PDL=0: plain launches)
     cudaStream_t nside[2] = {nullptr, nullptr};
     cudaEvent_t ev_nfork[2] = {nullptr, nullptr}, ev_njoin[2] = {nullptr, nullptr};
 };
@@ -296,7 +295,6 @@ extern "C" int srk_ctx_create(int device, int log_n, const uint64_t *primes,
     // key-switch workspace batch (several ranks sharing one GPU need a smaller one)
     if (const char *e = getenv("SRK_NTT_CHUNK")) c->ntt_chunk = std::max(1, atoi(e));
     if (const char *e = getenv("SRK_WS_BATCH")) c->ws_batch = std::max(1, atoi(e));
-    if (const char *e = getenv("SRK_PDL")) c->pdl = atoi(e) != 0;
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -525,30 +523,22 @@ static FuseArgs no_fuse() {
     return f;
 }
 
-// Launch with (pdl) or without the programmatic-stream-serialisation attribute: a
-// kernel that calls pdl_wait() before its first dependent access may be scheduled
-// while the previous kernel of the stream drains (its launch latency and prologue
-// overlap that tail).  Only kernels containing pdl_wait() may be launched with pdl.
+// cudaLaunchKernelEx wrapper (explicit config; arguments converted to the kernel's types)
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                             bool pdl, Args &&...args) {
+                             Args &&...args) {
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof cfg);
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 template <int LOG_T, bool INV, bool COL, int IO, int KM, int LOGN>
 static void launch_kernel_n(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
-                            const NttTables &tb, int log_n, const FuseArgs &ff, bool pdl) {
+                            const NttTables &tb, int log_n, const FuseArgs &ff) {
     // the attribute is per device: one bit per device ordinal
     static std::atomic<unsigned long long> attr_done{0};
     int dev = 0;
@@ -559,20 +549,19 @@ static void launch_kernel_n(dim3 grid, int threads, size_t smem, cudaStream_t s,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         attr_done.fetch_or(bit, std::memory_order_relaxed);
     }
-    launch_ex(ntt_pass_kernel<LOG_T, INV, COL, IO, KM, LOGN>, grid, dim3(threads), smem, s, pdl, bb, tb, log_n,
-              ff);
+    launch_ex(ntt_pass_kernel<LOG_T, INV, COL, IO, KM, LOGN>, grid, dim3(threads), smem, s, bb, tb, log_n, ff);
 }
 // ring 2^16 (every BASELINE config past config 1): compile-time shape
 template <int LOG_T, bool INV, bool COL, int IO, int KM>
 static void launch_kernel(dim3 grid, int threads, size_t smem, cudaStream_t s, const LimbBatch &bb,
-                          const NttTables &tb, int log_n, const FuseArgs &ff, bool pdl) {
+                          const NttTables &tb, int log_n, const FuseArgs &ff) {
     if constexpr (LOG_T == 8) {
         if (log_n == 16) {
-            launch_kernel_n<LOG_T, INV, COL, IO, KM, 16>(grid, threads, smem, s, bb, tb, log_n, ff, pdl);
+            launch_kernel_n<LOG_T, INV, COL, IO, KM, 16>(grid, threads, smem, s, bb, tb, log_n, ff);
             return;
         }
     }
-    launch_kernel_n<LOG_T, INV, COL, IO, KM, 0>(grid, threads, smem, s, bb, tb, log_n, ff, pdl);
+    launch_kernel_n<LOG_T, INV, COL, IO, KM, 0>(grid, threads, smem, s, bb, tb, log_n, ff);
 }
 
 template <int LOG_T, bool INV, bool COL, int IO>
@@ -621,9 +610,9 @@ static int launch_pass(const srk_ctx *c, LimbBatch b, int l0, int nlc, const Fus
     // rescale's FP64 spread needs the dropped prime < 2^41 too (IO 2 on either pass:
     // LD_SPREAD first, ST_RESCALE last)
     if (f64 && (IO != 2 || f.top_q < SRK_F64_Q))
-        launch_kernel<LOG_T, INV, COL, IO, 1>(grid, threads, smem, s, bb, tables(c), c->log_n, ff, c->pdl);
+        launch_kernel<LOG_T, INV, COL, IO, 1>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
     else
-        launch_kernel<LOG_T, INV, COL, IO, 2>(grid, threads, smem, s, bb, tables(c), c->log_n, ff, c->pdl);
+        launch_kernel<LOG_T, INV, COL, IO, 2>(grid, threads, smem, s, bb, tables(c), c->log_n, ff);
     LAUNCHED();
     return SRK_OK;
 }
@@ -1069,19 +1058,33 @@ static int moddown_conv(srk_ctx *c, const BconvPlan &pl, const uint64_t *z, long
     const long long n = c->n;
     const int ns = pl.n_src;
     if (ns > SRK_BCONV_MAXSRC) return fail(SRK_EINVAL, "ModDown with more than 17 source primes");
-    dim3 grid((unsigned)((n + SRK_BCONV_TILE - 1) / SRK_BCONV_TILE), 2 * B, (nout + SRK_BCONV_TG - 1) / SRK_BCONV_TG);
+    if (ns <= 4) {
+        // few sources: one coefficient per thread, sources in registers (bconv.cuh)
+        dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + SRK_BCONV_TG - 1) / SRK_BCONV_TG);
+        const dim3 g2 = conv_grid(c, grid);
+#define SRK_CONV_SMALL(K)                                                                                  \
+    case K:                                                                                                \
+        launch_ex(k_moddown_conv_small<K>, g2, dim3(256), 0, s, z, z_ct, z_ps, vround, pl.mhl, pl.fhl,     \
+                  pl.n_dst, pl.dst_corr, conv, cv_ct, cv_ps, c->d_pc, c->log_n);                           \
+        break;
+        switch (ns) { SRK_CONV_SMALL(1) SRK_CONV_SMALL(2) SRK_CONV_SMALL(3) SRK_CONV_SMALL(4) }
+#undef SRK_CONV_SMALL
+        LAUNCHED();
+        return SRK_OK;
+    }
+    const int tg = SRK_BCONV_TG;
+    dim3 grid((unsigned)((n + SRK_BCONV_TILE - 1) / SRK_BCONV_TILE), 2 * B, (nout + tg - 1) / tg);
     const dim3 g2 = conv_grid(c, grid);
     const int nbuf = bconv_nbuf(c, ns, g2.x < grid.x);
     const size_t smem = bconv_smem_bytes(ns, nbuf);
-    if (nbuf == 2) {
-        TRY(bconv_attr(k_moddown_conv<2>, smem));
-        launch_ex(k_moddown_conv<2>, g2, dim3(256), smem, s, c->pdl, z, z_ct, z_ps, ns, vround, pl.mhl, pl.fhl,
-                  pl.n_dst, pl.dst_corr, conv, cv_ct, cv_ps, c->d_pc, c->log_n);
-    } else {
-        TRY(bconv_attr(k_moddown_conv<1>, smem));
-        launch_ex(k_moddown_conv<1>, g2, dim3(256), smem, s, c->pdl, z, z_ct, z_ps, ns, vround, pl.mhl, pl.fhl,
-                  pl.n_dst, pl.dst_corr, conv, cv_ct, cv_ps, c->d_pc, c->log_n);
-    }
+#define SRK_MODDOWN_CONV(NB, TG)                                                                            \
+    do {                                                                                                    \
+        TRY(bconv_attr(k_moddown_conv<NB, TG>, smem));                                                      \
+        launch_ex(k_moddown_conv<NB, TG>, g2, dim3(256), smem, s, z, z_ct, z_ps, ns, vround, pl.mhl, pl.fhl, \
+                  pl.n_dst, pl.dst_corr, conv, cv_ct, cv_ps, c->d_pc, c->log_n);                            \
+    } while (0)
+    if (nbuf == 2) SRK_MODDOWN_CONV(2, 8); else SRK_MODDOWN_CONV(1, 8);
+#undef SRK_MODDOWN_CONV
     LAUNCHED();
     return SRK_OK;
 }
@@ -1204,7 +1207,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
 #define SRK_MODUP_CONV(W, NB)                                                     \
     do {                                                                          \
         TRY(bconv_attr(k_modup_conv<W, NB>, smem));                               \
-        launch_ex(k_modup_conv<W, NB>, g2, dim3(256), smem, s, c->pdl, m, c->d_pc, c->log_n); \
+        launch_ex(k_modup_conv<W, NB>, g2, dim3(256), smem, s, m, c->d_pc, c->log_n); \
     } while (0)
             if (nbuf == 2) {
                 if (wide0) SRK_MODUP_CONV(true, 2); else SRK_MODUP_CONV(false, 2);
@@ -1215,22 +1218,22 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         } else {
             // general parameter sets (wide scaling primes): 128-bit MAC + Barrett
             switch (alpha) {
-                case 1: launch_ex(k_modup<1>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 2: launch_ex(k_modup<2>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 3: launch_ex(k_modup<3>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 4: launch_ex(k_modup<4>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 5: launch_ex(k_modup<5>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 6: launch_ex(k_modup<6>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 7: launch_ex(k_modup<7>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 8: launch_ex(k_modup<8>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 9: launch_ex(k_modup<9>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 10: launch_ex(k_modup<10>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 11: launch_ex(k_modup<11>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 12: launch_ex(k_modup<12>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 13: launch_ex(k_modup<13>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 14: launch_ex(k_modup<14>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 15: launch_ex(k_modup<15>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
-                default: launch_ex(k_modup<16>, grid, dim3(256), 0, s, c->pdl, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 1: launch_ex(k_modup<1>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 2: launch_ex(k_modup<2>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 3: launch_ex(k_modup<3>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 4: launch_ex(k_modup<4>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 5: launch_ex(k_modup<5>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 6: launch_ex(k_modup<6>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 7: launch_ex(k_modup<7>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 8: launch_ex(k_modup<8>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 9: launch_ex(k_modup<9>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 10: launch_ex(k_modup<10>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 11: launch_ex(k_modup<11>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 12: launch_ex(k_modup<12>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 13: launch_ex(k_modup<13>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 14: launch_ex(k_modup<14>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 15: launch_ex(k_modup<15>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
+                default: launch_ex(k_modup<16>, grid, dim3(256), 0, s, m, (const PrimeConst *)c->d_pc, c->log_n); break;
             }
         }
         LAUNCHED();
@@ -1281,17 +1284,17 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
         {
             const int blocks = grid_for((long long)(ne - ka.t0) * n);
             switch (beta) {
-                case 1: launch_ex(k_ks_inner<1>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 2: launch_ex(k_ks_inner<2>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 3: launch_ex(k_ks_inner<3>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
-                case 4: launch_ex(k_ks_inner<4>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 1: launch_ex(k_ks_inner<1>, dim3(blocks), dim3(256), 0, so, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 2: launch_ex(k_ks_inner<2>, dim3(blocks), dim3(256), 0, so, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 3: launch_ex(k_ks_inner<3>, dim3(blocks), dim3(256), 0, so, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
+                case 4: launch_ex(k_ks_inner<4>, dim3(blocks), dim3(256), 0, so, ka, (const PrimeConst *)c->d_pc, c->log_n); break;
                 default:
                     if (beta <= 8)
-                        launch_ex(k_ks_inner<8>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n);
+                        launch_ex(k_ks_inner<8>, dim3(blocks), dim3(256), 0, so, ka, (const PrimeConst *)c->d_pc, c->log_n);
                     else if (beta <= 16)
-                        launch_ex(k_ks_inner<16>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n);
+                        launch_ex(k_ks_inner<16>, dim3(blocks), dim3(256), 0, so, ka, (const PrimeConst *)c->d_pc, c->log_n);
                     else
-                        launch_ex(k_ks_inner<64>, dim3(blocks), dim3(256), 0, so, c->pdl, ka, (const PrimeConst *)c->d_pc, c->log_n);
+                        launch_ex(k_ks_inner<64>, dim3(blocks), dim3(256), 0, so, ka, (const PrimeConst *)c->d_pc, c->log_n);
             }
             LAUNCHED();
         }
@@ -1324,7 +1327,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             //     N^-1 (S/s_k)^-1 folded in; rounding term over K+1 limbs
             const int ns = K + 1;
             const uint64_t pm = c->lc_pmod.w[level], pms = c->lc_pmod.ws[level];
-            launch_ex(k_prep_special, dim3(grid_for(2ll * B * ns * n)), dim3(256), 0, so, c->pdl,
+            launch_ex(k_prep_special, dim3(grid_for(2ll * B * ns * n)), dim3(256), 0, so,
                       (const uint64_t *)acc, 2ll * ne * n, (long long)ne * n, ko.add0, ko.add_ct,
                       (long long)nl * n, zb, pm, pms, (const PrimeConst *)c->d_pc, c->log_n, level, K, B);
             LAUNCHED();
@@ -1335,7 +1338,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             b.off_a = c->n_q;
             b.off_b = level - K;
             TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, so));
-            launch_ex(k_moddown_v, dim3(grid_for(2ll * B * n)), dim3(256), 0, so, c->pdl, (const uint64_t *)zb,
+            launch_ex(k_moddown_v, dim3(grid_for(2ll * B * n)), dim3(256), 0, so, (const uint64_t *)zb,
                       2ll * ns * n, (long long)ns * n, K, c->n_q, ns, level, vround, (const PrimeConst *)c->d_pc,
                       c->log_n, B);
             LAUNCHED();
@@ -1359,7 +1362,7 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
             b.split = 0;
             b.off_b = c->n_q;
             TRY(ntt_run(c, b, true, f, LD_PLAIN, ST_SCALE, so));
-            launch_ex(k_moddown_v, dim3(grid_for(2ll * B * n)), dim3(256), 0, so, c->pdl, (const uint64_t *)zb,
+            launch_ex(k_moddown_v, dim3(grid_for(2ll * B * n)), dim3(256), 0, so, (const uint64_t *)zb,
                       2ll * K * n, (long long)K * n, K, c->n_q, K, 0, vround, (const PrimeConst *)c->d_pc,
                       c->log_n, B);
             LAUNCHED();

@@ -76,14 +76,13 @@ __device__ __forceinline__ uint64_t bconv_finish(uint32_t sl, uint32_t sh, doubl
 // [n_src][n_dst] {m, m'} / {m/q, m'/q}; corr: [n_src+1][n_dst] = v P mod q_t.
 // Grid: x = tiles of 512 coefficients (grid-stride), y = (b, r), z = target groups.
 // ---------------------------------------------------------------------
-template <int NBUF>
+template <int NBUF, int TG>
 __global__ void __launch_bounds__(256, 2) k_moddown_conv(
     const uint64_t *__restrict__ z, long long z_ct, long long z_ps, int n_src,
     const uint8_t *__restrict__ vround, const ulonglong2 *__restrict__ mhl,
     const double2 *__restrict__ fhl, int n_dst, const uint64_t *__restrict__ corr,
     uint64_t *__restrict__ conv, long long c_ct, long long c_ps, const PrimeConst *__restrict__ pc,
     int log_n) {
-    constexpr int TG = SRK_BCONV_TG;
     extern __shared__ __align__(16) unsigned char bconv_dyn[];
     ulonglong2 *sy = reinterpret_cast<ulonglong2 *>(bconv_dyn);  // [NBUF][n_src][256]
     __shared__ double2 s_f[SRK_BCONV_MAXSRC][TG];
@@ -95,7 +94,6 @@ __global__ void __launch_bounds__(256, 2) k_moddown_conv(
     const int b = p >> 1, r = p & 1;
     const int t0 = blockIdx.z * TG, nt = min(n_dst - t0, TG);
     const int tid = threadIdx.x;
-    pdl_trigger();
     for (int i = tid; i < n_src * TG; i += blockDim.x) {
         const int k = i / TG, tt = i - k * TG;
         const ulonglong2 m = tt < nt ? __ldg(mhl + k * n_dst + t0 + tt) : make_ulonglong2(0, 0);
@@ -115,7 +113,6 @@ __global__ void __launch_bounds__(256, 2) k_moddown_conv(
     }
     if (tid < TG) s_q[tid] = tid < nt ? pc[t0 + tid].q : 1;
     __syncthreads();
-    pdl_wait();  // the staging above reads context tables only
     const uint64_t *zp = z + b * z_ct + r * z_ps;
     const long long tiles = (n + SRK_BCONV_TILE - 1) / SRK_BCONV_TILE;
     // stage tile `tile`'s sources (this thread's two coefficients of every limb)
@@ -190,6 +187,95 @@ __global__ void __launch_bounds__(256, 2) k_moddown_conv(
 }
 
 // ---------------------------------------------------------------------
+// The same conversion for K <= 4 sources (config 2's three special primes): the few
+// source words of a coefficient stay in registers, targets are the outer loop, and
+// the light per-thread state (one coefficient, 64 registers) lets four CTAs per SM
+// keep enough stores in flight -- the tile-staged kernel above is built for many
+// sources and runs this shape ~12% slower (473 vs 422 us per 32-ciphertext launch;
+// a variant with the constants in registers and the coefficients streaming: 720 us).
+// The next coefficient's sources are loaded before this one's stores (which loads
+// cannot pass).
+// ---------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(256, 4) k_moddown_conv_small(
+    const uint64_t *__restrict__ z, long long z_ct, long long z_ps, const uint8_t *__restrict__ vround,
+    const ulonglong2 *__restrict__ mhl, const double2 *__restrict__ fhl, int n_dst,
+    const uint64_t *__restrict__ corr, uint64_t *__restrict__ conv, long long c_ct, long long c_ps,
+    const PrimeConst *__restrict__ pc, int log_n) {
+    constexpr int TG = SRK_BCONV_TG;
+    __shared__ double2 s_f[TG][K];
+    __shared__ uint4 s_m[TG][K];           // {lo(m), hi(m), lo(m'), hi(m')}
+    __shared__ ulonglong2 s_c[K + 1][TG];  // per v: {(q - v P) mod q, bits of it / q}
+    __shared__ uint64_t s_q[TG];
+    const long long n = 1ll << log_n;
+    const int p = blockIdx.y;  // (b, r)
+    const int b = p >> 1, r = p & 1;
+    const int t0 = blockIdx.z * TG, nt = min(n_dst - t0, TG);
+    for (int i = threadIdx.x; i < nt * K; i += blockDim.x) {
+        const int tt = i / K, k = i - tt * K;
+        const ulonglong2 m = __ldg(mhl + k * n_dst + t0 + tt);
+        s_f[tt][k] = __ldg(fhl + k * n_dst + t0 + tt);
+        s_m[tt][k] = make_uint4((uint32_t)m.x, (uint32_t)(m.x >> 32), (uint32_t)m.y, (uint32_t)(m.y >> 32));
+    }
+    for (int i = threadIdx.x; i < (K + 1) * nt; i += blockDim.x) {
+        const int v = i / nt, tt = i - v * nt;
+        const uint64_t q = pc[t0 + tt].q, cv = __ldg(corr + v * n_dst + t0 + tt);
+        const uint64_t nc = cv ? q - cv : 0;
+        s_c[v][tt] = make_ulonglong2(nc, (uint64_t)__double_as_longlong((double)nc / (double)q));
+    }
+    if (threadIdx.x < nt) s_q[threadIdx.x] = pc[t0 + threadIdx.x].q;
+    __syncthreads();
+    const uint64_t *zp = z + b * z_ct + r * z_ps;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    uint64_t zn[K];
+    int vn = 0;
+    if (x < n) {
+#pragma unroll
+        for (int k = 0; k < K; k++) zn[k] = __ldg(zp + k * n + x);
+        vn = __ldg(vround + (long long)p * n + x);
+    }
+    for (; x < n; x += stride) {
+        uint32_t zl[K], zh[K];
+        double dl[K], dh[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            zl[k] = (uint32_t)zn[k];
+            zh[k] = (uint32_t)(zn[k] >> 32);
+            dl[k] = f64_of_u32(zl[k]);
+            dh[k] = f64_of_u32(zh[k]);
+        }
+        const int v = vn;
+        if (x + stride < n) {
+#pragma unroll
+            for (int k = 0; k < K; k++) zn[k] = __ldg(zp + k * n + x + stride);
+            vn = __ldg(vround + (long long)p * n + x + stride);
+        }
+        uint64_t *out = conv + b * c_ct + r * c_ps + (long long)t0 * n + x;
+#pragma unroll 4
+        for (int tt = 0; tt < TG; tt++) {
+            if (tt >= nt) break;
+            const ulonglong2 cv = s_c[v][tt];
+            uint32_t sl = (uint32_t)cv.x, sh = (uint32_t)(cv.x >> 32);
+            double T0 = __longlong_as_double((long long)cv.y), T1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                const double2 f = s_f[tt][k];
+                const uint4 m = s_m[tt][k];
+                T0 = fma(dl[k], f.x, T0);
+                T1 = fma(dh[k], f.y, T1);
+                mac_wide(sl, sh, zl[k], m.x);
+                mac_hi(sh, zl[k], m.y);
+                mac_wide(sl, sh, zh[k], m.z);
+                mac_hi(sh, zh[k], m.w);
+            }
+            *out = bconv_finish(sl, sh, T0 + T1, s_q[tt]);
+            out += n;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------
 // ModUp conversion of every digit (hybrid key switching): digit j's alpha source
 // limbs y_i (already scaled by (Q_j/q_i)^-1 in the INTT) -> every extended-basis
 // limb outside the digit, for targets q_t < 2^62.
@@ -234,7 +320,6 @@ __global__ void __launch_bounds__(256, 2) k_modup_conv(const __grid_constant__ M
     if (t0 >= nd) return;
     const int nt = min(nd - t0, TG);
     const int tid = threadIdx.x;
-    pdl_trigger();
     for (int i = tid; i < gs * TG; i += blockDim.x) {
         const int k = i / TG, tt = i - k * TG;
         ulonglong2 m = make_ulonglong2(0, 0);
@@ -256,7 +341,6 @@ __global__ void __launch_bounds__(256, 2) k_modup_conv(const __grid_constant__ M
         s_slot[tid] = ok ? __ldg(a.slot[j] + t0 + tid) : 0;
     }
     __syncthreads();
-    pdl_wait();  // the staging above reads context tables only
     const uint64_t *src = a.dc + b * a.dc_ct + (long long)g0 * n;
     uint64_t *dst = a.ext + b * a.ext_ct + j * a.ext_dig;
     const bool wide = WIDE0 && j == 0;

@@ -232,8 +232,6 @@ __global__ void __launch_bounds__(256) k_modup(const __grid_constant__ ModUpArgs
     const int nd = a.n_dst[j];
     if (t0 >= nd) return;
     const int t1 = min(nd, t0 + SRK_MODUP_TCH);
-    pdl_trigger();
-    pdl_wait();
     const uint64_t *src = a.dc + b * a.dc_ct + (long long)g0 * n;
     uint64_t *dst = a.ext + b * a.ext_ct + j * a.ext_dig;
     const uint64_t *mat = a.mat[j];
@@ -292,8 +290,6 @@ __global__ void __launch_bounds__(256) k_ks_inner(const __grid_constant__ KsInne
     const long long total = (long long)a.ne * n;  // acc poly stride
     const long long work = (long long)(a.ne - a.t0) * n;
     const Div32 dalpha = mk_div32(a.alpha);
-    pdl_trigger();
-    pdl_wait();
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < work;
          x += (long long)gridDim.x * blockDim.x) {
         const int t = a.t0 + (int)(x >> log_n);
@@ -354,8 +350,6 @@ __global__ void k_moddown_v(const uint64_t *__restrict__ z, long long z_ct, long
                             const PrimeConst *__restrict__ pc, int log_n, int batch) {
     const long long n = 1ll << log_n;
     const long long total = 2ll * batch * n;
-    pdl_trigger();
-    pdl_wait();
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
         const long long p = x >> log_n;
@@ -493,8 +487,6 @@ __global__ void k_prep_special(const uint64_t *__restrict__ acc, long long acc_c
     const long long total = 2ll * batch * per;
     const uint64_t ql = pc[level].q;
     const Div32 dv = mk_div32(K + 1);
-    pdl_trigger();
-    pdl_wait();
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
          x += (long long)gridDim.x * blockDim.x) {
         const long long p = div32((uint32_t)(x >> log_n), dv), xi = x - p * per;

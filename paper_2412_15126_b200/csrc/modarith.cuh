@@ -19,18 +19,6 @@
 #define SRK_HD static inline
 #endif
 
-#ifdef __CUDACC__
-// Programmatic dependent launch (sm_90+): a kernel launched with the
-// programmatic-stream-serialisation attribute may start while its predecessor
-// in the stream is still draining; it must not touch anything the predecessor
-// writes (or write anything it reads) before pdl_wait(), which returns once the
-// predecessor grid has completed and its memory is visible.  pdl_trigger() lets
-// the successor's CTAs be scheduled as soon as every CTA of this grid has
-// started.  Both are no-ops for a normally launched kernel.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-#endif
-
 struct PrimeConst {
     uint64_t q;       // modulus
     uint64_t two_q;   // 2q (lazy ranges)

@@ -563,7 +563,6 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB
     if constexpr (FIRST && (LD == LD_PLAIN || LD == LD_AUTO)) {
         if (f.src) lsrc = f.src + (long long)bi * f.src_ct + (long long)r * f.src_ps + (long long)t * n;
     }
-    pdl_trigger();
     const int tid = threadIdx.x;
     int sb, u;  // local sub-transform and thread-within-sub-transform
     if (COL) {
@@ -585,9 +584,6 @@ __global__ void __launch_bounds__(256, KM == 1 ? SRK_NTT_MINB_F64 : SRK_NTT_MINB
     const TwPtr tw = {(INV ? tb.itw : tb.tw) + (long long)pid * n, (INV ? tb.itwd : tb.twd) + (long long)pid * n};
     // arithmetic mode, uniform per launch: 2 = FP64 (q < 2^41), 0 = Harvey lazy integer
     constexpr int mode = KM == 1 ? 2 : 0;
-    // everything above reads launch parameters only; the limb data may still be in
-    // flight from the previous kernel of the stream (programmatic dependent launch)
-    pdl_wait();
     // the first loads need no prime constant: issue them before its (dependent) load
     uint64_t x[E];
     constexpr bool RAW = !(FIRST && LD == LD_SPREAD);
