@@ -8,8 +8,8 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 echo "launches rc=$?"
 python tools/kernel_roofline.py gpurun_out/prof/launches_psort1024.csv gpurun_out/prof/kernel_roofline_psort1024.json "tools/prof_pipe.py psort1024" > gpurun_out/prof/launches_psort1024.txt
 ncu --set full --import-source on --clock-control none --profile-from-start off --kernel-name-base mangled \
-    -k regex:"k_modup_f64ILi15|k_moddown_conv_f64_wide" -c 4 -f -o /tmp/rep/bconv python tools/prof_pipe.py psort1024 \
+    -k regex:"k_modup_conv|k_moddown_conv" -c 4 -f -o /tmp/rep/bconv python tools/prof_pipe.py psort1024 \
     > gpurun_out/prof/ncu_bconv.log 2>&1
 echo "bconv rc=$?"
 python tools/ncu_summary.py /tmp/rep/bconv.ncu-rep > gpurun_out/prof/ncu_full_bconv.txt
-cp /tmp/rep/bconv.ncu-rep gpurun_out/prof/
+python tools/pipe_util.py /tmp/rep/bconv.ncu-rep gpurun_out/prof/bconv_pipe_util.json "ncu --set full -k k_modup_conv|k_moddown_conv: python tools/prof_pipe.py psort1024" > /dev/null
