@@ -27,7 +27,7 @@
  * level l is uint64[2][l+1][N] in NTT form (limb i under prime i).  Keys are
  * uint64[dnum][2][n_q+n_p][N] indexed by prime id.  `stream` is a
  * cudaStream_t (NULL = legacy default stream).  `ws` is a device workspace of
- * at least srk_workspace_bytes(ctx) bytes, used stream-ordered.
+ * at least srk_workspace_bytes(ctx) bytes, 16-byte aligned, used stream-ordered.
  * Every function returns 0 on success or a negative code (SRK_E*) and sets a
  * thread-local message readable with srk_last_error(); nothing aborts.
  */

@@ -1136,6 +1136,8 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
     const int alpha = c->alpha, beta = (nl + alpha - 1) / alpha;
     if (beta > SRK_MAX_DIGITS) return fail(SRK_EINVAL, "too many digits");
     if (rescale_d && level < 1) return fail(SRK_EINVAL, "cannot rescale a level-0 ciphertext");
+    // the base conversions move coefficient pairs with 16-byte copies and stores
+    if (((uintptr_t)ws & 15) || (n & 1)) return fail(SRK_EINVAL, "key-switch workspace must be 16-byte aligned");
     uint64_t *dc = ws;                                 // [B][nl]
     uint64_t *ext = dc + (long long)B * nl * n;        // [B][beta][ne]
     // per-output scratch, one set per stream lane (outputs alternate between the
