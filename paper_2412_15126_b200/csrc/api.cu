@@ -1010,14 +1010,14 @@ extern "C" int srk_mul_plain_rescale(srk_ctx *c, const uint64_t *a, const uint64
 // ---------------------------------------------------------------------
 // hybrid key switching (keyswitch_impl below)
 // ---------------------------------------------------------------------
-// conversion grids: x shrunk by up to conv_cpt coefficients per thread (to amortise
-// the CTA's constant staging) only while >= ~3 waves of CTAs remain, so the
-// one-ciphertext ops of the pipelines keep enough CTAs in flight
+// conversion grids (x = target groups, y = polys, z = coefficient tiles): z shrunk by up
+// to conv_cpt tiles per CTA (to amortise the CTA's constant staging) only while >= ~3
+// waves of CTAs remain, so the one-ciphertext ops of the pipelines keep enough CTAs in flight
 static inline dim3 conv_grid(const srk_ctx *c, dim3 g) {
     const unsigned long long ctas = (unsigned long long)g.x * g.y * g.z;
     unsigned cpt = c->conv_cpt;
     while (cpt > 1 && ctas / cpt < 148ull * 8 * 3) cpt >>= 1;
-    return dim3(std::max(1u, g.x / cpt), g.y, g.z);
+    return dim3(g.x, g.y, std::max(1u, g.z / cpt));
 }
 
 // source-tile buffers of a conversion launch: two (the next tile streams in while
@@ -1060,7 +1060,7 @@ static int moddown_conv(srk_ctx *c, const BconvPlan &pl, const uint64_t *z, long
     if (ns > SRK_BCONV_MAXSRC) return fail(SRK_EINVAL, "ModDown with more than 17 source primes");
     if (ns <= 4) {
         // few sources: one coefficient per thread, sources in registers (bconv.cuh)
-        dim3 grid((unsigned)((n + 255) / 256), 2 * B, (nout + SRK_BCONV_TG - 1) / SRK_BCONV_TG);
+        dim3 grid((nout + SRK_BCONV_TG - 1) / SRK_BCONV_TG, 2 * B, (unsigned)((n + 255) / 256));
         const dim3 g2 = conv_grid(c, grid);
 #define SRK_CONV_SMALL(K)                                                                                  \
     case K:                                                                                                \
@@ -1073,9 +1073,9 @@ static int moddown_conv(srk_ctx *c, const BconvPlan &pl, const uint64_t *z, long
         return SRK_OK;
     }
     const int tg = SRK_BCONV_TG;
-    dim3 grid((unsigned)((n + SRK_BCONV_TILE - 1) / SRK_BCONV_TILE), 2 * B, (nout + tg - 1) / tg);
+    dim3 grid((nout + tg - 1) / tg, 2 * B, (unsigned)((n + SRK_BCONV_TILE - 1) / SRK_BCONV_TILE));
     const dim3 g2 = conv_grid(c, grid);
-    const int nbuf = bconv_nbuf(c, ns, g2.x < grid.x);
+    const int nbuf = bconv_nbuf(c, ns, g2.z < grid.z);
     const size_t smem = bconv_smem_bytes(ns, nbuf);
 #define SRK_MODDOWN_CONV(NB, TG)                                                                            \
     do {                                                                                                    \
@@ -1202,9 +1202,9 @@ static int keyswitch_impl(srk_ctx *c, const uint64_t *d, long long d_ct, const K
                 }
         dim3 grid((unsigned)((n + 255) / 256), B * beta, (maxd + SRK_MODUP_TCH - 1) / SRK_MODUP_TCH);
         if (f64ok && alpha <= 16) {
-            dim3 gb((unsigned)((n + SRK_BCONV_TILE - 1) / SRK_BCONV_TILE), B * beta, (maxd + SRK_BCONV_TG - 1) / SRK_BCONV_TG);
+            dim3 gb((maxd + SRK_BCONV_TG - 1) / SRK_BCONV_TG, B * beta, (unsigned)((n + SRK_BCONV_TILE - 1) / SRK_BCONV_TILE));
             const dim3 g2 = conv_grid(c, gb);
-            const int nbuf = bconv_nbuf(c, alpha, g2.x < gb.x);
+            const int nbuf = bconv_nbuf(c, alpha, g2.z < gb.z);
             const size_t smem = bconv_smem_bytes(alpha, nbuf);
 #define SRK_MODUP_CONV(W, NB)                                                     \
     do {                                                                          \

@@ -27,7 +27,7 @@
 #include "modarith.cuh"
 #include "ntt.cuh"
 
-#define SRK_BCONV_TG 8      // targets per CTA (blockIdx.z groups)
+#define SRK_BCONV_TG 8      // targets per CTA (blockIdx.x groups)
 #define SRK_BCONV_MAXSRC 17  // ModDown sources: K special primes (+ q_l for the fused rescale)
 #define SRK_BCONV_TILE 512   // coefficients per CTA tile (256 threads x 2)
 
@@ -74,7 +74,9 @@ __device__ __forceinline__ uint64_t bconv_finish(uint32_t sl, uint32_t sh, doubl
 // T0 = S0 / q, so the finished remainder is already conv[t].
 // z: B*2 polys (ct stride z_ct, poly stride z_ps) of n_src limbs; mhl / fhl:
 // [n_src][n_dst] {m, m'} / {m/q, m'/q}; corr: [n_src+1][n_dst] = v P mod q_t.
-// Grid: x = tiles of 512 coefficients (grid-stride), y = (b, r), z = target groups.
+// Grid: x = target groups, y = (b, r), z = tiles of 512 coefficients (grid-stride):
+// the CTAs that share a tile's source words are dispatched together, so the words
+// come from HBM once and from L2 for the other groups.
 // ---------------------------------------------------------------------
 template <int NBUF, int TG>
 __global__ void __launch_bounds__(256, 2) k_moddown_conv(
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(256, 2) k_moddown_conv(
     const long long n = 1ll << log_n;
     const int p = blockIdx.y;  // (b, r)
     const int b = p >> 1, r = p & 1;
-    const int t0 = blockIdx.z * TG, nt = min(n_dst - t0, TG);
+    const int t0 = blockIdx.x * TG, nt = min(n_dst - t0, TG);
     const int tid = threadIdx.x;
     for (int i = tid; i < n_src * TG; i += blockDim.x) {
         const int k = i / TG, tt = i - k * TG;
@@ -121,16 +123,16 @@ __global__ void __launch_bounds__(256, 2) k_moddown_conv(
         for (int k = 0; k < n_src; k++) cp_async16(sy + ((long long)buf * n_src + k) * 256 + tid, zp + k * n + x);
         cp_async_commit();
     };
-    long long tile = blockIdx.x;
+    long long tile = blockIdx.z;
     if (tile < tiles) stage(tile, 0);
-    for (int it = 0; tile < tiles; tile += gridDim.x, it++) {
+    for (int it = 0; tile < tiles; tile += gridDim.z, it++) {
         const int buf = NBUF == 2 ? (it & 1) : 0;
         const long long x = tile * SRK_BCONV_TILE + 2 * tid;
         const long long xl = min(x, n - 2);
         const uint32_t v2 = *reinterpret_cast<const uint16_t *>(vround + (long long)p * n + xl);
         if (NBUF == 2) {
-            if (tile + gridDim.x < tiles) {
-                stage(tile + gridDim.x, buf ^ 1);
+            if (tile + gridDim.z < tiles) {
+                stage(tile + gridDim.z, buf ^ 1);
                 cp_async_wait<1>();
             } else {
                 cp_async_wait<0>();
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(256, 2) k_moddown_conv(
                 }
             }
         }
-        if (NBUF == 1 && tile + gridDim.x < tiles) stage(tile + gridDim.x, 0);  // own slots: already consumed
+        if (NBUF == 1 && tile + gridDim.z < tiles) stage(tile + gridDim.z, 0);  // own slots: already consumed
         if (x < n) {
             uint64_t *out = conv + b * c_ct + r * c_ps + (long long)t0 * n + x;
 #pragma unroll
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(256, 4) k_moddown_conv_small(
     const long long n = 1ll << log_n;
     const int p = blockIdx.y;  // (b, r)
     const int b = p >> 1, r = p & 1;
-    const int t0 = blockIdx.z * TG, nt = min(n_dst - t0, TG);
+    const int t0 = blockIdx.x * TG, nt = min(n_dst - t0, TG);
     for (int i = threadIdx.x; i < nt * K; i += blockDim.x) {
         const int tt = i / K, k = i - tt * K;
         const ulonglong2 m = __ldg(mhl + k * n_dst + t0 + tt);
@@ -226,8 +228,8 @@ __global__ void __launch_bounds__(256, 4) k_moddown_conv_small(
     if (threadIdx.x < nt) s_q[threadIdx.x] = pc[t0 + threadIdx.x].q;
     __syncthreads();
     const uint64_t *zp = z + b * z_ct + r * z_ps;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.z * blockDim.x;
+    long long x = blockIdx.z * (long long)blockDim.x + threadIdx.x;
     uint64_t zn[K];
     int vn = 0;
     if (x < n) {
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(256, 4) k_moddown_conv_small(
 // Sources under primes < 2^41 enter whole (|term| < 2^41, T error < 2^-4 over 16
 // terms); a wider source (q_0 in digit 0: WIDE0) enters as halves with
 // m' = m 2^32 mod q_t like the ModDown sources.
-// Grid: x = tiles of 512 coefficients (grid-stride), y = b * beta + j, z = target groups.
+// Grid: x = target groups, y = b * beta + j, z = tiles of 512 coefficients (grid-stride).
 // ---------------------------------------------------------------------
 #ifndef SRK_MAX_DIGITS
 #define SRK_MAX_DIGITS 64
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(256, 2) k_modup_conv(const __grid_constant__ M
     const long long n = 1ll << log_n;
     const int b = blockIdx.y / a.beta, j = blockIdx.y - b * a.beta;
     const int g0 = j * a.alpha, gs = min(a.alpha, a.nl - g0);
-    const int t0 = blockIdx.z * TG;
+    const int t0 = blockIdx.x * TG;
     const int nd = a.n_dst[j];
     if (t0 >= nd) return;
     const int nt = min(nd - t0, TG);
@@ -350,14 +352,14 @@ __global__ void __launch_bounds__(256, 2) k_modup_conv(const __grid_constant__ M
         for (int k = 0; k < gs; k++) cp_async16(sy + ((long long)buf * a.alpha + k) * 256 + tid, src + k * n + x);
         cp_async_commit();
     };
-    long long tile = blockIdx.x;
+    long long tile = blockIdx.z;
     if (tile < tiles) stage(tile, 0);
-    for (int it = 0; tile < tiles; tile += gridDim.x, it++) {
+    for (int it = 0; tile < tiles; tile += gridDim.z, it++) {
         const int buf = NBUF == 2 ? (it & 1) : 0;
         const long long x = tile * SRK_BCONV_TILE + 2 * tid;
         if (NBUF == 2) {
-            if (tile + gridDim.x < tiles) {
-                stage(tile + gridDim.x, buf ^ 1);
+            if (tile + gridDim.z < tiles) {
+                stage(tile + gridDim.z, buf ^ 1);
                 cp_async_wait<1>();
             } else {
                 cp_async_wait<0>();
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(256, 2) k_modup_conv(const __grid_constant__ M
                 }
             }
         }
-        if (NBUF == 1 && tile + gridDim.x < tiles) stage(tile + gridDim.x, 0);  // own slots: already consumed
+        if (NBUF == 1 && tile + gridDim.z < tiles) stage(tile + gridDim.z, 0);  // own slots: already consumed
         if (x < n) {
 #pragma unroll
             for (int tt = 0; tt < TG; tt++) {
