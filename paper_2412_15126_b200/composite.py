@@ -15,15 +15,20 @@ comparison depth independent of the input gap's resolution target:
   g_3(x) = (4589 x - 16577 x^3 + 25614 x^5 - 12860 x^7) / 2^10.
 
 Each odd degree-7 polynomial is evaluated in multiplicative depth 3 with
-5 ct x ct and 4 ct x pt multiplications:
+4 ct x ct and 4 ct x pt multiplications (4 non-scalar products is the
+Paterson-Stockmeyer count for degree 7):
 
-    y = x^2, z = y^2
-    p(x) = a1 x + (a3 x) y + [a5 x + (a7 x) y] z
+    y = x^2,  z = y^2,  t7 = (a7 x) y
+    p(x) = a1 x + (a3 / a7) t7 + [a5 x + t7] z
 
-where the scalar products are issued directly at the level their sum needs
-(``mul_plain(..., level=...)`` on engines that support it), so no separate
-level-alignment step is paid.  A sign evaluation with (g, f) iterations uses
-3 (g + f) levels.
+The cubic term reuses t7 = a7 x^3 through one scalar product -- which also lands
+it on the level of the sum -- so a polynomial costs four key switches; the LAST
+polynomial of a composite keeps the five-product form a1 x + (a3 x) y +
+[a5 x + (a7 x) y] z, because the scalar a3 / a7 (7 for f_3) would multiply t7's
+noise straight into the output.  The scalar products are issued directly at the
+level their sum needs (``mul_plain(..., level=...)`` on engines that support
+it).  A sign evaluation with (g, f) iterations uses 3 (g + f) levels and
+4 (g + f) + 1 ct x ct products.
 """
 
 from __future__ import annotations
@@ -43,33 +48,43 @@ def _mul_plain_at(engine, x, c: float, level: int, site: str):
     return engine.mul_plain(x, c, site=site)
 
 
-def _three_products(engine, y, u3, u7, site):
-    """(y*y, u3*y, u7*y): one lock-step batch on engines that stack ciphertexts (the
-    pairs go to the kernels as a pointer table: y is not copied three times)."""
+def _products(engine, pairs, site):
+    """[a*b for (a, b) in pairs]: one lock-step batch on engines that stack ciphertexts
+    (the pairs go to the kernels as a pointer table: shared operands are not copied)."""
+    n = len(pairs)
+    y = pairs[0][0]
     mul_pairs = getattr(engine, "mul_pairs", None)
     if mul_pairs is not None:
-        prod = mul_pairs([(y, y), (u3, y), (u7, y)], site=f"{site}-quad")
-        if y.batch is None:
-            return tuple(engine.unstack(prod))
-        return tuple(engine.split(prod, 3))  # views: no copies
-    concat = getattr(engine, "concat", None)
-    if concat is None:
-        return (engine.mul(y, y, site=f"{site}-quad"), engine.mul(u3, y, site=f"{site}-x3"),
-                engine.mul(u7, y, site=f"{site}-x3"))
-    prod = engine.mul(concat([y, u3, u7]), concat([y, y, y]), site=f"{site}-quad")
+        prod = mul_pairs(list(pairs), site=f"{site}-quad")
+    else:
+        concat = getattr(engine, "concat", None)
+        if concat is None:
+            return tuple(engine.mul(a, b, site=f"{site}-quad") for a, b in pairs)
+        prod = engine.mul(concat([a for a, _ in pairs]), concat([b for _, b in pairs]), site=f"{site}-quad")
     if y.batch is None:
         return tuple(engine.unstack(prod))
-    return tuple(engine.split(prod, 3))  # views: no copies
+    return tuple(engine.split(prod, n))  # views: no copies
 
 
-def odd_poly_eval(engine, x, coeffs, site: str = "composite"):
-    """a1 x + a3 x^3 + a5 x^5 + a7 x^7 on ``x`` in depth 3 (coeffs = (a1, a3, a5, a7))."""
+def odd_poly_eval(engine, x, coeffs, site: str = "composite", lean: bool = True):
+    """a1 x + a3 x^3 + a5 x^5 + a7 x^7 on ``x`` in depth 3 (coeffs = (a1, a3, a5, a7)).
+
+    ``lean``: four ct x ct products -- the cubic term is (a3 / a7) t7, a scalar
+    multiple of t7 = (a7 x) x^2, instead of its own product (a3 x) x^2.  The scalar
+    also multiplies t7's key-switch / rescale noise (7x for f3, 1.3x for g3), which
+    is harmless wherever another polynomial follows (its flat regions squash it) and
+    is why the last polynomial of a composite is evaluated with five products.
+    """
     a1, a3, a5, a7 = (float(c) for c in coeffs)
     lvl = x.level
     y = engine.mul(x, x, site=f"{site}-sq")
-    u3 = engine.mul_plain(x, a3, site=f"{site}-c3")
     u7 = engine.mul_plain(x, a7, site=f"{site}-c7")
-    z, t3, t7 = _three_products(engine, y, u3, u7, site)
+    if lean and a7 != 0.0:
+        z, t7 = _products(engine, [(y, y), (u7, y)], site)  # x^4, a7 x^3 at level lvl - 2
+        t3 = engine.mul_plain(t7, a3 / a7, site=f"{site}-c3")  # a3 x^3 at level lvl - 3
+    else:
+        u3 = engine.mul_plain(x, a3, site=f"{site}-c3")
+        z, t3, t7 = _products(engine, [(y, y), (u3, y), (u7, y)], site)
     w = _mul_plain_at(engine, x, a5, lvl - 2, f"{site}-c5")
     t57 = engine.mul(engine.add(w, t7), z, site=f"{site}-x5")
     t1 = _mul_plain_at(engine, x, a1, lvl - 3, f"{site}-c1")
@@ -87,7 +102,7 @@ def composite_sign(engine, x, g_iters: int, f_iters: int, out_scale: float = 1.0
         raise ValueError("composite sign needs at least one polynomial")
     for idx, poly in enumerate(chain):
         coeffs = poly if idx < len(chain) - 1 else tuple(c * Fraction(out_scale) for c in poly)
-        x = odd_poly_eval(engine, x, coeffs, site=f"{site}-{idx}")
+        x = odd_poly_eval(engine, x, coeffs, site=f"{site}-{idx}", lean=idx < len(chain) - 1)
     return x
 
 
