@@ -27,8 +27,9 @@ polynomial of a composite keeps the five-product form a1 x + (a3 x) y +
 [a5 x + (a7 x) y] z, because the scalar a3 / a7 (7 for f_3) would multiply t7's
 noise straight into the output.  The scalar products are issued directly at the
 level their sum needs (``mul_plain(..., level=...)`` on engines that support
-it).  A sign evaluation with (g, f) iterations uses 3 (g + f) levels and
-4 (g + f) + 1 ct x ct products.
+it); on engines with ``linear_combination`` the two scalar terms a1 x and
+(a3 / a7) t7 are summed before ONE rescale.  A sign evaluation with (g, f)
+iterations uses 3 (g + f) levels and 4 (g + f) + 1 ct x ct products.
 """
 
 from __future__ import annotations
@@ -77,16 +78,22 @@ def odd_poly_eval(engine, x, coeffs, site: str = "composite", lean: bool = True)
     """
     a1, a3, a5, a7 = (float(c) for c in coeffs)
     lvl = x.level
+    lean = lean and a7 != 0.0
     y = engine.mul(x, x, site=f"{site}-sq")
     u7 = engine.mul_plain(x, a7, site=f"{site}-c7")
-    if lean and a7 != 0.0:
+    if lean:
         z, t7 = _products(engine, [(y, y), (u7, y)], site)  # x^4, a7 x^3 at level lvl - 2
-        t3 = engine.mul_plain(t7, a3 / a7, site=f"{site}-c3")  # a3 x^3 at level lvl - 3
     else:
         u3 = engine.mul_plain(x, a3, site=f"{site}-c3")
         z, t3, t7 = _products(engine, [(y, y), (u3, y), (u7, y)], site)
     w = _mul_plain_at(engine, x, a5, lvl - 2, f"{site}-c5")
     t57 = engine.mul(engine.add(w, t7), z, site=f"{site}-x5")
+    lincomb = getattr(engine, "linear_combination", None)
+    if lean and lincomb is not None:
+        # a1 x + (a3 / a7) t7 summed before ONE rescale, landing at level lvl - 3
+        return engine.add(lincomb([(x, a1), (t7, a3 / a7)], site=f"{site}-c13"), t57)
+    if lean:
+        t3 = engine.mul_plain(t7, a3 / a7, site=f"{site}-c3")  # a3 x^3 at level lvl - 3
     t1 = _mul_plain_at(engine, x, a1, lvl - 3, f"{site}-c1")
     return engine.add(engine.add(t1, t3), t57)
 
