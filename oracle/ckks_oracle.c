@@ -15,8 +15,14 @@
  * reference simulator's slots (engine.py:190-251) for the same circuit, which
  * tests/test_oracle_*.py check against golden fixtures made from the reference.
  *
- * Everything here is written for obviousness, not speed: radix-2 loops and
- * unsigned __int128 '%' reductions.  OpenMP only splits independent limbs.
+ * Everything here is written for obviousness: radix-2 loops and one exact
+ * 128-by-64-bit division per general product.  Two standard CPU techniques keep
+ * it an honest baseline for bench.py's cpu_baseline / reference arm (a CPU CKKS
+ * library does both): the transforms multiply by their precomputed twiddles
+ * with Shoup's method (w' = floor(w 2^64 / q), two multiplications and one
+ * conditional subtraction, the same canonical result), and on x86-64 the
+ * general product's remainder is the hardware divq instead of the __umodti3
+ * library call.  OpenMP only splits independent limbs.
  *
  * Conventions shared with the CUDA library (include/slotrank_b200.h):
  *   - prime table: ids 0..L are Q primes (q_0 60-bit base, q_1..q_L scaling),
@@ -44,15 +50,46 @@ typedef struct {
     uint64_t prime[ORC_MAX_PRIMES];
     uint64_t *psi_brv[ORC_MAX_PRIMES];  /* psi^brv(k) */
     uint64_t *ipsi_brv[ORC_MAX_PRIMES]; /* psi^-brv(k) */
-    uint64_t n_inv[ORC_MAX_PRIMES];
+    uint64_t *psi_sh[ORC_MAX_PRIMES];   /* floor(psi^brv(k) 2^64 / q) */
+    uint64_t *ipsi_sh[ORC_MAX_PRIMES];  /* floor(psi^-brv(k) 2^64 / q) */
+    uint64_t n_inv[ORC_MAX_PRIMES], n_inv_sh[ORC_MAX_PRIMES];
 } orc_ctx;
 
 /* ------------------------------------------------------------------ */
 /* scalar modular arithmetic                                           */
 /* ------------------------------------------------------------------ */
 
+/* a b mod q for a, b < q: the quotient is below q < 2^64, so the 128-by-64-bit
+ * hardware division cannot overflow */
 static inline uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q) {
+#if defined(__x86_64__) && !defined(ORC_NO_ASM)
+    if (a < q && b < q) {
+        uint64_t lo, hi, quo, rem;
+        __asm__("mulq %3" : "=a"(lo), "=d"(hi) : "a"(a), "rm"(b) : "cc");
+        __asm__("divq %4" : "=a"(quo), "=d"(rem) : "a"(lo), "d"(hi), "rm"(q) : "cc");
+        (void)quo;
+        return rem;
+    }
+#endif
     return (uint64_t)(((u128)a * b) % q);
+}
+/* x mod q for any 128-bit x (two hardware divisions: the high word first) */
+static inline uint64_t mod128(u128 x, uint64_t q) {
+#if defined(__x86_64__) && !defined(ORC_NO_ASM)
+    uint64_t hi = (uint64_t)(x >> 64) % q, lo = (uint64_t)x, quo, rem;
+    __asm__("divq %4" : "=a"(quo), "=d"(rem) : "a"(lo), "d"(hi), "rm"(q) : "cc");
+    (void)quo;
+    return rem;
+#else
+    return (uint64_t)(x % q);
+#endif
+}
+/* Shoup: a w mod q for a < q with ws = floor(w 2^64 / q); exact, canonical */
+static inline uint64_t shoup_const(uint64_t w, uint64_t q) { return (uint64_t)(((u128)w << 64) / q); }
+static inline uint64_t mulmod_shoup(uint64_t a, uint64_t w, uint64_t ws, uint64_t q) {
+    uint64_t hi = (uint64_t)(((u128)a * ws) >> 64);
+    uint64_t r = a * w - hi * q; /* in [0, 2q) */
+    return r >= q ? r - q : r;
 }
 static inline uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) {
     uint64_t s = a + b;
@@ -91,6 +128,8 @@ void orc_destroy(orc_ctx *c) {
     for (int i = 0; i < c->n_primes; i++) {
         free(c->psi_brv[i]);
         free(c->ipsi_brv[i]);
+        free(c->psi_sh[i]);
+        free(c->ipsi_sh[i]);
     }
     free(c);
 }
@@ -119,7 +158,14 @@ orc_ctx *orc_create(int log_n, const uint64_t *primes, const uint64_t *roots, in
             p = mulmod(p, psi, q);
             ip = mulmod(ip, ipsi, q);
         }
+        c->psi_sh[i] = (uint64_t *)malloc(sizeof(uint64_t) * c->n);
+        c->ipsi_sh[i] = (uint64_t *)malloc(sizeof(uint64_t) * c->n);
+        for (int k = 0; k < c->n; k++) {
+            c->psi_sh[i][k] = shoup_const(c->psi_brv[i][k], q);
+            c->ipsi_sh[i][k] = shoup_const(c->ipsi_brv[i][k], q);
+        }
         c->n_inv[i] = invmod((uint64_t)c->n, q);
+        c->n_inv_sh[i] = shoup_const(c->n_inv[i], q);
     }
     return c;
 }
@@ -135,14 +181,14 @@ static inline int ext_prime(const orc_ctx *c, int level, int j) {
 
 static void ntt_limb(const orc_ctx *c, uint64_t *a, int pid) {
     const uint64_t q = c->prime[pid];
-    const uint64_t *w = c->psi_brv[pid];
+    const uint64_t *w = c->psi_brv[pid], *wsh = c->psi_sh[pid];
     const int n = c->n;
     for (int m = 1, t = n >> 1; m < n; m <<= 1, t >>= 1) {
         for (int i = 0; i < m; i++) {
-            uint64_t wi = w[m + i];
+            uint64_t wi = w[m + i], ws = wsh[m + i];
             int j1 = 2 * i * t;
             for (int j = j1; j < j1 + t; j++) {
-                uint64_t u = a[j], v = mulmod(a[j + t], wi, q);
+                uint64_t u = a[j], v = mulmod_shoup(a[j + t], wi, ws, q);
                 a[j] = addmod(u, v, q);
                 a[j + t] = submod(u, v, q);
             }
@@ -152,20 +198,20 @@ static void ntt_limb(const orc_ctx *c, uint64_t *a, int pid) {
 
 static void intt_limb(const orc_ctx *c, uint64_t *a, int pid) {
     const uint64_t q = c->prime[pid];
-    const uint64_t *w = c->ipsi_brv[pid];
+    const uint64_t *w = c->ipsi_brv[pid], *wsh = c->ipsi_sh[pid];
     const int n = c->n;
     for (int m = n >> 1, t = 1; m >= 1; m >>= 1, t <<= 1) {
         for (int i = 0; i < m; i++) {
-            uint64_t wi = w[m + i];
+            uint64_t wi = w[m + i], ws = wsh[m + i];
             int j1 = 2 * i * t;
             for (int j = j1; j < j1 + t; j++) {
                 uint64_t u = a[j], v = a[j + t];
                 a[j] = addmod(u, v, q);
-                a[j + t] = mulmod(submod(u, v, q), wi, q);
+                a[j + t] = mulmod_shoup(submod(u, v, q), wi, ws, q);
             }
         }
     }
-    for (int j = 0; j < n; j++) a[j] = mulmod(a[j], c->n_inv[pid], q);
+    for (int j = 0; j < n; j++) a[j] = mulmod_shoup(a[j], c->n_inv[pid], c->n_inv_sh[pid], q);
 }
 
 /* a: uint64[nl][N], limb k under prime prime_ids[k] */
@@ -324,25 +370,22 @@ void orc_automorph(const orc_ctx *c, const uint64_t *a, uint64_t *out, int n_lim
 
 static inline uint32_t auto_index(uint32_t k, uint64_t g, int log_n);
 
-/* Base-extend d (uint64[level+1][N], NTT form) digit by digit and take the
- * inner product with the switching key: acc[r] over the extended basis
- * Q_level u P (uint64[2][level+1+K][N]).  galois != 1 applies X -> X^galois
- * to the extended digits (after base extension, so rotations of one
- * ciphertext can share it). */
-static void ks_inner_acc(const orc_ctx *c, const uint64_t *d, const uint64_t *key, int level,
-                         uint64_t galois, uint64_t *acc) {
-    const int n = c->n, nl = level + 1, K = c->n_p, ne = nl + K, np_all = c->n_primes;
+/* ModUp of every digit of d (uint64[level+1][N], NTT form): ext is
+ * uint64[beta][level+1+K][N], digit jd's limbs over the extended basis
+ * Q_level u P in NTT form (its own alpha limbs are copied). */
+static void modup_digits(const orc_ctx *c, const uint64_t *d, int level, uint64_t *ext_all) {
+    const int n = c->n, nl = level + 1, K = c->n_p, ne = nl + K;
     const int alpha = c->alpha, beta = (nl + alpha - 1) / alpha;
     uint64_t *dc = (uint64_t *)malloc(sizeof(uint64_t) * nl * n);
     memcpy(dc, d, sizeof(uint64_t) * nl * n);
+#pragma omp parallel for schedule(dynamic)
     for (int i = 0; i < nl; i++) intt_limb(c, dc + (size_t)i * n, i);
-    memset(acc, 0, sizeof(uint64_t) * 2 * ne * n);
-    uint64_t *ext = (uint64_t *)malloc(sizeof(uint64_t) * ne * n);
-
     for (int jd = 0; jd < beta; jd++) {
+        uint64_t *ext = ext_all + (size_t)jd * ne * n;
         const int g0 = jd * alpha, g1 = (jd + 1) * alpha < nl ? (jd + 1) * alpha : nl;
-        /* ModUp: y_i = [d_i * (Qhat_i)^-1]_{q_i},  Qhat_i = prod_{G\i} q */
+        /* y_i = [d_i * (Qhat_i)^-1]_{q_i},  Qhat_i = prod_{G\i} q */
         uint64_t *y = (uint64_t *)malloc(sizeof(uint64_t) * (g1 - g0) * n);
+#pragma omp parallel for
         for (int i = g0; i < g1; i++) {
             const uint64_t q = c->prime[i];
             uint64_t qhat = 1;
@@ -351,7 +394,7 @@ static void ks_inner_acc(const orc_ctx *c, const uint64_t *d, const uint64_t *ke
             const uint64_t qhinv = invmod(qhat, q);
             for (int j = 0; j < n; j++) y[(size_t)(i - g0) * n + j] = mulmod(dc[(size_t)i * n + j], qhinv, q);
         }
-#pragma omp parallel for
+#pragma omp parallel for schedule(dynamic)
         for (int t = 0; t < ne; t++) {
             const int pid = ext_prime(c, level, t);
             uint64_t *dst = ext + (size_t)t * n;
@@ -370,35 +413,58 @@ static void ks_inner_acc(const orc_ctx *c, const uint64_t *d, const uint64_t *ke
             for (int j = 0; j < n; j++) {
                 u128 s = 0;
                 for (int i = g0; i < g1; i++) s += (u128)y[(size_t)(i - g0) * n + j] * coef[i - g0];
-                dst[j] = (uint64_t)(s % p);
+                dst[j] = mod128(s, p);
             }
             ntt_limb(c, dst, pid);
         }
         free(y);
-        if (galois != 1) { /* automorphism of the extended digit (NTT domain gather) */
-            uint64_t *tmp = (uint64_t *)malloc(sizeof(uint64_t) * n);
-            for (int t = 0; t < ne; t++) {
-                uint64_t *e = ext + (size_t)t * n;
-                for (int j = 0; j < n; j++) tmp[j] = e[auto_index((uint32_t)j, galois, c->log_n)];
-                memcpy(e, tmp, sizeof(uint64_t) * n);
-            }
-            free(tmp);
-        }
-        /* inner product with digit jd of the key */
-#pragma omp parallel for
-        for (int t = 0; t < ne; t++) {
-            const int pid = ext_prime(c, level, t);
-            const uint64_t p = c->prime[pid];
+    }
+    free(dc);
+}
+
+/* acc[r] = sum_jd sigma_g(ext_jd) * key[jd][r] over the extended basis
+ * (uint64[2][level+1+K][N]); galois != 1 applies X -> X^galois to the extended
+ * digits as a gather of NTT slots (after the base extension, so rotations of
+ * one ciphertext share it). */
+static void ks_inner_from_ext(const orc_ctx *c, const uint64_t *ext_all, const uint64_t *key,
+                              int level, uint64_t galois, uint64_t *acc) {
+    const int n = c->n, nl = level + 1, K = c->n_p, ne = nl + K, np_all = c->n_primes;
+    const int alpha = c->alpha, beta = (nl + alpha - 1) / alpha;
+    uint32_t *perm = NULL;
+    if (galois != 1) {
+        perm = (uint32_t *)malloc(sizeof(uint32_t) * n);
+        for (int j = 0; j < n; j++) perm[j] = auto_index((uint32_t)j, galois, c->log_n);
+    }
+    memset(acc, 0, sizeof(uint64_t) * 2 * ne * n);
+#pragma omp parallel for schedule(dynamic)
+    for (int t = 0; t < ne; t++) {
+        const int pid = ext_prime(c, level, t);
+        const uint64_t p = c->prime[pid];
+        for (int jd = 0; jd < beta; jd++) {
+            const uint64_t *e = ext_all + ((size_t)jd * ne + t) * n;
             for (int r = 0; r < 2; r++) {
                 const uint64_t *kk = key + (((size_t)jd * 2 + r) * np_all + pid) * n;
                 uint64_t *ac = acc + ((size_t)r * ne + t) * n;
-                const uint64_t *e = ext + (size_t)t * n;
-                for (int j = 0; j < n; j++) ac[j] = addmod(ac[j], mulmod(e[j], kk[j], p), p);
+                if (perm)
+                    for (int j = 0; j < n; j++) ac[j] = addmod(ac[j], mulmod(e[perm[j]], kk[j], p), p);
+                else
+                    for (int j = 0; j < n; j++) ac[j] = addmod(ac[j], mulmod(e[j], kk[j], p), p);
             }
         }
     }
+    free(perm);
+}
+
+/* Base-extend d digit by digit and take the inner product with the switching
+ * key: acc[r] over the extended basis Q_level u P (uint64[2][level+1+K][N]). */
+static void ks_inner_acc(const orc_ctx *c, const uint64_t *d, const uint64_t *key, int level,
+                         uint64_t galois, uint64_t *acc) {
+    const int n = c->n, nl = level + 1, ne = nl + c->n_p;
+    const int beta = (nl + c->alpha - 1) / c->alpha;
+    uint64_t *ext = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)beta * ne * n);
+    modup_digits(c, d, level, ext);
+    ks_inner_from_ext(c, ext, key, level, galois, acc);
     free(ext);
-    free(dc);
 }
 
 /* Exact ModDown over a special basis S (ns limbs, prime ids sid[]):
@@ -412,6 +478,7 @@ static void moddown_exact(const orc_ctx *c, const uint64_t *xq, int no, const ui
                           const int *sid, uint64_t *out) {
     const int n = c->n;
     uint64_t *z = (uint64_t *)malloc(sizeof(uint64_t) * ns * n);
+#pragma omp parallel for
     for (int k = 0; k < ns; k++) {
         const uint64_t p = c->prime[sid[k]];
         memcpy(z + (size_t)k * n, xs + (size_t)k * n, sizeof(uint64_t) * n);
@@ -423,13 +490,18 @@ static void moddown_exact(const orc_ctx *c, const uint64_t *xq, int no, const ui
         for (int j = 0; j < n; j++) z[(size_t)k * n + j] = mulmod(z[(size_t)k * n + j], shinv, p);
     }
     uint64_t *vr = (uint64_t *)malloc(sizeof(uint64_t) * n);
+    uint64_t r1[ORC_MAX_PRIMES], r0[ORC_MAX_PRIMES];
+    for (int k = 0; k < ns; k++) {
+        const u128 R = (~(u128)0) / c->prime[sid[k]];
+        r1[k] = (uint64_t)(R >> 64);
+        r0[k] = (uint64_t)R;
+    }
+#pragma omp parallel for
     for (int j = 0; j < n; j++) {
         u128 frac = 0;
         for (int k = 0; k < ns; k++) {
             const uint64_t zk = z[(size_t)k * n + j];
-            const u128 R = (~(u128)0) / c->prime[sid[k]];
-            const uint64_t r1 = (uint64_t)(R >> 64), r0 = (uint64_t)R;
-            frac += (u128)(uint64_t)(zk * r1 + (uint64_t)(((u128)zk * r0) >> 64));
+            frac += (u128)(uint64_t)(zk * r1[k] + (uint64_t)(((u128)zk * r0[k]) >> 64));
         }
         vr[j] = (uint64_t)((frac + ((u128)1 << 63)) >> 64);
     }
@@ -450,7 +522,7 @@ static void moddown_exact(const orc_ctx *c, const uint64_t *xq, int no, const ui
         for (int j = 0; j < n; j++) {
             u128 s = 0;
             for (int k = 0; k < ns; k++) s += (u128)z[(size_t)k * n + j] * coef[k];
-            t[j] = submod((uint64_t)(s % q), mulmod(vr[j] % q, smod, q), q);
+            t[j] = submod(mod128(s, q), mulmod(vr[j] % q, smod, q), q);
         }
         ntt_limb(c, t, i);
         for (int j = 0; j < n; j++)
@@ -498,6 +570,7 @@ void orc_mul_relin_rescale(const orc_ctx *c, const uint64_t *a, const uint64_t *
         const uint64_t *ar = acc + (size_t)r * ne * n;
         const uint64_t *dr = d + (size_t)r * ps;
         /* X over Q_level: acc + P d ; over P: acc */
+#pragma omp parallel for
         for (int i = 0; i < nl; i++) {
             const uint64_t q = c->prime[i];
             uint64_t pm = 1;
@@ -529,6 +602,7 @@ void orc_mul_relin(const orc_ctx *c, const uint64_t *a, const uint64_t *b, const
     orc_tensor(c, a, b, d, level);
     uint64_t *u = (uint64_t *)malloc(sizeof(uint64_t) * 2 * ps);
     orc_keyswitch(c, d + 2 * ps, rlk, u, u + ps, level);
+#pragma omp parallel for
     for (int i = 0; i < nl; i++) {
         const uint64_t q = c->prime[i];
         for (int j = 0; j < n; j++) {
@@ -551,6 +625,7 @@ void orc_rotate(const orc_ctx *c, const uint64_t *a, const uint64_t *gkey, uint6
     orc_automorph(c, a, r0, nl, galois);
     uint64_t *u = (uint64_t *)malloc(sizeof(uint64_t) * 2 * ps);
     orc_keyswitch_g(c, a + ps, gkey, u, u + ps, level, galois);
+#pragma omp parallel for
     for (int i = 0; i < nl; i++) {
         const uint64_t q = c->prime[i];
         for (int j = 0; j < n; j++) {
@@ -561,6 +636,41 @@ void orc_rotate(const orc_ctx *c, const uint64_t *a, const uint64_t *gkey, uint6
     }
     free(u);
     free(r0);
+}
+
+/* n_rot rotations of one ciphertext sharing one base extension (hoisting):
+ * outs[r] = orc_rotate(a, gkeys[r], galois[r]) bit for bit. */
+void orc_rotate_hoisted(const orc_ctx *c, const uint64_t *a, const uint64_t *const *gkeys,
+                        const uint64_t *galois, int n_rot, uint64_t *const *outs, int level) {
+    const int n = c->n, nl = level + 1, K = c->n_p, ne = nl + K;
+    const int beta = (nl + c->alpha - 1) / c->alpha;
+    const size_t ps = (size_t)nl * n;
+    uint64_t *ext = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)beta * ne * n);
+    modup_digits(c, a + ps, level, ext);
+    uint64_t *acc = (uint64_t *)malloc(sizeof(uint64_t) * 2 * ne * n);
+    uint64_t *r0 = (uint64_t *)malloc(sizeof(uint64_t) * ps);
+    uint64_t *u0 = (uint64_t *)malloc(sizeof(uint64_t) * ps);
+    int sid[ORC_MAX_PRIMES];
+    for (int k = 0; k < K; k++) sid[k] = c->n_q + k;
+    for (int r = 0; r < n_rot; r++) {
+        uint64_t *out = outs[r];
+        ks_inner_from_ext(c, ext, gkeys[r], level, galois[r], acc);
+        moddown_exact(c, acc, nl, acc + (size_t)nl * n, K, sid, u0);
+        moddown_exact(c, acc + (size_t)ne * n, nl, acc + (size_t)ne * n + (size_t)nl * n, K, sid, out + ps);
+        orc_automorph(c, a, r0, nl, galois[r]);
+#pragma omp parallel for
+        for (int i = 0; i < nl; i++) {
+            const uint64_t q = c->prime[i];
+            for (int j = 0; j < n; j++) {
+                size_t x = (size_t)i * n + j;
+                out[x] = addmod(r0[x], u0[x], q);
+            }
+        }
+    }
+    free(u0);
+    free(r0);
+    free(acc);
+    free(ext);
 }
 
 /* ------------------------------------------------------------------ */

@@ -58,6 +58,7 @@ def lib():
                 "orc_mul_relin": ([P, P, P, P, P, c_int], None),
                 "orc_mul_relin_rescale": ([P, P, P, P, P, c_int], None),
                 "orc_rotate": ([P, P, P, P, c_int, c_uint64], None),
+                "orc_rotate_hoisted": ([P, P, P, P, c_int, P, c_int], None),
                 "orc_uniform_poly": ([P, P, c_int, P, c_uint64, c_uint64], None),
                 "orc_small_to_ntt": ([P, P, P, c_int, P], None),
                 "orc_keygen": ([P, P, P, P, c_uint64, c_uint64, P], None),
@@ -147,6 +148,17 @@ class OracleCKKS:
         out = np.empty((2, level + 1, self.n), dtype=_u64)
         self.L.orc_rotate(self.ctx, _p(a), _p(gkey), _p(out), level, galois)
         return out
+
+    def rotate_hoisted_raw(self, a, gkeys, galois, level):
+        """Rotations of one ciphertext sharing one base extension; each output
+        is bit-identical to rotate_raw (ckks_oracle.c orc_rotate_hoisted)."""
+        r = len(galois)
+        outs = [np.empty((2, level + 1, self.n), dtype=_u64) for _ in range(r)]
+        kp = np.array([_p(k) for k in gkeys], dtype=_u64)
+        op = np.array([_p(o) for o in outs], dtype=_u64)
+        g = np.array([int(x) for x in galois], dtype=_u64)
+        self.L.orc_rotate_hoisted(self.ctx, _p(a), _p(kp), _p(g), r, _p(op), level)
+        return outs
 
     def uniform(self, n_limbs, prime_ids, seed, stream_base):
         out = np.empty((n_limbs, self.n), dtype=_u64)

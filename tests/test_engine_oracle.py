@@ -144,3 +144,20 @@ def test_batched_ops_match_single(eng, x):
     for got, want in pairs:
         for g, w in zip(eng.unstack(got), want):
             assert g.level == w.level and np.array_equal(g.data, w.data)
+
+
+def test_hoisted_rotations_equal_single_rotations():
+    """orc_rotate_hoisted (the CPU baseline's rotations: one base extension for
+    all of them) is bit-identical to orc_rotate, at a full and at a lower level."""
+    p = preset("toy_deep")
+    eng = oracle_engine(p)
+    be = eng.backend
+    ct = eng.encrypt(np.linspace(-0.9, 0.9, 16))
+    two_n = 2 * p.ring_degree
+    galois = [pow(5, k, two_n) for k in (1, 2, 5)] + [two_n - 1]
+    for level in (ct.level, 2):
+        a = np.ascontiguousarray(ct.data[:, : level + 1])
+        keys = [be.galois_key(g) for g in galois]
+        outs = be.o.rotate_hoisted_raw(a, keys, galois, level)
+        for g, k, out in zip(galois, keys, outs):
+            assert np.array_equal(out, be.o.rotate_raw(a, k, g, level))
