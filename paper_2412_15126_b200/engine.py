@@ -337,13 +337,33 @@ class CKKSEngineCore:
     # ------------------------------------------------------------------
     # data movement
     # ------------------------------------------------------------------
-    def encrypt(self, values) -> Ciphertext:
-        """Pack ``values`` into the slots (zero padded) at full level."""
+    def encrypt(self, values, level: int | None = None) -> Ciphertext:
+        """Pack ``values`` into the slots (zero padded) at full level.
+
+        ``level`` (extension; the reference's ``encrypt`` has no such argument)
+        starts the ciphertext lower in the chain: a circuit of depth d needs only
+        level d, and every operation's cost grows with the level it runs at
+        (``circuit_depth`` measures d without touching ciphertext data)."""
         arr = np.asarray(values, dtype=np.float64).ravel()
         n = self.params.slot_count
         if arr.size > n:
             raise CapacityError(f"{arr.size} values do not fit in {n} slots")
-        return self._encrypt_at(arr, self.params.max_level)
+        if level is None:
+            level = self.params.max_level
+        if not 0 <= level <= self.params.max_level:
+            raise EngineError(f"level {level} outside the chain [0, {self.params.max_level}]")
+        return self._encrypt_at(arr, int(level))
+
+    def circuit_depth(self, circuit) -> int:
+        """Levels ``circuit(engine, ciphertext)`` consumes from a fresh ciphertext,
+        found on the level tracer (host bookkeeping only; ``levels.py``)."""
+        from .levels import level_tracer
+
+        t = level_tracer(self)
+        top = self.params.max_level
+        out = circuit(t, t.token(top))
+        outs = out if isinstance(out, (list, tuple)) else [out]
+        return top - min(o.level for o in outs)
 
     def _encrypt_at(self, arr: np.ndarray, level: int) -> Ciphertext:
         p = self.params

@@ -161,3 +161,23 @@ def test_hoisted_rotations_equal_single_rotations():
         outs = be.o.rotate_hoisted_raw(a, keys, galois, level)
         for g, k, out in zip(galois, keys, outs):
             assert np.array_equal(out, be.o.rotate_raw(a, k, g, level))
+
+
+def test_depth_fitted_encryption():
+    """engine.encrypt(level=d) with d = circuit_depth(circuit): the circuit ends at
+    level 0 with the same decrypted result as from the top of the chain; the depth
+    comes from the level tracer (no ciphertext data) and equals the levels consumed."""
+    eng = oracle_engine(preset("toy_deep"))
+    cfg = M.KernelConfig(mode="composite", composite=(3, 2))
+    v = np.array([0.30, 0.10, 0.80, 0.55, 0.20, 0.95, 0.65, 0.40])
+    depth = eng.circuit_depth(lambda e, c: M.rank(e, c, 8, cfg).ranks)
+    full = M.rank(eng, eng.encrypt(v), 8, cfg).ranks
+    assert depth == eng.params.max_level - full.level
+    fit = M.rank(eng, eng.encrypt(v, level=depth), 8, cfg).ranks
+    assert fit.level == 0
+    assert np.array_equal(np.rint(M.read_row(eng, fit, 8)), fractional_ranks(v))
+    assert np.abs(M.read_row(eng, fit, 8) - M.read_row(eng, full, 8)).max() < 1e-4
+    with pytest.raises(DepthBudgetError):
+        M.rank(eng, eng.encrypt(v, level=depth - 1), 8, cfg)
+    with pytest.raises(EngineError):
+        eng.encrypt(v, level=eng.params.max_level + 1)

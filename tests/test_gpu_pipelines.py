@@ -227,3 +227,34 @@ def test_concurrent_ops_from_host_threads(eng12):
         assert torch.equal(a, b.data)
     rep = eng12.cost_snapshot()
     assert rep.rotations == 8 and rep.ctct_mults == 8 and rep.additions == 8
+
+
+def test_depth_fitted_rank_bit_exact_and_cfg4_masks(require_cuda, eng_long):
+    """Inputs encrypted at the level the circuit's depth needs (engine.encrypt(level=...)):
+    the toy rank's limbs stay bit-equal to the CPU oracle's down to level 0, and the
+    cfg 4 argmin mask from level 39 of the long chain still selects the right index."""
+    from oracle.oracle import oracle_engine
+
+    p = preset("toy_deep")
+    gpu, cpu = M.B200Engine(p), oracle_engine(p)
+    v = np.array([0.30, 0.10, 0.80, 0.55, 0.20, 0.95, 0.65, 0.40])
+    cfg = M.KernelConfig(mode="composite", composite=(3, 2))
+    d = gpu.circuit_depth(lambda e, c: M.rank(e, c, 8, cfg).ranks)
+    assert d == cpu.circuit_depth(lambda e, c: M.rank(e, c, 8, cfg).ranks)
+    rg = M.rank(gpu, gpu.encrypt(v, level=d), 8, cfg).ranks
+    rc = M.rank(cpu, cpu.encrypt(v, level=d), 8, cfg).ranks
+    assert rg.level == rc.level == 0
+    assert np.array_equal(gpu.backend.to_host(rg.data), rc.data)
+    assert np.array_equal(np.rint(M.read_row(gpu, rg, 8)), fractional_ranks(v))
+
+    v128 = np.random.default_rng(0).choice(1024, 128, replace=False) / 1024
+    cfg4 = M.KernelConfig(mode="composite", composite=(4, 2), indicator_composite=(4, 2),
+                          tie_margin=2.0 ** -11)
+    q = M.StatisticQuery("min")
+    need = eng_long.circuit_depth(lambda e, c: M.order_statistic_mask(e, c, 128, q, cfg4))
+    assert need < eng_long.params.max_level
+    mask = M.order_statistic_mask(eng_long, eng_long.encrypt(v128, level=need), 128, q, cfg4)
+    assert mask.level == 0
+    m = M.read_row(eng_long, mask, 128)
+    assert int(np.argmax(m)) == int(np.argmin(v128))
+    assert np.abs(m - np.eye(128)[int(np.argmin(v128))]).max() < 1e-6
