@@ -509,13 +509,13 @@ def run_pipelines(torch, quick=False):
         need_m = eng.circuit_depth(lambda e, c, q=q: order_statistic_mask(e, c, 128, q, cfg4))
         need_v = eng.circuit_depth(lambda e, c, q=q: order_statistic_value(e, c, 128, q, cfg4))
         ctm, ctv = eng.encrypt(v128, level=need_m), eng.encrypt(v128, level=need_v)
-        full_dt, _ = _timed(torch, lambda q=q: read_row(eng, order_statistic_mask(eng, ct, 128, q, cfg4), 128))
+        full_dt, _ = _timed(torch, lambda q=q: read_row(eng, order_statistic_mask(eng, ct, 128, q, cfg4), 128), reps=2)
         cost, _ = _census(eng, lambda q=q: order_statistic_mask(eng, ctm, 128, q, cfg4))
-        dt, m = _timed(torch, lambda q=q: read_row(eng, order_statistic_mask(eng, ctm, 128, q, cfg4), 128))
+        dt, m = _timed(torch, lambda q=q: read_row(eng, order_statistic_mask(eng, ctm, 128, q, cfg4), 128), reps=2)
         gdt = _graph_latency(eng, lambda c, q=q: order_statistic_mask(eng, c, 128, q, cfg4), ctm)
-        full_vdt, _ = _timed(torch, lambda q=q: eng.decrypt(order_statistic_value(eng, ct, 128, q, cfg4))[0])
+        full_vdt, _ = _timed(torch, lambda q=q: eng.decrypt(order_statistic_value(eng, ct, 128, q, cfg4))[0], reps=2)
         vcost, _ = _census(eng, lambda q=q: order_statistic_value(eng, ctv, 128, q, cfg4))
-        vdt, val = _timed(torch, lambda q=q: eng.decrypt(order_statistic_value(eng, ctv, 128, q, cfg4))[0])
+        vdt, val = _timed(torch, lambda q=q: eng.decrypt(order_statistic_value(eng, ctv, 128, q, cfg4))[0], reps=2)
         vgdt = _graph_latency(eng, lambda c, q=q: order_statistic_value(eng, c, 128, q, cfg4), ctv)
         out[f"{name}_n128_s"] = {"latency_s": dt, "graph_replay_s": gdt,
                                  "start_level": need_m, "full_chain_latency_s": full_dt,
@@ -555,7 +555,7 @@ def run_pipelines(torch, quick=False):
         bvf = block_split(eng, v1024, level=need)
         first, _ = _timed(torch, lambda pk=pk: block_merge(eng, multi_rank(eng, bvf, scfg.kernel, packed=pk)))
         cost, _ = _census(eng, lambda pk=pk: multi_rank(eng, bvf, scfg.kernel, packed=pk))
-        warm, rk = _timed(torch, lambda pk=pk: block_merge(eng, multi_rank(eng, bvf, scfg.kernel, packed=pk)))
+        warm, rk = _timed(torch, lambda pk=pk: block_merge(eng, multi_rank(eng, bvf, scfg.kernel, packed=pk)), reps=2)
         out[name] = {"latency_s": first, "warm_latency_s": warm, "start_level": need,
                      "full_chain_latency_s": full,
                      "exact_ranks": bool(np.array_equal(np.rint(rk), _fr(v1024))),
