@@ -396,6 +396,38 @@ def run_sharded_sort(torch, dist):
     return out
 
 
+NVLINK_GBS = 900.0  # per direction per GPU through NVSwitch (B200_PROFILING.md)
+
+
+def projected_sharded_sort(torch, eng, bv, kcfg):
+    """N=1024 sort at 2/4/8 ranks PROJECTED from one GPU: rank 0's own kernels (the rank
+    with the most units under the round-robin deal) timed here through shard.py's
+    real code path with collectives that move no data (shard.ProjectedComm), plus the
+    bytes each collective would move at NVLink rate (ring all-reduce 2(W-1)/W S,
+    all-gather (W-1)/W S).  Not a measured multi-GPU latency."""
+    from paper_2412_15126_b200 import SortConfig
+    from paper_2412_15126_b200.shard import ProjectedComm, multi_sort_sharded
+
+    out = {}
+    for packed in (False, True):
+        scfg = SortConfig(kernel=kcfg, tie_correction=False, packed=packed)
+        for world in (2, 4, 8):
+            comm = ProjectedComm(0, world)
+            multi_sort_sharded(eng, bv, scfg, comm)  # warm-up (level plan, constants)
+            comm.all_reduce_bytes = comm.all_gather_bytes = comm.collectives = 0
+            dt, _ = _timed(torch, lambda: multi_sort_sharded(eng, bv, scfg, comm))
+            f = (world - 1) / world
+            comm_s = (2 * f * comm.all_reduce_bytes + f * comm.all_gather_bytes) / (NVLINK_GBS * 1e9)
+            out[f"{'packed' if packed else 'reference'}_w{world}"] = {
+                "rank0_compute_s": dt, "collectives": comm.collectives,
+                "all_reduce_bytes": comm.all_reduce_bytes, "all_gather_bytes": comm.all_gather_bytes,
+                "modelled_nvlink_s": comm_s, "projected_latency_s": dt + comm_s}
+    out["note"] = ("projection from ONE B200: rank 0's kernels of the W-rank sharded sort run here with "
+                   "data-free collectives (shard.ProjectedComm; outputs not meaningful), NVLink time "
+                   f"modelled at {NVLINK_GBS:.0f} GB/s per direction, no overlap assumed")
+    return out
+
+
 def _timed(torch, fn, reps=1):
     """Best-of-reps wall seconds of fn() bracketed by device syncs."""
     best, r = None, None
@@ -572,6 +604,7 @@ def run_pipelines(torch, quick=False):
                                   "max_abs_err": float(np.abs(srt - np.sort(v1024)).max()),
                                   "cost": cost, "params": "long", "gpus": 1,
                                   "layout": "two 128x128 blocks per ciphertext (opt-in, packing.py)"}
+    out["sort_n1024_sharded_projection"] = projected_sharded_sort(torch, eng, bv, scfg.kernel)
     del eng, bv
     torch.cuda.empty_cache()
     # the tie-corrected sort (block tie offsets) needs two more levels: long58

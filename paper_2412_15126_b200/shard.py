@@ -57,7 +57,7 @@ from .ranking import (
 )
 from .sorting import SortConfig, _neg_rank_targets, common_level, place_block
 
-__all__ = ["Comm", "multi_rank_sharded", "multi_sort_sharded"]
+__all__ = ["Comm", "ProjectedComm", "multi_rank_sharded", "multi_sort_sharded"]
 
 # The packed layout (packing.py, two blocks per ciphertext) shards the same way:
 # packed comparisons / placements are the units dealt round-robin, the
@@ -130,6 +130,46 @@ class Comm:
         self.dist.all_gather(parts, t.contiguous(), group=self.group)
         self.collectives += 1
         return torch.cat(parts)
+
+
+class ProjectedComm:
+    """ONE rank's share of a ``world``-rank run inside a single process, for timing
+    that rank's kernels when the other GPUs are absent.  The collectives move no
+    data -- ``all_reduce`` leaves the local partial sums, ``all_gather`` tiles the
+    local rows -- so the ciphertexts that come out are NOT the pipeline's result
+    (the multi-rank result is checked by the gloo / NCCL tests); the kernel work
+    of rank ``rank`` and the bytes each collective would move are exactly those of
+    the real run (levels come from the same cached plan).  ``bench.py`` reports
+    them as a projection, never as a measured multi-GPU latency."""
+
+    def __init__(self, rank: int, world: int):
+        if not 0 <= rank < world <= MAX_WORLD:
+            raise ValueError(f"need 0 <= rank < world <= {MAX_WORLD}")
+        self.rank, self.world = rank, world
+        self.collectives = self.level_syncs = 0
+        self.planned = self.recorder = None
+        self.all_reduce_bytes = self.all_gather_bytes = 0  # payload per rank / gathered total
+
+    def owner(self, unit_index: int) -> int:
+        return unit_index % self.world
+
+    def exchange_levels(self, levels):
+        if self.recorder is not None:
+            self.recorder.append(list(levels))
+        if not self.planned:
+            raise RuntimeError("ProjectedComm needs the cached level plan (_with_plan)")
+        return self.planned.pop(0)
+
+    def all_reduce(self, t):
+        self.collectives += 1
+        self.all_reduce_bytes += t.numel() * t.element_size()
+
+    def all_gather(self, t):
+        import torch
+
+        self.collectives += 1
+        self.all_gather_bytes += self.world * t.numel() * t.element_size()
+        return torch.cat([t] * self.world)
 
 
 class _TraceComm:

@@ -123,3 +123,32 @@ def test_three_rank_packed_sort_bit_identical(tmp_path):
         for i, blk in enumerate(res.blocks):
             assert np.array_equal(got[f"arr_{i}"], blk.data), (r, i)
     assert np.abs(M.block_merge(eng, res) - np.sort(PACKVALS)).max() < 5e-3
+
+
+def test_projected_comm_runs_one_ranks_share():
+    """shard.ProjectedComm (bench.py's one-GPU projection of the W-rank sort): rank r's
+    share runs through the real sharded code path with data-free collectives -- five
+    collectives, no level exchange, and over all ranks exactly the single-process
+    pipeline's ct x ct products (no unit is computed twice)."""
+    from oracle.oracle import oracle_engine
+    from paper_2412_15126_b200.shard import ProjectedComm, multi_sort_sharded
+
+    eng = oracle_engine(preset("toy_sort"))
+    bv = M.block_split(eng, VALUES)
+    scfg = M.SortConfig(kernel=KCFG, tie_correction=False)
+    eng.cost_reset()
+    M.multi_sort(eng, bv, scfg)
+    total = eng.cost_snapshot()
+    world, ctct, cmps = 2, 0, 0
+    for r in range(world):
+        comm = ProjectedComm(r, world)
+        eng.cost_reset()
+        out = multi_sort_sharded(eng, bv, scfg, comm)
+        c = eng.cost_snapshot()
+        assert len(out.blocks) == len(bv.blocks)
+        assert comm.collectives == 5 and comm.level_syncs == 0
+        assert comm.all_reduce_bytes > 0 and comm.all_gather_bytes > 0
+        assert c.ctct_mults < total.ctct_mults
+        ctct += c.ctct_mults
+        cmps += c.cmp_evals
+    assert ctct == total.ctct_mults and cmps == total.cmp_evals
