@@ -488,13 +488,15 @@ def run_pipelines(torch, quick=False):
     # the same rank started at the level its depth needs (engine.encrypt(level=...)):
     # 21 of the chain's 30 limbs carry the whole circuit
     need = eng.circuit_depth(lambda e, c: rank(e, c, 128, cfg).ranks)
-    ctf = eng.encrypt(v128, level=need)
-    dtf, resf = _timed(torch, lambda: read_row(eng, rank(eng, ctf, 128, cfg).ranks, 128), reps=3)
+    fitted = lambda c: rank(eng, eng.fit_depth(c, need), 128, cfg).ranks  # noqa: E731
+    dtf, resf = _timed(torch, lambda: read_row(eng, fitted(ct), 128), reps=3)
     out["rank_n128_depth_fitted_s"] = {
-        "latency_s": dtf, "graph_replay_s": _graph_latency(eng, lambda c: rank(eng, c, 128, cfg).ranks, ctf),
+        "latency_s": dtf, "graph_replay_s": _graph_latency(eng, fitted, ct),
         "exact_ranks": bool(np.array_equal(np.rint(resf), fractional_ranks(v128))),
         "max_rank_err": float(np.abs(resf - fractional_ranks(v128)).max()),
-        "start_level": need, "params": "cfg3 (input encrypted at level = circuit depth)",
+        "start_level": need,
+        "params": "cfg3 (the same full-chain input ciphertext, dropped to the circuit's depth inside the "
+                  "timed pipeline: engine.fit_depth)",
         "kernel": "composite g3^4 o f3^2"}
     # the reference's own comparison: Chebyshev interpolant, degree 1024
     ccfg = KernelConfig(mode="chebyshev", degree=1024)
@@ -536,19 +538,21 @@ def run_pipelines(torch, quick=False):
                          ("median_k64", StatisticQuery("kth", k=64), 63)):
         want = order[pos]
         order_statistic_value(eng, ct, 128, q, cfg4)  # warm-up keys
-        # inputs start at the level the circuit's depth needs (the long chain is sized for
-        # the N=1024 sort; a mask needs ~40 of its 57 limbs): engine.encrypt(level=...)
+        # the pipeline first drops the full-chain input to the level its depth needs (the long
+        # chain is sized for the N=1024 sort; a mask needs ~40 of its 57 limbs): engine.fit_depth,
+        # one fused multiply-and-rescale inside the timed region
         need_m = eng.circuit_depth(lambda e, c, q=q: order_statistic_mask(e, c, 128, q, cfg4))
         need_v = eng.circuit_depth(lambda e, c, q=q: order_statistic_value(e, c, 128, q, cfg4))
-        ctm, ctv = eng.encrypt(v128, level=need_m), eng.encrypt(v128, level=need_v)
+        fm = lambda c, q=q, d=need_m: order_statistic_mask(eng, eng.fit_depth(c, d), 128, q, cfg4)  # noqa: E731
+        fv = lambda c, q=q, d=need_v: order_statistic_value(eng, eng.fit_depth(c, d), 128, q, cfg4)  # noqa: E731
         full_dt, _ = _timed(torch, lambda q=q: read_row(eng, order_statistic_mask(eng, ct, 128, q, cfg4), 128), reps=2)
-        cost, _ = _census(eng, lambda q=q: order_statistic_mask(eng, ctm, 128, q, cfg4))
-        dt, m = _timed(torch, lambda q=q: read_row(eng, order_statistic_mask(eng, ctm, 128, q, cfg4), 128), reps=2)
-        gdt = _graph_latency(eng, lambda c, q=q: order_statistic_mask(eng, c, 128, q, cfg4), ctm)
+        cost, _ = _census(eng, lambda: fm(ct))
+        dt, m = _timed(torch, lambda: read_row(eng, fm(ct), 128), reps=2)
+        gdt = _graph_latency(eng, fm, ct)
         full_vdt, _ = _timed(torch, lambda q=q: eng.decrypt(order_statistic_value(eng, ct, 128, q, cfg4))[0], reps=2)
-        vcost, _ = _census(eng, lambda q=q: order_statistic_value(eng, ctv, 128, q, cfg4))
-        vdt, val = _timed(torch, lambda q=q: eng.decrypt(order_statistic_value(eng, ctv, 128, q, cfg4))[0], reps=2)
-        vgdt = _graph_latency(eng, lambda c, q=q: order_statistic_value(eng, c, 128, q, cfg4), ctv)
+        vcost, _ = _census(eng, lambda: fv(ct))
+        vdt, val = _timed(torch, lambda: eng.decrypt(fv(ct))[0], reps=2)
+        vgdt = _graph_latency(eng, fv, ct)
         out[f"{name}_n128_s"] = {"latency_s": dt, "graph_replay_s": gdt,
                                  "start_level": need_m, "full_chain_latency_s": full_dt,
                                  "index_ok": bool(int(np.argmax(m)) == int(want)),
@@ -557,8 +561,9 @@ def run_pipelines(torch, quick=False):
                                  "value_latency_s": vdt, "value_graph_replay_s": vgdt,
                                  "value_start_level": need_v, "value_full_chain_latency_s": full_vdt,
                                  "value": float(val), "value_err": float(abs(val - v128[want])),
-                                 "value_cost": vcost, "params": "long (inputs encrypted at level = circuit depth; "
-                                                                "full_chain_*: inputs at the top of the chain)",
+                                 "value_cost": vcost, "params": "long (the full-chain input dropped to the circuit's depth "
+                                                                "inside the timed pipeline, engine.fit_depth; "
+                                                                "full_chain_*: run from the top of the chain)",
                                  "note": "value = mask + SumC(mask*v) * Goldschmidt(SumC(mask)), 8 iterations"}
 
     # config 5: sort N=1024 (8 blocks of 128), composite comparisons
@@ -580,14 +585,16 @@ def run_pipelines(torch, quick=False):
     from oracle.plain import fractional_ranks as _fr
     for name, pk in (("rank_n1024_s", False), ("rank_n1024_packed_s", True)):
         full, _ = _timed(torch, lambda pk=pk: block_merge(eng, multi_rank(eng, bv, scfg.kernel, packed=pk)))
-        # blocks encrypted at the level the rank's depth needs (27 of the chain's 56)
+        # the full-chain blocks dropped to the level the rank's depth needs (27 of the chain's 56)
+        # inside the timed region (engine.fit_depth)
         need = eng.circuit_depth(lambda e, c, pk=pk: list(multi_rank(
             e, type(bv)(blocks=tuple(c for _ in bv.blocks), block_size=bv.block_size, total_len=bv.total_len),
             scfg.kernel, packed=pk).blocks))
-        bvf = block_split(eng, v1024, level=need)
-        first, _ = _timed(torch, lambda pk=pk: block_merge(eng, multi_rank(eng, bvf, scfg.kernel, packed=pk)))
-        cost, _ = _census(eng, lambda pk=pk: multi_rank(eng, bvf, scfg.kernel, packed=pk))
-        warm, rk = _timed(torch, lambda pk=pk: block_merge(eng, multi_rank(eng, bvf, scfg.kernel, packed=pk)), reps=2)
+        fit = lambda d=need: type(bv)(blocks=tuple(eng.fit_depth(b, d) for b in bv.blocks),  # noqa: E731
+                                      block_size=bv.block_size, total_len=bv.total_len)
+        first, _ = _timed(torch, lambda pk=pk: block_merge(eng, multi_rank(eng, fit(), scfg.kernel, packed=pk)))
+        cost, _ = _census(eng, lambda pk=pk: multi_rank(eng, fit(), scfg.kernel, packed=pk))
+        warm, rk = _timed(torch, lambda pk=pk: block_merge(eng, multi_rank(eng, fit(), scfg.kernel, packed=pk)), reps=2)
         out[name] = {"latency_s": first, "warm_latency_s": warm, "start_level": need,
                      "full_chain_latency_s": full,
                      "exact_ranks": bool(np.array_equal(np.rint(rk), _fr(v1024))),

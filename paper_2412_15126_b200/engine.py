@@ -354,6 +354,14 @@ class CKKSEngineCore:
             raise EngineError(f"level {level} outside the chain [0, {self.params.max_level}]")
         return self._encrypt_at(arr, int(level))
 
+    def fit_depth(self, ct: Ciphertext, circuit) -> Ciphertext:
+        """``ct`` dropped to the level ``circuit`` needs (one fused multiply-and-rescale
+        that discards the unused limbs, scale kept exact; ``at_level``): a ciphertext
+        encrypted at the top of a long chain runs a shallow circuit at the shallow
+        circuit's cost.  Unchanged when the circuit needs every level ``ct`` has."""
+        d = circuit if isinstance(circuit, int) else self.circuit_depth(circuit)  # a known depth, or trace it
+        return ct if ct.level <= d else self.at_level(ct, d)
+
     def circuit_depth(self, circuit) -> int:
         """Levels ``circuit(engine, ciphertext)`` consumes from a fresh ciphertext,
         found on the level tracer (host bookkeeping only; ``levels.py``)."""

@@ -177,6 +177,10 @@ def test_depth_fitted_encryption():
     assert fit.level == 0
     assert np.array_equal(np.rint(M.read_row(eng, fit, 8)), fractional_ranks(v))
     assert np.abs(M.read_row(eng, fit, 8) - M.read_row(eng, full, 8)).max() < 1e-4
+    dropped = eng.fit_depth(eng.encrypt(v), lambda e, c: M.rank(e, c, 8, cfg).ranks)
+    assert dropped.level == depth and eng.fit_depth(dropped, depth) is dropped
+    assert np.abs(eng.decrypt(dropped)[:8] - v).max() < TOL
+    assert np.array_equal(np.rint(M.read_row(eng, M.rank(eng, dropped, 8, cfg).ranks, 8)), fractional_ranks(v))
     with pytest.raises(DepthBudgetError):
         M.rank(eng, eng.encrypt(v, level=depth - 1), 8, cfg)
     with pytest.raises(EngineError):

@@ -246,6 +246,13 @@ def test_depth_fitted_rank_bit_exact_and_cfg4_masks(require_cuda, eng_long):
     assert rg.level == rc.level == 0
     assert np.array_equal(gpu.backend.to_host(rg.data), rc.data)
     assert np.array_equal(np.rint(M.read_row(gpu, rg, 8)), fractional_ranks(v))
+    # the same from a full-chain ciphertext: fit_depth drops the unused limbs first
+    circ = lambda e, c: M.rank(e, c, 8, cfg).ranks  # noqa: E731
+    fg, fc = gpu.fit_depth(gpu.encrypt(v), circ), cpu.fit_depth(cpu.encrypt(v), circ)
+    assert fg.level == fc.level == d
+    assert np.array_equal(gpu.backend.to_host(fg.data), fc.data)
+    rg = M.rank(gpu, fg, 8, cfg).ranks
+    assert rg.level == 0 and np.array_equal(gpu.backend.to_host(rg.data), M.rank(cpu, fc, 8, cfg).ranks.data)
 
     v128 = np.random.default_rng(0).choice(1024, 128, replace=False) / 1024
     cfg4 = M.KernelConfig(mode="composite", composite=(4, 2), indicator_composite=(4, 2),
@@ -253,7 +260,7 @@ def test_depth_fitted_rank_bit_exact_and_cfg4_masks(require_cuda, eng_long):
     q = M.StatisticQuery("min")
     need = eng_long.circuit_depth(lambda e, c: M.order_statistic_mask(e, c, 128, q, cfg4))
     assert need < eng_long.params.max_level
-    mask = M.order_statistic_mask(eng_long, eng_long.encrypt(v128, level=need), 128, q, cfg4)
+    mask = M.order_statistic_mask(eng_long, eng_long.fit_depth(eng_long.encrypt(v128), need), 128, q, cfg4)
     assert mask.level == 0
     m = M.read_row(eng_long, mask, 128)
     assert int(np.argmax(m)) == int(np.argmin(v128))
