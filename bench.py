@@ -489,6 +489,7 @@ def run_pipelines(torch, quick=False):
     # 21 of the chain's 30 limbs carry the whole circuit
     need = eng.circuit_depth(lambda e, c: rank(e, c, 128, cfg).ranks)
     fitted = lambda c: rank(eng, eng.fit_depth(c, need), 128, cfg).ranks  # noqa: E731
+    fitted(ct)  # warm-up: the dropped level's constants and allocator blocks
     dtf, resf = _timed(torch, lambda: read_row(eng, fitted(ct), 128), reps=3)
     out["rank_n128_depth_fitted_s"] = {
         "latency_s": dtf, "graph_replay_s": _graph_latency(eng, fitted, ct),
