@@ -237,19 +237,42 @@ def test_cfg4_masks_and_values_n128_vs_slotsim(eng_long, kind):
     assert verr < BOUNDS["cfg4_value"], verr
 
 
-def _multi_sort_check(eng, v, tie_correction, bound, packed=False):
-    scfg = M.SortConfig(kernel=M.KernelConfig(mode="composite", composite=(6, 2),
+def _multi_sort_check(eng, v, tie_correction, bound, packed=False, composite=(6, 2), fit=False):
+    scfg = M.SortConfig(kernel=M.KernelConfig(mode="composite", composite=composite,
                                               indicator_composite=(6, 2)), tie_correction=tie_correction,
                         packed=packed)
+    bv = M.block_split(eng, v)
+    if fit:  # blocks dropped to the circuit's depth first (engine.fit_depth; not a counted op)
+        depth = eng.circuit_depth(lambda e, c: list(M.multi_sort(
+            e, type(bv)(blocks=tuple(c for _ in bv.blocks), block_size=bv.block_size, total_len=bv.total_len),
+            scfg).blocks))
+        assert depth < eng.params.max_level
+        bv = type(bv)(blocks=tuple(eng.fit_depth(b, depth) for b in bv.blocks), block_size=bv.block_size,
+                      total_len=bv.total_len)
     eng.cost_reset()
-    out = M.block_merge(eng, M.multi_sort(eng, M.block_split(eng, v), scfg))
+    res = M.multi_sort(eng, bv, scfg)
+    if fit:
+        assert all(b.level == 0 for b in res.blocks)
+    out = M.block_merge(eng, res)
     sim = _sim(eng)
     ref = M.block_merge(sim, M.multi_sort(sim, M.block_split(sim, v), scfg))
     assert np.array_equal(np.argsort(out, kind="stable"), np.argsort(np.sort(v), kind="stable"))
     assert np.abs(out - np.sort(v)).max() < 1e-6
     err = float(np.abs(out - ref).max())
     assert err < bound, err
-    assert eng.cost_snapshot() == sim.cost_snapshot()
+    got, want = eng.cost_snapshot().__dict__, sim.cost_snapshot().__dict__
+    if fit:  # the drop is not an op, but the levels it skips are not "consumed" by the simulator
+        got.pop("levels_consumed"), want.pop("levels_consumed")
+    assert got == want
+
+
+@pytest.mark.parametrize("packed", [False, True])
+def test_cfg5_multi_sort_n1024_shallower_comparison_depth_fitted(eng_long, packed):
+    """bench.py's ``sort_n1024_cmp52*``: comparison g3^5 o f3^2 under the (6,2) indicator,
+    52 levels, blocks dropped to level 52 first: order exact, 1e-6 against the slot
+    oracle on the same circuit and against np.sort."""
+    v = np.random.default_rng(0).choice(8192, 1024, replace=False) / 8192
+    _multi_sort_check(eng_long, v, False, BOUNDS["cfg5_sort"], packed=packed, composite=(5, 2), fit=True)
 
 
 def test_cfg5_multi_sort_n1024_vs_slotsim(eng_long):
