@@ -64,6 +64,12 @@ int srk_ctx_create(int device, int log_n, const uint64_t *primes, const uint64_t
                    int n_p, int dnum, srk_ctx **out);
 int srk_ctx_destroy(srk_ctx *ctx);
 size_t srk_workspace_bytes(const srk_ctx *ctx);
+/* Optional: the caller's second stream.  Two independent op sequences (the
+ * ReplR and TransR+ReplC branches of the reference's rank_pipeline,
+ * ranking.py:158-159) issued on the caller's main stream and on `stream`, each
+ * with its own workspace, then run concurrently: ops on `stream` use the
+ * context's second set of internal streams.  NULL unregisters. */
+int srk_ctx_set_branch_stream(srk_ctx *ctx, void *stream);
 
 /* batched NTT over n_polys polys of n_limbs limbs each (limb i under prime
  * first_prime + i; poly p at data + p * poly_stride words).  Inputs and

@@ -29,6 +29,7 @@ EXPORTS = {
                        POINTER(c_void_p)],
     "srk_ctx_destroy": [c_void_p],
     "srk_workspace_bytes": [c_void_p],
+    "srk_ctx_set_branch_stream": [c_void_p, c_void_p],
     "srk_ntt": [c_void_p, _u64p, c_int, c_longlong, c_int, c_int, c_int, c_void_p],
     "srk_ntt_ext": [c_void_p, _u64p, c_int, c_longlong, c_int, c_int, c_void_p],
     "srk_addsub": [c_void_p, _u64p, _u64p, _u64p, c_int, c_int, c_void_p],

@@ -12,6 +12,7 @@ workspace is used stream-ordered, one workspace per stream.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -70,6 +71,8 @@ class CudaBackend:
         self._capture_keepalive: list = []  # pinned sources of copies captured in CUDA graphs
         self._key_lock = threading.Lock()
         self._call_lock = threading.RLock()
+        self._branch = None  # second stream for engine.parallel (run_parallel)
+        self._tls = threading.local()
         self.launches = 0
         self._sk_ntt = None
 
@@ -95,6 +98,32 @@ class CudaBackend:
             ws = torch.empty(self._ws_bytes, dtype=torch.uint8, device=self.device)
             self._ws[s] = ws
         return _ptr(ws)
+
+    def run_parallel(self, first, second):
+        """first() on the current stream, second() on the backend's branch stream (forked
+        before first's work is enqueued, joined after second's), each with its own
+        key-switch workspace.  Every use of the branch stream starts by waiting on the
+        current stream's tail and ends joined into it, so tensors crossing the two
+        streams are never recycled by the caching allocator while the other stream
+        can still touch them; also valid inside a CUDA-graph capture (fork / join
+        edges).  Nested calls (already on the branch stream) run in turn."""
+        if getattr(self._tls, "in_branch", False) or os.environ.get("SRK_BRANCH", "1") == "0":
+            return first(), second()
+        main = torch.cuda.current_stream(self.device)
+        if self._branch is None:
+            self._branch = torch.cuda.Stream(self.device)
+            _lib.check(self.lib.srk_ctx_set_branch_stream(self.ctx, self._branch.cuda_stream))
+        side = self._branch
+        side.wait_stream(main)
+        a = first()
+        self._tls.in_branch = True
+        try:
+            with torch.cuda.stream(side):
+                b = second()
+        finally:
+            self._tls.in_branch = False
+        main.wait_stream(side)
+        return a, b
 
     def release_workspace(self, stream_handle: int) -> None:
         """Drop the key-switch workspace cached for a stream that is going away."""

@@ -165,6 +165,7 @@ struct srk_ctx {
     int ntt_cta_threads = 128;  // threads per NTT pass CTA (128: 8 CTAs/SM, cheaper barriers)
     unsigned conv_cpt = 4;  // coefficients per thread of the conversions (amortises their staging)
     cudaStream_t nside[2] = {nullptr, nullptr};
+    cudaStream_t branch = nullptr;  // the caller's second stream (srk_ctx_set_branch_stream): NTT lane 1
     cudaEvent_t ev_nfork[2] = {nullptr, nullptr}, ev_njoin[2] = {nullptr, nullptr};
 };
 
@@ -484,6 +485,15 @@ static size_t relin_limbs(const srk_ctx *c, int level, int B) {
     return (size_t)B * (3 * nl + 2 * nl) + std::max(ks_limbs(c, level, B), rescale_limbs(level, B));
 }
 
+// Two op sequences issued alternately on the caller's main stream and on this
+// branch stream run side by side: ops on the branch stream use the context's second
+// set of internal NTT streams and events instead of queueing behind the main stream's.
+extern "C" int srk_ctx_set_branch_stream(srk_ctx *c, void *stream) {
+    if (!c) return fail(SRK_EINVAL, "null context");
+    c->branch = (cudaStream_t)stream;
+    return SRK_OK;
+}
+
 extern "C" size_t srk_workspace_bytes(const srk_ctx *c) {
     const int L = c->L;
     const int WB = c->ws_batch;
@@ -669,7 +679,7 @@ static int ntt_run(const srk_ctx *c, LimbBatch b, bool inverse, const FuseArgs &
         chunks.push_back({l0, nlc, f64, 0});
     }
     // independent chunks alternate between s and this lane's NTT side stream
-    const int lane = s == c->side ? 1 : 0;
+    const int lane = (s == c->side || (c->branch && s == c->branch)) ? 1 : 0;
     const bool two = c->ntt_streams >= 2 && chunks.size() >= 2 && c->nside[lane];
     if (two) {
         CU(cudaEventRecord(c->ev_nfork[lane], s));

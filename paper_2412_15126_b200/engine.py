@@ -354,6 +354,16 @@ class CKKSEngineCore:
             raise EngineError(f"level {level} outside the chain [0, {self.params.max_level}]")
         return self._encrypt_at(arr, int(level))
 
+    def parallel(self, first, second):
+        """``(first(), second())`` for two independent op sequences (the ReplR and
+        TransR + ReplC branches of a rank).  Host order, counters and trace are those
+        of calling them in turn; a backend with streams (``CudaBackend.run_parallel``)
+        issues the second on its branch stream, so at one ciphertext per op -- where
+        the kernels are latency-bound and leave most of the GPU idle -- the two
+        run side by side.  Results are bit-identical either way."""
+        run = getattr(self.backend, "run_parallel", None)
+        return run(first, second) if run is not None else (first(), second())
+
     def fit_depth(self, ct: Ciphertext, circuit) -> Ciphertext:
         """``ct`` dropped to the level ``circuit`` needs (one fused multiply-and-rescale
         that discards the unused limbs, scale kept exact; ``at_level``): a ciphertext
