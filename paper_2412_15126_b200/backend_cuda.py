@@ -317,6 +317,27 @@ class CudaBackend:
                    self.stream())
         return out
 
+    def lincomb_multi(self, terms, term_levels, residues_rows, level: int, batch=None) -> list:
+        """Several sums over the SAME terms: out_l = sum_i k[l][i] T_i (no rescale);
+        residues_rows: [n_out][n_terms][level+1] ints.  One pass over the terms per
+        eight outputs (srk_lincomb_multi).  Unbatched terms: ONE tensor [n_out][2][level+1][N];
+        batched terms: a list of n_out tensors."""
+        n_t, n_o = len(terms), len(residues_rows)
+        if batch is None:  # one stacked tensor: the caller rescales all sums in one batched call
+            block = self._out(level, n_o)
+            outs = [block[i] for i in range(n_o)]
+        else:
+            block, outs = None, [self._out(level, batch) for _ in range(n_o)]
+        k = np.array([[[int(r) for r in row] for row in rows] for rows in residues_rows],
+                     dtype=np.uint64).view(np.int64)
+        k_dev = self._h2d(k)
+        ptrs = (ctypes.c_void_p * n_t)(*[_ptr(t) for t in terms])
+        limbs = (ctypes.c_int * n_t)(*[lv + 1 for lv in term_levels])
+        optrs = (ctypes.c_void_p * n_o)(*[_ptr(o) for o in outs])
+        self._call("srk_lincomb_multi", ptrs, limbs, n_t, _ptr(k_dev), optrs, n_o, batch or 1, level,
+                   self.stream())
+        return outs if block is None else block
+
     def rotate(self, a, galois: int, level: int, batch=None) -> torch.Tensor:
         key = self.galois_key(galois)
         out = self._out(level, batch)

@@ -1692,6 +1692,47 @@ extern "C" int srk_lincomb(srk_ctx *c, const uint64_t *const *terms, const int *
     return SRK_OK;
 }
 
+// n_out linear combinations of the same terms: outs[l] = sum_i k[l][i] * terms[i]
+// (k: DEVICE residues [n_out][n_terms][level+1]); eight outputs per pass over the terms
+extern "C" int srk_lincomb_multi(srk_ctx *c, const uint64_t *const *terms, const int *term_limbs,
+                                 int n_terms, const uint64_t *k, uint64_t *const *outs, int n_out,
+                                 int batch, int level, void *stream) {
+    TRY(check_level(c, level));
+    if (n_terms < 1 || n_terms > SRK_LC_MAX) return fail(SRK_EINVAL, "1..64 terms");
+    if (n_out < 1) return fail(SRK_EINVAL, "no outputs");
+    LinCombArgs la;
+    memset(&la, 0, sizeof la);
+    for (int i = 0; i < n_terms; i++) {
+        if (term_limbs[i] < level + 1) return fail(SRK_EINVAL, "term below the output level");
+        la.term[i] = terms[i];
+        la.term_ps[i] = (long long)term_limbs[i] * c->n;
+        la.term_ct[i] = 2ll * term_limbs[i] * c->n;
+    }
+    la.n_terms = n_terms;
+    la.nl = level + 1;
+    la.batch = batch;
+    const long long total = 2ll * batch * (level + 1) * c->n;
+    const int stride = n_terms * (level + 1);
+    for (int l0 = 0; l0 < n_out; l0 += SRK_LC_OUTS) {
+        LinCombOuts lo;
+        memset(&lo, 0, sizeof lo);
+        lo.n_out = std::min(SRK_LC_OUTS, n_out - l0);
+        lo.k_out_stride = stride;
+        for (int l = 0; l < SRK_LC_OUTS; l++) lo.out[l] = outs[l0 + std::min(l, lo.n_out - 1)];
+        la.k = k + (long long)l0 * stride;
+        if (lo.n_out <= 1)
+            k_lincomb_multi<1><<<grid_for(total), 256, 0, S(stream)>>>(la, lo, c->d_pc, c->log_n);
+        else if (lo.n_out <= 2)
+            k_lincomb_multi<2><<<grid_for(total), 256, 0, S(stream)>>>(la, lo, c->d_pc, c->log_n);
+        else if (lo.n_out <= 4)
+            k_lincomb_multi<4><<<grid_for(total), 256, 0, S(stream)>>>(la, lo, c->d_pc, c->log_n);
+        else
+            k_lincomb_multi<8><<<grid_for(total), 256, 0, S(stream)>>>(la, lo, c->d_pc, c->log_n);
+        LAUNCHED();
+    }
+    return SRK_OK;
+}
+
 extern "C" int srk_reduce_mod(srk_ctx *c, uint64_t *data, int n_polys, int level, void *stream) {
     TRY(check_level(c, level));
     const long long total = (long long)n_polys * (level + 1) * c->n;

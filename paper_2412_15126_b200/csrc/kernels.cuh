@@ -544,6 +544,65 @@ __global__ void k_lincomb(const __grid_constant__ LinCombArgs a, const PrimeCons
     }
 }
 
+// Several linear combinations of the SAME terms (all BSGS leaf sums of a polynomial share
+// the baby-step ciphertexts): out_l = sum_i k[l][i][j] T_i for l < L, every term word
+// read once for all L outputs (one launch per 8 outputs instead of one pass over the
+// terms per output).  k: device [n_out][n_terms][nl]; outs: n_out destinations.
+#define SRK_LC_OUTS 8
+struct LinCombOuts {
+    uint64_t *out[SRK_LC_OUTS];
+    int n_out, k_out_stride;  // residue words between consecutive outputs' tables
+};
+template <int L>
+__global__ void __launch_bounds__(256) k_lincomb_multi(const __grid_constant__ LinCombArgs a,
+                                                       const __grid_constant__ LinCombOuts o,
+                                                       const PrimeConst *__restrict__ pc, int log_n) {
+    const long long n = 1ll << log_n;
+    const long long per = 2ll * a.nl * n;
+    const long long total = per * a.batch;
+    const Div32 d2 = mk_div32(2 * a.nl), d1 = mk_div32(a.nl);
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long b = div32((uint32_t)(x >> log_n), d2), xi = x - b * per;
+        const long long lr = xi >> log_n;
+        const int r = (int)div32((uint32_t)lr, d1), j = (int)(lr - (long long)r * a.nl);
+        const long long off = xi & (n - 1);
+        const PrimeConst P = pc[j];
+        const bool small = P.q < (1ull << 41);
+        U128 acc[L];
+#pragma unroll
+        for (int l = 0; l < L; l++) acc[l] = {0, 0};
+        for (int i0 = 0; i0 < a.n_terms; i0 += 8) {
+            const int ni = min(8, a.n_terms - i0);
+            uint64_t v[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++)  // the group's loads first: all in flight together
+                v[i] = i < ni ? __ldg(a.term[i0 + i] + b * a.term_ct[i0 + i] + r * a.term_ps[i0 + i] +
+                                      (long long)j * n + off)
+                              : 0;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                if (i < ni) {
+                    const uint64_t *kp = a.k + (long long)(i0 + i) * a.nl + j;
+#pragma unroll
+                    for (int l = 0; l < L; l++)  // rows past n_out repeat the last one (never stored)
+                        mac(acc[l], v[i], __ldg(kp + (long long)min(l, o.n_out - 1) * o.k_out_stride));
+                }
+            }
+            // keep the 128-bit sums bounded: reduce after every 8 products -- under a
+            // prime < 2^41 (every scaling prime) 64 products of residues stay below 2^88,
+            // so only the last group reduces
+            if (!small || i0 + 8 >= a.n_terms) {
+#pragma unroll
+                for (int l = 0; l < L; l++) acc[l] = {0, reduce_u128(acc[l], P)};
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < L; l++)
+            if (l < o.n_out) o.out[l][x] = acc[l].lo;
+    }
+}
+
 // square (NTT domain) of s over all primes: relinearisation source key
 __global__ void k_square(const uint64_t *__restrict__ s, uint64_t *__restrict__ out,
                          const PrimeConst *__restrict__ pc, int log_n, int n_limbs) {

@@ -572,6 +572,37 @@ class CKKSEngineCore:
             self._adds += (len(terms) - 1) * (nb or 1)
         return self._emit(data, o, max(t.rot_chain for t in cts), nb)
 
+    def linear_combinations(self, cts, coeff_rows, site: str = "lincomb") -> list:
+        """``[linear_combination(zip(cts, row)) for row in coeff_rows]`` -- the leaf sums of
+        one BSGS evaluation share their baby-step ciphertexts.  Same results, levels and
+        counters; a backend with ``lincomb_multi`` reads every term once per eight sums
+        instead of once per sum."""
+        multi = getattr(self.backend, "lincomb_multi", None)
+        if multi is None or len(coeff_rows) < 2:
+            return [self.linear_combination(list(zip(cts, row)), site=site) for row in coeff_rows]
+        self._check(*cts)
+        nb = self._nb(*cts)
+        lo = min(t.level for t in cts)
+        if lo < 1:
+            raise DepthBudgetError(site, lo)
+        o = lo - 1
+        pr = self.params
+        rows = [[self._residues(int(round(float(c) * pr.scales[o] * pr.q_primes[o + 1] / pr.scales[ct.level])),
+                                o + 1) for ct, c in zip(cts, row)] for row in coeff_rows]
+        sums = multi([t.data for t in cts], [t.level for t in cts], rows, o + 1, batch=nb)
+        if nb is None:  # the sums come stacked: one batched rescale, then views of its rows
+            scaled = self.backend.rescale(sums, o + 1, batch=len(rows))
+            datas = [self.backend.index(scaled, i) for i in range(len(rows))]
+        else:
+            datas = [self.backend.rescale(summed, o + 1, batch=nb) for summed in sums]
+        out = []
+        for data in datas:
+            with self._lock:
+                self._ctpt += len(cts) * (nb or 1)
+                self._adds += (len(cts) - 1) * (nb or 1)
+            out.append(self._emit(data, o, max(t.rot_chain for t in cts), nb))
+        return out
+
     def rotate(self, x: Ciphertext, k: int) -> Ciphertext:
         """Cyclic rotation of the slot vector; k > 0 rotates left (``engine.py:234``)."""
         self._check(x)

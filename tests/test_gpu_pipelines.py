@@ -265,3 +265,31 @@ def test_depth_fitted_rank_bit_exact_and_cfg4_masks(require_cuda, eng_long):
     m = M.read_row(eng_long, mask, 128)
     assert int(np.argmax(m)) == int(np.argmin(v128))
     assert np.abs(m - np.eye(128)[int(np.argmin(v128))]).max() < 1e-6
+
+
+@pytest.mark.parametrize("n_rows", [2, 3, 8, 11])
+def test_linear_combinations_equal_single_sums(eng12, n_rows):
+    """engine.linear_combinations (srk_lincomb_multi: every term read once per eight
+    sums) gives limb for limb the ciphertexts of one linear_combination per row --
+    terms at different levels, a batched stack, every output-group size."""
+    rng = np.random.default_rng(n_rows)
+    x = eng12.encrypt(rng.uniform(-1, 1, 64))
+    t2 = eng12.mul(x, x)
+    t3 = eng12.mul(t2, x)
+    cts = [x, t2, t3, eng12.add(t2, t3), eng12.mul_plain(t3, 0.5)]
+    rows = rng.uniform(-2, 2, (n_rows, len(cts))).tolist()
+    eng12.cost_reset()
+    many = eng12.linear_combinations(cts, rows)
+    cost_many = eng12.cost_snapshot()
+    eng12.cost_reset()
+    single = [eng12.linear_combination(list(zip(cts, row))) for row in rows]
+    assert eng12.cost_snapshot() == cost_many
+    for a, b in zip(many, single):
+        assert a.level == b.level
+        assert np.array_equal(eng12.backend.to_host(a.data), eng12.backend.to_host(b.data))
+    # lock-step batch of two ciphertexts per term
+    st = [eng12.stack([c, c]) for c in cts]
+    many_b = eng12.linear_combinations(st, rows)
+    for a, b in zip(many_b, single):
+        got = eng12.backend.to_host(eng12.unstack(a)[1].data)
+        assert np.array_equal(got, eng12.backend.to_host(b.data))

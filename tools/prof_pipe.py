@@ -12,10 +12,11 @@ import paper_2412_15126_b200 as M  # noqa: E402
 from paper_2412_15126_b200.params import preset  # noqa: E402
 
 what = sys.argv[1] if len(sys.argv) > 1 else "rank"
-if what == "rank":
+if what in ("rank", "cheb"):  # "cheb": the reference's Chebyshev d=1024 comparison
     eng = M.B200Engine(preset("cfg3"))
     v = np.random.default_rng(0).choice(1024, 128, replace=False) / 1024
-    cfg = M.KernelConfig(mode="composite", composite=(4, 2))
+    cfg = (M.KernelConfig(mode="composite", composite=(4, 2)) if what == "rank"
+           else M.KernelConfig(mode="chebyshev", degree=1024))
     ct = eng.encrypt(v)
     run = lambda: M.rank(eng, ct, 128, cfg).ranks  # noqa: E731
 else:
