@@ -188,11 +188,13 @@ int srk_lincomb(srk_ctx *ctx, const uint64_t *const *terms, const int *term_limb
                 const uint64_t *k, uint64_t *out, int batch, int level, void *stream);
 /* n_out leaf sums over the SAME terms (every BSGS leaf of a polynomial shares the
  * baby-step ciphertexts, reference chebyshev.py:206-222): outs[l] = sum_i k[l][i] *
- * terms[i]; k: DEVICE residues [n_out][n_terms][level+1]; outs: HOST array of device
- * pointers.  Each term word is read once per eight outputs. */
+ * terms[i]; k: DEVICE residues [n_out][n_terms][level+1]; kf: DEVICE doubles k / q_j in
+ * the same layout (limbs under primes < 2^41 then sum on the FP64 pipe, exactly) or
+ * NULL; outs: HOST array of device pointers.  Each term word is read once per eight
+ * outputs. */
 int srk_lincomb_multi(srk_ctx *ctx, const uint64_t *const *terms, const int *term_limbs, int n_terms,
-                      const uint64_t *k, uint64_t *const *outs, int n_out, int batch, int level,
-                      void *stream);
+                      const uint64_t *k, const double *kf, uint64_t *const *outs, int n_out, int batch,
+                      int level, void *stream);
 /* multi-GPU fix-up after an int64 all-reduce of n_polys polys of level+1
  * limbs (values < 2^63): reduce every limb mod its prime in place */
 int srk_reduce_mod(srk_ctx *ctx, uint64_t *data, int n_polys, int level, void *stream);

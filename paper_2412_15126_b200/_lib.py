@@ -77,8 +77,8 @@ EXPORTS = {
     "srk_decrypt_limb0": [c_void_p, _u64p, _u64p, _u64p, c_int, c_void_p, c_void_p],
     "srk_lincomb": [c_void_p, POINTER(c_void_p), POINTER(c_int), c_int, _u64p, _u64p, c_int, c_int,
                     c_void_p],
-    "srk_lincomb_multi": [c_void_p, POINTER(c_void_p), POINTER(c_int), c_int, _u64p, POINTER(c_void_p), c_int,
-                          c_int, c_int, c_void_p],
+    "srk_lincomb_multi": [c_void_p, POINTER(c_void_p), POINTER(c_int), c_int, _u64p, _u64p, POINTER(c_void_p),
+                          c_int, c_int, c_int, c_void_p],
     "srk_reduce_mod": [c_void_p, _u64p, c_int, c_int, c_void_p],
     "srk_encode_plain": [c_void_p, _u64p, _u64p, c_int, c_void_p],
 }

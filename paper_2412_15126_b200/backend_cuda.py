@@ -331,11 +331,14 @@ class CudaBackend:
         k = np.array([[[int(r) for r in row] for row in rows] for rows in residues_rows],
                      dtype=np.uint64).view(np.int64)
         k_dev = self._h2d(k)
+        # k / q_j for the FP64 path of the limbs under primes < 2^41 (exact there: k < 2^41)
+        q = np.array(self.params.q_primes[: level + 1], dtype=np.float64)
+        kf_dev = self._h2d(np.ascontiguousarray(k.view(np.uint64).astype(np.float64) / q).view(np.int64))
         ptrs = (ctypes.c_void_p * n_t)(*[_ptr(t) for t in terms])
         limbs = (ctypes.c_int * n_t)(*[lv + 1 for lv in term_levels])
         optrs = (ctypes.c_void_p * n_o)(*[_ptr(o) for o in outs])
-        self._call("srk_lincomb_multi", ptrs, limbs, n_t, _ptr(k_dev), optrs, n_o, batch or 1, level,
-                   self.stream())
+        self._call("srk_lincomb_multi", ptrs, limbs, n_t, _ptr(k_dev), _ptr(kf_dev), optrs, n_o, batch or 1,
+                   level, self.stream())
         return outs if block is None else block
 
     def rotate(self, a, galois: int, level: int, batch=None) -> torch.Tensor:

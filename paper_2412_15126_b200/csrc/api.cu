@@ -1693,13 +1693,15 @@ extern "C" int srk_lincomb(srk_ctx *c, const uint64_t *const *terms, const int *
 }
 
 // n_out linear combinations of the same terms: outs[l] = sum_i k[l][i] * terms[i]
-// (k: DEVICE residues [n_out][n_terms][level+1]); eight outputs per pass over the terms
+// (k: DEVICE residues [n_out][n_terms][level+1]; kf: k / q as doubles in the same layout,
+// or null); eight outputs per pass over the terms
 extern "C" int srk_lincomb_multi(srk_ctx *c, const uint64_t *const *terms, const int *term_limbs,
-                                 int n_terms, const uint64_t *k, uint64_t *const *outs, int n_out,
-                                 int batch, int level, void *stream) {
+                                 int n_terms, const uint64_t *k, const double *kf,
+                                 uint64_t *const *outs, int n_out, int batch, int level, void *stream) {
     TRY(check_level(c, level));
     if (n_terms < 1 || n_terms > SRK_LC_MAX) return fail(SRK_EINVAL, "1..64 terms");
     if (n_out < 1) return fail(SRK_EINVAL, "no outputs");
+    if (c->n % 256) return fail(SRK_EINVAL, "srk_lincomb_multi needs a ring degree divisible by 256");
     LinCombArgs la;
     memset(&la, 0, sizeof la);
     for (int i = 0; i < n_terms; i++) {
@@ -1720,6 +1722,7 @@ extern "C" int srk_lincomb_multi(srk_ctx *c, const uint64_t *const *terms, const
         lo.k_out_stride = stride;
         for (int l = 0; l < SRK_LC_OUTS; l++) lo.out[l] = outs[l0 + std::min(l, lo.n_out - 1)];
         la.k = k + (long long)l0 * stride;
+        lo.kf = kf ? kf + (long long)l0 * stride : nullptr;
         if (lo.n_out <= 1)
             k_lincomb_multi<1><<<grid_for(total), 256, 0, S(stream)>>>(la, lo, c->d_pc, c->log_n);
         else if (lo.n_out <= 2)

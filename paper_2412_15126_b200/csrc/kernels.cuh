@@ -551,25 +551,43 @@ __global__ void k_lincomb(const __grid_constant__ LinCombArgs a, const PrimeCons
 #define SRK_LC_OUTS 8
 struct LinCombOuts {
     uint64_t *out[SRK_LC_OUTS];
+    const double *kf;         // k / q per table entry (same layout as k), or null
     int n_out, k_out_stride;  // residue words between consecutive outputs' tables
 };
 template <int L>
 __global__ void __launch_bounds__(256) k_lincomb_multi(const __grid_constant__ LinCombArgs a,
                                                        const __grid_constant__ LinCombOuts o,
                                                        const PrimeConst *__restrict__ pc, int log_n) {
+    // this limb's table entries {k, bits of k / q} per (term, output), staged once per
+    // 256-element block (the block shares its limb: 256 divides N)
+    __shared__ ulonglong2 s_k[SRK_LC_MAX * L];
     const long long n = 1ll << log_n;
     const long long per = 2ll * a.nl * n;
     const long long total = per * a.batch;
     const Div32 d2 = mk_div32(2 * a.nl), d1 = mk_div32(a.nl);
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
-         x += (long long)gridDim.x * blockDim.x) {
-        const long long b = div32((uint32_t)(x >> log_n), d2), xi = x - b * per;
+    const int tid = threadIdx.x;
+    for (long long x0 = blockIdx.x * (long long)blockDim.x; x0 < total; x0 += (long long)gridDim.x * blockDim.x) {
+        const long long x = x0 + tid;
+        const long long b = div32((uint32_t)(x0 >> log_n), d2), xi = x0 - b * per;
         const long long lr = xi >> log_n;
         const int r = (int)div32((uint32_t)lr, d1), j = (int)(lr - (long long)r * a.nl);
-        const long long off = xi & (n - 1);
+        const long long off = (xi & (n - 1)) + tid;
         const PrimeConst P = pc[j];
-        const bool small = P.q < (1ull << 41);
-        U128 acc[L];
+        // under a prime < 2^41 (every scaling prime) with the k / q table: wrapped 64-bit
+        // sum S and FP64 quotient T = sum v (k / q), result S - round(T) q (the base
+        // conversions' recipe, bconv.cuh: exact while |T error| < 1/2 -- up to 32 terms
+        // below 2^41 keep T < 2^46, so 32 FMA roundings of <= 2^-8 plus the table's 2^-53
+        // relative error stay below 0.14); else 128-bit sums, reduced after every 8 products
+        const bool f64 = o.kf != nullptr && P.q < SRK_F64_Q && a.n_terms <= 32;
+        __syncthreads();  // the previous block's reads of s_k are done
+        for (int e = tid; e < a.n_terms * L; e += blockDim.x) {
+            const int i = e / L, l = e - i * L;  // rows past n_out repeat the last one (never stored)
+            const long long kl = (long long)i * a.nl + j + (long long)min(l, o.n_out - 1) * o.k_out_stride;
+            s_k[e] = make_ulonglong2(__ldg(a.k + kl),
+                                     f64 ? (uint64_t)__double_as_longlong(__ldg(o.kf + kl)) : 0ull);
+        }
+        __syncthreads();
+        U128 acc[L];  // f64 path: lo = S, hi = bits of T
 #pragma unroll
         for (int l = 0; l < L; l++) acc[l] = {0, 0};
         for (int i0 = 0; i0 < a.n_terms; i0 += 8) {
@@ -577,29 +595,49 @@ __global__ void __launch_bounds__(256) k_lincomb_multi(const __grid_constant__ L
             uint64_t v[8];
 #pragma unroll
             for (int i = 0; i < 8; i++)  // the group's loads first: all in flight together
-                v[i] = i < ni ? __ldg(a.term[i0 + i] + b * a.term_ct[i0 + i] + r * a.term_ps[i0 + i] +
-                                      (long long)j * n + off)
-                              : 0;
+                v[i] = (i < ni && x < total)
+                           ? __ldg(a.term[i0 + i] + b * a.term_ct[i0 + i] + r * a.term_ps[i0 + i] +
+                                   (long long)j * n + off)
+                           : 0;
 #pragma unroll
             for (int i = 0; i < 8; i++) {
                 if (i < ni) {
-                    const uint64_t *kp = a.k + (long long)(i0 + i) * a.nl + j;
+                    const ulonglong2 *kp = s_k + (i0 + i) * L;
+                    if (f64) {
+                        const uint32_t vl = (uint32_t)v[i], vh = (uint32_t)(v[i] >> 32);
+                        const double dv = f64_of_u64(v[i]);
 #pragma unroll
-                    for (int l = 0; l < L; l++)  // rows past n_out repeat the last one (never stored)
-                        mac(acc[l], v[i], __ldg(kp + (long long)min(l, o.n_out - 1) * o.k_out_stride));
+                        for (int l = 0; l < L; l++) {
+                            const ulonglong2 kk = kp[l];
+                            uint32_t sl = (uint32_t)acc[l].lo, sh = (uint32_t)(acc[l].lo >> 32);
+                            mac_wide(sl, sh, vl, (uint32_t)kk.x);
+                            mac_hi(sh, vl, (uint32_t)(kk.x >> 32));
+                            mac_hi(sh, vh, (uint32_t)kk.x);
+                            acc[l].lo = ((uint64_t)sh << 32) | sl;
+                            acc[l].hi = (uint64_t)__double_as_longlong(
+                                fma(dv, __longlong_as_double((long long)kk.y),
+                                    __longlong_as_double((long long)acc[l].hi)));
+                        }
+                    } else {
+#pragma unroll
+                        for (int l = 0; l < L; l++) mac(acc[l], v[i], kp[l].x);
+                    }
                 }
             }
-            // keep the 128-bit sums bounded: reduce after every 8 products -- under a
-            // prime < 2^41 (every scaling prime) 64 products of residues stay below 2^88,
-            // so only the last group reduces
-            if (!small || i0 + 8 >= a.n_terms) {
+            if (!f64) {
 #pragma unroll
                 for (int l = 0; l < L; l++) acc[l] = {0, reduce_u128(acc[l], P)};
             }
         }
+        if (x < total) {
 #pragma unroll
-        for (int l = 0; l < L; l++)
-            if (l < o.n_out) o.out[l][x] = acc[l].lo;
+            for (int l = 0; l < L; l++) {
+                if (l < o.n_out)
+                    o.out[l][x] = f64 ? bconv_finish((uint32_t)acc[l].lo, (uint32_t)(acc[l].lo >> 32),
+                                                     __longlong_as_double((long long)acc[l].hi), P.q)
+                                      : acc[l].lo;
+            }
+        }
     }
 }
 

@@ -293,3 +293,20 @@ def test_linear_combinations_equal_single_sums(eng12, n_rows):
     for a, b in zip(many_b, single):
         got = eng12.backend.to_host(eng12.unstack(a)[1].data)
         assert np.array_equal(got, eng12.backend.to_host(b.data))
+
+
+@pytest.mark.parametrize("repeat", [6, 7])
+def test_linear_combinations_many_terms(eng12, repeat):
+    """30 terms (the FP64-quotient sums of the limbs under 40-bit primes, at their
+    32-term limit's side) and 35 terms (128-bit sums everywhere): same limbs as the
+    single sums."""
+    rng = np.random.default_rng(repeat)
+    x = eng12.encrypt(rng.uniform(-1, 1, 64))
+    t2 = eng12.mul(x, x)
+    base = [x, t2, eng12.mul(t2, x), eng12.add(t2, x), eng12.mul_plain(t2, 0.25)]
+    cts = base * repeat
+    rows = rng.uniform(-3, 3, (5, len(cts))).tolist()
+    many = eng12.linear_combinations(cts, rows)
+    for a, row in zip(many, rows):
+        b = eng12.linear_combination(list(zip(cts, row)))
+        assert np.array_equal(eng12.backend.to_host(a.data), eng12.backend.to_host(b.data))
