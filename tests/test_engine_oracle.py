@@ -185,3 +185,28 @@ def test_depth_fitted_encryption():
         M.rank(eng, eng.encrypt(v, level=depth - 1), 8, cfg)
     with pytest.raises(EngineError):
         eng.encrypt(v, level=eng.params.max_level + 1)
+
+
+def test_levelwise_bsgs_equals_recursive_bsgs():
+    """chebyshev._bsgs_levelwise (giant-step products of one tree depth in one
+    engine.mul_pairs call; the GPU engine's path) yields the ciphertext, level and
+    counters of the recursive _bsgs, limb for limb, on the CPU oracle engine."""
+    import math
+
+    from paper_2412_15126_b200 import chebyshev as C
+
+    eng = oracle_engine(preset("toy_deep"))
+    x = eng.encrypt(np.linspace(-0.9, 0.9, 32))
+    for degree in (37, 64, 127):
+        poly = C._step_poly(degree)
+        coeffs = C._strip(np.asarray(poly.coeffs, dtype=np.float64))
+        m = max(1, math.ceil(math.log2(len(coeffs))))
+        bs = 1 << max(1, m // 2)
+        eng.cost_reset()
+        a_ct, a_c = C._bsgs(eng, coeffs, C._ChebPowers(eng, x), bs)
+        cost_a = eng.cost_snapshot()
+        eng.cost_reset()
+        b_ct, b_c = C._bsgs_levelwise(eng, coeffs, C._ChebPowers(eng, x), bs)
+        assert eng.cost_snapshot() == cost_a
+        assert a_c == b_c and a_ct.level == b_ct.level
+        assert np.array_equal(a_ct.data, b_ct.data)
