@@ -210,3 +210,25 @@ def test_levelwise_bsgs_equals_recursive_bsgs():
         assert eng.cost_snapshot() == cost_a
         assert a_c == b_c and a_ct.level == b_ct.level
         assert np.array_equal(a_ct.data, b_ct.data)
+
+
+def test_paired_goldschmidt_equals_sequential():
+    """goldschmidt_inverse's paired schedule (y_k and e_{k+1} in one engine.mul_pairs call,
+    taken when the backend has batched products) gives the sequential loop's ciphertext
+    limb for limb, with the same counters."""
+    from paper_2412_15126_b200 import chebyshev as C
+
+    eng = oracle_engine(preset("toy_deep"))
+    x = eng.encrypt(np.linspace(1.0, 7.5, 16))
+    eng.cost_reset()
+    par = C.goldschmidt_inverse(eng, x, (0.5, 8.5), 5)
+    cost = eng.cost_snapshot()
+    eng.backend.mul_relin_rescale_pairs = None  # hides the batched product: the sequential loop runs
+    try:
+        eng.cost_reset()
+        seq = C.goldschmidt_inverse(eng, x, (0.5, 8.5), 5)
+        assert eng.cost_snapshot() == cost
+    finally:
+        del eng.backend.mul_relin_rescale_pairs
+    assert par.level == seq.level and np.array_equal(par.data, seq.data)
+    assert np.abs(eng.decrypt(par)[:16] - 1.0 / np.linspace(1.0, 7.5, 16)).max() < 1e-3
